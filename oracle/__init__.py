@@ -1,0 +1,276 @@
+"""CPU oracle for the C-BFS hot path — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+``--impl reference`` leg may import this package.  It shares no code with the
+CUDA product (paper_2410_17226_b200/); its only common dependency is the
+input generator module ``cbfs_inputs`` (random numbers, no method arithmetic).
+
+Layers (each cites PAPER.md lines; readings R1..R26 are in DESIGN.md §2):
+  * csr_from_edges  — graph normalisation (R17): symmetrise, drop
+    self loops, sort + dedup, CSR.  numpy ``unique`` is the sort/dedup step.
+  * plain_bfs / brute_cluster — single-source BFS and the
+    definition of the cluster distance vector, in C.
+  * cluster_bfs / cluster_bfs_many — Alg. 1, sequential C.
+  * select_clusters — P:1061-1069 with R12, sequential C.
+  * query / query_stream — P:1013-1021, P:1074-1086 with R14-R16, C.
+  * budget_to_clusters — P:1445-1447.
+Pins live in tests/test_oracle_*.py.  Parity of every function here is pinned
+(no "parity unpinned" entries); see DESIGN.md §5.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+import cbfs_inputs
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+INF16 = 0xFFFF
+INF32 = 0xFFFFFFFF
+INT32_MAX = 2**31 - 1
+PAD = 0xFFFFFFFF
+
+
+def build(force: bool = False) -> str:
+    src = os.path.join(_HERE, "oracle.c")
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(src):
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-pthread", src, "-o", _LIB_PATH])
+    return _LIB_PATH
+
+
+def _P(t):
+    return ctypes.POINTER(t)
+
+
+_RANDFN = ctypes.CFUNCTYPE(ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64)
+_rand_cb = None
+
+
+def lib():
+    global _lib, _rand_cb
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB_PATH)
+        u32p, u64p, u16p, u8p, i32p = _P(ctypes.c_uint32), _P(ctypes.c_uint64), _P(ctypes.c_uint16), \
+            _P(ctypes.c_uint8), _P(ctypes.c_int32)
+        L.or_plain_bfs.argtypes = [ctypes.c_uint32, u64p, u32p, ctypes.c_uint32, u32p]
+        L.or_brute_cluster.argtypes = [ctypes.c_uint32, u64p, u32p, u32p, ctypes.c_uint32, ctypes.c_uint32, u16p, u64p]
+        L.or_cluster_bfs.argtypes = [ctypes.c_uint32, u64p, u32p, u32p, ctypes.c_uint32, ctypes.c_uint32, u16p, u64p,
+                                     u64p, u32p, u64p, ctypes.c_uint32]
+        L.or_cluster_bfs_many.argtypes = [ctypes.c_uint32, u64p, u32p, u32p, u8p, ctypes.c_uint32, ctypes.c_uint32,
+                                          ctypes.c_int, u16p, u64p, u64p, u64p]
+        L.or_hash_cluster.restype = ctypes.c_uint64
+        L.or_hash_cluster.argtypes = [ctypes.c_uint32, ctypes.c_uint32, u16p, u64p]
+        L.or_select_clusters.restype = ctypes.c_int64
+        L.or_select_clusters.argtypes = [ctypes.c_uint32, u64p, u32p, ctypes.c_uint32, ctypes.c_uint32,
+                                         ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64, _RANDFN, u32p, u8p]
+        L.or_query.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, u16p, u64p, ctypes.c_uint64, u32p,
+                               u32p, i32p]
+        L.or_query_stream.argtypes = [ctypes.c_uint32, u64p, u32p, u32p, u8p, ctypes.c_uint32, ctypes.c_uint32,
+                                      ctypes.c_uint64, u32p, u32p, ctypes.c_int, i32p]
+        L.or_record_bytes.restype = ctypes.c_int64
+        L.or_record_bytes.argtypes = [ctypes.c_uint32, ctypes.c_uint32]
+        L.or_budget_to_clusters.restype = ctypes.c_int64
+        L.or_budget_to_clusters.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32]
+        # the shared counter-based generator (cbfs_inputs) for random roots
+        _rand_cb = _RANDFN(lambda s, st, i: cbfs_inputs.lib().cg_rand(s, st, i))
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray, ct):
+    assert a.flags.c_contiguous, "array must be C-contiguous"
+    return a.ctypes.data_as(_P(ct))
+
+
+def default_threads() -> int:
+    return max(1, min(64, os.cpu_count() or 1))
+
+
+# ---------------------------------------------------------------- graph
+@dataclass
+class CSR:
+    """Symmetric, sorted, deduplicated CSR without self loops."""
+    n: int
+    off: np.ndarray   # uint64 [n+1]
+    cols: np.ndarray  # uint32 [m]
+
+    @property
+    def m(self) -> int:
+        return int(self.off[-1])
+
+    def degrees(self) -> np.ndarray:
+        return np.diff(self.off).astype(np.uint32)
+
+
+def csr_from_edges(n: int, src: np.ndarray, dst: np.ndarray) -> CSR:
+    """Normalise an undirected edge list (SPEC load_edge_list semantics, R17):
+    every pair {u,v} with u != v becomes arcs u->v and v->u; duplicates
+    removed; neighbour lists ascending.  m = number of arcs."""
+    src = np.asarray(src, dtype=np.uint64)
+    dst = np.asarray(dst, dtype=np.uint64)
+    if src.size and max(int(src.max()), int(dst.max())) >= n:
+        raise ValueError("vertex id out of range")
+    keep = src != dst
+    s, d = src[keep], dst[keep]
+    keys = np.unique(np.concatenate([(s << np.uint64(32)) | d, (d << np.uint64(32)) | s]))
+    rows = (keys >> np.uint64(32)).astype(np.int64)
+    cols = (keys & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+    counts = np.bincount(rows, minlength=n).astype(np.uint64)
+    off = np.zeros(n + 1, dtype=np.uint64)
+    np.cumsum(counts, out=off[1:])
+    return CSR(n, off, np.ascontiguousarray(cols))
+
+
+def csr_from_edgelist(el) -> CSR:
+    return csr_from_edges(el.n, el.src, el.dst)
+
+
+# ---------------------------------------------------------------- BFS
+def plain_bfs(g: CSR, s: int) -> np.ndarray:
+    dist = np.empty(g.n, np.uint32)
+    rc = lib().or_plain_bfs(g.n, _p(g.off, ctypes.c_uint64), _p(g.cols, ctypes.c_uint32), s,
+                            _p(dist, ctypes.c_uint32))
+    if rc:
+        raise ValueError("bad source")
+    return dist
+
+
+@dataclass
+class ClusterResult:
+    dist: np.ndarray   # uint16 [n], INF16 = unreachable
+    sub: np.ndarray    # uint64 [d+1][n]
+    stats: np.ndarray  # uint64 [4]: rounds, sumF, sumE, sum_{reached} deg
+    round_F: np.ndarray | None = None
+    round_E: np.ndarray | None = None
+
+
+def _sources(S) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(S, dtype=np.uint32))
+
+
+def brute_cluster(g: CSR, S, d: int):
+    """Definition P:630-639 via k queue BFS runs.  Returns (dist, sub, over)
+    where over=True means some source lies more than d beyond Delta_v."""
+    S = _sources(S)
+    dist = np.empty(g.n, np.uint16)
+    sub = np.empty((d + 1, g.n), np.uint64)
+    rc = lib().or_brute_cluster(g.n, _p(g.off, ctypes.c_uint64), _p(g.cols, ctypes.c_uint32),
+                                _p(S, ctypes.c_uint32), len(S), d, _p(dist, ctypes.c_uint16),
+                                _p(sub, ctypes.c_uint64))
+    if rc < 0:
+        raise ValueError("invalid cluster")
+    return dist, sub, bool(rc)
+
+
+def cluster_bfs(g: CSR, S, d: int, max_rounds: int = 1 << 16) -> ClusterResult:
+    """Alg. 1, sequential."""
+    S = _sources(S)
+    dist = np.empty(g.n, np.uint16)
+    sub = np.empty((d + 1, g.n), np.uint64)
+    stats = np.zeros(4, np.uint64)
+    rF = np.zeros(max_rounds, np.uint32)
+    rE = np.zeros(max_rounds, np.uint64)
+    rc = lib().or_cluster_bfs(g.n, _p(g.off, ctypes.c_uint64), _p(g.cols, ctypes.c_uint32), _p(S, ctypes.c_uint32),
+                              len(S), d, _p(dist, ctypes.c_uint16), _p(sub, ctypes.c_uint64),
+                              _p(stats, ctypes.c_uint64), _p(rF, ctypes.c_uint32), _p(rE, ctypes.c_uint64),
+                              max_rounds)
+    if rc:
+        raise ValueError("invalid cluster (k=0, k>64, duplicate or out-of-range source)")
+    R = int(stats[0])
+    return ClusterResult(dist, sub, stats, rF[:min(R, max_rounds)].copy(), rE[:min(R, max_rounds)].copy())
+
+
+def cluster_bfs_many(g: CSR, sources: np.ndarray, sizes: np.ndarray, d: int, threads: int | None = None,
+                     want_outputs: bool = True):
+    """Alg. 1 per cluster, clusters over host threads.  sources [C][64] uint32,
+    sizes [C] uint8.  Returns dict(dist [C][n], sub [C][d+1][n], stats [C][4],
+    hash [C])."""
+    sources = np.ascontiguousarray(sources, dtype=np.uint32)
+    sizes = np.ascontiguousarray(sizes, dtype=np.uint8)
+    C = sources.shape[0]
+    assert sources.shape == (C, 64) and sizes.shape == (C,)
+    stats = np.zeros((C, 4), np.uint64)
+    h = np.zeros(C, np.uint64)
+    dist = np.empty((C, g.n), np.uint16) if want_outputs else None
+    sub = np.empty((C, d + 1, g.n), np.uint64) if want_outputs else None
+    rc = lib().or_cluster_bfs_many(g.n, _p(g.off, ctypes.c_uint64), _p(g.cols, ctypes.c_uint32),
+                                   _p(sources, ctypes.c_uint32), _p(sizes, ctypes.c_uint8), C, d,
+                                   threads or default_threads(),
+                                   _p(dist, ctypes.c_uint16) if want_outputs else None,
+                                   _p(sub, ctypes.c_uint64) if want_outputs else None,
+                                   _p(stats, ctypes.c_uint64), _p(h, ctypes.c_uint64))
+    if rc:
+        raise ValueError("invalid cluster in batch")
+    return dict(dist=dist, sub=sub, stats=stats, hash=h)
+
+
+def hash_cluster(dist: np.ndarray, sub: np.ndarray) -> int:
+    d = sub.shape[0] - 1
+    dist = np.ascontiguousarray(dist, dtype=np.uint16)
+    sub = np.ascontiguousarray(sub, dtype=np.uint64)
+    return int(lib().or_hash_cluster(dist.shape[0], d, _p(dist, ctypes.c_uint16), _p(sub, ctypes.c_uint64)))
+
+
+# ---------------------------------------------------------------- selection
+ROOT_DEGREE, ROOT_RANDOM = 0, 1
+
+
+def select_clusters(g: CSR, r: int, k: int, d: int, policy: int = ROOT_DEGREE, seed: int = 0):
+    """P:1061-1069 with R12.  Returns (sources [r'][64] uint32 padded with
+    0xFFFFFFFF, sizes [r'] uint8)."""
+    lib()
+    out = np.full((max(r, 1), 64), PAD, np.uint32)
+    sizes = np.zeros(max(r, 1), np.uint8)
+    got = lib().or_select_clusters(g.n, _p(g.off, ctypes.c_uint64), _p(g.cols, ctypes.c_uint32), r, k, d, policy,
+                                   seed, _rand_cb, _p(out, ctypes.c_uint32), _p(sizes, ctypes.c_uint8))
+    if got < 0:
+        raise ValueError("bad selection arguments")
+    return out[:got].copy(), sizes[:got].copy()
+
+
+# ---------------------------------------------------------------- queries
+def query(dist: np.ndarray, sub: np.ndarray, s: np.ndarray, t: np.ndarray) -> np.ndarray:
+    """dist [C][n] uint16, sub [C][d+1][n] uint64 (cluster-major labels)."""
+    dist = np.ascontiguousarray(dist, dtype=np.uint16)
+    sub = np.ascontiguousarray(sub, dtype=np.uint64)
+    C, n = dist.shape
+    d = sub.shape[1] - 1
+    s = np.ascontiguousarray(s, dtype=np.uint32)
+    t = np.ascontiguousarray(t, dtype=np.uint32)
+    out = np.empty(len(s), np.int32)
+    rc = lib().or_query(n, d, C, _p(dist, ctypes.c_uint16), _p(sub, ctypes.c_uint64), len(s),
+                        _p(s, ctypes.c_uint32), _p(t, ctypes.c_uint32), _p(out, ctypes.c_int32))
+    if rc:
+        raise ValueError("query vertex out of range")
+    return out
+
+
+def query_stream(g: CSR, sources, sizes, d: int, s, t, threads: int | None = None) -> np.ndarray:
+    sources = np.ascontiguousarray(sources, dtype=np.uint32)
+    sizes = np.ascontiguousarray(sizes, dtype=np.uint8)
+    s = np.ascontiguousarray(s, dtype=np.uint32)
+    t = np.ascontiguousarray(t, dtype=np.uint32)
+    out = np.empty(len(s), np.int32)
+    rc = lib().or_query_stream(g.n, _p(g.off, ctypes.c_uint64), _p(g.cols, ctypes.c_uint32),
+                               _p(sources, ctypes.c_uint32), _p(sizes, ctypes.c_uint8), sources.shape[0], d, len(s),
+                               _p(s, ctypes.c_uint32), _p(t, ctypes.c_uint32), threads or default_threads(),
+                               _p(out, ctypes.c_int32))
+    if rc:
+        raise ValueError("bad stream query")
+    return out
+
+
+def record_bytes(w: int, d: int) -> int:
+    return int(lib().or_record_bytes(w, d))
+
+
+def budget_to_clusters(t: int, w: int, d: int) -> int:
+    return int(lib().or_budget_to_clusters(t, w, d))
