@@ -1,0 +1,202 @@
+/*
+ * cbfs.h — C-ABI of libcbfs.so, the B200 (sm_100a) Cluster-BFS library.
+ *
+ * Implements the data-parallel hot path of "Parallel Cluster-BFS and
+ * Applications to Shortest Paths" (arXiv 2410.17226; citations P:n are lines
+ * of its PAPER.md, R1..R26 the readings listed in DESIGN.md §2):
+ *   graph build      -> cbfs_graph_create / cbfs_graph_create_csr
+ *   cluster selection -> cbfs_select_clusters
+ *   C-BFS, Alg. 1, direction-optimised EdgeMap,
+ *     batched over clusters      -> cbfs_run
+ *   distance decode  -> cbfs_decode
+ *   landmark labels -> cbfs_run with planes = d
+ *   landmark query  -> cbfs_query_distance
+ *   fused build + query (streaming index)      -> cbfs_query_stream
+ *
+ * Conventions (all functions):
+ *  - Return CBFS_OK (0) or a negative cbfs_status; cbfs_last_error() gives a
+ *    thread-local message.  Argument errors are detected on the host before
+ *    any work is queued.  Device-side argument errors (duplicate / out of
+ *    range sources held in device memory) and CUDA faults are reported by the
+ *    call that detects them; the call then leaves outputs unspecified.
+ *  - `stream` is a cudaStream_t (NULL = the legacy default stream).  Calls
+ *    are stream-ordered; every function that returns a host-visible value
+ *    synchronises the stream before returning.  cbfs_run / cbfs_query_stream
+ *    synchronise once per traversal round (they read the frontier size).
+ *  - Pointers documented "device" must be device memory of the graph's
+ *    device; "host" pointers are ordinary host memory.  All caller buffers
+ *    are caller-owned; the library never frees them.  Handles are
+ *    library-owned and released with cbfs_graph_destroy.
+ *  - Vertex ids at the API are ORIGINAL ids (R18); an internal degree
+ *    relabelling (CBFS_RELABEL_DEGREE) is invisible to callers.
+ *  - Bit j of a bit-subset is the j-th source of the cluster's source list,
+ *    LSB first (R11); k <= 64 so a bit-subset is one uint64_t.
+ *  - A graph handle owns the traversal workspace: calls that traverse
+ *    (cbfs_run, cbfs_query_stream) on the SAME handle must not run
+ *    concurrently.  Handles are independent of each other.
+ */
+#ifndef CBFS_H
+#define CBFS_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct cbfs_graph cbfs_graph;
+typedef void* cbfs_stream; /* cudaStream_t */
+
+enum cbfs_status {
+  CBFS_OK = 0,
+  CBFS_EINVAL = -1,        /* bad argument                                  */
+  CBFS_ENOMEM = -2,        /* device allocation failed                      */
+  CBFS_ECUDA = -3,         /* CUDA error (message in cbfs_last_error)       */
+  CBFS_EOVERFLOW = -4,     /* a finite distance does not fit dist_bytes     */
+  CBFS_EUNSUPPORTED = -5   /* k > 64, d > CBFS_MAX_D, n > CBFS_MAX_N ...    */
+};
+
+#define CBFS_MAX_K 64u
+#define CBFS_MAX_D 31u
+#define CBFS_MAX_N (1u << 27)          /* (vertex, cluster-lane) pairs pack into 32 bits */
+#define CBFS_PAD 0xFFFFFFFFu           /* source-list padding                */
+#define CBFS_UNREACHED_U16 0xFFFFu     /* Delta sentinel, dist_bytes == 2    */
+#define CBFS_UNREACHED_U8 0xFFu        /* Delta sentinel, dist_bytes == 1    */
+#define CBFS_QUERY_UNREACHED 0x7FFFFFFF /* query answer when no cluster reaches both ends */
+
+/* graph flags */
+enum { CBFS_RELABEL_DEGREE = 2, CBFS_INPUT_DEVICE = 4 };
+/* cluster root policies (R12) */
+enum { CBFS_ROOT_DEGREE = 0, CBFS_ROOT_RANDOM = 1 };
+/* EdgeMap direction policy (R8: parity-neutral) */
+enum { CBFS_DIR_AUTO = 0, CBFS_DIR_PUSH = 1, CBFS_DIR_PULL = 2 };
+
+/* --------------------------------------------------------------- graph
+ * cbfs_graph_create — build the device CSR of an UNDIRECTED graph from an
+ * edge list (R17): every pair {src[e], dst[e]} with src != dst
+ * becomes arcs in both directions, self loops are dropped, duplicates
+ * removed, neighbour lists sorted.  n vertices, ids in [0, n).
+ *   src, dst : [n_pairs] uint32 — host, or device if flags & CBFS_INPUT_DEVICE
+ *   flags    : CBFS_RELABEL_DEGREE (internal degree-descending order,
+ *              ties by id) | CBFS_INPUT_DEVICE
+ *   device   : CUDA ordinal; the handle lives there.
+ * Errors: EINVAL (null out, id >= n), EUNSUPPORTED (n > CBFS_MAX_N or more
+ * than 2^32-1 arcs), ENOMEM, ECUDA.  Synchronises. */
+int cbfs_graph_create(uint32_t n, const uint32_t* src, const uint32_t* dst, uint64_t n_pairs, uint32_t flags,
+                      int device, cbfs_stream stream, cbfs_graph** out);
+
+/* Same, from a CSR whose arcs are read as undirected pairs (offsets [n+1]
+ * uint64, cols [m] uint32); the result is the normalised symmetric CSR. */
+int cbfs_graph_create_csr(uint32_t n, const uint64_t* offsets, const uint32_t* cols, uint64_t m, uint32_t flags,
+                          int device, cbfs_stream stream, cbfs_graph** out);
+
+/* n, number of arcs m (directed CSR entries, R17), max degree (host outs, any may be NULL). */
+int cbfs_graph_info(const cbfs_graph* g, uint32_t* n, uint64_t* m, uint32_t* max_degree);
+
+/* Copy the normalised CSR in ORIGINAL-id order to host buffers
+ * offsets [n+1] uint64, cols [m] uint32. Synchronises. */
+int cbfs_graph_export_csr(const cbfs_graph* g, uint64_t* offsets, uint32_t* cols);
+
+int cbfs_graph_destroy(cbfs_graph* g);
+
+/* --------------------------------------------------------------- selection
+ * cbfs_select_clusters — "Selecting Landmarks in Clusters" (R12):
+ * repeat r times: root = best unmarked non-isolated vertex (policy DEGREE:
+ * highest degree, ties by smaller id; policy RANDOM: draw
+ * v_t = floor(rand(seed,1,t) * n / 2^64), t = 0,1,..., until unmarked and
+ * non-isolated), members = up to k-1 unmarked vertices within floor(d/2) hops
+ * (marked vertices may be passed through), best (degree desc, id asc) first;
+ * mark them all.  Stops early when nothing unmarked and non-isolated is left.
+ *   out_sources : device [r][64] uint32, row = [root, members...], padded
+ *                 with CBFS_PAD
+ *   out_sizes   : device [r] uint8 (cluster size k_c)
+ *   out_r       : host, number of clusters produced (<= r)
+ * Errors: EINVAL (k == 0, null outputs), EUNSUPPORTED (k > 64, d > MAX_D).
+ * rand() is the counter-based SplitMix64 of include/cbfs_gen.h, implemented
+ * independently in this library.  Synchronises. */
+int cbfs_select_clusters(const cbfs_graph* g, uint32_t r, uint32_t k, uint32_t d, uint32_t root_policy,
+                         uint64_t seed, uint32_t* out_sources, uint8_t* out_sizes, uint32_t* out_r,
+                         cbfs_stream stream);
+
+/* --------------------------------------------------------------- C-BFS
+ * cbfs_run — Cluster-BFS (Alg. 1, with R1 seeding, R3 cap, R4
+ * claim, R5 output) from each of `n_clusters` clusters, d = the cluster
+ * diameter bound.  For every cluster c and vertex v it produces the cluster
+ * distance vector <S_v[0..d], Delta_v>.  A cluster whose true
+ * diameter exceeds d is not an error (R9): the output is Alg. 1's, exactly.
+ *   sources   : device [n_clusters][64] uint32 original ids, row c holds
+ *               sizes[c] distinct ids then padding (ignored)
+ *   sizes     : device [n_clusters] uint8, 1..64
+ *   d         : 0..CBFS_MAX_D
+ *   dist_bytes: 1 or 2 — width of out_dist entries (sentinel 0xFF / 0xFFFF)
+ *   out_dist  : device [n][n_clusters] (row = original vertex id), Delta_v,
+ *               or NULL
+ *   out_masks : device [planes][n][n_clusters] uint64, S_v[i] for
+ *               i < planes, or NULL
+ *   planes    : d+1 (full vectors) or d (landmark-label records, R14: the
+ *               last subset is implied, S_v[d] = S \ U_{i<d} S_v[i])
+ *   out_stats : device [n_clusters][4] uint64 {rounds, sum_i |F_i|,
+ *               sum_i E_i (E_i = sum of frontier degrees), sum of degrees of
+ *               reached vertices}, or NULL
+ *   direction : CBFS_DIR_AUTO / PUSH / PULL (identical outputs, R8)
+ * Errors: EINVAL (k == 0, duplicate or out-of-range source, bad dist_bytes /
+ * planes), EUNSUPPORTED (k > 64, d > MAX_D), EOVERFLOW (dist_bytes == 1 and a
+ * Delta > 254), ENOMEM, ECUDA.  Synchronises once per round. */
+int cbfs_run(cbfs_graph* g, const uint32_t* sources, const uint8_t* sizes, uint32_t n_clusters, uint32_t d,
+             uint32_t dist_bytes, void* out_dist, uint64_t* out_masks, uint32_t planes, uint64_t* out_stats,
+             uint32_t direction, cbfs_stream stream);
+
+/* Same computation with HOST buffers (sources, sizes, out_dist, out_masks,
+ * out_stats all host memory, pinned recommended): inputs are copied in, each
+ * batch of 32 clusters is traversed into device staging and copied out while
+ * the next batch runs.  Used for the end-to-end measurement. */
+int cbfs_run_host(cbfs_graph* g, const uint32_t* sources, const uint8_t* sizes, uint32_t n_clusters, uint32_t d,
+                  uint32_t dist_bytes, void* out_dist, uint64_t* out_masks, uint32_t planes, uint64_t* out_stats,
+                  uint32_t direction, cbfs_stream stream);
+
+/* cbfs_decode — distances of every source of ONE cluster:
+ * delta(s_j, v) = Delta_v + i for the unique i with bit j in S_v[i]
+ * (S_v[d] reconstructed when planes == d), CBFS_UNREACHED_U16 otherwise.
+ *   dist, masks : device, the cbfs_run output layout ([n][C], [planes][n][C])
+ *   c           : cluster column, k = sizes_host value for that cluster
+ *   out         : device [k][n] uint16
+ * Errors: EINVAL. */
+int cbfs_decode(uint32_t n, uint32_t C, uint32_t d, uint32_t planes, const void* dist, uint32_t dist_bytes,
+                const uint64_t* masks, uint32_t c, uint32_t k, uint16_t* out, cbfs_stream stream);
+
+/* --------------------------------------------------------------- queries
+ * cbfs_query_distance — landmark query with clustered landmarks
+ * (R15, R16): for each pair (s[q], t[q]),
+ *   best = min over clusters c with both Delta finite of
+ *          Delta_s + Delta_t + min{ i+j : S_s[i] & S_t[j] != 0 },
+ * min-merged into inout_best[q] (initialise to CBFS_QUERY_UNREACHED).
+ *   n, C, d, planes, dist, dist_bytes, masks : a label store in the
+ *         cbfs_run layout (planes = d or d+1)
+ *   sizes : device [C] uint8 (needed for S_v[d] = FULL & ~U when planes == d)
+ *   s, t  : device [q] uint32 original ids;  inout_best : device [q] int32
+ * Errors: EINVAL (null pointers, planes not d or d+1).  Ids >= n: the
+ * answer for that pair is left unchanged and the call returns EINVAL. */
+int cbfs_query_distance(uint32_t n, uint32_t C, uint32_t d, uint32_t planes, const void* dist, uint32_t dist_bytes,
+                        const uint64_t* masks, const uint8_t* sizes, const uint32_t* s, const uint32_t* t,
+                        uint64_t q, int32_t* inout_best, cbfs_stream stream);
+
+/* cbfs_query_stream — build the landmark labels of `n_clusters` clusters
+ * batch by batch and answer the q queries against each batch as soon as it
+ * is built, min-merging into inout_best; the full label store is never
+ * resident (config 5).  Same semantics as cbfs_run (planes = d+1 internally)
+ * followed by cbfs_query_distance over all clusters. */
+int cbfs_query_stream(cbfs_graph* g, const uint32_t* sources, const uint8_t* sizes, uint32_t n_clusters, uint32_t d,
+                      const uint32_t* s, const uint32_t* t, uint64_t q, int32_t* inout_best, uint64_t* out_stats,
+                      cbfs_stream stream);
+
+/* --------------------------------------------------------------- misc */
+/* Direction switch: pull when the frontier's arc count exceeds m / alpha
+ * (start 20; tunable, parity-neutral R8). */
+int cbfs_set_direction_alpha(double alpha);
+/* Number of kernels this library launched on this thread since the last reset. */
+uint64_t cbfs_launch_count(int reset);
+const char* cbfs_last_error(void);
+const char* cbfs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,108 @@
+// common.cuh — shared internals of libcbfs.so (product side only; the oracle
+// under oracle/ shares nothing with this file).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+
+#include "../../include/cbfs.h"
+
+namespace cbfs {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+void count_launch(uint64_t k = 1);
+
+#define CBFS_CUDA(call)                                  \
+  do {                                                   \
+    cudaError_t _e = (call);                             \
+    if (_e != cudaSuccess) return ::cbfs::cuda_fail(_e, #call); \
+  } while (0)
+
+#define CBFS_LAUNCHED()                                           \
+  do {                                                            \
+    ::cbfs::count_launch();                                       \
+    cudaError_t _e = cudaGetLastError();                          \
+    if (_e != cudaSuccess) return ::cbfs::cuda_fail(_e, "kernel launch"); \
+  } while (0)
+
+constexpr uint16_t INF16 = 0xFFFFu;
+constexpr uint32_t LANES = 32;  // clusters per batch = warp lanes (vertex-major state)
+
+// ---------------------------------------------------------------- graph
+struct Graph {
+  int device = 0;
+  uint32_t n = 0;
+  uint64_t m = 0;            // arcs
+  uint32_t max_degree = 0;
+  bool relabeled = false;
+  // internal CSR (internal ids; == original ids unless relabeled)
+  uint64_t* off = nullptr;   // [n+1]
+  uint32_t* cols = nullptr;  // [m]
+  // original-id CSR (only when relabeled; else aliases off/cols)
+  uint64_t* off_orig = nullptr;
+  uint32_t* cols_orig = nullptr;
+  uint32_t* perm = nullptr;  // internal -> original (null if identity)
+  uint32_t* inv = nullptr;   // original -> internal (null if identity)
+  uint32_t* rank = nullptr;  // internal id -> position in (deg desc, orig id asc) order
+  uint32_t* order = nullptr; // position -> internal id
+  // pull-kernel chunk table: first vertex of every PULL_CHUNK arcs
+  uint32_t* chunk_v = nullptr;
+  uint64_t n_chunks = 0;
+  // traversal workspace (lazily allocated, sized n*LANES)
+  struct Work* work = nullptr;
+};
+
+constexpr uint32_t PULL_CHUNK = 256;  // arcs per warp in the dense pull kernel
+
+int graph_free(Graph* g);
+int ensure_work(Graph* g);
+
+// one batch (<= 32 clusters) of cbfs_run; outputs use row stride C and start
+// at column cbase
+struct RunArgs {
+  const uint32_t* sources;  // device, batch base ([nb][64])
+  const uint8_t* sizes;     // device, batch base ([nb])
+  uint32_t nb, d, planes, dist_bytes, C, cbase, direction;
+  void* out_dist;           // device [n][C] or null
+  uint64_t* out_masks;      // device [planes][n][C] or null
+  uint64_t* out_stats;      // device [nb][4] or null
+};
+int run_batch(Graph* g, const RunArgs& a, cudaStream_t st);
+int check_run_args(const Graph* g, const void* sources, const void* sizes, uint32_t n_clusters, uint32_t d,
+                   uint32_t dist_bytes, uint32_t planes, uint32_t direction);
+
+// ---------------------------------------------------------------- RNG
+// Counter-based SplitMix64 with the same definition as the input generator
+// (implemented here independently of the generator library).
+__host__ __device__ inline uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+__host__ __device__ inline uint64_t crand(uint64_t seed, uint64_t stream, uint64_t index) {
+  uint64_t key = mix64(seed * 0x9E3779B97F4A7C15ULL + stream * 0xD1B54A32D192ED03ULL + 0x632BE59BD9B4E019ULL);
+  return mix64(key + (index + 1) * 0x9E3779B97F4A7C15ULL);
+}
+__host__ __device__ inline uint64_t bounded(uint64_t x, uint64_t n) {
+#ifdef __CUDA_ARCH__
+  return __umul64hi(x, n);
+#else
+  return (uint64_t)(((unsigned __int128)x * n) >> 64);
+#endif
+}
+
+__host__ __device__ inline uint64_t full_mask(uint32_t k) { return k >= 64 ? ~0ULL : ((1ULL << k) - 1); }
+
+inline unsigned grid_for(uint64_t items, unsigned block, unsigned cap = 148u * 64u) {
+  uint64_t g = (items + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (unsigned)g;
+}
+
+}  // namespace cbfs

@@ -1,0 +1,414 @@
+// graph.cu — device CSR builder (§8(a) row A0, R17, R18).
+//
+// Undirected pairs -> 64-bit arc keys (u<<32|v and v<<32|u; self loops map to
+// a sentinel row n) -> CUB radix sort over the low 32+ceil(log2(n+1)) bits ->
+// unique -> CSR (u64 offsets, u32 cols).  Optional degree relabelling: order
+// vertices by (degree desc, original id asc), rebuild the CSR in that order
+// (hubs get small ids, so their vertex-major rows share cache lines and L2
+// sets).  The rank array used by cluster selection is the same order.
+#include <cub/cub.cuh>
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace cbfs {
+
+// ------------------------------------------------------------- errors
+static thread_local std::string g_err;
+static thread_local uint64_t g_launches = 0;
+void set_error(const std::string& m) { g_err = m; }
+int fail(int code, const std::string& m) {
+  g_err = m;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  g_err = std::string(what) + ": " + cudaGetErrorString(e);
+  return e == cudaErrorMemoryAllocation ? CBFS_ENOMEM : CBFS_ECUDA;
+}
+void count_launch(uint64_t k) { g_launches += k; }
+uint64_t launches(int reset) {
+  uint64_t v = g_launches;
+  if (reset) g_launches = 0;
+  return v;
+}
+
+// ------------------------------------------------------------- kernels
+__global__ void k_make_keys(const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst, uint64_t P,
+                            uint32_t n, uint64_t* __restrict__ keys, int* __restrict__ bad) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < P; e += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t u = src[e], v = dst[e];
+    uint64_t a, b;
+    if (u >= n || v >= n) {
+      *bad = 1;
+      a = b = (uint64_t)n << 32;
+    } else if (u == v) {
+      a = b = (uint64_t)n << 32;  // self loop -> sentinel row n, dropped after unique
+    } else {
+      a = ((uint64_t)u << 32) | v;
+      b = ((uint64_t)v << 32) | u;
+    }
+    keys[2 * e] = a;
+    keys[2 * e + 1] = b;
+  }
+}
+
+// CSR arcs -> pair keys (each arc u->v contributes u<<32|v and v<<32|u)
+__global__ void k_csr_keys(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cols, uint32_t n,
+                           uint64_t* __restrict__ keys, int* __restrict__ bad) {
+  for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < n; u += (uint64_t)gridDim.x * blockDim.x) {
+    for (uint64_t e = off[u]; e < off[u + 1]; ++e) {
+      uint32_t v = cols[e];
+      uint64_t a, b;
+      if (v >= n) { *bad = 1; a = b = (uint64_t)n << 32; }
+      else if (v == u) { a = b = (uint64_t)n << 32; }
+      else { a = ((uint64_t)u << 32) | v; b = ((uint64_t)v << 32) | u; }
+      keys[2 * e] = a;
+      keys[2 * e + 1] = b;
+    }
+  }
+}
+
+__global__ void k_split_keys(const uint64_t* __restrict__ keys, uint64_t m, uint32_t n, uint32_t* __restrict__ cols,
+                             uint64_t* __restrict__ off) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e <= m; e += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t r = e < m ? (uint32_t)(keys[e] >> 32) : n;
+    uint32_t rp = e > 0 ? (uint32_t)(keys[e - 1] >> 32) : 0;
+    if (e < m) cols[e] = (uint32_t)keys[e];
+    if (e == 0) {
+      for (uint32_t x = 0; x <= r; ++x) off[x] = 0;
+    } else {
+      for (uint32_t x = rp + 1; x <= r; ++x) off[x] = e;
+    }
+  }
+}
+
+__global__ void k_degree_keys(const uint64_t* __restrict__ off, uint32_t n, uint64_t* __restrict__ keys,
+                              uint32_t* __restrict__ maxdeg) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t deg = (uint32_t)(off[v + 1] - off[v]);
+    keys[v] = ((uint64_t)(0xFFFFFFFFu - deg) << 32) | v;  // ascending = degree desc, id asc
+    atomicMax(maxdeg, deg);
+  }
+}
+
+__global__ void k_order_from_keys(const uint64_t* __restrict__ keys, uint32_t n, uint32_t* __restrict__ order,
+                                  uint32_t* __restrict__ rank) {
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n; p += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t v = (uint32_t)keys[p];
+    order[p] = v;
+    rank[v] = (uint32_t)p;
+  }
+}
+
+__global__ void k_relabel_keys(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cols, uint32_t n,
+                               const uint32_t* __restrict__ inv, uint64_t* __restrict__ keys) {
+  for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < n; u += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t iu = (uint64_t)inv[u] << 32;
+    for (uint64_t e = off[u]; e < off[u + 1]; ++e) keys[e] = iu | inv[cols[e]];
+  }
+}
+
+__global__ void k_identity(uint32_t* a, uint32_t n) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x)
+    a[v] = (uint32_t)v;
+}
+
+__global__ void k_chunk_table(const uint64_t* __restrict__ off, uint32_t n, uint32_t* __restrict__ chunk_v) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t lo = (off[v] + PULL_CHUNK - 1) / PULL_CHUNK, hi = (off[v + 1] + PULL_CHUNK - 1) / PULL_CHUNK;
+    for (uint64_t w = lo; w < hi; ++w) chunk_v[w] = (uint32_t)v;
+  }
+}
+
+// ------------------------------------------------------------- helpers
+static int bits_for(uint64_t x) {
+  int b = 0;
+  while ((1ULL << b) <= x && b < 63) ++b;
+  return b;
+}
+
+// sort + unique the 2P keys in `keys` (device, length L); returns arcs in
+// `*out_keys` (device, freshly allocated, caller frees) and m.
+static int sort_unique(uint64_t* keys, uint64_t L, uint32_t n, cudaStream_t st, uint64_t** out_keys, uint64_t* m) {
+  uint64_t* alt = nullptr;
+  void* tmp = nullptr;
+  size_t tb = 0;
+  int64_t* d_num = nullptr;
+  int end_bit = 32 + bits_for(n);
+  if (end_bit > 64) end_bit = 64;
+  CBFS_CUDA(cudaMallocAsync(&alt, sizeof(uint64_t) * (L ? L : 1), st));
+  cub::DoubleBuffer<uint64_t> db(keys, alt);
+  CBFS_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, db, L, 0, end_bit, st));
+  CBFS_CUDA(cudaMallocAsync(&tmp, tb, st));
+  CBFS_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, db, L, 0, end_bit, st));
+  count_launch(end_bit / 7);
+  CBFS_CUDA(cudaFreeAsync(tmp, st));
+  uint64_t* sorted = db.Current();
+  uint64_t* other = db.Alternate();
+  size_t tb2 = 0;
+  CBFS_CUDA(cudaMallocAsync(&d_num, sizeof(int64_t), st));
+  CBFS_CUDA(cub::DeviceSelect::Unique(nullptr, tb2, sorted, other, d_num, (int64_t)L, st));
+  CBFS_CUDA(cudaMallocAsync(&tmp, tb2, st));
+  CBFS_CUDA(cub::DeviceSelect::Unique(tmp, tb2, sorted, other, d_num, (int64_t)L, st));
+  count_launch(2);
+  CBFS_CUDA(cudaFreeAsync(tmp, st));
+  int64_t num = 0;
+  CBFS_CUDA(cudaMemcpyAsync(&num, d_num, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CBFS_CUDA(cudaStreamSynchronize(st));
+  uint64_t last = 0;
+  if (num > 0) {
+    CBFS_CUDA(cudaMemcpyAsync(&last, other + num - 1, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    CBFS_CUDA(cudaStreamSynchronize(st));
+    if ((last >> 32) == n) --num;  // sentinel row of self loops
+  }
+  CBFS_CUDA(cudaFreeAsync(d_num, st));
+  // `keys` and `alt` are both ours now: keep the unique keys, free the other
+  CBFS_CUDA(cudaFreeAsync(sorted, st));
+  *out_keys = other;
+  *m = (uint64_t)num;
+  return CBFS_OK;
+}
+
+static int keys_to_csr(const uint64_t* keys, uint64_t m, uint32_t n, cudaStream_t st, uint64_t** off, uint32_t** cols) {
+  CBFS_CUDA(cudaMallocAsync(off, sizeof(uint64_t) * (n + 1ULL), st));
+  CBFS_CUDA(cudaMallocAsync(cols, sizeof(uint32_t) * (m ? m : 1), st));
+  if (m == 0) {
+    CBFS_CUDA(cudaMemsetAsync(*off, 0, sizeof(uint64_t) * (n + 1ULL), st));
+    return CBFS_OK;
+  }
+  k_split_keys<<<grid_for(m + 1, 256), 256, 0, st>>>(keys, m, n, *cols, *off);
+  CBFS_LAUNCHED();
+  return CBFS_OK;
+}
+
+int graph_free(Graph* g) {
+  if (!g) return CBFS_OK;
+  cudaSetDevice(g->device);
+  if (g->off_orig && g->off_orig != g->off) cudaFree(g->off_orig);
+  if (g->cols_orig && g->cols_orig != g->cols) cudaFree(g->cols_orig);
+  cudaFree(g->off);
+  cudaFree(g->cols);
+  cudaFree(g->perm);
+  cudaFree(g->inv);
+  cudaFree(g->rank);
+  cudaFree(g->order);
+  cudaFree(g->chunk_v);
+  extern void work_free(Graph*);
+  work_free(g);
+  delete g;
+  return CBFS_OK;
+}
+
+// build from device keys buffer (length L = 2 * pairs), consumes `keys`
+static int build_from_keys(uint64_t* keys, uint64_t L, uint32_t n, uint32_t flags, int device, cudaStream_t st,
+                           cbfs_graph** out) {
+  Graph* g = new Graph();
+  g->device = device;
+  g->n = n;
+  uint64_t* uk = nullptr;
+  int rc = sort_unique(keys, L, n, st, &uk, &g->m);
+  if (rc) { delete g; return rc; }
+  if (g->m > 0xFFFFFFFFull) { cudaFree(uk); delete g; return fail(CBFS_EUNSUPPORTED, "more than 2^32-1 arcs"); }
+  rc = keys_to_csr(uk, g->m, n, st, &g->off, &g->cols);
+  if (rc) { delete g; return rc; }
+  CBFS_CUDA(cudaFreeAsync(uk, st));
+  // degree order (deg desc, original id asc)
+  uint64_t* dk = nullptr;
+  uint32_t* d_max = nullptr;
+  CBFS_CUDA(cudaMallocAsync(&dk, sizeof(uint64_t) * (n ? n : 1), st));
+  CBFS_CUDA(cudaMallocAsync(&d_max, sizeof(uint32_t), st));
+  CBFS_CUDA(cudaMemsetAsync(d_max, 0, sizeof(uint32_t), st));
+  CBFS_CUDA(cudaMalloc(&g->rank, sizeof(uint32_t) * (n ? n : 1)));
+  CBFS_CUDA(cudaMalloc(&g->order, sizeof(uint32_t) * (n ? n : 1)));
+  if (n) {
+    k_degree_keys<<<grid_for(n, 256), 256, 0, st>>>(g->off, n, dk, d_max);
+    CBFS_LAUNCHED();
+    uint64_t* alt = nullptr;
+    void* tmp = nullptr;
+    size_t tb = 0;
+    CBFS_CUDA(cudaMallocAsync(&alt, sizeof(uint64_t) * n, st));
+    cub::DoubleBuffer<uint64_t> db(dk, alt);
+    CBFS_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, db, (uint64_t)n, 0, 64, st));
+    CBFS_CUDA(cudaMallocAsync(&tmp, tb, st));
+    CBFS_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, db, (uint64_t)n, 0, 64, st));
+    count_launch(8);
+    CBFS_CUDA(cudaFreeAsync(tmp, st));
+    if (flags & CBFS_RELABEL_DEGREE) {
+      // perm = order (internal x -> original), inv = rank
+      CBFS_CUDA(cudaMalloc(&g->perm, sizeof(uint32_t) * n));
+      CBFS_CUDA(cudaMalloc(&g->inv, sizeof(uint32_t) * n));
+      k_order_from_keys<<<grid_for(n, 256), 256, 0, st>>>(db.Current(), n, g->perm, g->inv);
+      CBFS_LAUNCHED();
+      // internal CSR: keys (inv[u] << 32 | inv[v]) sorted
+      uint64_t* rk = nullptr;
+      CBFS_CUDA(cudaMallocAsync(&rk, sizeof(uint64_t) * (g->m ? g->m : 1), st));
+      k_relabel_keys<<<grid_for(n, 256), 256, 0, st>>>(g->off, g->cols, n, g->inv, rk);
+      CBFS_LAUNCHED();
+      uint64_t* ralt = nullptr;
+      CBFS_CUDA(cudaMallocAsync(&ralt, sizeof(uint64_t) * (g->m ? g->m : 1), st));
+      cub::DoubleBuffer<uint64_t> rdb(rk, ralt);
+      int end_bit = 32 + bits_for(n);
+      size_t tb3 = 0;
+      CBFS_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb3, rdb, g->m, 0, end_bit, st));
+      CBFS_CUDA(cudaMallocAsync(&tmp, tb3, st));
+      CBFS_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb3, rdb, g->m, 0, end_bit, st));
+      count_launch(end_bit / 7);
+      CBFS_CUDA(cudaFreeAsync(tmp, st));
+      g->off_orig = g->off;
+      g->cols_orig = g->cols;
+      g->off = nullptr;
+      g->cols = nullptr;
+      int rc2 = keys_to_csr(rdb.Current(), g->m, n, st, &g->off, &g->cols);
+      if (rc2) return rc2;
+      CBFS_CUDA(cudaFreeAsync(rk, st));
+      CBFS_CUDA(cudaFreeAsync(ralt, st));
+      // in internal ids the degree order is the identity
+      k_identity<<<grid_for(n, 256), 256, 0, st>>>(g->rank, n);
+      CBFS_LAUNCHED();
+      k_identity<<<grid_for(n, 256), 256, 0, st>>>(g->order, n);
+      CBFS_LAUNCHED();
+      g->relabeled = true;
+    } else {
+      k_order_from_keys<<<grid_for(n, 256), 256, 0, st>>>(db.Current(), n, g->order, g->rank);
+      CBFS_LAUNCHED();
+      g->off_orig = g->off;
+      g->cols_orig = g->cols;
+    }
+    CBFS_CUDA(cudaFreeAsync(alt, st));
+  } else {
+    g->off_orig = g->off;
+    g->cols_orig = g->cols;
+  }
+  CBFS_CUDA(cudaFreeAsync(dk, st));
+  CBFS_CUDA(cudaMemcpyAsync(&g->max_degree, d_max, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  CBFS_CUDA(cudaFreeAsync(d_max, st));
+  // pull chunk table
+  g->n_chunks = (g->m + PULL_CHUNK - 1) / PULL_CHUNK;
+  CBFS_CUDA(cudaMalloc(&g->chunk_v, sizeof(uint32_t) * (g->n_chunks ? g->n_chunks : 1)));
+  if (g->n_chunks) {
+    k_chunk_table<<<grid_for(n, 256), 256, 0, st>>>(g->off, n, g->chunk_v);
+    CBFS_LAUNCHED();
+  }
+  CBFS_CUDA(cudaStreamSynchronize(st));
+  *out = reinterpret_cast<cbfs_graph*>(g);
+  return CBFS_OK;
+}
+
+}  // namespace cbfs
+
+using namespace cbfs;
+
+extern "C" {
+
+int cbfs_graph_create(uint32_t n, const uint32_t* src, const uint32_t* dst, uint64_t n_pairs, uint32_t flags,
+                      int device, cbfs_stream stream, cbfs_graph** out) {
+  if (!out) return fail(CBFS_EINVAL, "out is null");
+  *out = nullptr;
+  if (n_pairs && (!src || !dst)) return fail(CBFS_EINVAL, "null edge arrays");
+  if (n > CBFS_MAX_N) return fail(CBFS_EUNSUPPORTED, "n exceeds CBFS_MAX_N");
+  CBFS_CUDA(cudaSetDevice(device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint32_t *ds = src, *dd = dst;
+  uint32_t *tmp_s = nullptr, *tmp_d = nullptr;
+  if (!(flags & CBFS_INPUT_DEVICE) && n_pairs) {
+    CBFS_CUDA(cudaMallocAsync(&tmp_s, sizeof(uint32_t) * n_pairs, st));
+    CBFS_CUDA(cudaMallocAsync(&tmp_d, sizeof(uint32_t) * n_pairs, st));
+    CBFS_CUDA(cudaMemcpyAsync(tmp_s, src, sizeof(uint32_t) * n_pairs, cudaMemcpyHostToDevice, st));
+    CBFS_CUDA(cudaMemcpyAsync(tmp_d, dst, sizeof(uint32_t) * n_pairs, cudaMemcpyHostToDevice, st));
+    ds = tmp_s;
+    dd = tmp_d;
+  }
+  uint64_t L = 2 * n_pairs;
+  uint64_t* keys = nullptr;
+  int* bad = nullptr;
+  CBFS_CUDA(cudaMallocAsync(&keys, sizeof(uint64_t) * (L ? L : 1), st));
+  CBFS_CUDA(cudaMallocAsync(&bad, sizeof(int), st));
+  CBFS_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+  if (n_pairs) {
+    k_make_keys<<<grid_for(n_pairs, 256), 256, 0, st>>>(ds, dd, n_pairs, n, keys, bad);
+    CBFS_LAUNCHED();
+  }
+  int hbad = 0;
+  CBFS_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CBFS_CUDA(cudaStreamSynchronize(st));
+  CBFS_CUDA(cudaFreeAsync(bad, st));
+  if (tmp_s) CBFS_CUDA(cudaFreeAsync(tmp_s, st));
+  if (tmp_d) CBFS_CUDA(cudaFreeAsync(tmp_d, st));
+  if (hbad) {
+    cudaFreeAsync(keys, st);
+    return fail(CBFS_EINVAL, "edge endpoint >= n");
+  }
+  return build_from_keys(keys, L, n, flags, device, st, out);
+}
+
+int cbfs_graph_create_csr(uint32_t n, const uint64_t* offsets, const uint32_t* cols, uint64_t m, uint32_t flags,
+                          int device, cbfs_stream stream, cbfs_graph** out) {
+  if (!out || !offsets || (m && !cols)) return fail(CBFS_EINVAL, "null argument");
+  *out = nullptr;
+  if (n > CBFS_MAX_N) return fail(CBFS_EUNSUPPORTED, "n exceeds CBFS_MAX_N");
+  CBFS_CUDA(cudaSetDevice(device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint64_t* doff = offsets;
+  const uint32_t* dcols = cols;
+  uint64_t* to = nullptr;
+  uint32_t* tc = nullptr;
+  if (!(flags & CBFS_INPUT_DEVICE)) {
+    if (offsets[n] != m) return fail(CBFS_EINVAL, "offsets[n] != m");
+    CBFS_CUDA(cudaMallocAsync(&to, sizeof(uint64_t) * (n + 1ULL), st));
+    CBFS_CUDA(cudaMallocAsync(&tc, sizeof(uint32_t) * (m ? m : 1), st));
+    CBFS_CUDA(cudaMemcpyAsync(to, offsets, sizeof(uint64_t) * (n + 1ULL), cudaMemcpyHostToDevice, st));
+    if (m) CBFS_CUDA(cudaMemcpyAsync(tc, cols, sizeof(uint32_t) * m, cudaMemcpyHostToDevice, st));
+    doff = to;
+    dcols = tc;
+  }
+  uint64_t L = 2 * m;
+  uint64_t* keys = nullptr;
+  int* bad = nullptr;
+  CBFS_CUDA(cudaMallocAsync(&keys, sizeof(uint64_t) * (L ? L : 1), st));
+  CBFS_CUDA(cudaMallocAsync(&bad, sizeof(int), st));
+  CBFS_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+  if (n) {
+    k_csr_keys<<<grid_for(n, 256), 256, 0, st>>>(doff, dcols, n, keys, bad);
+    CBFS_LAUNCHED();
+  }
+  int hbad = 0;
+  CBFS_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CBFS_CUDA(cudaStreamSynchronize(st));
+  CBFS_CUDA(cudaFreeAsync(bad, st));
+  if (to) CBFS_CUDA(cudaFreeAsync(to, st));
+  if (tc) CBFS_CUDA(cudaFreeAsync(tc, st));
+  if (hbad) {
+    cudaFreeAsync(keys, st);
+    return fail(CBFS_EINVAL, "column id >= n");
+  }
+  return build_from_keys(keys, L, n, flags, device, st, out);
+}
+
+int cbfs_graph_info(const cbfs_graph* gh, uint32_t* n, uint64_t* m, uint32_t* max_degree) {
+  const Graph* g = reinterpret_cast<const Graph*>(gh);
+  if (!g) return fail(CBFS_EINVAL, "null graph");
+  if (n) *n = g->n;
+  if (m) *m = g->m;
+  if (max_degree) *max_degree = g->max_degree;
+  return CBFS_OK;
+}
+
+int cbfs_graph_export_csr(const cbfs_graph* gh, uint64_t* offsets, uint32_t* cols) {
+  const Graph* g = reinterpret_cast<const Graph*>(gh);
+  if (!g || !offsets || (g->m && !cols)) return fail(CBFS_EINVAL, "null argument");
+  CBFS_CUDA(cudaSetDevice(g->device));
+  CBFS_CUDA(cudaMemcpy(offsets, g->off_orig, sizeof(uint64_t) * (g->n + 1ULL), cudaMemcpyDeviceToHost));
+  if (g->m) CBFS_CUDA(cudaMemcpy(cols, g->cols_orig, sizeof(uint32_t) * g->m, cudaMemcpyDeviceToHost));
+  return CBFS_OK;
+}
+
+int cbfs_graph_destroy(cbfs_graph* gh) { return graph_free(reinterpret_cast<Graph*>(gh)); }
+
+const char* cbfs_last_error(void) { return g_err.c_str(); }
+const char* cbfs_version(void) { return "cbfs-b200 0.1 (sm_100a)"; }
+uint64_t cbfs_launch_count(int reset) { return launches(reset); }
+
+}  // extern "C"

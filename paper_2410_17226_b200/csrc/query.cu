@@ -1,0 +1,285 @@
+// query.cu — distance decode (§8(a) A9), landmark query (A11,
+// P:1013-1021 and P:1074-1086, R14-R16), the fused streaming build+query
+// used when the label store cannot be resident (H3), and the host-buffer
+// variant of cbfs_run used for end-to-end timing.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+namespace cbfs {
+
+
+template <int DB>
+__device__ __forceinline__ uint32_t load_dist(const void* p, uint64_t idx) {
+  if (DB == 1) {
+    const uint8_t x = ((const uint8_t*)p)[idx];
+    return x == 0xFFu ? 0xFFFFFFFFu : x;
+  } else {
+    const uint16_t x = ((const uint16_t*)p)[idx];
+    return x == 0xFFFFu ? 0xFFFFFFFFu : x;
+  }
+}
+
+// ------------------------------------------------------------------ decode
+template <int DB>
+__global__ void k_decode(uint32_t n, uint32_t C, uint32_t d, uint32_t planes, const void* __restrict__ dist,
+                         const uint64_t* __restrict__ masks, uint32_t c, uint32_t k, uint16_t* __restrict__ out) {
+  const uint64_t full = full_mask(k);
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t dv = load_dist<DB>(dist, v * C + c);
+    uint64_t S[CBFS_MAX_D + 1];
+    uint64_t uni = 0;
+    for (uint32_t i = 0; i < planes; ++i) { S[i] = masks[((uint64_t)i * n + v) * C + c]; uni |= S[i]; }
+    if (planes == d) S[d] = dv == 0xFFFFFFFFu ? 0 : (full & ~uni);  // R14
+    for (uint32_t j = 0; j < k; ++j) {
+      uint32_t r = 0xFFFFu;
+      if (dv != 0xFFFFFFFFu)
+        for (uint32_t i = 0; i <= d; ++i)
+          if ((S[i] >> j) & 1ULL) { r = dv + i; break; }
+      out[(uint64_t)j * n + v] = (uint16_t)(r > 0xFFFFu ? 0xFFFFu : r);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ query
+// One warp per query pair, lane over clusters.  Per cluster: skip when
+// either Delta is unreachable (R16); else the smallest i+j with
+// S_s[i] & S_t[j] != 0, scanning i+j = 0..2d; S_x[d] is
+// rebuilt from the other subsets when the store keeps only d (R14).
+template <int DB>
+__global__ void __launch_bounds__(256) k_query(uint32_t n, uint32_t C, uint32_t d, uint32_t planes,
+                                               const void* __restrict__ dist, const uint64_t* __restrict__ masks,
+                                               const uint8_t* __restrict__ sizes, const uint32_t* __restrict__ s,
+                                               const uint32_t* __restrict__ t, uint64_t q,
+                                               int32_t* __restrict__ best, int* __restrict__ bad) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+  for (uint64_t qi = warp; qi < q; qi += nwarps) {
+    const uint32_t a = s[qi], b = t[qi];
+    if (a >= n || b >= n) {
+      if (lane == 0) *bad = 1;
+      continue;
+    }
+    int32_t mine = 0x7FFFFFFF;
+    for (uint32_t c = lane; c < C; c += 32) {
+      const uint32_t da = load_dist<DB>(dist, (uint64_t)a * C + c);
+      const uint32_t db = load_dist<DB>(dist, (uint64_t)b * C + c);
+      if (da == 0xFFFFFFFFu || db == 0xFFFFFFFFu) continue;
+      if ((int32_t)(da + db) >= mine) continue;  // cannot improve (value >= da + db)
+      uint64_t Sa[CBFS_MAX_D + 1], Sb[CBFS_MAX_D + 1];
+      uint64_t ua = 0, ub = 0;
+      for (uint32_t i = 0; i < planes; ++i) {
+        Sa[i] = masks[((uint64_t)i * n + a) * C + c];
+        Sb[i] = masks[((uint64_t)i * n + b) * C + c];
+        ua |= Sa[i];
+        ub |= Sb[i];
+      }
+      if (planes == d) {
+        const uint64_t full = full_mask(sizes[c]);
+        Sa[d] = full & ~ua;
+        Sb[d] = full & ~ub;
+      }
+      for (uint32_t tt = 0; tt <= 2 * d; ++tt) {
+        bool hit = false;
+        const uint32_t i0 = tt > d ? tt - d : 0, i1 = tt < d ? tt : d;
+        for (uint32_t i = i0; i <= i1; ++i)
+          if (Sa[i] & Sb[tt - i]) { hit = true; break; }
+        if (hit) {
+          const int32_t val = (int32_t)(da + db + tt);
+          if (val < mine) mine = val;
+          break;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mine = min(mine, __shfl_xor_sync(0xFFFFFFFFu, mine, o));
+    if (lane == 0 && mine < best[qi]) best[qi] = mine;
+  }
+}
+
+static int launch_query(uint32_t n, uint32_t C, uint32_t d, uint32_t planes, const void* dist, uint32_t dist_bytes,
+                        const uint64_t* masks, const uint8_t* sizes, const uint32_t* s, const uint32_t* t, uint64_t q,
+                        int32_t* best, int* bad, cudaStream_t st) {
+  if (q == 0 || C == 0) return CBFS_OK;
+  const unsigned blocks = grid_for(q * 32, 256, 148u * 8u * 8u);
+  if (dist_bytes == 1)
+    k_query<1><<<blocks, 256, 0, st>>>(n, C, d, planes, dist, masks, sizes, s, t, q, best, bad);
+  else
+    k_query<2><<<blocks, 256, 0, st>>>(n, C, d, planes, dist, masks, sizes, s, t, q, best, bad);
+  CBFS_LAUNCHED();
+  return CBFS_OK;
+}
+
+}  // namespace cbfs
+
+using namespace cbfs;
+
+extern "C" {
+
+int cbfs_decode(uint32_t n, uint32_t C, uint32_t d, uint32_t planes, const void* dist, uint32_t dist_bytes,
+                const uint64_t* masks, uint32_t c, uint32_t k, uint16_t* out, cbfs_stream stream) {
+  if (!dist || !masks || !out) return fail(CBFS_EINVAL, "null argument");
+  if (c >= C || k == 0 || k > CBFS_MAX_K) return fail(CBFS_EINVAL, "bad cluster index or k");
+  if (d > CBFS_MAX_D || (planes != d + 1 && !(planes == d && d > 0))) return fail(CBFS_EINVAL, "bad d/planes");
+  if (dist_bytes != 1 && dist_bytes != 2) return fail(CBFS_EINVAL, "dist_bytes must be 1 or 2");
+  if (n == 0) return CBFS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dist_bytes == 1)
+    k_decode<1><<<grid_for(n, 256), 256, 0, st>>>(n, C, d, planes, dist, masks, c, k, out);
+  else
+    k_decode<2><<<grid_for(n, 256), 256, 0, st>>>(n, C, d, planes, dist, masks, c, k, out);
+  CBFS_LAUNCHED();
+  return CBFS_OK;
+}
+
+int cbfs_query_distance(uint32_t n, uint32_t C, uint32_t d, uint32_t planes, const void* dist, uint32_t dist_bytes,
+                        const uint64_t* masks, const uint8_t* sizes, const uint32_t* s, const uint32_t* t, uint64_t q,
+                        int32_t* inout_best, cbfs_stream stream) {
+  if (q && (!s || !t || !inout_best)) return fail(CBFS_EINVAL, "null query arrays");
+  if (C && (!dist || !masks || !sizes)) return fail(CBFS_EINVAL, "null label arrays");
+  if (d > CBFS_MAX_D || (planes != d + 1 && !(planes == d && d > 0))) return fail(CBFS_EINVAL, "bad d/planes");
+  if (dist_bytes != 1 && dist_bytes != 2) return fail(CBFS_EINVAL, "dist_bytes must be 1 or 2");
+  cudaStream_t st = (cudaStream_t)stream;
+  int* bad = nullptr;
+  CBFS_CUDA(cudaMallocAsync(&bad, sizeof(int), st));
+  CBFS_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+  int rc = launch_query(n, C, d, planes, dist, dist_bytes, masks, sizes, s, t, q, inout_best, bad, st);
+  if (rc) return rc;
+  int hbad = 0;
+  CBFS_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CBFS_CUDA(cudaFreeAsync(bad, st));
+  CBFS_CUDA(cudaStreamSynchronize(st));
+  if (hbad) return fail(CBFS_EINVAL, "query vertex id >= n");
+  return CBFS_OK;
+}
+
+int cbfs_query_stream(cbfs_graph* gh, const uint32_t* sources, const uint8_t* sizes, uint32_t n_clusters, uint32_t d,
+                      const uint32_t* s, const uint32_t* t, uint64_t q, int32_t* inout_best, uint64_t* out_stats,
+                      cbfs_stream stream) {
+  Graph* g = reinterpret_cast<Graph*>(gh);
+  int rc = check_run_args(g, sources, sizes, n_clusters, d, 2, d + 1, CBFS_DIR_AUTO);
+  if (rc) return rc;
+  if (q && (!s || !t || !inout_best)) return fail(CBFS_EINVAL, "null query arrays");
+  CBFS_CUDA(cudaSetDevice(g->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  rc = ensure_work(g);
+  if (rc) return rc;
+  const uint32_t n = g->n;
+  const uint32_t planes = d + 1;
+  uint16_t* bdist = nullptr;
+  uint64_t* bmasks = nullptr;
+  int* bad = nullptr;
+  CBFS_CUDA(cudaMallocAsync(&bdist, sizeof(uint16_t) * (uint64_t)n * LANES + 16, st));
+  CBFS_CUDA(cudaMallocAsync(&bmasks, sizeof(uint64_t) * (uint64_t)planes * n * LANES + 16, st));
+  CBFS_CUDA(cudaMallocAsync(&bad, sizeof(int), st));
+  CBFS_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+  for (uint32_t cb = 0; cb < n_clusters && rc == CBFS_OK; cb += LANES) {
+    const uint32_t nb = std::min<uint32_t>(LANES, n_clusters - cb);
+    CBFS_CUDA(cudaMemsetAsync(bdist, 0xFF, sizeof(uint16_t) * (uint64_t)n * LANES, st));
+    CBFS_CUDA(cudaMemsetAsync(bmasks, 0, sizeof(uint64_t) * (uint64_t)planes * n * LANES, st));
+    RunArgs a;
+    a.sources = sources + (uint64_t)cb * 64;
+    a.sizes = sizes + cb;
+    a.nb = nb; a.d = d; a.planes = planes; a.dist_bytes = 2; a.C = LANES; a.cbase = 0;
+    a.direction = CBFS_DIR_AUTO;
+    a.out_dist = bdist;
+    a.out_masks = bmasks;
+    a.out_stats = out_stats ? out_stats + (uint64_t)cb * 4 : nullptr;
+    rc = run_batch(g, a, st);
+    if (rc) break;
+    // lanes >= nb stay unreachable (dist 0xFFFF), so the query skips them
+    rc = launch_query(n, LANES, d, planes, bdist, 2, bmasks, sizes + cb, s, t, q, inout_best, bad, st);
+  }
+  int hbad = 0;
+  CBFS_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CBFS_CUDA(cudaFreeAsync(bdist, st));
+  CBFS_CUDA(cudaFreeAsync(bmasks, st));
+  CBFS_CUDA(cudaFreeAsync(bad, st));
+  CBFS_CUDA(cudaStreamSynchronize(st));
+  if (rc) return rc;
+  if (hbad) return fail(CBFS_EINVAL, "query vertex id >= n");
+  return CBFS_OK;
+}
+
+int cbfs_run_host(cbfs_graph* gh, const uint32_t* sources, const uint8_t* sizes, uint32_t n_clusters, uint32_t d,
+                  uint32_t dist_bytes, void* out_dist, uint64_t* out_masks, uint32_t planes, uint64_t* out_stats,
+                  uint32_t direction, cbfs_stream stream) {
+  Graph* g = reinterpret_cast<Graph*>(gh);
+  int rc = check_run_args(g, sources, sizes, n_clusters, d, dist_bytes, planes, direction);
+  if (rc) return rc;
+  CBFS_CUDA(cudaSetDevice(g->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  rc = ensure_work(g);
+  if (rc) return rc;
+  const uint32_t n = g->n;
+  const uint64_t C = n_clusters;
+  uint32_t* dsrc = nullptr;
+  uint8_t* dsz = nullptr;
+  uint64_t* dstats = nullptr;
+  CBFS_CUDA(cudaMallocAsync(&dsrc, sizeof(uint32_t) * 64 * (C ? C : 1), st));
+  CBFS_CUDA(cudaMallocAsync(&dsz, C ? C : 1, st));
+  CBFS_CUDA(cudaMallocAsync(&dstats, sizeof(uint64_t) * 4 * (C ? C : 1), st));
+  if (C) {
+    CBFS_CUDA(cudaMemcpyAsync(dsrc, sources, sizeof(uint32_t) * 64 * C, cudaMemcpyHostToDevice, st));
+    CBFS_CUDA(cudaMemcpyAsync(dsz, sizes, C, cudaMemcpyHostToDevice, st));
+  }
+  // double-buffered device staging for one batch: [n][32] dist, [planes][n][32] masks
+  cudaStream_t cp;
+  CBFS_CUDA(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
+  void* sd[2] = {nullptr, nullptr};
+  uint64_t* sm[2] = {nullptr, nullptr};
+  cudaEvent_t done[2], copied[2];
+  for (int b = 0; b < 2; ++b) {
+    if (out_dist) CBFS_CUDA(cudaMallocAsync(&sd[b], (uint64_t)n * LANES * dist_bytes + 16, st));
+    if (out_masks) CBFS_CUDA(cudaMallocAsync(&sm[b], sizeof(uint64_t) * (uint64_t)planes * n * LANES + 16, st));
+    CBFS_CUDA(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming));
+    CBFS_CUDA(cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming));
+    CBFS_CUDA(cudaEventRecord(copied[b], cp));
+  }
+  int slot = 0;
+  for (uint32_t cb = 0; cb < n_clusters && rc == CBFS_OK; cb += LANES, slot ^= 1) {
+    const uint32_t nb = std::min<uint32_t>(LANES, n_clusters - cb);
+    CBFS_CUDA(cudaStreamWaitEvent(st, copied[slot], 0));  // staging slot free again
+    if (out_dist) CBFS_CUDA(cudaMemsetAsync(sd[slot], 0xFF, (uint64_t)n * LANES * dist_bytes, st));
+    if (out_masks) CBFS_CUDA(cudaMemsetAsync(sm[slot], 0, sizeof(uint64_t) * (uint64_t)planes * n * LANES, st));
+    RunArgs a;
+    a.sources = dsrc + (uint64_t)cb * 64;
+    a.sizes = dsz + cb;
+    a.nb = nb; a.d = d; a.planes = planes; a.dist_bytes = dist_bytes; a.C = LANES; a.cbase = 0;
+    a.direction = direction;
+    a.out_dist = sd[slot];
+    a.out_masks = sm[slot];
+    a.out_stats = dstats + (uint64_t)cb * 4;
+    rc = run_batch(g, a, st);
+    if (rc) break;
+    CBFS_CUDA(cudaEventRecord(done[slot], st));
+    CBFS_CUDA(cudaStreamWaitEvent(cp, done[slot], 0));
+    if (out_dist)
+      CBFS_CUDA(cudaMemcpy2DAsync((uint8_t*)out_dist + (uint64_t)cb * dist_bytes, C * dist_bytes, sd[slot],
+                                  (uint64_t)LANES * dist_bytes, (uint64_t)nb * dist_bytes, n, cudaMemcpyDeviceToHost,
+                                  cp));
+    if (out_masks)
+      CBFS_CUDA(cudaMemcpy2DAsync(out_masks + cb, C * sizeof(uint64_t), sm[slot], LANES * sizeof(uint64_t),
+                                  (uint64_t)nb * sizeof(uint64_t), (uint64_t)planes * n, cudaMemcpyDeviceToHost, cp));
+    CBFS_CUDA(cudaEventRecord(copied[slot], cp));
+  }
+  CBFS_CUDA(cudaStreamSynchronize(cp));
+  if (rc == CBFS_OK && out_stats && C)
+    CBFS_CUDA(cudaMemcpyAsync(out_stats, dstats, sizeof(uint64_t) * 4 * C, cudaMemcpyDeviceToHost, st));
+  CBFS_CUDA(cudaStreamSynchronize(st));
+  for (int b = 0; b < 2; ++b) {
+    if (sd[b]) cudaFree(sd[b]);
+    if (sm[b]) cudaFree(sm[b]);
+    cudaEventDestroy(done[b]);
+    cudaEventDestroy(copied[b]);
+  }
+  cudaStreamDestroy(cp);
+  cudaFree(dsrc);
+  cudaFree(dsz);
+  cudaFree(dstats);
+  return rc;
+}
+
+}  // extern "C"

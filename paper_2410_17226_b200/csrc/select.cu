@@ -1,0 +1,219 @@
+// select.cu — cluster selection (§8(a) row A1): "Selecting Landmarks in
+// Clusters", with reading R12.
+//
+// The greedy rule is inherently sequential (each cluster's marks constrain
+// the next), so one 1024-thread CTA runs the cluster loop and parallelises
+// inside a cluster: the root scan over the (degree desc, id asc) order, the
+// floor(d/2)-hop ball expansion, and a 4-pass block radix select of the k-1
+// best candidates (rank = position in that order; ranks are unique, so the
+// (k-1)-th smallest rank is an exact threshold).
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace cbfs {
+
+constexpr int SEL_THREADS = 1024;
+
+struct SelScratch {
+  uint8_t* marked;
+  uint32_t* stamp;
+  uint32_t* fa;    // BFS level lists
+  uint32_t* fb;
+  uint32_t* cand;  // candidate ranks
+};
+
+__global__ void __launch_bounds__(SEL_THREADS, 1)
+k_select(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cols, const uint32_t* __restrict__ rank,
+         const uint32_t* __restrict__ order, const uint32_t* __restrict__ perm, const uint32_t* __restrict__ inv,
+         uint32_t n, uint32_t r, uint32_t k, uint32_t d, uint32_t policy, uint64_t seed, SelScratch S,
+         uint32_t* __restrict__ out_sources, uint8_t* __restrict__ out_sizes, uint32_t* __restrict__ out_count) {
+  __shared__ unsigned s_best, s_na, s_nb, s_nc, s_nsel, s_done, s_root;
+  __shared__ unsigned long long s_avail, s_cursor, s_tdraw;
+  __shared__ unsigned hist[256];
+  __shared__ unsigned s_need, s_prefix, s_pmask;
+  __shared__ unsigned sel[64];
+  const unsigned tid = threadIdx.x;
+  const uint32_t h = d / 2;
+  // available = unmarked non-isolated vertices
+  if (tid == 0) { s_avail = 0; s_cursor = 0; s_tdraw = 0; }
+  __syncthreads();
+  unsigned long long loc = 0;
+  for (uint32_t v = tid; v < n; v += SEL_THREADS) loc += off[v + 1] > off[v];
+  atomicAdd(&s_avail, loc);
+  __syncthreads();
+  uint32_t produced = 0;
+  for (uint32_t c = 0; c < r; ++c) {
+    // ---- root (R12)
+    if (tid == 0) { s_done = 0; s_root = 0xFFFFFFFFu; if (s_avail == 0) s_done = 1; }
+    __syncthreads();
+    if (s_done) break;
+    if (policy == CBFS_ROOT_DEGREE) {
+      for (;;) {
+        if (tid == 0) s_best = 0xFFFFFFFFu;
+        __syncthreads();
+        const unsigned long long p = s_cursor + tid;
+        if (p < n) {
+          const uint32_t x = order[p];
+          if (!S.marked[x] && off[x + 1] > off[x]) atomicMin(&s_best, (unsigned)tid);
+        }
+        __syncthreads();
+        if (s_best != 0xFFFFFFFFu) {
+          if (tid == 0) { s_cursor += s_best; s_root = order[s_cursor]; }
+          __syncthreads();
+          break;
+        }
+        if (tid == 0) s_cursor += SEL_THREADS;
+        __syncthreads();
+        if (s_cursor >= n) break;
+      }
+    } else {
+      if (tid == 0) {
+        for (;;) {
+          const uint32_t v = (uint32_t)bounded(crand(seed, 1, s_tdraw++), n);
+          const uint32_t x = inv ? inv[v] : v;
+          if (!S.marked[x] && off[x + 1] > off[x]) { s_root = x; break; }
+        }
+      }
+      __syncthreads();
+    }
+    if (s_root == 0xFFFFFFFFu) break;
+    const uint32_t root = s_root;
+    const uint32_t tag = c + 1;
+    // ---- floor(d/2)-hop ball through all vertices; unmarked ones are candidates
+    if (tid == 0) { s_na = 1; s_nc = 0; S.fa[0] = root; S.stamp[root] = tag; }
+    __syncthreads();
+    uint32_t* fa = S.fa;
+    uint32_t* fb = S.fb;
+    for (uint32_t lev = 1; lev <= h; ++lev) {
+      if (tid == 0) s_nb = 0;
+      __syncthreads();
+      const unsigned na = s_na;
+      for (unsigned q = 0; q < na; ++q) {
+        const uint32_t u = fa[q];
+        const uint64_t b = off[u], e = off[u + 1];
+        for (uint64_t t = b + tid; t < e; t += SEL_THREADS) {
+          const uint32_t v = cols[t];
+          if (atomicExch(&S.stamp[v], tag) != tag) {
+            if (lev < h) fb[atomicAdd(&s_nb, 1u)] = v;
+            if (!S.marked[v]) S.cand[atomicAdd(&s_nc, 1u)] = rank[v];
+          }
+        }
+      }
+      __syncthreads();
+      if (tid == 0) s_na = s_nb;
+      uint32_t* tmp = fa; fa = fb; fb = tmp;
+      __syncthreads();
+    }
+    // ---- best k-1 candidates by rank (degree desc, id asc)
+    const unsigned nc = s_nc;
+    const unsigned want = k - 1;
+    if (tid == 0) { s_nsel = 0; s_need = want; s_prefix = 0; s_pmask = 0; }
+    __syncthreads();
+    unsigned thr = 0xFFFFFFFFu;
+    if (want > 0 && nc > want) {
+      for (int pass = 0; pass < 4; ++pass) {
+        const int shift = 24 - 8 * pass;
+        for (unsigned b = tid; b < 256; b += SEL_THREADS) hist[b] = 0;
+        __syncthreads();
+        const unsigned pre = s_prefix, pm = s_pmask;
+        for (unsigned t = tid; t < nc; t += SEL_THREADS) {
+          const unsigned rk = S.cand[t];
+          if ((rk & pm) == pre) atomicAdd(&hist[(rk >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (tid == 0) {
+          unsigned cum = 0, need = s_need, b = 0;
+          for (; b < 256; ++b) {
+            if (cum + hist[b] >= need) break;
+            cum += hist[b];
+          }
+          s_need = need - cum;
+          s_prefix = pre | (b << shift);
+          s_pmask = pm | (255u << shift);
+        }
+        __syncthreads();
+      }
+      thr = s_prefix;  // the want-th smallest rank
+    }
+    if (want > 0) {
+      for (unsigned t = tid; t < nc; t += SEL_THREADS) {
+        const unsigned rk = S.cand[t];
+        if (rk <= thr) sel[atomicAdd(&s_nsel, 1u)] = rk;
+      }
+    }
+    __syncthreads();
+    const unsigned ns = s_nsel;
+    // order the selected members by rank; write the cluster in original ids
+    uint32_t* outS = out_sources + (uint64_t)c * 64;
+    if (tid < 64) {
+      uint32_t val = 0xFFFFFFFFu;
+      if (tid == 0) val = perm ? perm[root] : root;
+      outS[tid] = val;
+    }
+    __syncthreads();
+    unsigned long long dec = 0;
+    if (tid < ns) {
+      const unsigned rk = sel[tid];
+      unsigned pos = 0;
+      for (unsigned j = 0; j < ns; ++j) pos += sel[j] < rk;
+      const uint32_t x = order[rk];
+      outS[1 + pos] = perm ? perm[x] : x;
+      S.marked[x] = 1;
+      dec += off[x + 1] > off[x];
+    }
+    if (tid == 0) {
+      S.marked[root] = 1;
+      dec += 1;  // root is non-isolated
+      out_sizes[c] = (uint8_t)(1 + ns);
+    }
+    if (dec) atomicAdd(&s_avail, (unsigned long long)0 - dec);  // subtract
+    ++produced;
+    __syncthreads();
+  }
+  if (tid == 0) *out_count = produced;
+}
+
+}  // namespace cbfs
+
+using namespace cbfs;
+
+extern "C" int cbfs_select_clusters(const cbfs_graph* gh, uint32_t r, uint32_t k, uint32_t d, uint32_t root_policy,
+                                    uint64_t seed, uint32_t* out_sources, uint8_t* out_sizes, uint32_t* out_r,
+                                    cbfs_stream stream) {
+  const Graph* g = reinterpret_cast<const Graph*>(gh);
+  if (!g || !out_r || (r && (!out_sources || !out_sizes))) return fail(CBFS_EINVAL, "null argument");
+  if (k == 0) return fail(CBFS_EINVAL, "k must be >= 1");
+  if (k > CBFS_MAX_K) return fail(CBFS_EUNSUPPORTED, "k > 64");
+  if (d > CBFS_MAX_D) return fail(CBFS_EUNSUPPORTED, "d > CBFS_MAX_D");
+  if (root_policy > CBFS_ROOT_RANDOM) return fail(CBFS_EINVAL, "bad root policy");
+  *out_r = 0;
+  if (r == 0 || g->n == 0) return CBFS_OK;
+  CBFS_CUDA(cudaSetDevice(g->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint32_t n = g->n;
+  SelScratch S;
+  uint32_t* d_count = nullptr;
+  CBFS_CUDA(cudaMallocAsync(&S.marked, n, st));
+  CBFS_CUDA(cudaMallocAsync(&S.stamp, sizeof(uint32_t) * n, st));
+  CBFS_CUDA(cudaMallocAsync(&S.fa, sizeof(uint32_t) * n, st));
+  CBFS_CUDA(cudaMallocAsync(&S.fb, sizeof(uint32_t) * n, st));
+  CBFS_CUDA(cudaMallocAsync(&S.cand, sizeof(uint32_t) * n, st));
+  CBFS_CUDA(cudaMallocAsync(&d_count, sizeof(uint32_t), st));
+  CBFS_CUDA(cudaMemsetAsync(S.marked, 0, n, st));
+  CBFS_CUDA(cudaMemsetAsync(S.stamp, 0, sizeof(uint32_t) * n, st));
+  CBFS_CUDA(cudaMemsetAsync(out_sources, 0xFF, sizeof(uint32_t) * 64ULL * r, st));
+  CBFS_CUDA(cudaMemsetAsync(out_sizes, 0, r, st));
+  k_select<<<1, SEL_THREADS, 0, st>>>(g->off, g->cols, g->rank, g->order, g->perm, g->inv, n, r, k, d, root_policy,
+                                      seed, S, out_sources, out_sizes, d_count);
+  CBFS_LAUNCHED();
+  CBFS_CUDA(cudaMemcpyAsync(out_r, d_count, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  CBFS_CUDA(cudaFreeAsync(S.marked, st));
+  CBFS_CUDA(cudaFreeAsync(S.stamp, st));
+  CBFS_CUDA(cudaFreeAsync(S.fa, st));
+  CBFS_CUDA(cudaFreeAsync(S.fb, st));
+  CBFS_CUDA(cudaFreeAsync(S.cand, st));
+  CBFS_CUDA(cudaFreeAsync(d_count, st));
+  CBFS_CUDA(cudaStreamSynchronize(st));
+  return CBFS_OK;
+}
