@@ -1,0 +1,436 @@
+#!/usr/bin/env python3
+"""bench.py — C-BFS source-edges/s on B200 (BASELINE.json `metric`).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2_rmat20]
+
+Workload (N=1): BASELINE.json configs[1] — RMAT scale 20, edge factor 16,
+a/b/c/d = .57/.19/.19/.05, symmetrised; 1,024 clusters of up to 64 sources
+(highest-degree root + its best neighbours, d = 2); outputs the
+full cluster distance vectors (u8 Delta + 3 u64 bit-subset planes per
+vertex per cluster).  Synthetic seeded input (cbfs_inputs, seed 2).
+
+One step = the whole hot path over the resident edge list: A0 CSR build
+(symmetrise, dedup, degree relabel) -> A1 cluster selection -> A2-A8 C-BFS of
+every cluster -> output vectors in HBM.  `value` = sum_c |S_c| * m_c / T,
+m_c = arcs whose tail is reachable from S_c, T = device time
+of the K steps (CUDA events on the launching stream, max over ranks).
+
+N>1 (torchrun, one rank per GPU, NCCL): weak scaling — rank r runs its own
+block of 1,024 clusters of an N*1,024-cluster selection over the replicated
+graph; no data-path collective (clusters are independent); only the
+timing MAX and the unit totals are all-reduced.
+
+`--impl reference` times the CPU oracle (oracle/, sequential Alg. 1 per
+cluster, clusters over all host cores) on a bounded sample of the same
+workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import cbfs_inputs as ci  # noqa: E402
+
+METRIC = "C-BFS source-edges/sec (GTEPS x sources)"
+UNIT = "source-edges/s"
+BYTES_PER_FRONTIER_ARC = 22     # 4 B column + 2 B Delta cap read + 16 B OR-update
+BYTES_PER_FRONTIER_ENTRY = 40   # offsets, frontier id w/r, next read, seen RMW
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy peak)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int, period_ms: int = 500):
+        self.gpu = gpu_index
+        self.period = period_ms
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", str(self.period)],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=5)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ distributed plumbing
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    return world, rank, local
+
+
+def allreduce_max(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def allreduce_sum(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def shard(n_clusters_per_rank: int, world: int, rank: int):
+    """Weak scaling: an N*C-cluster selection, rank r owns the block [r*C, (r+1)*C)."""
+    return n_clusters_per_rank * world, rank * n_clusters_per_rank
+
+
+# ------------------------------------------------------------------ CPU oracle sample
+def oracle_sample(cfg_name: str, el, threads: int, n_sample: int, world: int = 1):
+    """The oracle as it stands, on a bounded sample of the config's clusters:
+    every (C/n_sample)-th cluster of the selection.  Returns dict."""
+    import oracle as orc
+    cfg = ci.CONFIGS[cfg_name]
+    t0 = time.perf_counter()
+    g = orc.csr_from_edgelist(el)
+    t_build = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    pol = orc.ROOT_RANDOM if cfg["root"] == "random" else orc.ROOT_DEGREE
+    src, sz = orc.select_clusters(g, cfg["clusters"] * world, cfg["k"], cfg["d"], pol, cfg["root_seed"])
+    t_sel = time.perf_counter() - t0
+    C = len(sz)
+    idx = np.linspace(0, C - 1, min(n_sample, C)).round().astype(int)
+    t0 = time.perf_counter()
+    res = orc.cluster_bfs_many(g, src[idx], sz[idx], cfg["d"], threads=threads, want_outputs=False)
+    t_run = time.perf_counter() - t0
+    units = float((sz[idx].astype(np.float64) * res["stats"][:, 3].astype(np.float64)).sum())
+    return dict(units=units, seconds=t_run, clusters=len(idx), build_s=t_build, select_s=t_sel, graph=g)
+
+
+def cpu_info():
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return os.cpu_count() or 1, model
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    cfg = ci.CONFIGS[args.config]
+    el = ci.make_graph(args.config)
+    cores, model = cpu_info()
+    vals, secs = [], []
+    for it in range(args.warmup + args.steps):
+        r = oracle_sample(args.config, el, cores, args.ref_sample)
+        if it >= args.warmup:
+            vals.append(r["units"] / r["seconds"])
+            secs.append(r["seconds"])
+    value = float(np.mean(vals)) if vals else 0.0
+    sample = (f"{r['clusters']} of {cfg['clusters']} clusters (evenly spaced over the degree-ordered selection), "
+              f"sequential Alg. 1 per cluster over {cores} threads; CSR build ({r['build_s']:.1f}s) and "
+              f"selection ({r['select_s']:.1f}s) excluded")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * float(np.mean(secs)) if secs else None,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": args.config, "graph": el.name, "n": el.n, "clusters": cfg["clusters"],
+                       "k": cfg["k"], "d": cfg["d"]},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+                             "cpu": model},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, world, rank, local):
+    import torch
+
+    import paper_2410_17226_b200 as cb
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    cfg = ci.CONFIGS[args.config]
+    d, k = cfg["d"], cfg["k"]
+    C = cfg["clusters"]
+    r_total, first = shard(C, world, rank)
+    policy = cb.CBFS_ROOT_RANDOM if cfg["root"] == "random" else cb.CBFS_ROOT_DEGREE
+    relabel = cfg["kind"] in ("rmat", "er")
+    dist_bytes = 1 if cfg["kind"] in ("rmat", "er") else 2
+
+    t0 = time.perf_counter()
+    el = ci.make_graph(args.config)
+    log(f"[rank {rank}] generated {el.name}: n={el.n} pairs={len(el.src)} in {time.perf_counter() - t0:.1f}s")
+    src_h = torch.from_numpy(el.src.view(np.int32)).pin_memory()
+    dst_h = torch.from_numpy(el.dst.view(np.int32)).pin_memory()
+    src_d, dst_d = src_h.to(dev), dst_h.to(dev)
+    n = el.n
+    dist_out = torch.empty((n, C), dtype=torch.uint8 if dist_bytes == 1 else torch.int16, device=dev)
+    masks_out = torch.empty((d + 1, n, C), dtype=torch.int64, device=dev)
+    stats = torch.zeros((C, 4), dtype=torch.int64, device=dev)
+    sel_src = torch.empty((r_total, 64), dtype=torch.int32, device=dev)
+    sel_sz = torch.empty((r_total,), dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # 256 MiB > 126 MB L2
+    stream = torch.cuda.current_stream()
+    if args.alpha:
+        cb.cbfs_set_direction_alpha(args.alpha)
+
+    phase_ms = {"build": 0.0, "select": 0.0, "cbfs": 0.0}
+
+    def step(timed_phases: bool):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        evs[0].record(stream)
+        h = cb.cbfs_graph_create(n, src_d, dst_d, cb.CBFS_RELABEL_DEGREE if relabel else 0, local, stream)
+        evs[1].record(stream)
+        got = cb.cbfs_select_clusters(h, r_total, k, d, policy, cfg["root_seed"], sel_src, sel_sz, stream)
+        assert got == r_total, f"selection produced {got} < {r_total} clusters"
+        evs[2].record(stream)
+        cb.cbfs_run(h, sel_src[first:first + C], sel_sz[first:first + C], C, d, dist_bytes, dist_out, masks_out,
+                    d + 1, stats, args.direction, stream)
+        evs[3].record(stream)
+        cb.cbfs_graph_destroy(h)
+        if timed_phases:
+            torch.cuda.synchronize()
+            phase_ms["build"] += evs[0].elapsed_time(evs[1])
+            phase_ms["select"] += evs[1].elapsed_time(evs[2])
+            phase_ms["cbfs"] += evs[2].elapsed_time(evs[3])
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local, args.clock_ms)
+    if not args.no_clocks:
+        clocks.start()
+    cb.cbfs_launch_count(reset=True)
+    cb.cbfs_profile_enable(True)
+    cb.cbfs_profile_read(reset=True)
+    total_ms = 0.0
+    for _ in range(args.steps):
+        flush.zero_()  # L2 flush between timed steps (outside the timed region)
+        barrier(world)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step(True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+        total_ms += e0.elapsed_time(e1)
+    launches = cb.cbfs_launch_count(reset=True)
+    prof = cb.cbfs_profile_read(reset=True)
+    cb.cbfs_profile_enable(False)
+    clk = clocks.stop()
+    phase_ms = {kk: v / args.steps for kk, v in phase_ms.items()}  # per timed step
+    st = stats.cpu().numpy().view(np.uint64)
+    sizes = sel_sz[first:first + C].cpu().numpy().astype(np.float64)
+    units_step = float((sizes * st[:, 3].astype(np.float64)).sum())
+    n_h, m_h, maxdeg = None, None, None
+    hh = cb.cbfs_graph_create(n, src_d, dst_d, 0, local, stream)
+    n_h, m_h, maxdeg = cb.cbfs_graph_info(hh)
+    cb.cbfs_graph_destroy(hh)
+    units_wholegraph = float(sizes.sum()) * m_h
+
+    T = allreduce_max(total_ms, world) / 1000.0
+    units_all = allreduce_sum(units_step * args.steps, world)
+    value = units_all / T
+
+    # ---- roofline of the dominant kernel (per-launch algorithmic bytes / avg duration)
+    peak, peak_src = peaks()
+    dom = max(prof, key=lambda kk: prof[kk]["ms"])
+    pk = prof[dom]
+    if dom == "fold":
+        alg_bytes = BYTES_PER_FRONTIER_ENTRY * pk["entries"]
+    else:
+        alg_bytes = BYTES_PER_FRONTIER_ARC * pk["arcs"]
+    achieved = alg_bytes / (pk["ms"] / 1000.0) / 1e9 if pk["ms"] > 0 else 0.0
+    traffic = None
+    ncu_json = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(ncu_json):
+        try:
+            traffic = json.load(open(ncu_json)).get("traffic_per_launch", {}).get(dom)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": f"k_{dom}", "launches": pk["launches"],
+                "avg_launch_ms": pk["ms"] / max(1, pk["launches"]),
+                "alg_bytes_per_launch": alg_bytes / max(1, pk["launches"]),
+                "model": (f"{BYTES_PER_FRONTIER_ARC} B per frontier (entry, arc) pair" if dom != "fold" else
+                          f"{BYTES_PER_FRONTIER_ENTRY} B per frontier entry") + " (SURVEY §8(d))",
+                "peak_source": peak_src, "kernels": prof}
+
+    # ---- end to end through the public API with host buffers (rank-local)
+    e2e = None
+    if not args.no_e2e:
+        import ctypes
+        hd = torch.empty((n, C), dtype=dist_out.dtype).pin_memory()
+        hm = torch.empty((d + 1, n, C), dtype=torch.int64).pin_memory()
+        hs = torch.zeros((C, 4), dtype=torch.int64).pin_memory()
+        hsrc = torch.empty((r_total, 64), dtype=torch.int32).pin_memory()
+        hsz = torch.empty((r_total,), dtype=torch.uint8).pin_memory()
+        e2e_ms = 0.0
+        for it in range(args.e2e_warmup + args.e2e_steps):
+            barrier(world)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            h = cb.cbfs_graph_create(n, src_h, dst_h, cb.CBFS_RELABEL_DEGREE if relabel else 0, local, stream)
+            cb.cbfs_select_clusters(h, r_total, k, d, policy, cfg["root_seed"], sel_src, sel_sz, stream)
+            hsrc.copy_(sel_src)
+            hsz.copy_(sel_sz)
+            cb._check(cb._lib.cbfs_run_host(h, ctypes.c_void_p(hsrc[first:].data_ptr()),
+                                            ctypes.c_void_p(hsz[first:].data_ptr()), C, d, dist_bytes,
+                                            ctypes.c_void_p(hd.data_ptr()), ctypes.c_void_p(hm.data_ptr()), d + 1,
+                                            ctypes.c_void_p(hs.data_ptr()), args.direction,
+                                            ctypes.c_void_p(stream.cuda_stream)))
+            cb.cbfs_graph_destroy(h)
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            if it >= args.e2e_warmup:
+                e2e_ms += 1000 * dt
+        Te = allreduce_max(e2e_ms, world) / 1000.0
+        units_e = allreduce_sum(units_step * args.e2e_steps, world)
+        h2d = 2 * 4 * len(el.src) + 64 * 4 * C + C
+        d2h = (hd.numel() * hd.element_size() + hm.numel() * 8 + hs.numel() * 8 + r_total * 65)
+        e2e = {"value": units_e / Te, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "steps": args.e2e_steps, "ms_per_step": 1000 * Te / args.e2e_steps,
+               "timing": "host wall clock around the public C-ABI calls, max over ranks"}
+
+    # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cores, model = cpu_info()
+        r = oracle_sample(args.config, el, cores, args.ref_sample)
+        cpu = {"value": r["units"] / r["seconds"], "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": (f"{r['clusters']} of {C} clusters evenly spaced over the selection, sequential Alg. 1 per "
+                          f"cluster over {cores} threads, {r['seconds']:.1f}s; CSR build {r['build_s']:.1f}s and "
+                          f"selection {r['select_s']:.1f}s not included"),
+               "cpu": model}
+
+    if rank == 0:
+        K = args.steps
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+            "ms_per_step": 1000 * T / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u64", "data": "synthetic",
+            "config": {"workload": args.config, "graph": el.name, "n": n, "arcs": m_h, "max_degree": maxdeg,
+                       "clusters_per_gpu": C, "k": k, "d": d, "dist_bytes": dist_bytes, "relabel": relabel,
+                       "parallelism": f"clusters sharded, {world} rank(s), graph replicated",
+                       "step": "A0 CSR build + A1 selection + A2-A8 C-BFS of all clusters (full vectors)",
+                       "l2": "flushed between timed steps (256 MiB write); inputs 134 MB and outputs 26 GB > L2",
+                       "units_per_step_rank0": units_step,
+                       "value_whole_graph_m": float(sizes.sum()) * m_h * args.steps * world / T,
+                       "phase_ms_rank0": {kk: round(v, 3) for kk, v in phase_ms.items()},
+                       "cbfs_only_value": units_step / (phase_ms["cbfs"] / 1000.0) if phase_ms["cbfs"] else None,
+                       "direction": ["auto", "push", "pull"][args.direction],
+                       "alpha": args.alpha or 20.0},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2_rmat20")
+    ap.add_argument("--direction", type=int, default=0)
+    ap.add_argument("--alpha", type=float, default=0.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-warmup", type=int, default=1)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ref-sample", type=int, default=32)
+    ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--clock-ms", type=int, default=500)
+    args = ap.parse_args()
+    world, rank, local = dist_init()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -56,7 +56,7 @@ enum cbfs_status {
 
 #define CBFS_MAX_K 64u
 #define CBFS_MAX_D 31u
-#define CBFS_MAX_N (1u << 27)          /* (vertex, cluster-lane) pairs pack into 32 bits */
+#define CBFS_MAX_N (1u << 26)          /* (vertex, cluster-in-batch) pairs pack into 32 bits */
 #define CBFS_PAD 0xFFFFFFFFu           /* source-list padding                */
 #define CBFS_UNREACHED_U16 0xFFFFu     /* Delta sentinel, dist_bytes == 2    */
 #define CBFS_UNREACHED_U8 0xFFu        /* Delta sentinel, dist_bytes == 1    */
@@ -147,7 +147,7 @@ int cbfs_run(cbfs_graph* g, const uint32_t* sources, const uint8_t* sizes, uint3
 /* Same computation with HOST buffers (sources, sizes, out_dist, out_masks,
  * out_stats all host memory, pinned recommended): inputs are copied in, each
  * batch of 32 clusters is traversed into device staging and copied out while
- * the next batch runs.  Used for the end-to-end measurement. */
+ * the next batch runs (batches of 64 clusters).  Used for the end-to-end measurement. */
 int cbfs_run_host(cbfs_graph* g, const uint32_t* sources, const uint8_t* sizes, uint32_t n_clusters, uint32_t d,
                   uint32_t dist_bytes, void* out_dist, uint64_t* out_masks, uint32_t planes, uint64_t* out_stats,
                   uint32_t direction, cbfs_stream stream);
@@ -191,6 +191,14 @@ int cbfs_query_stream(cbfs_graph* g, const uint32_t* sources, const uint8_t* siz
 /* Direction switch: pull when the frontier's arc count exceeds m / alpha
  * (start 20; tunable, parity-neutral R8). */
 int cbfs_set_direction_alpha(double alpha);
+/* Kernel-level timing of the C-BFS engine (process-wide, not thread-safe):
+ * when enabled, CUDA events are recorded on the launching stream around every
+ * fold / push / pull launch and read after the round's synchronisation.
+ * cbfs_profile_read fills arrays of 3 entries indexed {0 fold, 1 push,
+ * 2 pull}: total device ms, launches, frontier (entry, arc) pairs and
+ * frontier entries processed (host pointers, any may be NULL). */
+int cbfs_profile_enable(int on);
+int cbfs_profile_read(double* ms, uint64_t* launches, uint64_t* arcs, uint64_t* entries, int reset);
 /* Number of kernels this library launched on this thread since the last reset. */
 uint64_t cbfs_launch_count(int reset);
 const char* cbfs_last_error(void);

@@ -24,7 +24,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 # ------------------------------------------------------------------ constants (include/cbfs.h)
 CBFS_OK, CBFS_EINVAL, CBFS_ENOMEM, CBFS_ECUDA, CBFS_EOVERFLOW, CBFS_EUNSUPPORTED = 0, -1, -2, -3, -4, -5
-CBFS_MAX_K, CBFS_MAX_D, CBFS_MAX_N = 64, 31, 1 << 27
+CBFS_MAX_K, CBFS_MAX_D, CBFS_MAX_N = 64, 31, 1 << 26
 CBFS_PAD = 0xFFFFFFFF
 CBFS_UNREACHED_U16, CBFS_UNREACHED_U8 = 0xFFFF, 0xFF
 CBFS_QUERY_UNREACHED = 0x7FFFFFFF
@@ -54,6 +54,8 @@ _sig("cbfs_decode", [_u32, _u32, _u32, _u32, _vp, _u32, _vp, _u32, _u32, _vp, _v
 _sig("cbfs_query_distance", [_u32, _u32, _u32, _u32, _vp, _u32, _vp, _vp, _vp, _vp, _u64, _vp, _vp])
 _sig("cbfs_query_stream", [_vp, _vp, _vp, _u32, _u32, _vp, _vp, _u64, _vp, _vp, _vp])
 _sig("cbfs_set_direction_alpha", [ctypes.c_double])
+_sig("cbfs_profile_enable", [_i32])
+_sig("cbfs_profile_read", [_vp, _vp, _vp, _vp, _i32])
 _sig("cbfs_launch_count", [_i32], _u64)
 _sig("cbfs_last_error", [], ctypes.c_char_p)
 _sig("cbfs_version", [], ctypes.c_char_p)
@@ -164,6 +166,18 @@ def cbfs_query_stream(h, sources, sizes, n_clusters, d, s, t, inout_best, out_st
 
 def cbfs_set_direction_alpha(alpha: float):
     _check(_lib.cbfs_set_direction_alpha(alpha))
+
+
+def cbfs_profile_enable(on: bool = True):
+    _check(_lib.cbfs_profile_enable(int(on)))
+
+
+def cbfs_profile_read(reset: bool = False) -> dict:
+    ms = np.zeros(3, np.float64); la = np.zeros(3, np.uint64); arcs = np.zeros(3, np.uint64)
+    ent = np.zeros(3, np.uint64)
+    _check(_lib.cbfs_profile_read(_ptr(ms), _ptr(la), _ptr(arcs), _ptr(ent), int(reset)))
+    return {name: dict(ms=float(ms[i]), launches=int(la[i]), arcs=int(arcs[i]), entries=int(ent[i]))
+            for i, name in enumerate(("fold", "push", "pull"))}
 
 
 def cbfs_launch_count(reset: bool = False) -> int:

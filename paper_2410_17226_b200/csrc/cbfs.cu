@@ -1,28 +1,30 @@
 // cbfs.cu — the C-BFS engine (§8(a) rows A2-A8): Alg. 1 of PAPER.md
 // with the direction-optimised EdgeMap, run for a
-// batch of 32 clusters at once in lock-step rounds.
+// batch of LANES = 64 clusters at once in lock-step rounds.
 //
 // B200 design:
-//  * vertex-major state: for vertex v the 32 clusters of a batch own the 32
-//    consecutive words seen[v*32 + c] / pend[v*32 + c] (u64 bit-subsets,
-//    P:641-645) and dist[v*32 + c] (u16 Delta).  A warp with lane c =
-//    cluster c reads one neighbour's state for all clusters as one coalesced
-//    256-byte access, so random neighbour gathers use whole sectors.
+//  * vertex-major state: for vertex v the 64 clusters of a batch own the 64
+//    consecutive words seen[v*64 + c] / pend[v*64 + c] (u64 bit-subsets,
+//    P:641-645) and dist[v*64 + c] (u16 Delta).  In the dense pull a
+//    warp reads one neighbour's state for all 64 clusters as one coalesced
+//    512-byte access (16 B per lane, lane l = clusters 2l and 2l+1), so the
+//    random neighbour gathers move whole sectors and one load instruction
+//    serves two clusters.
 //  * S_next of Alg. 1 is kept as `pend` = S_next \ S_seen (the bits that
 //    arrived this round and are not yet folded).  pend is zero outside the
 //    pending entries; the first writer that turns a pend word non-zero owns
 //    the claim (R4), so no separate r[] array is needed.
-//  * a frontier is a list of packed (v*32 + c) entries; the pending list of
+//  * a frontier is a list of packed (v*64 + c) entries; the pending list of
 //    round i IS F_i.
 //  * round i = fold kernel (vertex phase P:714-720) -> push kernel (sparse,
 //    P:1758-1768, edge-balanced over the frontier's arcs, 64-bit atomicOr)
-//    or pull kernel (dense, warp per 256-arc CSR chunk, lane per
-//    cluster, no atomics except on chunk-boundary vertices).  Kernel
-//    boundaries are the barriers that H9 requires between the two phases.
+//    or pull kernel (dense).  Kernel boundaries are the
+//    barriers that H9 requires between the two phases.
 #include <cub/cub.cuh>
 
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -30,88 +32,150 @@
 namespace cbfs {
 
 struct Work {
-  uint64_t cap = 0;       // n * LANES
-  uint64_t* seen = nullptr;
-  uint64_t* pend = nullptr;
-  uint16_t* dist = nullptr;
-  uint32_t* listA = nullptr;
+  uint64_t cap = 0;                     // n * LANES entries
+  uint64_t* seen = nullptr;             // [n][64] S_seen
+  uint64_t* pend = nullptr;             // [n][64] S_next \ S_seen (pending)
+  uint16_t* dist = nullptr;             // [n][64] Delta
+  uint32_t* listA = nullptr;            // frontier lists (packed v*64+c)
   uint32_t* listB = nullptr;
-  uint64_t* pre = nullptr;   // [cap + 1]
-  uint32_t* ubits = nullptr; // [n/32 + 1]
-  unsigned long long* ctr = nullptr;  // [0] next count, [1] next E, [2] error bits
-  unsigned long long* h_ctr = nullptr; // pinned mirror
-  uint64_t* bstats = nullptr; // [LANES][4]
+  uint64_t* pre = nullptr;              // [cap + 1] degrees -> exclusive prefix (push)
+  uint32_t* ubits = nullptr;            // 2 x [n/32 + 1]: union frontier U_i, U_{i+1}
+  unsigned long long* ctr = nullptr;    // [0] next count, [1] next E, [2] error bits
+  unsigned long long* h_ctr = nullptr;  // pinned mirror
+  uint64_t* bstats = nullptr;           // [LANES][4]
   void* scan_tmp = nullptr;
   size_t scan_bytes = 0;
 };
 
 static double g_alpha = 20.0;
 
-void work_free(Graph* g) {
-  Work* w = g->work;
-  if (!w) return;
+// ---- optional per-kernel timing (cbfs_profile_*): CUDA events recorded on
+// the launching stream around each fold / push / pull launch; read after the
+// round's synchronisation, so no extra sync is added.
+enum { PK_FOLD = 0, PK_PUSH = 1, PK_PULL = 2, PK_N = 4 };
+struct Prof {
+  bool on = false;
+  double ms[PK_N] = {0, 0, 0, 0};
+  uint64_t launches[PK_N] = {0, 0, 0, 0};
+  uint64_t arcs[PK_N] = {0, 0, 0, 0};     // frontier (entry, arc) pairs processed
+  uint64_t entries[PK_N] = {0, 0, 0, 0};  // frontier entries processed
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+};
+static Prof g_prof;
+
+// The traversal workspace is cached per device and reused by every graph
+// handle (allocating and mapping a few GB per cbfs_run would cost tens of
+// ms).  A traversal holds the device's lock for its duration.
+constexpr int MAX_DEV = 64;
+static Work* g_work[MAX_DEV];
+static std::mutex g_work_mu[MAX_DEV];
+
+static void work_release_buffers(Work* w) {
   cudaFree(w->seen); cudaFree(w->pend); cudaFree(w->dist); cudaFree(w->listA); cudaFree(w->listB);
   cudaFree(w->pre); cudaFree(w->ubits); cudaFree(w->ctr); cudaFreeHost(w->h_ctr); cudaFree(w->bstats);
   cudaFree(w->scan_tmp);
-  delete w;
-  g->work = nullptr;
+  *w = Work();
 }
 
-int ensure_work(Graph* g) {
-  if (g->work) return CBFS_OK;
-  Work* w = new Work();
-  g->work = w;
-  const uint64_t cap = (uint64_t)(g->n ? g->n : 1) * LANES;
+void work_free(Graph* g) { g->work = nullptr; }  // the cache outlives graphs
+
+static int work_grow(Work* w, uint32_t n) {
+  const uint64_t cap = (uint64_t)(n ? n : 1) * LANES;
+  if (w->cap >= cap) return CBFS_OK;
+  work_release_buffers(w);
   w->cap = cap;
+  const uint64_t ubw = 2 * (((uint64_t)cap / LANES >> 5) + 1);
   CBFS_CUDA(cudaMalloc(&w->seen, cap * sizeof(uint64_t)));
   CBFS_CUDA(cudaMalloc(&w->pend, cap * sizeof(uint64_t)));
   CBFS_CUDA(cudaMalloc(&w->dist, cap * sizeof(uint16_t)));
   CBFS_CUDA(cudaMalloc(&w->listA, cap * sizeof(uint32_t)));
   CBFS_CUDA(cudaMalloc(&w->listB, cap * sizeof(uint32_t)));
   CBFS_CUDA(cudaMalloc(&w->pre, (cap + 1) * sizeof(uint64_t)));
-  CBFS_CUDA(cudaMalloc(&w->ubits, ((g->n >> 5) + 1) * sizeof(uint32_t)));
+  CBFS_CUDA(cudaMalloc(&w->ubits, ubw * sizeof(uint32_t)));
   CBFS_CUDA(cudaMalloc(&w->ctr, 4 * sizeof(unsigned long long)));
   CBFS_CUDA(cudaMallocHost(&w->h_ctr, 4 * sizeof(unsigned long long)));
   CBFS_CUDA(cudaMalloc(&w->bstats, LANES * 4 * sizeof(uint64_t)));
   CBFS_CUDA(cudaMemset(w->pend, 0, cap * sizeof(uint64_t)));  // zero-invariant from here on
-  CBFS_CUDA(cudaMemset(w->ubits, 0, ((g->n >> 5) + 1) * sizeof(uint32_t)));
+  CBFS_CUDA(cudaMemset(w->ubits, 0, ubw * sizeof(uint32_t)));  // both bitmaps zero between runs
   CBFS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, w->scan_bytes, w->pre, w->pre, cap));
   CBFS_CUDA(cudaMalloc(&w->scan_tmp, w->scan_bytes ? w->scan_bytes : 1));
+  CBFS_CUDA(cudaDeviceSynchronize());
   return CBFS_OK;
+}
+
+WorkLease::WorkLease(Graph* g) : g_(g) {
+  if (g->device < 0 || g->device >= MAX_DEV) { rc = fail(CBFS_EUNSUPPORTED, "device ordinal >= 64"); return; }
+  g_work_mu[g->device].lock();
+  locked_ = true;
+  if (!g_work[g->device]) g_work[g->device] = new Work();
+  rc = work_grow(g_work[g->device], g->n);
+  if (rc == CBFS_OK) g->work = g_work[g->device];
+}
+
+WorkLease::~WorkLease() {
+  if (g_) g_->work = nullptr;
+  if (locked_) g_work_mu[g_->device].unlock();
 }
 
 enum : unsigned long long { ERR_BAD_SOURCE = 1, ERR_DUP_SOURCE = 2, ERR_BAD_SIZE = 4, ERR_OVERFLOW = 8 };
 
+constexpr unsigned FULLW = 0xFFFFFFFFu;
+constexpr uint32_t LSHIFT = 6;  // log2(LANES)
+static_assert((1u << LSHIFT) == LANES, "LANES must be 64");
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+
 // warp-aggregated append of `e` for lanes with `flag`
 __device__ __forceinline__ void warp_append(bool flag, uint32_t e, uint32_t* __restrict__ list,
                                             unsigned long long* __restrict__ count) {
-  const unsigned FULL = 0xFFFFFFFFu;
-  unsigned mask = __ballot_sync(FULL, flag);
+  unsigned mask = __ballot_sync(FULLW, flag);
   if (!mask) return;
-  const int lane = threadIdx.x & 31;
+  const uint32_t lane = lane_id();
   const int leader = __ffs(mask) - 1;
   unsigned long long base = 0;
-  if (lane == leader) base = atomicAdd(count, (unsigned long long)__popc(mask));
-  base = __shfl_sync(FULL, base, leader);
+  if ((int)lane == leader) base = atomicAdd(count, (unsigned long long)__popc(mask));
+  base = __shfl_sync(FULLW, base, leader);
   if (flag) list[base + __popc(mask & ((1u << lane) - 1))] = e;
 }
 
 __device__ __forceinline__ unsigned long long warp_sum(unsigned long long x) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULLW, x, o);
   return x;
+}
+
+// union-frontier bit of vertex v, one atomic per distinct word in the warp
+__device__ __forceinline__ void warp_set_bit(bool flag, uint32_t v, uint32_t* __restrict__ bits) {
+  const uint32_t word = flag ? (v >> 5) : 0xFFFFFFFFu;
+  const unsigned grp = __match_any_sync(FULLW, word);
+  const unsigned b = __reduce_or_sync(grp, flag ? (1u << (v & 31)) : 0u);
+  if (flag && lane_id() == (uint32_t)(__ffs(grp) - 1)) atomicOr(&bits[word], b);
+}
+
+// ------------------------------------------------------------------ stats
+// Per-cluster statistics are counted where an entry is CLAIMED for the next
+// frontier (so the fold stays a pure streaming kernel): bstats[c] =
+// {rounds, sum_i |F_i|, sum_i E_i, sum of degrees of first visits}.
+__device__ __forceinline__ void stats_flush(uint64_t* __restrict__ bstats, uint32_t c, unsigned long long aF,
+                                            unsigned long long aE, unsigned long long aM, uint32_t rounds) {
+  if (!aF) return;
+  atomicAdd((unsigned long long*)&bstats[c * 4 + 1], aF);
+  atomicAdd((unsigned long long*)&bstats[c * 4 + 2], aE);
+  if (aM) atomicAdd((unsigned long long*)&bstats[c * 4 + 3], aM);
+  atomicMax((unsigned long long*)&bstats[c * 4 + 0], (unsigned long long)rounds);
 }
 
 // ------------------------------------------------------------------ init
 // R1 seeding (S_next[s_j] = {s_j}; F_0 = S): pend[s_j, c] = bit j.
 __global__ void k_seed(const uint32_t* __restrict__ sources, const uint8_t* __restrict__ sizes, uint32_t nb,
                        uint32_t n, const uint32_t* __restrict__ inv, const uint64_t* __restrict__ off,
-                       uint64_t* __restrict__ pend, uint32_t* __restrict__ list, unsigned long long* __restrict__ ctr) {
-  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;  // one warp per (cluster, 32 sources)
+                       uint64_t* __restrict__ pend, uint32_t* __restrict__ list, uint32_t* __restrict__ ubits0,
+                       uint64_t* __restrict__ bstats, unsigned long long* __restrict__ ctr) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;  // 64 threads per cluster
   const uint32_t c = t >> 6, j = t & 63;
   bool claim = false;
-  uint32_t e = 0;
-  unsigned long long degsum = 0;
+  uint32_t e = 0, x = 0;
+  unsigned long long deg = 0;
   if (c < nb) {
     const uint32_t k = sizes[c];
     if (k == 0 || k > 64) {
@@ -121,76 +185,87 @@ __global__ void k_seed(const uint32_t* __restrict__ sources, const uint8_t* __re
       if (s >= n) {
         atomicOr(&ctr[2], ERR_BAD_SOURCE);
       } else {
-        const uint32_t x = inv ? inv[s] : s;
-        e = x * LANES + c;
+        x = inv ? inv[s] : s;
+        e = (x << LSHIFT) + c;
         unsigned long long old = atomicOr((unsigned long long*)&pend[e], 1ULL << j);
-        if (old != 0) atomicOr(&ctr[2], ERR_DUP_SOURCE);  // R2
-        else { claim = true; degsum = off[x + 1] - off[x]; }
+        if (old != 0) {
+          atomicOr(&ctr[2], ERR_DUP_SOURCE);  // R2
+        } else {
+          claim = true;
+          deg = off[x + 1] - off[x];
+          atomicAdd((unsigned long long*)&bstats[c * 4 + 1], 1ULL);
+          atomicAdd((unsigned long long*)&bstats[c * 4 + 2], deg);
+          atomicAdd((unsigned long long*)&bstats[c * 4 + 3], deg);
+          atomicMax((unsigned long long*)&bstats[c * 4 + 0], 1ULL);
+        }
       }
     }
   }
   warp_append(claim, e, list, &ctr[0]);
-  degsum = warp_sum(degsum);
-  if ((threadIdx.x & 31) == 0 && degsum) atomicAdd(&ctr[1], degsum);
+  warp_set_bit(claim, x, ubits0);
+  deg = warp_sum(claim ? deg : 0);
+  if (lane_id() == 0 && deg) atomicAdd(&ctr[1], deg);
 }
 
 // ------------------------------------------------------------------ fold
 // Vertex phase: S_new = S_next[u] \ S_seen[u] (= pend), set
-// Delta_u on first visit, S_u[i - Delta_u] = S_new, S_seen[u] |= S_new.
-// Also: outputs, union-frontier bitmap, per-cluster stats, degrees for the
-// push scan.
+// Delta_u on first visit, S_u[i - Delta_u] = S_new, S_seen[u] |= S_new; plus
+// the output writes and the degrees for the push scan.  Independent per
+// entry; FOLD_ILP entries per thread are loaded before any is used.
+constexpr int FOLD_ILP = 4;
+
 template <int DB>
 __global__ void __launch_bounds__(256) k_fold(const uint32_t* __restrict__ F, uint32_t nF, uint32_t i,
                                               uint64_t* __restrict__ seen, uint64_t* __restrict__ pend,
                                               uint16_t* __restrict__ dist, const uint64_t* __restrict__ off,
                                               const uint32_t* __restrict__ perm, uint32_t n, uint32_t C,
                                               uint32_t cbase, uint32_t planes, void* __restrict__ out_dist,
-                                              uint64_t* __restrict__ out_masks, uint32_t* __restrict__ ubits,
-                                              uint64_t* __restrict__ pre, uint64_t* __restrict__ bstats,
-                                              unsigned long long* __restrict__ ctr) {
-  __shared__ unsigned long long sF[LANES], sE[LANES], sM[LANES];
-  __shared__ unsigned sR[LANES];
-  if (threadIdx.x < LANES) { sF[threadIdx.x] = sE[threadIdx.x] = sM[threadIdx.x] = 0; sR[threadIdx.x] = 0; }
-  __syncthreads();
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nF; t += gridDim.x * blockDim.x) {
-    const uint32_t e = F[t];
-    const uint32_t v = e >> 5, c = e & 31;
-    const uint64_t nw = pend[e];
-    pend[e] = 0;
-    uint32_t dv = dist[e];
-    const bool first = dv == INF16;
-    if (first) { dv = i; dist[e] = (uint16_t)i; }
-    seen[e] |= nw;
-    const uint64_t deg = off[v + 1] - off[v];
-    pre[t] = deg;
-    atomicOr(&ubits[v >> 5], 1u << (v & 31));
-    const uint32_t orig = perm ? perm[v] : v;
-    const uint64_t col = (uint64_t)orig * C + cbase + c;
-    if (first && out_dist) {
-      if (DB == 1) {
-        if (i > 254) atomicOr(&ctr[2], ERR_OVERFLOW);
-        ((uint8_t*)out_dist)[col] = (uint8_t)(i > 254 ? 254 : i);
-      } else {
-        ((uint16_t*)out_dist)[col] = (uint16_t)i;
+                                              uint64_t* __restrict__ out_masks, uint64_t* __restrict__ pre,
+                                              int write_pre, unsigned long long* __restrict__ ctr) {
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+  bool overflow = false;
+  for (uint64_t t0 = tid; t0 < nF; t0 += nth * FOLD_ILP) {
+    uint32_t e[FOLD_ILP];
+    uint64_t nw[FOLD_ILP], sv[FOLD_ILP];
+    uint32_t dv[FOLD_ILP];
+#pragma unroll
+    for (int q = 0; q < FOLD_ILP; ++q) {
+      const uint64_t t = t0 + q * nth;
+      e[q] = t < nF ? F[t] : 0xFFFFFFFFu;
+    }
+#pragma unroll
+    for (int q = 0; q < FOLD_ILP; ++q) {
+      if (e[q] != 0xFFFFFFFFu) {
+        nw[q] = pend[e[q]];
+        sv[q] = seen[e[q]];
+        dv[q] = dist[e[q]];
       }
     }
-    const uint32_t oi = i - dv;
-    if (out_masks && oi < planes) out_masks[(uint64_t)oi * n * C + col] = nw;
-    atomicAdd(&sF[c], 1ULL);
-    atomicAdd(&sE[c], (unsigned long long)deg);
-    if (first) atomicAdd(&sM[c], (unsigned long long)deg);
-    atomicMax(&sR[c], i + 1);
-  }
-  __syncthreads();
-  if (threadIdx.x < LANES) {
-    const uint32_t c = threadIdx.x;
-    if (sF[c]) {
-      atomicAdd((unsigned long long*)&bstats[c * 4 + 1], sF[c]);
-      atomicAdd((unsigned long long*)&bstats[c * 4 + 2], sE[c]);
-      if (sM[c]) atomicAdd((unsigned long long*)&bstats[c * 4 + 3], sM[c]);
-      atomicMax((unsigned long long*)&bstats[c * 4 + 0], (unsigned long long)sR[c]);
+#pragma unroll
+    for (int q = 0; q < FOLD_ILP; ++q) {
+      if (e[q] == 0xFFFFFFFFu) continue;
+      const uint32_t v = e[q] >> LSHIFT, c = e[q] & (LANES - 1);
+      pend[e[q]] = 0;
+      seen[e[q]] = sv[q] | nw[q];
+      const bool first = dv[q] == INF16;
+      if (first) { dv[q] = i; dist[e[q]] = (uint16_t)i; }
+      if (write_pre) pre[t0 + q * nth] = off[v + 1] - off[v];
+      const uint32_t orig = perm ? perm[v] : v;
+      const uint64_t col = (uint64_t)orig * C + cbase + c;
+      if (first && out_dist) {
+        if (DB == 1) {
+          overflow |= i > 254;
+          ((uint8_t*)out_dist)[col] = (uint8_t)(i > 254 ? 254 : i);
+        } else {
+          ((uint16_t*)out_dist)[col] = (uint16_t)i;
+        }
+      }
+      const uint32_t oi = i - dv[q];
+      if (out_masks && oi < planes) out_masks[(uint64_t)oi * n * C + col] = nw[q];
     }
   }
+  if (overflow) atomicOr(&ctr[2], ERR_OVERFLOW);
 }
 
 // ------------------------------------------------------------------ push
@@ -204,9 +279,13 @@ __global__ void __launch_bounds__(256) k_push(const uint64_t* __restrict__ off, 
                                               const uint32_t* __restrict__ F, const uint64_t* __restrict__ pre,
                                               uint32_t nF, uint64_t total, const uint64_t* __restrict__ seen,
                                               const uint16_t* __restrict__ dist, uint64_t* __restrict__ pend,
-                                              uint32_t* __restrict__ out_list, unsigned long long* __restrict__ ctr,
+                                              uint32_t* __restrict__ out_list, uint32_t* __restrict__ ubits_next,
+                                              uint64_t* __restrict__ bstats, unsigned long long* __restrict__ ctr,
                                               uint32_t i, uint32_t d) {
-  const int lane = threadIdx.x & 31;
+  __shared__ unsigned long long sF[LANES], sE[LANES], sM[LANES];
+  for (uint32_t c = threadIdx.x; c < LANES; c += blockDim.x) sF[c] = sE[c] = sM[c] = 0;
+  __syncthreads();
+  const uint32_t lane = lane_id();
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
   unsigned long long degsum = 0;
@@ -222,116 +301,269 @@ __global__ void __launch_bounds__(256) k_push(const uint64_t* __restrict__ off, 
       }
       idx = lo;
     }
-    idx = __shfl_sync(0xFFFFFFFFu, idx, 0);
+    idx = __shfl_sync(FULLW, idx, 0);
     for (uint64_t p0 = start; p0 < end; p0 += 32) {
       const uint64_t p = p0 + lane;
       bool claim = false;
-      uint32_t ev = 0;
+      uint32_t ev = 0, v = 0;
       if (p < end) {
         while (pre[idx + 1] <= p) ++idx;
         const uint32_t e = F[idx];
-        const uint32_t u = e >> 5, c = e & 31;
-        const uint32_t v = cols[off[u] + (p - pre[idx])];
-        ev = v * LANES + c;
+        const uint32_t u = e >> LSHIFT, c = e & (LANES - 1);
+        v = cols[off[u] + (p - pre[idx])];
+        ev = (v << LSHIFT) + c;
         const uint32_t dv = dist[ev];
         if (dv == INF16 || (int)i - (int)dv < (int)d) {  // P:722, R3
           const uint64_t x = seen[e] & ~seen[ev];
           if (x) {
             const unsigned long long old = atomicOr((unsigned long long*)&pend[ev], (unsigned long long)x);
             claim = old == 0;  // first setter wins (R4)
-            if (claim) degsum += off[v + 1] - off[v];
+            if (claim) {
+              const unsigned long long deg = off[v + 1] - off[v];
+              degsum += deg;
+              atomicAdd(&sF[c], 1ULL);
+              atomicAdd(&sE[c], deg);
+              if (dv == INF16) atomicAdd(&sM[c], deg);
+            }
           }
         }
       }
       warp_append(claim, ev, out_list, &ctr[0]);
+      warp_set_bit(claim, v, ubits_next);
     }
   }
   degsum = warp_sum(degsum);
   if (lane == 0 && degsum) atomicAdd(&ctr[1], degsum);
+  __syncthreads();
+  for (uint32_t c = threadIdx.x; c < LANES; c += blockDim.x) stats_flush(bstats, c, sF[c], sE[c], sM[c], i + 2);
 }
 
 // ------------------------------------------------------------------ pull
 // EdgeMap-Dense: every vertex v that can still receive (cap
 // P:722 and S_seen[v] != S) ORs S_seen[u] over its neighbours u in the union
-// frontier; lane c = cluster c.  No first-hit break (R7): stop only when the
+// frontier.  No first-hit break (R7): a vertex stops only when its
 // accumulated subset is full.  Neighbours not in F_i^c contribute only bits v
-// already holds (reading R7a), so one union-frontier test per
-// arc serves all 32 clusters.
+// already holds (R7a), so one union-frontier test per arc
+// serves all 64 clusters.  Lane l owns clusters 2l, 2l+1 (one 16-byte word
+// pair per state row).
+//
+// A warp owns a PULL_CHUNK-arc slice of the CSR; its vertices are handled in
+// groups of up to 32:
+//   (1) one coalesced load gives the group's 32 offsets;
+//   (2) the group's per-vertex state rows are loaded back to back; cap and
+//       first-visit bits are kept in registers;
+//   (3) pass A streams the group's arcs 32 at a time (coalesced columns +
+//       union-frontier bits), finds each arc's vertex by a shuffle binary
+//       search and compacts the useful neighbours into a shared-memory list
+//       that is sorted by vertex, with per-vertex counts;
+//   (4) pass B walks each active vertex's segment of the list, gathering
+//       PULL_MLP neighbour rows at a time into a register accumulator
+//       (no per-arc vertex bookkeeping), with the R7 full-subset early exit,
+//       and decides the vertex's claims;
+//   (5) the group's claims are appended with one atomic.
 constexpr int PULL_MLP = 8;
+constexpr int PULL_WARPS = 8;  // warps per block
 
-__global__ void __launch_bounds__(256) k_pull(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cols,
-                                              const uint32_t* __restrict__ chunk_v, uint64_t n_chunks, uint64_t m,
-                                              const uint64_t* __restrict__ seen, const uint16_t* __restrict__ dist,
-                                              uint64_t* __restrict__ pend, const uint32_t* __restrict__ ubits,
-                                              const uint8_t* __restrict__ sizes, uint32_t nb,
-                                              uint32_t* __restrict__ out_list, unsigned long long* __restrict__ ctr,
-                                              uint32_t i, uint32_t d) {
-  const unsigned FULLW = 0xFFFFFFFFu;
-  const int lane = threadIdx.x & 31;
+struct U2 {
+  uint64_t a, b;
+};
+__device__ __forceinline__ U2 ld2(const uint64_t* p) {
+  const ulonglong2 x = __ldg(reinterpret_cast<const ulonglong2*>(p));
+  return {x.x, x.y};
+}
+
+__global__ void __launch_bounds__(PULL_WARPS * 32, 3) k_pull(
+    const uint64_t* __restrict__ off, const uint32_t* __restrict__ cols, const uint32_t* __restrict__ chunk_v,
+    uint64_t n_chunks, uint64_t m, uint32_t n, const uint64_t* __restrict__ seen, const uint16_t* __restrict__ dist,
+    uint64_t* __restrict__ pend, const uint32_t* __restrict__ ubits, uint32_t* __restrict__ ubits_next,
+    const uint8_t* __restrict__ sizes, uint32_t nb, uint32_t* __restrict__ out_list, uint64_t* __restrict__ bstats,
+    unsigned long long* __restrict__ ctr, uint32_t i, uint32_t d) {
+  __shared__ uint32_t s_list[PULL_WARPS][PULL_CHUNK];
+  __shared__ uint32_t s_cnt[PULL_WARPS][32];
+  const uint32_t lane = lane_id();
+  const uint32_t wib = threadIdx.x >> 5;
+  uint32_t* list = s_list[wib];
+  uint32_t* cnt = s_cnt[wib];
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
-  const uint64_t full = (uint32_t)lane < nb ? full_mask(sizes[lane]) : 0ULL;
-  unsigned long long degsum = 0;
+  const uint32_t c0 = 2 * lane, c1 = 2 * lane + 1;
+  const uint64_t full0 = c0 < nb ? full_mask(sizes[c0]) : 0ULL;
+  const uint64_t full1 = c1 < nb ? full_mask(sizes[c1]) : 0ULL;
+  const unsigned lt = (1u << lane) - 1;
+  unsigned long long aF0 = 0, aE0 = 0, aM0 = 0, aF1 = 0, aE1 = 0, aM1 = 0, degsum = 0;
+  const uint64_t* seen2 = seen + 2 * lane;  // lane's word pair of row 0
+  const uint32_t* dist2 = reinterpret_cast<const uint32_t*>(dist) + lane;
+
   for (uint64_t w = warp; w < n_chunks; w += nwarps) {
-    uint64_t e0 = w * PULL_CHUNK;
+    const uint64_t e0 = w * PULL_CHUNK;
     const uint64_t e1 = min(e0 + PULL_CHUNK, m);
     uint32_t v = chunk_v[w];
-    while (e0 < e1) {
-      const uint64_t vb = off[v], ve = off[v + 1];
-      const uint64_t lo = max(vb, e0), hi = min(ve, e1);
-      if (lo >= hi) { ++v; continue; }
-      const uint64_t x = (uint64_t)v * LANES + lane;
-      const uint32_t dv = dist[x];
-      const uint64_t sv = seen[x];
-      const bool cap = full != 0 && (dv == INF16 || (int)i - (int)dv < (int)d) && sv != full;
-      if (__ballot_sync(FULLW, cap)) {
-        uint64_t acc = 0;
-        for (uint64_t e = lo; e < hi; e += 32) {
-          const uint32_t myu = (e + lane < hi) ? cols[e + lane] : 0xFFFFFFFFu;
-          const bool inF = myu != 0xFFFFFFFFu && ((__ldg(&ubits[myu >> 5]) >> (myu & 31)) & 1u);
-          unsigned fm = __ballot_sync(FULLW, inF);
-          while (fm) {
-            uint64_t g[PULL_MLP];
+    uint64_t e = e0;
+    while (e < e1) {
+      // ---- (1) offsets of up to 32 vertices v .. v+31
+      const uint32_t vj = v + lane;
+      const uint64_t ob = vj < n ? off[vj] : m;
+      const uint64_t oe = vj < n ? off[vj + 1] : m;
+      const uint32_t nv = __popc(__ballot_sync(FULLW, vj < n && ob < e1));  // a prefix of lanes
+      const uint64_t lo_j = max(ob, e0), hi_j = min(oe, e1);
+      const unsigned hasarcs = __ballot_sync(FULLW, lane < nv && lo_j < hi_j);
+      const uint64_t ge = __shfl_sync(FULLW, hi_j, nv - 1);  // group arc end
+      // ---- (2) per-vertex state rows
+      unsigned cap0 = 0, cap1 = 0, inf0 = 0, inf1 = 0, actv = 0;
+      for (uint32_t j0 = 0; j0 < nv; j0 += 4) {
+        uint32_t dq[4];
+        U2 sq[4];
 #pragma unroll
-            for (int q = 0; q < PULL_MLP; ++q) {
-              g[q] = 0;
-              if (fm) {
-                const int j = __ffs(fm) - 1;
-                fm &= fm - 1;
-                const uint32_t u = __shfl_sync(FULLW, myu, j);
-                g[q] = seen[(uint64_t)u * LANES + lane];
-              }
-            }
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t j = j0 + q;
+          dq[q] = 0xFFFFFFFFu;
+          sq[q] = {0, 0};
+          if (j < nv && ((hasarcs >> j) & 1u)) {
+            dq[q] = dist2[(uint64_t)(v + j) * (LANES / 2)];
+            sq[q] = ld2(seen2 + (uint64_t)(v + j) * LANES);
+          }
+        }
 #pragma unroll
-            for (int q = 0; q < PULL_MLP; ++q) acc |= g[q];
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t j = j0 + q;
+          if (j < nv && ((hasarcs >> j) & 1u)) {
+            const uint32_t d0 = dq[q] & 0xFFFFu, d1 = dq[q] >> 16;
+            const bool k0 = full0 != 0 && (d0 == INF16 || (int)i - (int)d0 < (int)d) && sq[q].a != full0;
+            const bool k1 = full1 != 0 && (d1 == INF16 || (int)i - (int)d1 < (int)d) && sq[q].b != full1;
+            cap0 |= (unsigned)k0 << j;
+            cap1 |= (unsigned)k1 << j;
+            inf0 |= (unsigned)(d0 == INF16) << j;
+            inf1 |= (unsigned)(d1 == INF16) << j;
+            if (__ballot_sync(FULLW, k0 || k1)) actv |= 1u << j;
           }
-          if (!__ballot_sync(FULLW, cap && ((acc | sv) != full))) break;
         }
-        const uint64_t nw = acc & ~sv;
-        bool claim = false;
-        if (cap && nw) {
-          if (vb >= e0 && ve <= e1) {  // this warp owns all of v's arcs
-            pend[x] = nw;
-            claim = true;
-          } else {
-            claim = atomicOr((unsigned long long*)&pend[x], (unsigned long long)nw) == 0;
-          }
-          if (claim) degsum += ve - vb;
-        }
-        warp_append(claim, (uint32_t)x, out_list, &ctr[0]);
       }
-      e0 = hi;
-      ++v;
+      if (actv) {
+        // ---- (3) pass A: compact useful neighbours, sorted by vertex
+        cnt[lane] = 0;
+        __syncwarp();
+        uint32_t nl = 0;
+        for (uint64_t wb = e; wb < ge; wb += 32) {
+          const uint64_t a = wb + lane;
+          const bool inr = a < ge;
+          const uint32_t u = inr ? cols[a] : 0u;
+          uint32_t jv = 0;  // largest j < nv with ob_j <= a
+#pragma unroll
+          for (int step = 16; step > 0; step >>= 1) {
+            const uint32_t cand = jv + step;
+            const uint64_t oc = __shfl_sync(FULLW, ob, cand & 31);
+            if (cand < nv && oc <= a) jv = cand;
+          }
+          const bool want = inr && ((actv >> jv) & 1u) && ((__ldg(&ubits[u >> 5]) >> (u & 31)) & 1u);
+          const unsigned fm = __ballot_sync(FULLW, want);
+          if (want) list[nl + __popc(fm & lt)] = u;
+          const unsigned grp = __match_any_sync(FULLW, want ? jv : 0xFFFFFFFFu);
+          if (want && lane == (uint32_t)(__ffs(grp) - 1)) cnt[jv] += __popc(grp);
+          nl += __popc(fm);
+          __syncwarp();
+        }
+        // per-vertex segment starts (exclusive scan of counts, lane = vertex)
+        const uint32_t myc = cnt[lane];
+        uint32_t incl = myc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(FULLW, incl, o);
+          if (lane >= (uint32_t)o) incl += y;
+        }
+        const uint32_t seg0 = incl - myc;
+        // ---- (4) pass B: gather per active vertex, decide claims
+        unsigned myb0 = 0, myb1 = 0;  // lane j: claim ballots of vertex j
+        unsigned rem = actv;
+        while (rem) {
+          const uint32_t j = __ffs(rem) - 1;
+          rem &= rem - 1;
+          const uint32_t s0 = __shfl_sync(FULLW, seg0, j);
+          const uint32_t sn = __shfl_sync(FULLW, myc, j);
+          const uint64_t row = (uint64_t)(v + j) * LANES;
+          const U2 sv = ld2(seen2 + row);
+          const bool k0 = (cap0 >> j) & 1u, k1 = (cap1 >> j) & 1u;
+          uint64_t acc0 = 0, acc1 = 0;
+          for (uint32_t q0 = 0; q0 < sn; q0 += 32) {
+            const uint32_t qe = min(q0 + 32, sn);
+            uint32_t q = q0;
+            for (; q + PULL_MLP <= qe; q += PULL_MLP) {
+              U2 g[PULL_MLP];
+#pragma unroll
+              for (int r = 0; r < PULL_MLP; ++r) g[r] = ld2(seen2 + (uint64_t)list[s0 + q + r] * LANES);
+#pragma unroll
+              for (int r = 0; r < PULL_MLP; ++r) { acc0 |= g[r].a; acc1 |= g[r].b; }
+            }
+            for (; q < qe; ++q) {
+              const U2 g = ld2(seen2 + (uint64_t)list[s0 + q] * LANES);
+              acc0 |= g.a;
+              acc1 |= g.b;
+            }
+            // R7: stop once every capped lane holds its full subset
+            if (!__ballot_sync(FULLW, (k0 && ((acc0 | sv.a) != full0)) || (k1 && ((acc1 | sv.b) != full1)))) break;
+          }
+          const uint64_t nw0 = k0 ? (acc0 & ~sv.a) : 0, nw1 = k1 ? (acc1 & ~sv.b) : 0;
+          bool cl0 = false, cl1 = false;
+          const uint64_t ob_j = __shfl_sync(FULLW, ob, j), oe_j = __shfl_sync(FULLW, oe, j);
+          if (nw0 | nw1) {
+            uint64_t* pp = pend + row + 2 * lane;
+            if (ob_j >= e0 && oe_j <= e1) {  // this warp owns all of v's arcs
+              *reinterpret_cast<ulonglong2*>(pp) = make_ulonglong2(nw0, nw1);
+              cl0 = nw0 != 0;
+              cl1 = nw1 != 0;
+            } else {
+              if (nw0) cl0 = atomicOr((unsigned long long*)pp, (unsigned long long)nw0) == 0;
+              if (nw1) cl1 = atomicOr((unsigned long long*)(pp + 1), (unsigned long long)nw1) == 0;
+            }
+            const unsigned long long deg = oe_j - ob_j;
+            if (cl0) { aF0 += 1; aE0 += deg; if ((inf0 >> j) & 1u) aM0 += deg; degsum += deg; }
+            if (cl1) { aF1 += 1; aE1 += deg; if ((inf1 >> j) & 1u) aM1 += deg; degsum += deg; }
+          }
+          const unsigned b0 = __ballot_sync(FULLW, cl0), b1 = __ballot_sync(FULLW, cl1);
+          if (lane == j) { myb0 = b0; myb1 = b1; }
+        }
+        // ---- (5) one append for the group; entries of a vertex in cluster order
+        const uint32_t ccount = __popc(myb0) + __popc(myb1);
+        uint32_t cinc = ccount;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(FULLW, cinc, o);
+          if (lane >= (uint32_t)o) cinc += y;
+        }
+        const uint32_t total = __shfl_sync(FULLW, cinc, 31);
+        if (total) {
+          unsigned long long base = 0;
+          if (lane == 0) base = atomicAdd(&ctr[0], (unsigned long long)total);
+          base = __shfl_sync(FULLW, base, 0);
+          const uint32_t cexcl = cinc - ccount;
+          unsigned rem2 = __ballot_sync(FULLW, ccount != 0);
+          while (rem2) {
+            const uint32_t j = __ffs(rem2) - 1;
+            rem2 &= rem2 - 1;
+            const unsigned b0 = __shfl_sync(FULLW, myb0, j), b1 = __shfl_sync(FULLW, myb1, j);
+            const uint32_t oj = __shfl_sync(FULLW, cexcl, j);
+            const bool h0 = (b0 >> lane) & 1u, h1 = (b1 >> lane) & 1u;
+            const uint32_t r = oj + __popc(b0 & lt) + __popc(b1 & lt);
+            const uint32_t ebase = ((v + j) << LSHIFT) + 2 * lane;
+            if (h0) out_list[base + r] = ebase;
+            if (h1) out_list[base + r + h0] = ebase + 1;
+          }
+        }
+        warp_set_bit(ccount != 0, v + lane, ubits_next);
+        __syncwarp();
+      }
+      e = ge;
+      v += nv;
     }
   }
   degsum = warp_sum(degsum);
   if (lane == 0 && degsum) atomicAdd(&ctr[1], degsum);
+  stats_flush(bstats, c0, aF0, aE0, aM0, i + 2);
+  stats_flush(bstats, c1, aF1, aE1, aM1, i + 2);
 }
 
 __global__ void k_set_u64(uint64_t* p, uint64_t v) { *p = v; }
 
 // ------------------------------------------------------------------ driver
-
 static int sync_ctr(Work* w, cudaStream_t st) {
   CBFS_CUDA(cudaMemcpyAsync(w->h_ctr, w->ctr, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   CBFS_CUDA(cudaStreamSynchronize(st));
@@ -341,18 +573,20 @@ static int sync_ctr(Work* w, cudaStream_t st) {
 int run_batch(Graph* g, const RunArgs& a, cudaStream_t st) {
   Work* w = g->work;
   const uint32_t n = g->n;
+  const uint64_t ub_words = (n >> 5) + 1;
   CBFS_CUDA(cudaMemsetAsync(w->seen, 0, (uint64_t)n * LANES * sizeof(uint64_t), st));
   CBFS_CUDA(cudaMemsetAsync(w->dist, 0xFF, (uint64_t)n * LANES * sizeof(uint16_t), st));
   CBFS_CUDA(cudaMemsetAsync(w->bstats, 0, LANES * 4 * sizeof(uint64_t), st));
   CBFS_CUDA(cudaMemsetAsync(w->ctr, 0, 3 * sizeof(unsigned long long), st));
   k_seed<<<(a.nb * 64 + 255) / 256, 256, 0, st>>>(a.sources, a.sizes, a.nb, n, g->inv, g->off, w->pend, w->listA,
-                                                   w->ctr);
+                                                   w->ubits, w->bstats, w->ctr);
   CBFS_LAUNCHED();
   int rc = sync_ctr(w, st);
   if (rc) return rc;
   if (w->h_ctr[2]) {
-    // leave pend zero-invariant for the next call
+    // leave pend and the bitmaps zero for the next call
     CBFS_CUDA(cudaMemsetAsync(w->pend, 0, (uint64_t)n * LANES * sizeof(uint64_t), st));
+    CBFS_CUDA(cudaMemsetAsync(w->ubits, 0, 2 * ub_words * sizeof(uint32_t), st));
     CBFS_CUDA(cudaStreamSynchronize(st));
     if (w->h_ctr[2] & ERR_BAD_SIZE) return fail(CBFS_EINVAL, "cluster size must be 1..64");
     if (w->h_ctr[2] & ERR_BAD_SOURCE) return fail(CBFS_EINVAL, "source id >= n");
@@ -364,36 +598,57 @@ int run_batch(Graph* g, const RunArgs& a, cudaStream_t st) {
   bool overflow = false;
   for (uint32_t i = 0; nF > 0; ++i) {
     if (i >= 0xFFFEu) return fail(CBFS_EOVERFLOW, "more than 65534 rounds");
-    const unsigned fb = grid_for(nF, 256);
+    uint32_t* ub_cur = w->ubits + (i & 1) * ub_words;        // U_i (built by the previous edge phase)
+    uint32_t* ub_nxt = w->ubits + ((i + 1) & 1) * ub_words;  // U_{i+1} (zero)
+    const bool pull = a.direction == CBFS_DIR_PULL ||
+                      (a.direction == CBFS_DIR_AUTO && (double)E * g_alpha > (double)g->m * (double)a.nb);
+    const int write_pre = pull ? 0 : 1;
+    const unsigned fb = grid_for((nF + FOLD_ILP - 1) / FOLD_ILP, 256);
+    if (g_prof.on) CBFS_CUDA(cudaEventRecord(g_prof.ev[0], st));
     if (a.dist_bytes == 1)
       k_fold<1><<<fb, 256, 0, st>>>(cur, (uint32_t)nF, i, w->seen, w->pend, w->dist, g->off, g->perm, n, a.C, a.cbase,
-                                    a.planes, a.out_dist, a.out_masks, w->ubits, w->pre, w->bstats, w->ctr);
+                                    a.planes, a.out_dist, a.out_masks, w->pre, write_pre, w->ctr);
     else
       k_fold<2><<<fb, 256, 0, st>>>(cur, (uint32_t)nF, i, w->seen, w->pend, w->dist, g->off, g->perm, n, a.C, a.cbase,
-                                    a.planes, a.out_dist, a.out_masks, w->ubits, w->pre, w->bstats, w->ctr);
+                                    a.planes, a.out_dist, a.out_masks, w->pre, write_pre, w->ctr);
     CBFS_LAUNCHED();
+    if (g_prof.on) CBFS_CUDA(cudaEventRecord(g_prof.ev[1], st));
     CBFS_CUDA(cudaMemsetAsync(w->ctr, 0, 2 * sizeof(unsigned long long), st));
-    bool pull = a.direction == CBFS_DIR_PULL ||
-                (a.direction == CBFS_DIR_AUTO && (double)E * g_alpha > (double)g->m * (double)a.nb);
+    int kind = -1;
     if (pull) {
-      const unsigned pb = grid_for(g->n_chunks * 32, 256, 148u * 8u * 4u);
-      k_pull<<<pb, 256, 0, st>>>(g->off, g->cols, g->chunk_v, g->n_chunks, g->m, w->seen, w->dist, w->pend, w->ubits,
-                                 a.sizes, a.nb, nxt, w->ctr, i, a.d);
+      kind = PK_PULL;
+      if (g_prof.on) CBFS_CUDA(cudaEventRecord(g_prof.ev[2], st));
+      const unsigned pb = grid_for(g->n_chunks * 32, PULL_WARPS * 32, 148u * 8u);
+      k_pull<<<pb, PULL_WARPS * 32, 0, st>>>(g->off, g->cols, g->chunk_v, g->n_chunks, g->m, n, w->seen, w->dist,
+                                             w->pend, ub_cur, ub_nxt, a.sizes, a.nb, nxt, w->bstats, w->ctr, i, a.d);
       CBFS_LAUNCHED();
+      if (g_prof.on) CBFS_CUDA(cudaEventRecord(g_prof.ev[3], st));
     } else if (E > 0) {
+      kind = PK_PUSH;
       CBFS_CUDA(cub::DeviceScan::ExclusiveSum(w->scan_tmp, w->scan_bytes, w->pre, w->pre, nF, st));
       count_launch(2);
       k_set_u64<<<1, 1, 0, st>>>(w->pre + nF, E);
       CBFS_LAUNCHED();
       const uint64_t warps = (E + PUSH_CHUNK - 1) / PUSH_CHUNK;
       const unsigned pb = grid_for(warps * 32, 256, 148u * 8u * 4u);
+      if (g_prof.on) CBFS_CUDA(cudaEventRecord(g_prof.ev[2], st));
       k_push<<<pb, 256, 0, st>>>(g->off, g->cols, cur, w->pre, (uint32_t)nF, E, w->seen, w->dist, w->pend, nxt,
-                                 w->ctr, i, a.d);
+                                 ub_nxt, w->bstats, w->ctr, i, a.d);
       CBFS_LAUNCHED();
+      if (g_prof.on) CBFS_CUDA(cudaEventRecord(g_prof.ev[3], st));
     }
-    CBFS_CUDA(cudaMemsetAsync(w->ubits, 0, ((n >> 5) + 1) * sizeof(uint32_t), st));
+    CBFS_CUDA(cudaMemsetAsync(ub_cur, 0, ub_words * sizeof(uint32_t), st));  // U_i consumed
     rc = sync_ctr(w, st);
     if (rc) return rc;
+    if (g_prof.on) {
+      float ms = 0;
+      CBFS_CUDA(cudaEventElapsedTime(&ms, g_prof.ev[0], g_prof.ev[1]));
+      g_prof.ms[PK_FOLD] += ms; g_prof.launches[PK_FOLD] += 1; g_prof.entries[PK_FOLD] += nF;
+      if (kind >= 0) {
+        CBFS_CUDA(cudaEventElapsedTime(&ms, g_prof.ev[2], g_prof.ev[3]));
+        g_prof.ms[kind] += ms; g_prof.launches[kind] += 1; g_prof.entries[kind] += nF; g_prof.arcs[kind] += E;
+      }
+    }
     if (w->h_ctr[2] & ERR_OVERFLOW) overflow = true;
     nF = w->h_ctr[0];
     E = w->h_ctr[1];
@@ -431,8 +686,8 @@ int cbfs_run(cbfs_graph* gh, const uint32_t* sources, const uint8_t* sizes, uint
   if (rc) return rc;
   CBFS_CUDA(cudaSetDevice(g->device));
   cudaStream_t st = (cudaStream_t)stream;
-  rc = ensure_work(g);
-  if (rc) return rc;
+  WorkLease lease(g);
+  if (lease.rc) return lease.rc;
   const uint64_t C = n_clusters;
   if (out_dist) CBFS_CUDA(cudaMemsetAsync(out_dist, 0xFF, (uint64_t)g->n * C * dist_bytes, st));
   if (out_masks) CBFS_CUDA(cudaMemsetAsync(out_masks, 0, (uint64_t)planes * g->n * C * sizeof(uint64_t), st));
@@ -454,6 +709,25 @@ int cbfs_run(cbfs_graph* gh, const uint32_t* sources, const uint8_t* sizes, uint
     if (rc) return rc;
   }
   CBFS_CUDA(cudaStreamSynchronize(st));
+  return CBFS_OK;
+}
+
+int cbfs_profile_enable(int on) {
+  if (on && !g_prof.ev[0])
+    for (int k = 0; k < 4; ++k) CBFS_CUDA(cudaEventCreate(&g_prof.ev[k]));
+  g_prof.on = on != 0;
+  return CBFS_OK;
+}
+
+int cbfs_profile_read(double* ms, uint64_t* launches, uint64_t* arcs, uint64_t* entries, int reset) {
+  for (int k = 0; k < 3; ++k) {
+    if (ms) ms[k] = g_prof.ms[k];
+    if (launches) launches[k] = g_prof.launches[k];
+    if (arcs) arcs[k] = g_prof.arcs[k];
+    if (entries) entries[k] = g_prof.entries[k];
+  }
+  if (reset)
+    for (int k = 0; k < PK_N; ++k) g_prof.ms[k] = 0, g_prof.launches[k] = g_prof.arcs[k] = g_prof.entries[k] = 0;
   return CBFS_OK;
 }
 

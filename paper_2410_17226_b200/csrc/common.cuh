@@ -31,7 +31,7 @@ void count_launch(uint64_t k = 1);
   } while (0)
 
 constexpr uint16_t INF16 = 0xFFFFu;
-constexpr uint32_t LANES = 32;  // clusters per batch = warp lanes (vertex-major state)
+constexpr uint32_t LANES = 64;  // clusters per batch (vertex-major state rows of 64 words)
 
 // ---------------------------------------------------------------- graph
 struct Graph {
@@ -60,7 +60,16 @@ struct Graph {
 constexpr uint32_t PULL_CHUNK = 256;  // arcs per warp in the dense pull kernel
 
 int graph_free(Graph* g);
-int ensure_work(Graph* g);
+
+// RAII lease of the device's cached traversal workspace (sets g->work)
+struct WorkLease {
+  explicit WorkLease(Graph* g);
+  ~WorkLease();
+  int rc = CBFS_OK;
+ private:
+  Graph* g_;
+  bool locked_ = false;
+};
 
 // one batch (<= 32 clusters) of cbfs_run; outputs use row stride C and start
 // at column cbase

@@ -35,6 +35,20 @@ uint64_t launches(int reset) {
   return v;
 }
 
+// Keep freed memory in the device's stream-ordered pool: with the default
+// release threshold (0) every synchronisation hands the pool back to the
+// driver and the next allocation pays for page mapping again.
+void keep_pool(int device) {
+  static bool done[64] = {false};
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = ~0ULL;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[device] = true;
+}
+
 // ------------------------------------------------------------- kernels
 __global__ void k_make_keys(const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst, uint64_t P,
                             uint32_t n, uint64_t* __restrict__ keys, int* __restrict__ bad) {
@@ -103,11 +117,12 @@ __global__ void k_order_from_keys(const uint64_t* __restrict__ keys, uint32_t n,
   }
 }
 
-__global__ void k_relabel_keys(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cols, uint32_t n,
-                               const uint32_t* __restrict__ inv, uint64_t* __restrict__ keys) {
-  for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < n; u += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t iu = (uint64_t)inv[u] << 32;
-    for (uint64_t e = off[u]; e < off[u + 1]; ++e) keys[e] = iu | inv[cols[e]];
+// arc-parallel: (u<<32|v) -> (inv[u]<<32 | inv[v])
+__global__ void k_relabel_keys(const uint64_t* __restrict__ arcs, uint64_t m, const uint32_t* __restrict__ inv,
+                               uint64_t* __restrict__ keys) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t a = arcs[e];
+    keys[e] = ((uint64_t)inv[a >> 32] << 32) | inv[(uint32_t)a];
   }
 }
 
@@ -187,15 +202,14 @@ static int keys_to_csr(const uint64_t* keys, uint64_t m, uint32_t n, cudaStream_
 int graph_free(Graph* g) {
   if (!g) return CBFS_OK;
   cudaSetDevice(g->device);
-  if (g->off_orig && g->off_orig != g->off) cudaFree(g->off_orig);
-  if (g->cols_orig && g->cols_orig != g->cols) cudaFree(g->cols_orig);
-  cudaFree(g->off);
-  cudaFree(g->cols);
-  cudaFree(g->perm);
-  cudaFree(g->inv);
-  cudaFree(g->rank);
-  cudaFree(g->order);
-  cudaFree(g->chunk_v);
+  // all graph arrays come from the stream-ordered pool; free them in order
+  // on the legacy stream (after any work that used them)
+  cudaStream_t s0 = 0;
+  if (g->off_orig && g->off_orig != g->off) cudaFreeAsync(g->off_orig, s0);
+  if (g->cols_orig && g->cols_orig != g->cols) cudaFreeAsync(g->cols_orig, s0);
+  void* ps[] = {g->off, g->cols, g->perm, g->inv, g->rank, g->order, g->chunk_v};
+  for (void* p : ps)
+    if (p) cudaFreeAsync(p, s0);
   extern void work_free(Graph*);
   work_free(g);
   delete g;
@@ -211,18 +225,17 @@ static int build_from_keys(uint64_t* keys, uint64_t L, uint32_t n, uint32_t flag
   uint64_t* uk = nullptr;
   int rc = sort_unique(keys, L, n, st, &uk, &g->m);
   if (rc) { delete g; return rc; }
-  if (g->m > 0xFFFFFFFFull) { cudaFree(uk); delete g; return fail(CBFS_EUNSUPPORTED, "more than 2^32-1 arcs"); }
+  if (g->m > 0xFFFFFFFFull) { cudaFreeAsync(uk, st); delete g; return fail(CBFS_EUNSUPPORTED, "more than 2^32-1 arcs"); }
   rc = keys_to_csr(uk, g->m, n, st, &g->off, &g->cols);
   if (rc) { delete g; return rc; }
-  CBFS_CUDA(cudaFreeAsync(uk, st));
   // degree order (deg desc, original id asc)
   uint64_t* dk = nullptr;
   uint32_t* d_max = nullptr;
   CBFS_CUDA(cudaMallocAsync(&dk, sizeof(uint64_t) * (n ? n : 1), st));
   CBFS_CUDA(cudaMallocAsync(&d_max, sizeof(uint32_t), st));
   CBFS_CUDA(cudaMemsetAsync(d_max, 0, sizeof(uint32_t), st));
-  CBFS_CUDA(cudaMalloc(&g->rank, sizeof(uint32_t) * (n ? n : 1)));
-  CBFS_CUDA(cudaMalloc(&g->order, sizeof(uint32_t) * (n ? n : 1)));
+  CBFS_CUDA(cudaMallocAsync(&g->rank, sizeof(uint32_t) * (n ? n : 1), st));
+  CBFS_CUDA(cudaMallocAsync(&g->order, sizeof(uint32_t) * (n ? n : 1), st));
   if (n) {
     k_degree_keys<<<grid_for(n, 256), 256, 0, st>>>(g->off, n, dk, d_max);
     CBFS_LAUNCHED();
@@ -238,17 +251,20 @@ static int build_from_keys(uint64_t* keys, uint64_t L, uint32_t n, uint32_t flag
     CBFS_CUDA(cudaFreeAsync(tmp, st));
     if (flags & CBFS_RELABEL_DEGREE) {
       // perm = order (internal x -> original), inv = rank
-      CBFS_CUDA(cudaMalloc(&g->perm, sizeof(uint32_t) * n));
-      CBFS_CUDA(cudaMalloc(&g->inv, sizeof(uint32_t) * n));
+      CBFS_CUDA(cudaMallocAsync(&g->perm, sizeof(uint32_t) * n, st));
+      CBFS_CUDA(cudaMallocAsync(&g->inv, sizeof(uint32_t) * n, st));
       k_order_from_keys<<<grid_for(n, 256), 256, 0, st>>>(db.Current(), n, g->perm, g->inv);
       CBFS_LAUNCHED();
-      // internal CSR: keys (inv[u] << 32 | inv[v]) sorted
+      // internal CSR: keys (inv[u] << 32 | inv[v]) sorted; the original
+      // arc keys' buffer is reused as the sort's alternate buffer
       uint64_t* rk = nullptr;
       CBFS_CUDA(cudaMallocAsync(&rk, sizeof(uint64_t) * (g->m ? g->m : 1), st));
-      k_relabel_keys<<<grid_for(n, 256), 256, 0, st>>>(g->off, g->cols, n, g->inv, rk);
-      CBFS_LAUNCHED();
-      uint64_t* ralt = nullptr;
-      CBFS_CUDA(cudaMallocAsync(&ralt, sizeof(uint64_t) * (g->m ? g->m : 1), st));
+      if (g->m) {
+        k_relabel_keys<<<grid_for(g->m, 256), 256, 0, st>>>(uk, g->m, g->inv, rk);
+        CBFS_LAUNCHED();
+      }
+      uint64_t* ralt = uk;
+      uk = nullptr;
       cub::DoubleBuffer<uint64_t> rdb(rk, ralt);
       int end_bit = 32 + bits_for(n);
       size_t tb3 = 0;
@@ -283,11 +299,12 @@ static int build_from_keys(uint64_t* keys, uint64_t L, uint32_t n, uint32_t flag
     g->cols_orig = g->cols;
   }
   CBFS_CUDA(cudaFreeAsync(dk, st));
+  if (uk) CBFS_CUDA(cudaFreeAsync(uk, st));
   CBFS_CUDA(cudaMemcpyAsync(&g->max_degree, d_max, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   CBFS_CUDA(cudaFreeAsync(d_max, st));
   // pull chunk table
   g->n_chunks = (g->m + PULL_CHUNK - 1) / PULL_CHUNK;
-  CBFS_CUDA(cudaMalloc(&g->chunk_v, sizeof(uint32_t) * (g->n_chunks ? g->n_chunks : 1)));
+  CBFS_CUDA(cudaMallocAsync(&g->chunk_v, sizeof(uint32_t) * (g->n_chunks ? g->n_chunks : 1), st));
   if (g->n_chunks) {
     k_chunk_table<<<grid_for(n, 256), 256, 0, st>>>(g->off, n, g->chunk_v);
     CBFS_LAUNCHED();
@@ -310,6 +327,7 @@ int cbfs_graph_create(uint32_t n, const uint32_t* src, const uint32_t* dst, uint
   if (n_pairs && (!src || !dst)) return fail(CBFS_EINVAL, "null edge arrays");
   if (n > CBFS_MAX_N) return fail(CBFS_EUNSUPPORTED, "n exceeds CBFS_MAX_N");
   CBFS_CUDA(cudaSetDevice(device));
+  keep_pool(device);
   cudaStream_t st = (cudaStream_t)stream;
   const uint32_t *ds = src, *dd = dst;
   uint32_t *tmp_s = nullptr, *tmp_d = nullptr;
@@ -350,6 +368,7 @@ int cbfs_graph_create_csr(uint32_t n, const uint64_t* offsets, const uint32_t* c
   *out = nullptr;
   if (n > CBFS_MAX_N) return fail(CBFS_EUNSUPPORTED, "n exceeds CBFS_MAX_N");
   CBFS_CUDA(cudaSetDevice(device));
+  keep_pool(device);
   cudaStream_t st = (cudaStream_t)stream;
   const uint64_t* doff = offsets;
   const uint32_t* dcols = cols;

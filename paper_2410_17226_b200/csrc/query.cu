@@ -164,8 +164,8 @@ int cbfs_query_stream(cbfs_graph* gh, const uint32_t* sources, const uint8_t* si
   if (q && (!s || !t || !inout_best)) return fail(CBFS_EINVAL, "null query arrays");
   CBFS_CUDA(cudaSetDevice(g->device));
   cudaStream_t st = (cudaStream_t)stream;
-  rc = ensure_work(g);
-  if (rc) return rc;
+  WorkLease lease(g);
+  if (lease.rc) return lease.rc;
   const uint32_t n = g->n;
   const uint32_t planes = d + 1;
   uint16_t* bdist = nullptr;
@@ -211,8 +211,8 @@ int cbfs_run_host(cbfs_graph* gh, const uint32_t* sources, const uint8_t* sizes,
   if (rc) return rc;
   CBFS_CUDA(cudaSetDevice(g->device));
   cudaStream_t st = (cudaStream_t)stream;
-  rc = ensure_work(g);
-  if (rc) return rc;
+  WorkLease lease(g);
+  if (lease.rc) return lease.rc;
   const uint32_t n = g->n;
   const uint64_t C = n_clusters;
   uint32_t* dsrc = nullptr;
@@ -270,15 +270,15 @@ int cbfs_run_host(cbfs_graph* gh, const uint32_t* sources, const uint8_t* sizes,
     CBFS_CUDA(cudaMemcpyAsync(out_stats, dstats, sizeof(uint64_t) * 4 * C, cudaMemcpyDeviceToHost, st));
   CBFS_CUDA(cudaStreamSynchronize(st));
   for (int b = 0; b < 2; ++b) {
-    if (sd[b]) cudaFree(sd[b]);
-    if (sm[b]) cudaFree(sm[b]);
+    if (sd[b]) cudaFreeAsync(sd[b], st);
+    if (sm[b]) cudaFreeAsync(sm[b], st);
     cudaEventDestroy(done[b]);
     cudaEventDestroy(copied[b]);
   }
   cudaStreamDestroy(cp);
-  cudaFree(dsrc);
-  cudaFree(dsz);
-  cudaFree(dstats);
+  cudaFreeAsync(dsrc, st);
+  cudaFreeAsync(dsz, st);
+  cudaFreeAsync(dstats, st);
   return rc;
 }
 
