@@ -188,8 +188,9 @@ int cbfs_query_stream(cbfs_graph* g, const uint32_t* sources, const uint8_t* siz
                       cbfs_stream stream);
 
 /* --------------------------------------------------------------- misc */
-/* Direction switch: pull when the frontier's arc count exceeds m / alpha
- * (start 20; tunable, parity-neutral R8). */
+/* Direction switch: pull when the frontier's (cluster, arc) pair count
+ * exceeds batch_clusters * m / alpha (default 100; S:186 suggests 20 for a
+ * single source; tunable, parity-neutral R8). */
 int cbfs_set_direction_alpha(double alpha);
 /* Kernel-level timing of the C-BFS engine (process-wide, not thread-safe):
  * when enabled, CUDA events are recorded on the launching stream around every

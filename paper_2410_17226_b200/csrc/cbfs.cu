@@ -47,7 +47,7 @@ struct Work {
   size_t scan_bytes = 0;
 };
 
-static double g_alpha = 20.0;
+static double g_alpha = 100.0;
 
 // ---- optional per-kernel timing (cbfs_profile_*): CUDA events recorded on
 // the launching stream around each fold / push / pull launch; read after the
@@ -85,7 +85,7 @@ static int work_grow(Work* w, uint32_t n) {
   work_release_buffers(w);
   w->cap = cap;
   const uint64_t ubw = 2 * (((uint64_t)cap / LANES >> 5) + 1);
-  CBFS_CUDA(cudaMalloc(&w->seen, cap * sizeof(uint64_t)));
+  CBFS_CUDA(cudaMalloc(&w->seen, (cap + LANES) * sizeof(uint64_t)));  // + all-zero row n
   CBFS_CUDA(cudaMalloc(&w->pend, cap * sizeof(uint64_t)));
   CBFS_CUDA(cudaMalloc(&w->dist, cap * sizeof(uint16_t)));
   CBFS_CUDA(cudaMalloc(&w->listA, cap * sizeof(uint32_t)));
@@ -361,8 +361,27 @@ __global__ void __launch_bounds__(256) k_push(const uint64_t* __restrict__ off, 
 //       (no per-arc vertex bookkeeping), with the R7 full-subset early exit,
 //       and decides the vertex's claims;
 //   (5) the group's claims are appended with one atomic.
-constexpr int PULL_MLP = 8;
-constexpr int PULL_WARPS = 8;  // warps per block
+#ifndef CBFS_PULL_MLP
+#define CBFS_PULL_MLP 8
+#endif
+#ifndef CBFS_PULL_MINB
+#define CBFS_PULL_MINB 8
+#endif
+constexpr int PULL_MLP = CBFS_PULL_MLP;  // neighbour rows in flight per warp
+#ifndef CBFS_PULL_WARPS
+#define CBFS_PULL_WARPS 4
+#endif
+constexpr int PULL_WARPS = CBFS_PULL_WARPS;  // warps per block
+
+#ifdef CBFS_PULL_STATS
+__device__ unsigned long long g_dbg[8];
+extern "C" int cbfs_debug_read(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, g_dbg, sizeof(g_dbg));
+  unsigned long long z[8] = {0};
+  cudaMemcpyToSymbol(g_dbg, z, sizeof(z));
+  return 0;
+}
+#endif
 
 struct U2 {
   uint64_t a, b;
@@ -372,14 +391,15 @@ __device__ __forceinline__ U2 ld2(const uint64_t* p) {
   return {x.x, x.y};
 }
 
-__global__ void __launch_bounds__(PULL_WARPS * 32, 3) k_pull(
+__global__ void __launch_bounds__(PULL_WARPS * 32, CBFS_PULL_MINB) k_pull(
     const uint64_t* __restrict__ off, const uint32_t* __restrict__ cols, const uint32_t* __restrict__ chunk_v,
     uint64_t n_chunks, uint64_t m, uint32_t n, const uint64_t* __restrict__ seen, const uint16_t* __restrict__ dist,
     uint64_t* __restrict__ pend, const uint32_t* __restrict__ ubits, uint32_t* __restrict__ ubits_next,
     const uint8_t* __restrict__ sizes, uint32_t nb, uint32_t* __restrict__ out_list, uint64_t* __restrict__ bstats,
     unsigned long long* __restrict__ ctr, uint32_t i, uint32_t d) {
-  __shared__ uint32_t s_list[PULL_WARPS][PULL_CHUNK];
+  __shared__ uint32_t s_list[PULL_WARPS][PULL_CHUNK + 32];
   __shared__ uint32_t s_cnt[PULL_WARPS][32];
+  __shared__ unsigned long long s_stat[PULL_WARPS][3][LANES];  // per-warp F / E / M per cluster
   const uint32_t lane = lane_id();
   const uint32_t wib = threadIdx.x >> 5;
   uint32_t* list = s_list[wib];
@@ -390,7 +410,9 @@ __global__ void __launch_bounds__(PULL_WARPS * 32, 3) k_pull(
   const uint64_t full0 = c0 < nb ? full_mask(sizes[c0]) : 0ULL;
   const uint64_t full1 = c1 < nb ? full_mask(sizes[c1]) : 0ULL;
   const unsigned lt = (1u << lane) - 1;
-  unsigned long long aF0 = 0, aE0 = 0, aM0 = 0, aF1 = 0, aE1 = 0, aM1 = 0, degsum = 0;
+  unsigned long long degsum = 0;
+  unsigned long long(*stat)[LANES] = s_stat[wib];
+  stat[0][c0] = stat[0][c1] = stat[1][c0] = stat[1][c1] = stat[2][c0] = stat[2][c1] = 0;
   const uint64_t* seen2 = seen + 2 * lane;  // lane's word pair of row 0
   const uint32_t* dist2 = reinterpret_cast<const uint32_t*>(dist) + lane;
 
@@ -439,7 +461,8 @@ __global__ void __launch_bounds__(PULL_WARPS * 32, 3) k_pull(
         }
       }
       if (actv) {
-        // ---- (3) pass A: compact useful neighbours, sorted by vertex
+        // ---- (3) pass A: compact useful neighbours as (vertex << 27 | u),
+        // sorted by vertex, and count them per vertex
         cnt[lane] = 0;
         __syncwarp();
         uint32_t nl = 0;
@@ -456,50 +479,56 @@ __global__ void __launch_bounds__(PULL_WARPS * 32, 3) k_pull(
           }
           const bool want = inr && ((actv >> jv) & 1u) && ((__ldg(&ubits[u >> 5]) >> (u & 31)) & 1u);
           const unsigned fm = __ballot_sync(FULLW, want);
-          if (want) list[nl + __popc(fm & lt)] = u;
+          if (want) list[nl + __popc(fm & lt)] = (jv << 27) | u;
           const unsigned grp = __match_any_sync(FULLW, want ? jv : 0xFFFFFFFFu);
           if (want && lane == (uint32_t)(__ffs(grp) - 1)) cnt[jv] += __popc(grp);
           nl += __popc(fm);
           __syncwarp();
         }
-        // per-vertex segment starts (exclusive scan of counts, lane = vertex)
+#ifdef CBFS_PULL_STATS
+        if (lane == 0) { atomicAdd(&g_dbg[0], 1ULL); atomicAdd(&g_dbg[1], (unsigned long long)__popc(actv));
+                         atomicAdd(&g_dbg[2], (unsigned long long)nl); atomicAdd(&g_dbg[3], (unsigned long long)(ge - e)); }
+#endif
         const uint32_t myc = cnt[lane];
-        uint32_t incl = myc;
+        uint32_t incl = myc;  // per-vertex segment ends (inclusive scan, lane = vertex)
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const uint32_t y = __shfl_up_sync(FULLW, incl, o);
           if (lane >= (uint32_t)o) incl += y;
         }
-        const uint32_t seg0 = incl - myc;
-        // ---- (4) pass B: gather per active vertex, decide claims
+        __syncwarp();
+        // ---- (4) pass B: per active vertex, gather its segment PULL_MLP rows
+        // at a time into a register accumulator, checking the R7 full-subset
+        // exit every batch, then decide the vertex's claims
         unsigned myb0 = 0, myb1 = 0;  // lane j: claim ballots of vertex j
         unsigned rem = actv;
         while (rem) {
           const uint32_t j = __ffs(rem) - 1;
           rem &= rem - 1;
-          const uint32_t s0 = __shfl_sync(FULLW, seg0, j);
-          const uint32_t sn = __shfl_sync(FULLW, myc, j);
+          const uint32_t s1 = __shfl_sync(FULLW, incl, j);
+          const uint32_t s0 = s1 - __shfl_sync(FULLW, myc, j);
           const uint64_t row = (uint64_t)(v + j) * LANES;
           const U2 sv = ld2(seen2 + row);
           const bool k0 = (cap0 >> j) & 1u, k1 = (cap1 >> j) & 1u;
           uint64_t acc0 = 0, acc1 = 0;
-          for (uint32_t q0 = 0; q0 < sn; q0 += 32) {
-            const uint32_t qe = min(q0 + 32, sn);
-            uint32_t q = q0;
-            for (; q + PULL_MLP <= qe; q += PULL_MLP) {
-              U2 g[PULL_MLP];
+          for (uint32_t q = s0; q < s1; q += PULL_MLP) {
+            U2 g[PULL_MLP];
 #pragma unroll
-              for (int r = 0; r < PULL_MLP; ++r) g[r] = ld2(seen2 + (uint64_t)list[s0 + q + r] * LANES);
+            for (int r = 0; r < PULL_MLP; ++r) {
+              const uint32_t x = q + r < s1 ? list[q + r] : n;  // past the segment: the zero row
+              g[r] = ld2(seen2 + (uint64_t)(x & 0x7FFFFFFu) * LANES);
+            }
 #pragma unroll
-              for (int r = 0; r < PULL_MLP; ++r) { acc0 |= g[r].a; acc1 |= g[r].b; }
-            }
-            for (; q < qe; ++q) {
-              const U2 g = ld2(seen2 + (uint64_t)list[s0 + q] * LANES);
-              acc0 |= g.a;
-              acc1 |= g.b;
-            }
+            for (int r = 0; r < PULL_MLP; ++r) { acc0 |= g[r].a; acc1 |= g[r].b; }
             // R7: stop once every capped lane holds its full subset
-            if (!__ballot_sync(FULLW, (k0 && ((acc0 | sv.a) != full0)) || (k1 && ((acc1 | sv.b) != full1)))) break;
+            if (q + PULL_MLP < s1 &&
+                !__ballot_sync(FULLW, (k0 && ((acc0 | sv.a) & full0) != full0) ||
+                                          (k1 && ((acc1 | sv.b) & full1) != full1))) {
+#ifdef CBFS_PULL_STATS
+              if (lane == 0) { atomicAdd(&g_dbg[4], 1ULL); atomicAdd(&g_dbg[5], (unsigned long long)(s1 - q - PULL_MLP)); }
+#endif
+              break;
+            }
           }
           const uint64_t nw0 = k0 ? (acc0 & ~sv.a) : 0, nw1 = k1 ? (acc1 & ~sv.b) : 0;
           bool cl0 = false, cl1 = false;
@@ -515,8 +544,8 @@ __global__ void __launch_bounds__(PULL_WARPS * 32, 3) k_pull(
               if (nw1) cl1 = atomicOr((unsigned long long*)(pp + 1), (unsigned long long)nw1) == 0;
             }
             const unsigned long long deg = oe_j - ob_j;
-            if (cl0) { aF0 += 1; aE0 += deg; if ((inf0 >> j) & 1u) aM0 += deg; degsum += deg; }
-            if (cl1) { aF1 += 1; aE1 += deg; if ((inf1 >> j) & 1u) aM1 += deg; degsum += deg; }
+            if (cl0) { stat[0][c0] += 1; stat[1][c0] += deg; if ((inf0 >> j) & 1u) stat[2][c0] += deg; degsum += deg; }
+            if (cl1) { stat[0][c1] += 1; stat[1][c1] += deg; if ((inf1 >> j) & 1u) stat[2][c1] += deg; degsum += deg; }
           }
           const unsigned b0 = __ballot_sync(FULLW, cl0), b1 = __ballot_sync(FULLW, cl1);
           if (lane == j) { myb0 = b0; myb1 = b1; }
@@ -557,8 +586,8 @@ __global__ void __launch_bounds__(PULL_WARPS * 32, 3) k_pull(
   }
   degsum = warp_sum(degsum);
   if (lane == 0 && degsum) atomicAdd(&ctr[1], degsum);
-  stats_flush(bstats, c0, aF0, aE0, aM0, i + 2);
-  stats_flush(bstats, c1, aF1, aE1, aM1, i + 2);
+  stats_flush(bstats, c0, stat[0][c0], stat[1][c0], stat[2][c0], i + 2);
+  stats_flush(bstats, c1, stat[0][c1], stat[1][c1], stat[2][c1], i + 2);
 }
 
 __global__ void k_set_u64(uint64_t* p, uint64_t v) { *p = v; }
@@ -574,7 +603,7 @@ int run_batch(Graph* g, const RunArgs& a, cudaStream_t st) {
   Work* w = g->work;
   const uint32_t n = g->n;
   const uint64_t ub_words = (n >> 5) + 1;
-  CBFS_CUDA(cudaMemsetAsync(w->seen, 0, (uint64_t)n * LANES * sizeof(uint64_t), st));
+  CBFS_CUDA(cudaMemsetAsync(w->seen, 0, (uint64_t)(n + 1) * LANES * sizeof(uint64_t), st));
   CBFS_CUDA(cudaMemsetAsync(w->dist, 0xFF, (uint64_t)n * LANES * sizeof(uint16_t), st));
   CBFS_CUDA(cudaMemsetAsync(w->bstats, 0, LANES * 4 * sizeof(uint64_t), st));
   CBFS_CUDA(cudaMemsetAsync(w->ctr, 0, 3 * sizeof(unsigned long long), st));

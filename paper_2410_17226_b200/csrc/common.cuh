@@ -57,7 +57,10 @@ struct Graph {
   struct Work* work = nullptr;
 };
 
-constexpr uint32_t PULL_CHUNK = 256;  // arcs per warp in the dense pull kernel
+#ifndef CBFS_PULL_CHUNK
+#define CBFS_PULL_CHUNK 256
+#endif
+constexpr uint32_t PULL_CHUNK = CBFS_PULL_CHUNK;  // arcs per warp task in the dense pull kernel
 
 int graph_free(Graph* g);
 

@@ -29,6 +29,7 @@ def step(parts):
     torch.cuda.synchronize(); t["destroy"] = time.perf_counter() - t0
     return t
 
+if os.environ.get("ALPHA"): cb.cbfs_set_direction_alpha(float(os.environ["ALPHA"]))
 for it in range(3):
     step(None)
 for prof in (False, True, False):
