@@ -45,6 +45,9 @@ METRIC = "C-BFS source-edges/sec (GTEPS x sources)"
 UNIT = "source-edges/s"
 BYTES_PER_FRONTIER_ARC = 22     # 4 B column + 2 B Delta cap read + 16 B OR-update
 BYTES_PER_FRONTIER_ENTRY = 40   # offsets, frontier id w/r, next read, seen RMW
+BYTES_PER_ARC = 4                # batched pull: one u32 CSR column per arc per launch
+BYTES_PER_VROW = 64 * 2 + 64 * 8  # batched pull: a vertex's Delta row + S_seen row (64 clusters)
+BYTES_PER_ROW = 64 * 8           # batched pull: one 64-cluster bit-subset row
 
 
 def log(*a):
@@ -304,6 +307,7 @@ def run_ours(args, world, rank, local):
     n_h, m_h, maxdeg = None, None, None
     hh = cb.cbfs_graph_create(n, src_d, dst_d, 0, local, stream)
     n_h, m_h, maxdeg = cb.cbfs_graph_info(hh)
+    n_ni = cb.cbfs_graph_nonisolated(hh)
     cb.cbfs_graph_destroy(hh)
     units_wholegraph = float(sizes.sum()) * m_h
 
@@ -315,25 +319,34 @@ def run_ours(args, world, rank, local):
     peak, peak_src = peaks()
     dom = max(prof, key=lambda kk: prof[kk]["ms"])
     pk = prof[dom]
-    if dom == "fold":
+    if dom == "pull":
+        # compulsory HBM bytes of one batched pull launch: every CSR column once,
+        # every non-isolated vertex's state row (64 x u16 Delta + 64 x u64 S_seen), every distinct
+        # frontier row once, every claimed row written once
+        alg_bytes = (pk["launches"] * (BYTES_PER_ARC * m_h + BYTES_PER_VROW * n_ni)
+                     + BYTES_PER_ROW * (pk["u_in"] + pk["u_out"]))
+        model = (f"{BYTES_PER_ARC} B per CSR arc + {BYTES_PER_VROW} B per non-isolated vertex row + "
+                 f"{BYTES_PER_ROW} B per distinct frontier row read and per claimed row written")
+    elif dom == "fold":
         alg_bytes = BYTES_PER_FRONTIER_ENTRY * pk["entries"]
+        model = f"{BYTES_PER_FRONTIER_ENTRY} B per frontier (vertex, cluster) entry (SURVEY §8(d))"
     else:
         alg_bytes = BYTES_PER_FRONTIER_ARC * pk["arcs"]
+        model = f"{BYTES_PER_FRONTIER_ARC} B per frontier (cluster, arc) pair (SURVEY §8(d))"
     achieved = alg_bytes / (pk["ms"] / 1000.0) / 1e9 if pk["ms"] > 0 else 0.0
     traffic = None
     ncu_json = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(ncu_json):
         try:
-            traffic = json.load(open(ncu_json)).get("traffic_per_launch", {}).get(dom)
+            traffic = json.load(open(ncu_json)).get("traffic_per_launch", {}).get(f"k_{dom}")
         except Exception:
             traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": f"k_{dom}", "launches": pk["launches"],
                 "avg_launch_ms": pk["ms"] / max(1, pk["launches"]),
-                "alg_bytes_per_launch": alg_bytes / max(1, pk["launches"]),
-                "model": (f"{BYTES_PER_FRONTIER_ARC} B per frontier (entry, arc) pair" if dom != "fold" else
-                          f"{BYTES_PER_FRONTIER_ENTRY} B per frontier entry") + " (SURVEY §8(d))",
-                "peak_source": peak_src, "kernels": prof}
+                "alg_bytes_per_launch": alg_bytes / max(1, pk["launches"]), "model": model,
+                "peak_source": peak_src, "kernels": prof,
+                "share_of_cbfs_time": pk["ms"] / max(1e-9, sum(v["ms"] for v in prof.values()))}
 
     # ---- end to end through the public API with host buffers (rank-local)
     e2e = None
@@ -398,7 +411,7 @@ def run_ours(args, world, rank, local):
                        "phase_ms_rank0": {kk: round(v, 3) for kk, v in phase_ms.items()},
                        "cbfs_only_value": units_step / (phase_ms["cbfs"] / 1000.0) if phase_ms["cbfs"] else None,
                        "direction": ["auto", "push", "pull"][args.direction],
-                       "alpha": args.alpha or 20.0},
+                       "alpha": args.alpha or 100.0},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk,
         }

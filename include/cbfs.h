@@ -196,10 +196,15 @@ int cbfs_set_direction_alpha(double alpha);
  * when enabled, CUDA events are recorded on the launching stream around every
  * fold / push / pull launch and read after the round's synchronisation.
  * cbfs_profile_read fills arrays of 3 entries indexed {0 fold, 1 push,
- * 2 pull}: total device ms, launches, frontier (entry, arc) pairs and
- * frontier entries processed (host pointers, any may be NULL). */
+ * 2 pull}: total device ms, launches, frontier (cluster, arc) pairs,
+ * frontier (vertex, cluster) entries, distinct frontier vertices |U_i| and
+ * distinct vertices claimed for the next frontier |U_{i+1}| summed over the
+ * launches (host pointers, any may be NULL). */
 int cbfs_profile_enable(int on);
-int cbfs_profile_read(double* ms, uint64_t* launches, uint64_t* arcs, uint64_t* entries, int reset);
+int cbfs_profile_read(double* ms, uint64_t* launches, uint64_t* arcs, uint64_t* entries, uint64_t* u_in,
+                      uint64_t* u_out, int reset);
+/* Number of vertices with at least one arc. */
+int cbfs_graph_nonisolated(const cbfs_graph* g, uint32_t* count);
 /* Number of kernels this library launched on this thread since the last reset. */
 uint64_t cbfs_launch_count(int reset);
 const char* cbfs_last_error(void);

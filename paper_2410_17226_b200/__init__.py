@@ -55,7 +55,8 @@ _sig("cbfs_query_distance", [_u32, _u32, _u32, _u32, _vp, _u32, _vp, _vp, _vp, _
 _sig("cbfs_query_stream", [_vp, _vp, _vp, _u32, _u32, _vp, _vp, _u64, _vp, _vp, _vp])
 _sig("cbfs_set_direction_alpha", [ctypes.c_double])
 _sig("cbfs_profile_enable", [_i32])
-_sig("cbfs_profile_read", [_vp, _vp, _vp, _vp, _i32])
+_sig("cbfs_profile_read", [_vp, _vp, _vp, _vp, _vp, _vp, _i32])
+_sig("cbfs_graph_nonisolated", [_vp, ctypes.POINTER(_u32)])
 _sig("cbfs_launch_count", [_i32], _u64)
 _sig("cbfs_last_error", [], ctypes.c_char_p)
 _sig("cbfs_version", [], ctypes.c_char_p)
@@ -173,11 +174,18 @@ def cbfs_profile_enable(on: bool = True):
 
 
 def cbfs_profile_read(reset: bool = False) -> dict:
-    ms = np.zeros(3, np.float64); la = np.zeros(3, np.uint64); arcs = np.zeros(3, np.uint64)
-    ent = np.zeros(3, np.uint64)
-    _check(_lib.cbfs_profile_read(_ptr(ms), _ptr(la), _ptr(arcs), _ptr(ent), int(reset)))
-    return {name: dict(ms=float(ms[i]), launches=int(la[i]), arcs=int(arcs[i]), entries=int(ent[i]))
+    ms = np.zeros(3, np.float64)
+    la, arcs, ent, ui, uo = (np.zeros(3, np.uint64) for _ in range(5))
+    _check(_lib.cbfs_profile_read(_ptr(ms), _ptr(la), _ptr(arcs), _ptr(ent), _ptr(ui), _ptr(uo), int(reset)))
+    return {name: dict(ms=float(ms[i]), launches=int(la[i]), arcs=int(arcs[i]), entries=int(ent[i]),
+                       u_in=int(ui[i]), u_out=int(uo[i]))
             for i, name in enumerate(("fold", "push", "pull"))}
+
+
+def cbfs_graph_nonisolated(h) -> int:
+    c = _u32()
+    _check(_lib.cbfs_graph_nonisolated(h, ctypes.byref(c)))
+    return c.value
 
 
 def cbfs_launch_count(reset: bool = False) -> int:

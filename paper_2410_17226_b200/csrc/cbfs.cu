@@ -40,7 +40,7 @@ struct Work {
   uint32_t* listB = nullptr;
   uint64_t* pre = nullptr;              // [cap + 1] degrees -> exclusive prefix (push)
   uint32_t* ubits = nullptr;            // 2 x [n/32 + 1]: union frontier U_i, U_{i+1}
-  unsigned long long* ctr = nullptr;    // [0] next count, [1] next E, [2] error bits
+  unsigned long long* ctr = nullptr;    // [0] next count, [1] next E, [2] error bits, [3] |U_next|
   unsigned long long* h_ctr = nullptr;  // pinned mirror
   uint64_t* bstats = nullptr;           // [LANES][4]
   void* scan_tmp = nullptr;
@@ -59,6 +59,8 @@ struct Prof {
   uint64_t launches[PK_N] = {0, 0, 0, 0};
   uint64_t arcs[PK_N] = {0, 0, 0, 0};     // frontier (entry, arc) pairs processed
   uint64_t entries[PK_N] = {0, 0, 0, 0};  // frontier entries processed
+  uint64_t u_in[PK_N] = {0, 0, 0, 0};     // distinct frontier vertices |U_i|
+  uint64_t u_out[PK_N] = {0, 0, 0, 0};    // distinct claimed vertices |U_{i+1}|
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 };
 static Prof g_prof;
@@ -145,11 +147,13 @@ __device__ __forceinline__ unsigned long long warp_sum(unsigned long long x) {
 }
 
 // union-frontier bit of vertex v, one atomic per distinct word in the warp
-__device__ __forceinline__ void warp_set_bit(bool flag, uint32_t v, uint32_t* __restrict__ bits) {
+// returns the number of bits this lane newly set (distinct vertices added)
+__device__ __forceinline__ uint32_t warp_set_bit(bool flag, uint32_t v, uint32_t* __restrict__ bits) {
   const uint32_t word = flag ? (v >> 5) : 0xFFFFFFFFu;
   const unsigned grp = __match_any_sync(FULLW, word);
   const unsigned b = __reduce_or_sync(grp, flag ? (1u << (v & 31)) : 0u);
-  if (flag && lane_id() == (uint32_t)(__ffs(grp) - 1)) atomicOr(&bits[word], b);
+  if (flag && lane_id() == (uint32_t)(__ffs(grp) - 1)) return __popc(b & ~atomicOr(&bits[word], b));
+  return 0;
 }
 
 // ------------------------------------------------------------------ stats
@@ -202,9 +206,11 @@ __global__ void k_seed(const uint32_t* __restrict__ sources, const uint8_t* __re
     }
   }
   warp_append(claim, e, list, &ctr[0]);
-  warp_set_bit(claim, x, ubits0);
+  unsigned long long nu = warp_set_bit(claim, x, ubits0);
   deg = warp_sum(claim ? deg : 0);
+  nu = warp_sum(nu);
   if (lane_id() == 0 && deg) atomicAdd(&ctr[1], deg);
+  if (lane_id() == 0 && nu) atomicAdd(&ctr[3], nu);
 }
 
 // ------------------------------------------------------------------ fold
@@ -288,7 +294,7 @@ __global__ void __launch_bounds__(256) k_push(const uint64_t* __restrict__ off, 
   const uint32_t lane = lane_id();
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
-  unsigned long long degsum = 0;
+  unsigned long long degsum = 0, nu = 0;
   for (uint64_t w = warp; w * PUSH_CHUNK < total; w += nwarps) {
     const uint64_t start = w * PUSH_CHUNK;
     const uint64_t end = min(start + PUSH_CHUNK, total);
@@ -329,11 +335,13 @@ __global__ void __launch_bounds__(256) k_push(const uint64_t* __restrict__ off, 
         }
       }
       warp_append(claim, ev, out_list, &ctr[0]);
-      warp_set_bit(claim, v, ubits_next);
+      nu += warp_set_bit(claim, v, ubits_next);
     }
   }
   degsum = warp_sum(degsum);
+  nu = warp_sum(nu);
   if (lane == 0 && degsum) atomicAdd(&ctr[1], degsum);
+  if (lane == 0 && nu) atomicAdd(&ctr[3], nu);
   __syncthreads();
   for (uint32_t c = threadIdx.x; c < LANES; c += blockDim.x) stats_flush(bstats, c, sF[c], sE[c], sM[c], i + 2);
 }
@@ -410,7 +418,7 @@ __global__ void __launch_bounds__(PULL_WARPS * 32, CBFS_PULL_MINB) k_pull(
   const uint64_t full0 = c0 < nb ? full_mask(sizes[c0]) : 0ULL;
   const uint64_t full1 = c1 < nb ? full_mask(sizes[c1]) : 0ULL;
   const unsigned lt = (1u << lane) - 1;
-  unsigned long long degsum = 0;
+  unsigned long long degsum = 0, nu = 0;
   unsigned long long(*stat)[LANES] = s_stat[wib];
   stat[0][c0] = stat[0][c1] = stat[1][c0] = stat[1][c1] = stat[2][c0] = stat[2][c1] = 0;
   const uint64_t* seen2 = seen + 2 * lane;  // lane's word pair of row 0
@@ -577,7 +585,7 @@ __global__ void __launch_bounds__(PULL_WARPS * 32, CBFS_PULL_MINB) k_pull(
             if (h1) out_list[base + r + h0] = ebase + 1;
           }
         }
-        warp_set_bit(ccount != 0, v + lane, ubits_next);
+        nu += warp_set_bit(ccount != 0, v + lane, ubits_next);
         __syncwarp();
       }
       e = ge;
@@ -585,7 +593,9 @@ __global__ void __launch_bounds__(PULL_WARPS * 32, CBFS_PULL_MINB) k_pull(
     }
   }
   degsum = warp_sum(degsum);
+  nu = warp_sum(nu);
   if (lane == 0 && degsum) atomicAdd(&ctr[1], degsum);
+  if (lane == 0 && nu) atomicAdd(&ctr[3], nu);
   stats_flush(bstats, c0, stat[0][c0], stat[1][c0], stat[2][c0], i + 2);
   stats_flush(bstats, c1, stat[0][c1], stat[1][c1], stat[2][c1], i + 2);
 }
@@ -594,7 +604,7 @@ __global__ void k_set_u64(uint64_t* p, uint64_t v) { *p = v; }
 
 // ------------------------------------------------------------------ driver
 static int sync_ctr(Work* w, cudaStream_t st) {
-  CBFS_CUDA(cudaMemcpyAsync(w->h_ctr, w->ctr, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  CBFS_CUDA(cudaMemcpyAsync(w->h_ctr, w->ctr, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   CBFS_CUDA(cudaStreamSynchronize(st));
   return CBFS_OK;
 }
@@ -606,7 +616,7 @@ int run_batch(Graph* g, const RunArgs& a, cudaStream_t st) {
   CBFS_CUDA(cudaMemsetAsync(w->seen, 0, (uint64_t)(n + 1) * LANES * sizeof(uint64_t), st));
   CBFS_CUDA(cudaMemsetAsync(w->dist, 0xFF, (uint64_t)n * LANES * sizeof(uint16_t), st));
   CBFS_CUDA(cudaMemsetAsync(w->bstats, 0, LANES * 4 * sizeof(uint64_t), st));
-  CBFS_CUDA(cudaMemsetAsync(w->ctr, 0, 3 * sizeof(unsigned long long), st));
+  CBFS_CUDA(cudaMemsetAsync(w->ctr, 0, 4 * sizeof(unsigned long long), st));
   k_seed<<<(a.nb * 64 + 255) / 256, 256, 0, st>>>(a.sources, a.sizes, a.nb, n, g->inv, g->off, w->pend, w->listA,
                                                    w->ubits, w->bstats, w->ctr);
   CBFS_LAUNCHED();
@@ -621,7 +631,7 @@ int run_batch(Graph* g, const RunArgs& a, cudaStream_t st) {
     if (w->h_ctr[2] & ERR_BAD_SOURCE) return fail(CBFS_EINVAL, "source id >= n");
     return fail(CBFS_EINVAL, "duplicate source in a cluster");
   }
-  uint64_t nF = w->h_ctr[0], E = w->h_ctr[1];
+  uint64_t nF = w->h_ctr[0], E = w->h_ctr[1], U = w->h_ctr[3];
   uint32_t* cur = w->listA;
   uint32_t* nxt = w->listB;
   bool overflow = false;
@@ -643,6 +653,7 @@ int run_batch(Graph* g, const RunArgs& a, cudaStream_t st) {
     CBFS_LAUNCHED();
     if (g_prof.on) CBFS_CUDA(cudaEventRecord(g_prof.ev[1], st));
     CBFS_CUDA(cudaMemsetAsync(w->ctr, 0, 2 * sizeof(unsigned long long), st));
+    CBFS_CUDA(cudaMemsetAsync(w->ctr + 3, 0, sizeof(unsigned long long), st));
     int kind = -1;
     if (pull) {
       kind = PK_PULL;
@@ -676,11 +687,13 @@ int run_batch(Graph* g, const RunArgs& a, cudaStream_t st) {
       if (kind >= 0) {
         CBFS_CUDA(cudaEventElapsedTime(&ms, g_prof.ev[2], g_prof.ev[3]));
         g_prof.ms[kind] += ms; g_prof.launches[kind] += 1; g_prof.entries[kind] += nF; g_prof.arcs[kind] += E;
+        g_prof.u_in[kind] += U; g_prof.u_out[kind] += w->h_ctr[3];
       }
     }
     if (w->h_ctr[2] & ERR_OVERFLOW) overflow = true;
     nF = w->h_ctr[0];
     E = w->h_ctr[1];
+    U = w->h_ctr[3];
     std::swap(cur, nxt);
   }
   if (a.out_stats)
@@ -748,15 +761,19 @@ int cbfs_profile_enable(int on) {
   return CBFS_OK;
 }
 
-int cbfs_profile_read(double* ms, uint64_t* launches, uint64_t* arcs, uint64_t* entries, int reset) {
+int cbfs_profile_read(double* ms, uint64_t* launches, uint64_t* arcs, uint64_t* entries, uint64_t* u_in,
+                      uint64_t* u_out, int reset) {
   for (int k = 0; k < 3; ++k) {
     if (ms) ms[k] = g_prof.ms[k];
     if (launches) launches[k] = g_prof.launches[k];
     if (arcs) arcs[k] = g_prof.arcs[k];
     if (entries) entries[k] = g_prof.entries[k];
+    if (u_in) u_in[k] = g_prof.u_in[k];
+    if (u_out) u_out[k] = g_prof.u_out[k];
   }
   if (reset)
-    for (int k = 0; k < PK_N; ++k) g_prof.ms[k] = 0, g_prof.launches[k] = g_prof.arcs[k] = g_prof.entries[k] = 0;
+    for (int k = 0; k < PK_N; ++k)
+      g_prof.ms[k] = 0, g_prof.launches[k] = g_prof.arcs[k] = g_prof.entries[k] = g_prof.u_in[k] = g_prof.u_out[k] = 0;
   return CBFS_OK;
 }
 

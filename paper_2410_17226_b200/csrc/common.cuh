@@ -39,6 +39,7 @@ struct Graph {
   uint32_t n = 0;
   uint64_t m = 0;            // arcs
   uint32_t max_degree = 0;
+  uint32_t n_nonisolated = 0;
   bool relabeled = false;
   // internal CSR (internal ids; == original ids unless relabeled)
   uint64_t* off = nullptr;   // [n+1]

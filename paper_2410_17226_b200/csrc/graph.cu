@@ -105,6 +105,7 @@ __global__ void k_degree_keys(const uint64_t* __restrict__ off, uint32_t n, uint
     uint32_t deg = (uint32_t)(off[v + 1] - off[v]);
     keys[v] = ((uint64_t)(0xFFFFFFFFu - deg) << 32) | v;  // ascending = degree desc, id asc
     atomicMax(maxdeg, deg);
+    if (deg) atomicAdd(maxdeg + 1, 1u);  // non-isolated count
   }
 }
 
@@ -232,8 +233,8 @@ static int build_from_keys(uint64_t* keys, uint64_t L, uint32_t n, uint32_t flag
   uint64_t* dk = nullptr;
   uint32_t* d_max = nullptr;
   CBFS_CUDA(cudaMallocAsync(&dk, sizeof(uint64_t) * (n ? n : 1), st));
-  CBFS_CUDA(cudaMallocAsync(&d_max, sizeof(uint32_t), st));
-  CBFS_CUDA(cudaMemsetAsync(d_max, 0, sizeof(uint32_t), st));
+  CBFS_CUDA(cudaMallocAsync(&d_max, 2 * sizeof(uint32_t), st));
+  CBFS_CUDA(cudaMemsetAsync(d_max, 0, 2 * sizeof(uint32_t), st));
   CBFS_CUDA(cudaMallocAsync(&g->rank, sizeof(uint32_t) * (n ? n : 1), st));
   CBFS_CUDA(cudaMallocAsync(&g->order, sizeof(uint32_t) * (n ? n : 1), st));
   if (n) {
@@ -300,7 +301,11 @@ static int build_from_keys(uint64_t* keys, uint64_t L, uint32_t n, uint32_t flag
   }
   CBFS_CUDA(cudaFreeAsync(dk, st));
   if (uk) CBFS_CUDA(cudaFreeAsync(uk, st));
-  CBFS_CUDA(cudaMemcpyAsync(&g->max_degree, d_max, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  uint32_t hm[2] = {0, 0};
+  CBFS_CUDA(cudaMemcpyAsync(hm, d_max, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  CBFS_CUDA(cudaStreamSynchronize(st));
+  g->max_degree = hm[0];
+  g->n_nonisolated = hm[1];
   CBFS_CUDA(cudaFreeAsync(d_max, st));
   // pull chunk table
   g->n_chunks = (g->m + PULL_CHUNK - 1) / PULL_CHUNK;
@@ -412,6 +417,13 @@ int cbfs_graph_info(const cbfs_graph* gh, uint32_t* n, uint64_t* m, uint32_t* ma
   if (n) *n = g->n;
   if (m) *m = g->m;
   if (max_degree) *max_degree = g->max_degree;
+  return CBFS_OK;
+}
+
+int cbfs_graph_nonisolated(const cbfs_graph* gh, uint32_t* count) {
+  const Graph* g = reinterpret_cast<const Graph*>(gh);
+  if (!g || !count) return fail(CBFS_EINVAL, "null argument");
+  *count = g->n_nonisolated;
   return CBFS_OK;
 }
 
