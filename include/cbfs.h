@@ -144,6 +144,18 @@ int cbfs_run(cbfs_graph* g, const uint32_t* sources, const uint8_t* sizes, uint3
              uint32_t dist_bytes, void* out_dist, uint64_t* out_masks, uint32_t planes, uint64_t* out_stats,
              uint32_t direction, cbfs_stream stream);
 
+/* cbfs_select_and_run — cbfs_select_clusters followed by cbfs_run over the
+ * selected clusters, overlapped: the (sequential) selection runs on a side
+ * stream and publishes each cluster as it is fixed, and each batch of 64
+ * clusters is traversed as soon as its clusters exist.  Same arguments and
+ * outputs as the two calls (out_sources / out_sizes device [r][64] / [r];
+ * outputs use row stride C = r; columns >= *out_r stay unreached).
+ * Synchronises. */
+int cbfs_select_and_run(cbfs_graph* g, uint32_t r, uint32_t k, uint32_t d, uint32_t root_policy, uint64_t seed,
+                        uint32_t* out_sources, uint8_t* out_sizes, uint32_t* out_r, uint32_t dist_bytes,
+                        void* out_dist, uint64_t* out_masks, uint32_t planes, uint64_t* out_stats,
+                        uint32_t direction, cbfs_stream stream);
+
 /* Same computation with HOST buffers (sources, sizes, out_dist, out_masks,
  * out_stats all host memory, pinned recommended): inputs are copied in, each
  * batch of 32 clusters is traversed into device staging and copied out while

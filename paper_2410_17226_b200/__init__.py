@@ -49,6 +49,8 @@ _sig("cbfs_graph_export_csr", [_vp, _vp, _vp])
 _sig("cbfs_graph_destroy", [_vp])
 _sig("cbfs_select_clusters", [_vp, _u32, _u32, _u32, _u32, _u64, _vp, _vp, ctypes.POINTER(_u32), _vp])
 _sig("cbfs_run", [_vp, _vp, _vp, _u32, _u32, _u32, _vp, _vp, _u32, _vp, _u32, _vp])
+_sig("cbfs_select_and_run", [_vp, _u32, _u32, _u32, _u32, _u64, _vp, _vp, ctypes.POINTER(_u32), _u32, _vp, _vp,
+                              _u32, _vp, _u32, _vp])
 _sig("cbfs_run_host", [_vp, _vp, _vp, _u32, _u32, _u32, _vp, _vp, _u32, _vp, _u32, _vp])
 _sig("cbfs_decode", [_u32, _u32, _u32, _u32, _vp, _u32, _vp, _u32, _u32, _vp, _vp])
 _sig("cbfs_query_distance", [_u32, _u32, _u32, _u32, _vp, _u32, _vp, _vp, _vp, _vp, _u64, _vp, _vp])
@@ -143,6 +145,15 @@ def cbfs_run(h, sources, sizes, n_clusters, d, dist_bytes, out_dist, out_masks, 
              direction=CBFS_DIR_AUTO, stream=None):
     _check(_lib.cbfs_run(h, _ptr(sources), _ptr(sizes), n_clusters, d, dist_bytes, _ptr(out_dist), _ptr(out_masks),
                          planes, _ptr(out_stats), direction, _stream(stream)))
+
+
+def cbfs_select_and_run(h, r, k, d, root_policy, seed, out_sources, out_sizes, dist_bytes, out_dist, out_masks,
+                        planes, out_stats=None, direction=CBFS_DIR_AUTO, stream=None) -> int:
+    got = _u32()
+    _check(_lib.cbfs_select_and_run(h, r, k, d, root_policy, seed, _ptr(out_sources), _ptr(out_sizes),
+                                    ctypes.byref(got), dist_bytes, _ptr(out_dist), _ptr(out_masks), planes,
+                                    _ptr(out_stats), direction, _stream(stream)))
+    return got.value
 
 
 def cbfs_run_host(h, sources, sizes, n_clusters, d, dist_bytes, out_dist, out_masks, planes, out_stats=None,

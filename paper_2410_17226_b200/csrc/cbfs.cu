@@ -754,6 +754,89 @@ int cbfs_run(cbfs_graph* gh, const uint32_t* sources, const uint8_t* sizes, uint
   return CBFS_OK;
 }
 
+// A1 overlapped with A2-A8: the selection CTA runs on a side stream and
+// publishes each finished cluster through mapped host memory; batch b of the
+// traversal starts as soon as clusters [64b, 64b+64) exist.
+int cbfs_select_and_run(cbfs_graph* gh, uint32_t r, uint32_t k, uint32_t d, uint32_t root_policy, uint64_t seed,
+                        uint32_t* out_sources, uint8_t* out_sizes, uint32_t* out_r, uint32_t dist_bytes,
+                        void* out_dist, uint64_t* out_masks, uint32_t planes, uint64_t* out_stats,
+                        uint32_t direction, cbfs_stream stream) {
+  Graph* g = reinterpret_cast<Graph*>(gh);
+  int rc = check_select_args(g, r, k, d, root_policy, out_sources, out_sizes);
+  if (rc) return rc;
+  rc = check_run_args(g, out_sources, out_sizes, r, d, dist_bytes, planes, direction);
+  if (rc) return rc;
+  if (!out_r) return fail(CBFS_EINVAL, "null out_r");
+  *out_r = 0;
+  if (r == 0 || g->n == 0) return CBFS_OK;
+  CBFS_CUDA(cudaSetDevice(g->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  WorkLease lease(g);
+  if (lease.rc) return lease.rc;
+  static cudaStream_t side[MAX_DEV];
+  static volatile uint32_t* prog_h[MAX_DEV];
+  static uint32_t* prog_d[MAX_DEV];
+  static uint32_t* count_d[MAX_DEV];
+  const int dv = g->device;
+  if (!side[dv]) {  // guarded by the device lease
+    CBFS_CUDA(cudaStreamCreateWithFlags(&side[dv], cudaStreamNonBlocking));
+    void* hp = nullptr;
+    CBFS_CUDA(cudaHostAlloc(&hp, 2 * sizeof(uint32_t), cudaHostAllocMapped));
+    prog_h[dv] = (volatile uint32_t*)hp;
+    CBFS_CUDA(cudaHostGetDevicePointer((void**)&prog_d[dv], hp, 0));
+    CBFS_CUDA(cudaMalloc(&count_d[dv], sizeof(uint32_t)));
+  }
+  volatile uint32_t* prog = prog_h[dv];
+  prog[0] = 0;
+  prog[1] = 0;
+  cudaEvent_t ready;
+  CBFS_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  CBFS_CUDA(cudaEventRecord(ready, st));  // selection after the caller's prior work (graph build)
+  CBFS_CUDA(cudaStreamWaitEvent(side[dv], ready, 0));
+  CBFS_CUDA(cudaEventDestroy(ready));
+  rc = select_launch(g, r, k, d, root_policy, seed, out_sources, out_sizes, count_d[dv], prog_d[dv], side[dv]);
+  if (rc) return rc;
+  const uint64_t C = r;
+  if (out_dist) CBFS_CUDA(cudaMemsetAsync(out_dist, 0xFF, (uint64_t)g->n * C * dist_bytes, st));
+  if (out_masks) CBFS_CUDA(cudaMemsetAsync(out_masks, 0, (uint64_t)planes * g->n * C * sizeof(uint64_t), st));
+  uint32_t produced = 0;
+  for (uint32_t cb = 0; cb < r; cb += LANES) {
+    const uint32_t need = std::min<uint32_t>(r, cb + LANES);
+    for (;;) {  // wait until the batch's clusters are published (or selection ended)
+      const uint32_t p = prog[0];
+      if (p >= need || prog[1]) break;
+      if (cudaStreamQuery(side[dv]) != cudaErrorNotReady && !(prog[0] >= need) && !prog[1]) {
+        CBFS_CUDA(cudaStreamSynchronize(side[dv]));
+        return fail(CBFS_ECUDA, "cluster selection ended without publishing");
+      }
+    }
+    produced = prog[0];
+    if (cb >= produced) break;
+    RunArgs a;
+    a.sources = out_sources + (uint64_t)cb * 64;
+    a.sizes = out_sizes + cb;
+    a.nb = std::min<uint32_t>(LANES, produced - cb);
+    a.d = d;
+    a.planes = planes;
+    a.dist_bytes = dist_bytes;
+    a.C = r;
+    a.cbase = cb;
+    a.direction = direction;
+    a.out_dist = out_dist;
+    a.out_masks = out_masks;
+    a.out_stats = out_stats ? out_stats + (uint64_t)cb * 4 : nullptr;
+    rc = run_batch(g, a, st);
+    if (rc) {
+      cudaStreamSynchronize(side[dv]);
+      return rc;
+    }
+  }
+  CBFS_CUDA(cudaStreamSynchronize(side[dv]));
+  CBFS_CUDA(cudaStreamSynchronize(st));
+  *out_r = prog[0];
+  return CBFS_OK;
+}
+
 int cbfs_profile_enable(int on) {
   if (on && !g_prof.ev[0])
     for (int k = 0; k < 4; ++k) CBFS_CUDA(cudaEventCreate(&g_prof.ev[k]));

@@ -86,6 +86,11 @@ struct RunArgs {
   uint64_t* out_stats;      // device [nb][4] or null
 };
 int run_batch(Graph* g, const RunArgs& a, cudaStream_t st);
+int select_launch(const Graph* g, uint32_t r, uint32_t k, uint32_t d, uint32_t root_policy, uint64_t seed,
+                  uint32_t* out_sources, uint8_t* out_sizes, uint32_t* d_count, volatile uint32_t* progress,
+                  cudaStream_t st);
+int check_select_args(const Graph* g, uint32_t r, uint32_t k, uint32_t d, uint32_t root_policy,
+                      const void* out_sources, const void* out_sizes);
 int check_run_args(const Graph* g, const void* sources, const void* sizes, uint32_t n_clusters, uint32_t d,
                    uint32_t dist_bytes, uint32_t planes, uint32_t direction);
 

@@ -27,7 +27,8 @@ __global__ void __launch_bounds__(SEL_THREADS, 1)
 k_select(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cols, const uint32_t* __restrict__ rank,
          const uint32_t* __restrict__ order, const uint32_t* __restrict__ perm, const uint32_t* __restrict__ inv,
          uint32_t n, uint32_t r, uint32_t k, uint32_t d, uint32_t policy, uint64_t seed, SelScratch S,
-         uint32_t* __restrict__ out_sources, uint8_t* __restrict__ out_sizes, uint32_t* __restrict__ out_count) {
+         uint32_t* __restrict__ out_sources, uint8_t* __restrict__ out_sizes, uint32_t* __restrict__ out_count,
+         volatile uint32_t* progress) {
   __shared__ unsigned s_best, s_na, s_nb, s_nc, s_nsel, s_done, s_root;
   __shared__ unsigned long long s_avail, s_cursor, s_tdraw;
   __shared__ unsigned hist[256];
@@ -169,50 +170,83 @@ k_select(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cols, co
     }
     if (dec) atomicAdd(&s_avail, (unsigned long long)0 - dec);  // subtract
     ++produced;
+    if (progress) __threadfence();
     __syncthreads();
+    if (progress && tid == 0) {  // publish cluster c to a concurrent traversal (cbfs_select_and_run)
+      __threadfence_system();
+      progress[0] = produced;
+    }
   }
-  if (tid == 0) *out_count = produced;
+  if (tid == 0) {
+    *out_count = produced;
+    if (progress) {
+      __threadfence_system();
+      progress[0] = produced;
+      progress[1] = 1;
+    }
+  }
 }
 
 }  // namespace cbfs
 
 using namespace cbfs;
 
-extern "C" int cbfs_select_clusters(const cbfs_graph* gh, uint32_t r, uint32_t k, uint32_t d, uint32_t root_policy,
-                                    uint64_t seed, uint32_t* out_sources, uint8_t* out_sizes, uint32_t* out_r,
-                                    cbfs_stream stream) {
-  const Graph* g = reinterpret_cast<const Graph*>(gh);
-  if (!g || !out_r || (r && (!out_sources || !out_sizes))) return fail(CBFS_EINVAL, "null argument");
-  if (k == 0) return fail(CBFS_EINVAL, "k must be >= 1");
-  if (k > CBFS_MAX_K) return fail(CBFS_EUNSUPPORTED, "k > 64");
-  if (d > CBFS_MAX_D) return fail(CBFS_EUNSUPPORTED, "d > CBFS_MAX_D");
-  if (root_policy > CBFS_ROOT_RANDOM) return fail(CBFS_EINVAL, "bad root policy");
-  *out_r = 0;
-  if (r == 0 || g->n == 0) return CBFS_OK;
-  CBFS_CUDA(cudaSetDevice(g->device));
-  cudaStream_t st = (cudaStream_t)stream;
+namespace cbfs {
+// Queue the selection on `st`; the count lands in device memory *d_count and,
+// if `progress` (mapped pinned host memory) is given, is published after
+// every cluster.
+int select_launch(const Graph* g, uint32_t r, uint32_t k, uint32_t d, uint32_t root_policy, uint64_t seed,
+                  uint32_t* out_sources, uint8_t* out_sizes, uint32_t* d_count, volatile uint32_t* progress,
+                  cudaStream_t st) {
   const uint32_t n = g->n;
   SelScratch S;
-  uint32_t* d_count = nullptr;
   CBFS_CUDA(cudaMallocAsync(&S.marked, n, st));
   CBFS_CUDA(cudaMallocAsync(&S.stamp, sizeof(uint32_t) * n, st));
   CBFS_CUDA(cudaMallocAsync(&S.fa, sizeof(uint32_t) * n, st));
   CBFS_CUDA(cudaMallocAsync(&S.fb, sizeof(uint32_t) * n, st));
   CBFS_CUDA(cudaMallocAsync(&S.cand, sizeof(uint32_t) * n, st));
-  CBFS_CUDA(cudaMallocAsync(&d_count, sizeof(uint32_t), st));
   CBFS_CUDA(cudaMemsetAsync(S.marked, 0, n, st));
   CBFS_CUDA(cudaMemsetAsync(S.stamp, 0, sizeof(uint32_t) * n, st));
   CBFS_CUDA(cudaMemsetAsync(out_sources, 0xFF, sizeof(uint32_t) * 64ULL * r, st));
   CBFS_CUDA(cudaMemsetAsync(out_sizes, 0, r, st));
   k_select<<<1, SEL_THREADS, 0, st>>>(g->off, g->cols, g->rank, g->order, g->perm, g->inv, n, r, k, d, root_policy,
-                                      seed, S, out_sources, out_sizes, d_count);
+                                      seed, S, out_sources, out_sizes, d_count, progress);
   CBFS_LAUNCHED();
-  CBFS_CUDA(cudaMemcpyAsync(out_r, d_count, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   CBFS_CUDA(cudaFreeAsync(S.marked, st));
   CBFS_CUDA(cudaFreeAsync(S.stamp, st));
   CBFS_CUDA(cudaFreeAsync(S.fa, st));
   CBFS_CUDA(cudaFreeAsync(S.fb, st));
   CBFS_CUDA(cudaFreeAsync(S.cand, st));
+  return CBFS_OK;
+}
+
+int check_select_args(const Graph* g, uint32_t r, uint32_t k, uint32_t d, uint32_t root_policy,
+                      const void* out_sources, const void* out_sizes) {
+  if (!g || (r && (!out_sources || !out_sizes))) return fail(CBFS_EINVAL, "null argument");
+  if (k == 0) return fail(CBFS_EINVAL, "k must be >= 1");
+  if (k > CBFS_MAX_K) return fail(CBFS_EUNSUPPORTED, "k > 64");
+  if (d > CBFS_MAX_D) return fail(CBFS_EUNSUPPORTED, "d > CBFS_MAX_D");
+  if (root_policy > CBFS_ROOT_RANDOM) return fail(CBFS_EINVAL, "bad root policy");
+  return CBFS_OK;
+}
+}  // namespace cbfs
+
+extern "C" int cbfs_select_clusters(const cbfs_graph* gh, uint32_t r, uint32_t k, uint32_t d, uint32_t root_policy,
+                                    uint64_t seed, uint32_t* out_sources, uint8_t* out_sizes, uint32_t* out_r,
+                                    cbfs_stream stream) {
+  const Graph* g = reinterpret_cast<const Graph*>(gh);
+  int rc = check_select_args(g, r, k, d, root_policy, out_sources, out_sizes);
+  if (rc) return rc;
+  if (!out_r) return fail(CBFS_EINVAL, "null out_r");
+  *out_r = 0;
+  if (r == 0 || g->n == 0) return CBFS_OK;
+  CBFS_CUDA(cudaSetDevice(g->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  uint32_t* d_count = nullptr;
+  CBFS_CUDA(cudaMallocAsync(&d_count, sizeof(uint32_t), st));
+  rc = select_launch(g, r, k, d, root_policy, seed, out_sources, out_sizes, d_count, nullptr, st);
+  if (rc) return rc;
+  CBFS_CUDA(cudaMemcpyAsync(out_r, d_count, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   CBFS_CUDA(cudaFreeAsync(d_count, st));
   CBFS_CUDA(cudaStreamSynchronize(st));
   return CBFS_OK;

@@ -331,3 +331,29 @@ def test_c2_full_size_sampled():
         assert np.array_equal(st[c], om["stats"][j]), c
     allst = orc.cluster_bfs_many(ref, src, sz, d, want_outputs=False)["stats"]
     assert np.array_equal(st, allst)
+
+
+@pytest.mark.parametrize("policy,r", [(0, 150), (1, 70), (0, 5000)])
+def test_select_and_run_equals_separate_calls(policy, r):
+    """A1 overlapped with A2-A8 (cbfs_select_and_run) == cbfs_select_clusters + cbfs_run == oracle."""
+    el = random_el(91, 5000, "rmat")
+    ref = orc.csr_from_edgelist(el)
+    g = gpu_graph(el, relabel=True)
+    d = 2
+    src = torch.empty((r, 64), dtype=torch.int32, device="cuda:0")
+    sz = torch.empty((r,), dtype=torch.uint8, device="cuda:0")
+    dist = torch.empty((g.n, r), dtype=torch.uint8, device="cuda:0")
+    masks = torch.empty((d + 1, g.n, r), dtype=torch.int64, device="cuda:0")
+    stats = torch.zeros((r, 4), dtype=torch.int64, device="cuda:0")
+    got = cb.cbfs_select_and_run(g.h, r, 64, d, policy, 5, src, sz, 1, dist, masks, d + 1, stats)
+    osrc, osz = orc.select_clusters(ref, r, 64, d, policy, seed=5)
+    assert got == len(osz) and got <= r
+    assert np.array_equal(np_u32(src[:got]), osrc) and np.array_equal(sz[:got].cpu().numpy(), osz)
+    om = orc.cluster_bfs_many(ref, osrc, osz, d)
+    gd = dist.cpu().numpy().astype(np.uint16)
+    gd[gd == 0xFF] = 0xFFFF
+    assert np.array_equal(gd.T[:got], om["dist"])
+    assert np.array_equal(np_u64(masks).transpose(2, 0, 1)[:got], om["sub"])
+    assert np.array_equal(stats.cpu().numpy().view(np.uint64)[:got], om["stats"])
+    if got < r:  # columns past the selected clusters stay unreached
+        assert np.all(gd.T[got:] == 0xFFFF) and not np.any(np_u64(masks).transpose(2, 0, 1)[got:])
