@@ -31,9 +31,10 @@
  *    relabelling (CBFS_RELABEL_DEGREE) is invisible to callers.
  *  - Bit j of a bit-subset is the j-th source of the cluster's source list,
  *    LSB first (R11); k <= 64 so a bit-subset is one uint64_t.
- *  - A graph handle owns the traversal workspace: calls that traverse
- *    (cbfs_run, cbfs_query_stream) on the SAME handle must not run
- *    concurrently.  Handles are independent of each other.
+ *  - Traversals use a per-device cached workspace (several batch slots, each
+ *    with its own CUDA stream); calls that traverse on the same device are
+ *    serialised by a lock.  The calls order their work after the caller's
+ *    prior work on `stream` and make `stream` wait for all of it.
  */
 #ifndef CBFS_H
 #define CBFS_H
@@ -217,6 +218,9 @@ int cbfs_profile_read(double* ms, uint64_t* launches, uint64_t* arcs, uint64_t* 
                       uint64_t* u_out, int reset);
 /* Number of vertices with at least one arc. */
 int cbfs_graph_nonisolated(const cbfs_graph* g, uint32_t* count);
+/* Maximum number of 64-cluster batches traversed concurrently (each with its
+ * own workspace and stream; fewer if device memory is short).  Default 3. */
+int cbfs_set_concurrency(int batches);
 /* Number of kernels this library launched on this thread since the last reset. */
 uint64_t cbfs_launch_count(int reset);
 const char* cbfs_last_error(void);

@@ -56,6 +56,7 @@ _sig("cbfs_decode", [_u32, _u32, _u32, _u32, _vp, _u32, _vp, _u32, _u32, _vp, _v
 _sig("cbfs_query_distance", [_u32, _u32, _u32, _u32, _vp, _u32, _vp, _vp, _vp, _vp, _u64, _vp, _vp])
 _sig("cbfs_query_stream", [_vp, _vp, _vp, _u32, _u32, _vp, _vp, _u64, _vp, _vp, _vp])
 _sig("cbfs_set_direction_alpha", [ctypes.c_double])
+_sig("cbfs_set_concurrency", [_i32])
 _sig("cbfs_profile_enable", [_i32])
 _sig("cbfs_profile_read", [_vp, _vp, _vp, _vp, _vp, _vp, _i32])
 _sig("cbfs_graph_nonisolated", [_vp, ctypes.POINTER(_u32)])
@@ -178,6 +179,10 @@ def cbfs_query_stream(h, sources, sizes, n_clusters, d, s, t, inout_best, out_st
 
 def cbfs_set_direction_alpha(alpha: float):
     _check(_lib.cbfs_set_direction_alpha(alpha))
+
+
+def cbfs_set_concurrency(batches: int):
+    _check(_lib.cbfs_set_concurrency(batches))
 
 
 def cbfs_profile_enable(on: bool = True):

@@ -25,15 +25,20 @@
 #include <algorithm>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
 
 namespace cbfs {
 
-struct Work {
+// One in-flight batch of LANES clusters: its workspace, its stream, and the
+// state of its round loop.  Several slots run concurrently (run_batches), so
+// the small rounds and the latency-bound dense rounds of different batches
+// overlap on the GPU.
+struct Slot {
   uint64_t cap = 0;                     // n * LANES entries
-  uint64_t* seen = nullptr;             // [n][64] S_seen
+  uint64_t* seen = nullptr;             // [n+1][64] S_seen (row n stays zero)
   uint64_t* pend = nullptr;             // [n][64] S_next \ S_seen (pending)
   uint16_t* dist = nullptr;             // [n][64] Delta
   uint32_t* listA = nullptr;            // frontier lists (packed v*64+c)
@@ -45,48 +50,71 @@ struct Work {
   uint64_t* bstats = nullptr;           // [LANES][4]
   void* scan_tmp = nullptr;
   size_t scan_bytes = 0;
+  cudaStream_t s = nullptr;
+  cudaEvent_t ready = nullptr;  // counters of the last queued round are on the host
+  cudaEvent_t pe[4] = {nullptr, nullptr, nullptr, nullptr};  // profiling
+  // round-loop state
+  bool busy = false;
+  bool seeding = false;
+  RunArgs a{};
+  uint32_t i = 0;
+  uint64_t nF = 0, E = 0, U = 0;
+  uint32_t *cur = nullptr, *nxt = nullptr;
+  int kind = -1;
+  bool overflow = false;
+};
+
+struct DevSlots {
+  std::vector<Slot*> slots;
+  uint64_t cap = 0;
 };
 
 static double g_alpha = 100.0;
+static int g_max_slots = 4;
 
 // ---- optional per-kernel timing (cbfs_profile_*): CUDA events recorded on
 // the launching stream around each fold / push / pull launch; read after the
-// round's synchronisation, so no extra sync is added.
+// round's counters arrive, so no extra sync is added.  With concurrent
+// batches a launch's time includes the time it shares the GPU.
 enum { PK_FOLD = 0, PK_PUSH = 1, PK_PULL = 2, PK_N = 4 };
 struct Prof {
   bool on = false;
   double ms[PK_N] = {0, 0, 0, 0};
   uint64_t launches[PK_N] = {0, 0, 0, 0};
-  uint64_t arcs[PK_N] = {0, 0, 0, 0};     // frontier (entry, arc) pairs processed
+  uint64_t arcs[PK_N] = {0, 0, 0, 0};     // frontier (cluster, arc) pairs processed
   uint64_t entries[PK_N] = {0, 0, 0, 0};  // frontier entries processed
   uint64_t u_in[PK_N] = {0, 0, 0, 0};     // distinct frontier vertices |U_i|
   uint64_t u_out[PK_N] = {0, 0, 0, 0};    // distinct claimed vertices |U_{i+1}|
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 };
 static Prof g_prof;
 
-// The traversal workspace is cached per device and reused by every graph
-// handle (allocating and mapping a few GB per cbfs_run would cost tens of
-// ms).  A traversal holds the device's lock for its duration.
+// The slots are cached per device and reused by every graph handle
+// (allocating and mapping a few GB per cbfs_run would cost tens of ms).  A
+// traversal holds the device's lock for its duration.
 constexpr int MAX_DEV = 64;
-static Work* g_work[MAX_DEV];
+static DevSlots g_dev[MAX_DEV];
 static std::mutex g_work_mu[MAX_DEV];
 
-static void work_release_buffers(Work* w) {
+static void slot_free(Slot* w) {
   cudaFree(w->seen); cudaFree(w->pend); cudaFree(w->dist); cudaFree(w->listA); cudaFree(w->listB);
   cudaFree(w->pre); cudaFree(w->ubits); cudaFree(w->ctr); cudaFreeHost(w->h_ctr); cudaFree(w->bstats);
   cudaFree(w->scan_tmp);
-  *w = Work();
+  if (w->s) cudaStreamDestroy(w->s);
+  if (w->ready) cudaEventDestroy(w->ready);
+  for (int k = 0; k < 4; ++k)
+    if (w->pe[k]) cudaEventDestroy(w->pe[k]);
+  delete w;
 }
 
 void work_free(Graph* g) { g->work = nullptr; }  // the cache outlives graphs
 
-static int work_grow(Work* w, uint32_t n) {
-  const uint64_t cap = (uint64_t)(n ? n : 1) * LANES;
-  if (w->cap >= cap) return CBFS_OK;
-  work_release_buffers(w);
+static uint64_t slot_bytes(uint64_t cap) {
+  return (cap + LANES) * 8 + cap * 8 + cap * 2 + cap * 8 + (cap + 1) * 8 + cap / 4;
+}
+
+static int slot_alloc(Slot* w, uint64_t cap) {
   w->cap = cap;
-  const uint64_t ubw = 2 * (((uint64_t)cap / LANES >> 5) + 1);
+  const uint64_t ubw = 2 * ((cap / LANES >> 5) + 1);
   CBFS_CUDA(cudaMalloc(&w->seen, (cap + LANES) * sizeof(uint64_t)));  // + all-zero row n
   CBFS_CUDA(cudaMalloc(&w->pend, cap * sizeof(uint64_t)));
   CBFS_CUDA(cudaMalloc(&w->dist, cap * sizeof(uint16_t)));
@@ -98,9 +126,31 @@ static int work_grow(Work* w, uint32_t n) {
   CBFS_CUDA(cudaMallocHost(&w->h_ctr, 4 * sizeof(unsigned long long)));
   CBFS_CUDA(cudaMalloc(&w->bstats, LANES * 4 * sizeof(uint64_t)));
   CBFS_CUDA(cudaMemset(w->pend, 0, cap * sizeof(uint64_t)));  // zero-invariant from here on
-  CBFS_CUDA(cudaMemset(w->ubits, 0, ubw * sizeof(uint32_t)));  // both bitmaps zero between runs
+  CBFS_CUDA(cudaMemset(w->ubits, 0, ubw * sizeof(uint32_t)));  // both bitmaps zero between batches
   CBFS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, w->scan_bytes, w->pre, w->pre, cap));
   CBFS_CUDA(cudaMalloc(&w->scan_tmp, w->scan_bytes ? w->scan_bytes : 1));
+  CBFS_CUDA(cudaStreamCreateWithFlags(&w->s, cudaStreamNonBlocking));
+  CBFS_CUDA(cudaEventCreateWithFlags(&w->ready, cudaEventDisableTiming));
+  for (int k = 0; k < 4; ++k) CBFS_CUDA(cudaEventCreate(&w->pe[k]));
+  return CBFS_OK;
+}
+
+static int work_grow(DevSlots& D, uint32_t n) {
+  const uint64_t cap = (uint64_t)(n ? n : 1) * LANES;
+  if (D.cap >= cap && !D.slots.empty()) return CBFS_OK;
+  for (Slot* w : D.slots) slot_free(w);
+  D.slots.clear();
+  D.cap = cap;
+  size_t fr = 0, tot = 0;
+  CBFS_CUDA(cudaMemGetInfo(&fr, &tot));
+  // as many concurrent batches as half the free memory allows (>= 1)
+  int P = (int)std::min<uint64_t>((uint64_t)g_max_slots, std::max<uint64_t>(1, (fr / 2) / slot_bytes(cap)));
+  for (int k = 0; k < P; ++k) {
+    Slot* w = new Slot();
+    D.slots.push_back(w);
+    int rc = slot_alloc(w, cap);
+    if (rc) return rc;
+  }
   CBFS_CUDA(cudaDeviceSynchronize());
   return CBFS_OK;
 }
@@ -109,9 +159,8 @@ WorkLease::WorkLease(Graph* g) : g_(g) {
   if (g->device < 0 || g->device >= MAX_DEV) { rc = fail(CBFS_EUNSUPPORTED, "device ordinal >= 64"); return; }
   g_work_mu[g->device].lock();
   locked_ = true;
-  if (!g_work[g->device]) g_work[g->device] = new Work();
-  rc = work_grow(g_work[g->device], g->n);
-  if (rc == CBFS_OK) g->work = g_work[g->device];
+  rc = work_grow(g_dev[g->device], g->n);
+  if (rc == CBFS_OK) g->work = reinterpret_cast<struct Work*>(&g_dev[g->device]);
 }
 
 WorkLease::~WorkLease() {
@@ -603,16 +652,23 @@ __global__ void __launch_bounds__(PULL_WARPS * 32, CBFS_PULL_MINB) k_pull(
 __global__ void k_set_u64(uint64_t* p, uint64_t v) { *p = v; }
 
 // ------------------------------------------------------------------ driver
-static int sync_ctr(Work* w, cudaStream_t st) {
-  CBFS_CUDA(cudaMemcpyAsync(w->h_ctr, w->ctr, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-  CBFS_CUDA(cudaStreamSynchronize(st));
+static int queue_counters(Slot* w) {
+  CBFS_CUDA(cudaMemcpyAsync(w->h_ctr, w->ctr, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, w->s));
+  CBFS_CUDA(cudaEventRecord(w->ready, w->s));
   return CBFS_OK;
 }
 
-int run_batch(Graph* g, const RunArgs& a, cudaStream_t st) {
-  Work* w = g->work;
+// queue init + seeding of batch `a` on the slot's stream
+static int slot_start(Graph* g, Slot* w, const RunArgs& a) {
   const uint32_t n = g->n;
-  const uint64_t ub_words = (n >> 5) + 1;
+  cudaStream_t st = w->s;
+  w->a = a;
+  w->busy = true;
+  w->seeding = true;
+  w->overflow = false;
+  w->i = 0;
+  w->cur = w->listA;
+  w->nxt = w->listB;
   CBFS_CUDA(cudaMemsetAsync(w->seen, 0, (uint64_t)(n + 1) * LANES * sizeof(uint64_t), st));
   CBFS_CUDA(cudaMemsetAsync(w->dist, 0xFF, (uint64_t)n * LANES * sizeof(uint16_t), st));
   CBFS_CUDA(cudaMemsetAsync(w->bstats, 0, LANES * 4 * sizeof(uint64_t), st));
@@ -620,88 +676,189 @@ int run_batch(Graph* g, const RunArgs& a, cudaStream_t st) {
   k_seed<<<(a.nb * 64 + 255) / 256, 256, 0, st>>>(a.sources, a.sizes, a.nb, n, g->inv, g->off, w->pend, w->listA,
                                                    w->ubits, w->bstats, w->ctr);
   CBFS_LAUNCHED();
-  int rc = sync_ctr(w, st);
-  if (rc) return rc;
-  if (w->h_ctr[2]) {
-    // leave pend and the bitmaps zero for the next call
-    CBFS_CUDA(cudaMemsetAsync(w->pend, 0, (uint64_t)n * LANES * sizeof(uint64_t), st));
-    CBFS_CUDA(cudaMemsetAsync(w->ubits, 0, 2 * ub_words * sizeof(uint32_t), st));
-    CBFS_CUDA(cudaStreamSynchronize(st));
-    if (w->h_ctr[2] & ERR_BAD_SIZE) return fail(CBFS_EINVAL, "cluster size must be 1..64");
-    if (w->h_ctr[2] & ERR_BAD_SOURCE) return fail(CBFS_EINVAL, "source id >= n");
-    return fail(CBFS_EINVAL, "duplicate source in a cluster");
-  }
-  uint64_t nF = w->h_ctr[0], E = w->h_ctr[1], U = w->h_ctr[3];
-  uint32_t* cur = w->listA;
-  uint32_t* nxt = w->listB;
-  bool overflow = false;
-  for (uint32_t i = 0; nF > 0; ++i) {
-    if (i >= 0xFFFEu) return fail(CBFS_EOVERFLOW, "more than 65534 rounds");
-    uint32_t* ub_cur = w->ubits + (i & 1) * ub_words;        // U_i (built by the previous edge phase)
-    uint32_t* ub_nxt = w->ubits + ((i + 1) & 1) * ub_words;  // U_{i+1} (zero)
-    const bool pull = a.direction == CBFS_DIR_PULL ||
-                      (a.direction == CBFS_DIR_AUTO && (double)E * g_alpha > (double)g->m * (double)a.nb);
-    const int write_pre = pull ? 0 : 1;
-    const unsigned fb = grid_for((nF + FOLD_ILP - 1) / FOLD_ILP, 256);
-    if (g_prof.on) CBFS_CUDA(cudaEventRecord(g_prof.ev[0], st));
-    if (a.dist_bytes == 1)
-      k_fold<1><<<fb, 256, 0, st>>>(cur, (uint32_t)nF, i, w->seen, w->pend, w->dist, g->off, g->perm, n, a.C, a.cbase,
-                                    a.planes, a.out_dist, a.out_masks, w->pre, write_pre, w->ctr);
-    else
-      k_fold<2><<<fb, 256, 0, st>>>(cur, (uint32_t)nF, i, w->seen, w->pend, w->dist, g->off, g->perm, n, a.C, a.cbase,
-                                    a.planes, a.out_dist, a.out_masks, w->pre, write_pre, w->ctr);
+  return queue_counters(w);
+}
+
+// queue round w->i (fold + edge phase) of the slot's batch
+static int slot_round(Graph* g, Slot* w) {
+  const uint32_t n = g->n;
+  const uint64_t ub_words = (n >> 5) + 1;
+  const RunArgs& a = w->a;
+  cudaStream_t st = w->s;
+  const uint32_t i = w->i;
+  const uint64_t nF = w->nF, E = w->E;
+  uint32_t* ub_cur = w->ubits + (i & 1) * ub_words;        // U_i (built by the previous edge phase)
+  uint32_t* ub_nxt = w->ubits + ((i + 1) & 1) * ub_words;  // U_{i+1} (zero)
+  const bool pull = a.direction == CBFS_DIR_PULL ||
+                    (a.direction == CBFS_DIR_AUTO && (double)E * g_alpha > (double)g->m * (double)a.nb);
+  const int write_pre = pull ? 0 : 1;
+  const unsigned fb = grid_for((nF + FOLD_ILP - 1) / FOLD_ILP, 256);
+  if (g_prof.on) CBFS_CUDA(cudaEventRecord(w->pe[0], st));
+  if (a.dist_bytes == 1)
+    k_fold<1><<<fb, 256, 0, st>>>(w->cur, (uint32_t)nF, i, w->seen, w->pend, w->dist, g->off, g->perm, n, a.C,
+                                  a.cbase, a.planes, a.out_dist, a.out_masks, w->pre, write_pre, w->ctr);
+  else
+    k_fold<2><<<fb, 256, 0, st>>>(w->cur, (uint32_t)nF, i, w->seen, w->pend, w->dist, g->off, g->perm, n, a.C,
+                                  a.cbase, a.planes, a.out_dist, a.out_masks, w->pre, write_pre, w->ctr);
+  CBFS_LAUNCHED();
+  if (g_prof.on) CBFS_CUDA(cudaEventRecord(w->pe[1], st));
+  CBFS_CUDA(cudaMemsetAsync(w->ctr, 0, 2 * sizeof(unsigned long long), st));
+  CBFS_CUDA(cudaMemsetAsync(w->ctr + 3, 0, sizeof(unsigned long long), st));
+  w->kind = -1;
+  if (pull) {
+    w->kind = PK_PULL;
+    if (g_prof.on) CBFS_CUDA(cudaEventRecord(w->pe[2], st));
+    const unsigned pb = grid_for(g->n_chunks * 32, PULL_WARPS * 32, 148u * 8u);
+    k_pull<<<pb, PULL_WARPS * 32, 0, st>>>(g->off, g->cols, g->chunk_v, g->n_chunks, g->m, n, w->seen, w->dist,
+                                           w->pend, ub_cur, ub_nxt, a.sizes, a.nb, w->nxt, w->bstats, w->ctr, i, a.d);
     CBFS_LAUNCHED();
-    if (g_prof.on) CBFS_CUDA(cudaEventRecord(g_prof.ev[1], st));
-    CBFS_CUDA(cudaMemsetAsync(w->ctr, 0, 2 * sizeof(unsigned long long), st));
-    CBFS_CUDA(cudaMemsetAsync(w->ctr + 3, 0, sizeof(unsigned long long), st));
-    int kind = -1;
-    if (pull) {
-      kind = PK_PULL;
-      if (g_prof.on) CBFS_CUDA(cudaEventRecord(g_prof.ev[2], st));
-      const unsigned pb = grid_for(g->n_chunks * 32, PULL_WARPS * 32, 148u * 8u);
-      k_pull<<<pb, PULL_WARPS * 32, 0, st>>>(g->off, g->cols, g->chunk_v, g->n_chunks, g->m, n, w->seen, w->dist,
-                                             w->pend, ub_cur, ub_nxt, a.sizes, a.nb, nxt, w->bstats, w->ctr, i, a.d);
-      CBFS_LAUNCHED();
-      if (g_prof.on) CBFS_CUDA(cudaEventRecord(g_prof.ev[3], st));
-    } else if (E > 0) {
-      kind = PK_PUSH;
-      CBFS_CUDA(cub::DeviceScan::ExclusiveSum(w->scan_tmp, w->scan_bytes, w->pre, w->pre, nF, st));
-      count_launch(2);
-      k_set_u64<<<1, 1, 0, st>>>(w->pre + nF, E);
-      CBFS_LAUNCHED();
-      const uint64_t warps = (E + PUSH_CHUNK - 1) / PUSH_CHUNK;
-      const unsigned pb = grid_for(warps * 32, 256, 148u * 8u * 4u);
-      if (g_prof.on) CBFS_CUDA(cudaEventRecord(g_prof.ev[2], st));
-      k_push<<<pb, 256, 0, st>>>(g->off, g->cols, cur, w->pre, (uint32_t)nF, E, w->seen, w->dist, w->pend, nxt,
-                                 ub_nxt, w->bstats, w->ctr, i, a.d);
-      CBFS_LAUNCHED();
-      if (g_prof.on) CBFS_CUDA(cudaEventRecord(g_prof.ev[3], st));
+    if (g_prof.on) CBFS_CUDA(cudaEventRecord(w->pe[3], st));
+  } else if (E > 0) {
+    w->kind = PK_PUSH;
+    CBFS_CUDA(cub::DeviceScan::ExclusiveSum(w->scan_tmp, w->scan_bytes, w->pre, w->pre, nF, st));
+    count_launch(2);
+    k_set_u64<<<1, 1, 0, st>>>(w->pre + nF, E);
+    CBFS_LAUNCHED();
+    const uint64_t warps = (E + PUSH_CHUNK - 1) / PUSH_CHUNK;
+    const unsigned pb = grid_for(warps * 32, 256, 148u * 8u * 4u);
+    if (g_prof.on) CBFS_CUDA(cudaEventRecord(w->pe[2], st));
+    k_push<<<pb, 256, 0, st>>>(g->off, g->cols, w->cur, w->pre, (uint32_t)nF, E, w->seen, w->dist, w->pend, w->nxt,
+                               ub_nxt, w->bstats, w->ctr, i, a.d);
+    CBFS_LAUNCHED();
+    if (g_prof.on) CBFS_CUDA(cudaEventRecord(w->pe[3], st));
+  }
+  CBFS_CUDA(cudaMemsetAsync(ub_cur, 0, ub_words * sizeof(uint32_t), st));  // U_i consumed
+  return queue_counters(w);
+}
+
+// The slot's counters arrived: account the finished round, then queue the
+// next one or finish the batch.  Returns 1 when the batch finished.
+static int slot_step(Graph* g, Slot* w, BatchSource& src, int slot, int* err) {
+  const uint32_t n = g->n;
+  if (w->seeding) {
+    w->seeding = false;
+    if (w->h_ctr[2]) {  // bad sources: restore the zero invariants, report
+      CBFS_CUDA(cudaMemsetAsync(w->pend, 0, (uint64_t)n * LANES * sizeof(uint64_t), w->s));
+      CBFS_CUDA(cudaMemsetAsync(w->ubits, 0, 2 * ((n >> 5) + 1) * sizeof(uint32_t), w->s));
+      CBFS_CUDA(cudaStreamSynchronize(w->s));
+      w->busy = false;
+      if (w->h_ctr[2] & ERR_BAD_SIZE) *err = fail(CBFS_EINVAL, "cluster size must be 1..64");
+      else if (w->h_ctr[2] & ERR_BAD_SOURCE) *err = fail(CBFS_EINVAL, "source id >= n");
+      else *err = fail(CBFS_EINVAL, "duplicate source in a cluster");
+      return 1;
     }
-    CBFS_CUDA(cudaMemsetAsync(ub_cur, 0, ub_words * sizeof(uint32_t), st));  // U_i consumed
-    rc = sync_ctr(w, st);
-    if (rc) return rc;
+  } else {
     if (g_prof.on) {
       float ms = 0;
-      CBFS_CUDA(cudaEventElapsedTime(&ms, g_prof.ev[0], g_prof.ev[1]));
-      g_prof.ms[PK_FOLD] += ms; g_prof.launches[PK_FOLD] += 1; g_prof.entries[PK_FOLD] += nF;
-      if (kind >= 0) {
-        CBFS_CUDA(cudaEventElapsedTime(&ms, g_prof.ev[2], g_prof.ev[3]));
-        g_prof.ms[kind] += ms; g_prof.launches[kind] += 1; g_prof.entries[kind] += nF; g_prof.arcs[kind] += E;
-        g_prof.u_in[kind] += U; g_prof.u_out[kind] += w->h_ctr[3];
+      CBFS_CUDA(cudaEventElapsedTime(&ms, w->pe[0], w->pe[1]));
+      g_prof.ms[PK_FOLD] += ms; g_prof.launches[PK_FOLD] += 1; g_prof.entries[PK_FOLD] += w->nF;
+      if (w->kind >= 0) {
+        CBFS_CUDA(cudaEventElapsedTime(&ms, w->pe[2], w->pe[3]));
+        g_prof.ms[w->kind] += ms; g_prof.launches[w->kind] += 1; g_prof.entries[w->kind] += w->nF;
+        g_prof.arcs[w->kind] += w->E; g_prof.u_in[w->kind] += w->U; g_prof.u_out[w->kind] += w->h_ctr[3];
       }
     }
-    if (w->h_ctr[2] & ERR_OVERFLOW) overflow = true;
-    nF = w->h_ctr[0];
-    E = w->h_ctr[1];
-    U = w->h_ctr[3];
-    std::swap(cur, nxt);
+    if (w->h_ctr[2] & ERR_OVERFLOW) w->overflow = true;
+    std::swap(w->cur, w->nxt);
+    ++w->i;
   }
-  if (a.out_stats)
-    CBFS_CUDA(cudaMemcpyAsync(a.out_stats, w->bstats, (uint64_t)a.nb * 4 * sizeof(uint64_t), cudaMemcpyDeviceToDevice,
-                              st));
-  if (overflow) return fail(CBFS_EOVERFLOW, "a distance exceeds 254 with dist_bytes == 1");
-  return CBFS_OK;
+  w->nF = w->h_ctr[0];
+  w->E = w->h_ctr[1];
+  w->U = w->h_ctr[3];
+  if (w->nF == 0) {  // batch done
+    if (w->a.out_stats)
+      CBFS_CUDA(cudaMemcpyAsync(w->a.out_stats, w->bstats, (uint64_t)w->a.nb * 4 * sizeof(uint64_t),
+                                cudaMemcpyDeviceToDevice, w->s));
+    int rc = src.finished(w->a, slot, w->s);
+    w->busy = false;
+    if (rc) *err = rc;
+    if (w->overflow && !*err) *err = fail(CBFS_EOVERFLOW, "a distance exceeds 254 with dist_bytes == 1");
+    return 1;
+  }
+  if (w->i >= 0xFFFEu) {
+    *err = fail(CBFS_EOVERFLOW, "more than 65534 rounds");
+    return 1;  // pend is left non-zero only for this slot's pending entries; cleared below
+  }
+  int rc = slot_round(g, w);
+  if (rc) { *err = rc; return 1; }
+  return 0;
 }
+
+// Drive all batches of `src` through the device's slots; every slot stream
+// first waits for the caller's prior work on `st`, and `st` waits for all of
+// them at the end.
+int run_batches(Graph* g, BatchSource& src, cudaStream_t st) {
+  DevSlots& D = *reinterpret_cast<DevSlots*>(g->work);
+  const int P = (int)D.slots.size();
+  cudaEvent_t start;
+  CBFS_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  CBFS_CUDA(cudaEventRecord(start, st));
+  for (Slot* w : D.slots) CBFS_CUDA(cudaStreamWaitEvent(w->s, start, 0));
+  CBFS_CUDA(cudaEventDestroy(start));
+  int err = CBFS_OK;
+  bool exhausted = false;
+  for (;;) {
+    bool progressed = false, any_busy = false;
+    for (int k = 0; k < P; ++k) {
+      Slot* w = D.slots[k];
+      if (w->busy) {
+        const cudaError_t q = cudaEventQuery(w->ready);
+        if (q == cudaSuccess) {
+          slot_step(g, w, src, k, &err);
+          progressed = true;
+        } else if (q != cudaErrorNotReady) {
+          err = cuda_fail(q, "batch round");
+          w->busy = false;
+        }
+      }
+      if (!w->busy && !exhausted && err == CBFS_OK) {
+        RunArgs a{};
+        const int got = src.next(a);
+        if (got < 0) exhausted = true;
+        if (got > 0) {
+          int rc = src.bind(a, k, w->s);
+          if (rc == CBFS_OK) rc = slot_start(g, w, a);
+          if (rc) err = rc;
+          progressed = true;
+        }
+      }
+      any_busy |= w->busy;
+    }
+    if (!any_busy && (exhausted || err != CBFS_OK)) break;
+    if (!progressed) std::this_thread::yield();
+  }
+  cudaEvent_t done;
+  CBFS_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+  for (Slot* w : D.slots) {
+    CBFS_CUDA(cudaEventRecord(done, w->s));
+    CBFS_CUDA(cudaStreamWaitEvent(st, done, 0));
+  }
+  CBFS_CUDA(cudaEventDestroy(done));
+  if (err != CBFS_OK) {
+    // restore the zero invariants of every slot for the next call
+    CBFS_CUDA(cudaDeviceSynchronize());
+    for (Slot* w : D.slots) {
+      CBFS_CUDA(cudaMemset(w->pend, 0, D.cap * sizeof(uint64_t)));
+      CBFS_CUDA(cudaMemset(w->ubits, 0, 2 * ((D.cap / LANES >> 5) + 1) * sizeof(uint32_t)));
+      w->busy = false;
+    }
+  }
+  return err;
+}
+
+int ArraySource::next(RunArgs& a) {
+  if (next_c >= n_clusters) return -1;
+  a = proto;
+  a.sources = sources + (uint64_t)next_c * 64;
+  a.sizes = sizes + next_c;
+  a.nb = std::min<uint32_t>(LANES, n_clusters - next_c);
+  a.cbase = proto.cbase + next_c;
+  a.out_stats = out_stats ? out_stats + (uint64_t)next_c * 4 : nullptr;
+  next_c += a.nb;
+  return 1;
+}
+
+int num_slots(const Graph* g) { return (int)reinterpret_cast<const DevSlots*>(g->work)->slots.size(); }
 
 int check_run_args(const Graph* g, const void* sources, const void* sizes, uint32_t n_clusters, uint32_t d,
                    uint32_t dist_bytes, uint32_t planes, uint32_t direction) {
@@ -733,30 +890,45 @@ int cbfs_run(cbfs_graph* gh, const uint32_t* sources, const uint8_t* sizes, uint
   const uint64_t C = n_clusters;
   if (out_dist) CBFS_CUDA(cudaMemsetAsync(out_dist, 0xFF, (uint64_t)g->n * C * dist_bytes, st));
   if (out_masks) CBFS_CUDA(cudaMemsetAsync(out_masks, 0, (uint64_t)planes * g->n * C * sizeof(uint64_t), st));
-  for (uint32_t cb = 0; cb < n_clusters; cb += LANES) {
-    RunArgs a;
-    a.sources = sources + (uint64_t)cb * 64;
-    a.sizes = sizes + cb;
-    a.nb = std::min<uint32_t>(LANES, n_clusters - cb);
-    a.d = d;
-    a.planes = planes;
-    a.dist_bytes = dist_bytes;
-    a.C = n_clusters;
-    a.cbase = cb;
-    a.direction = direction;
-    a.out_dist = out_dist;
-    a.out_masks = out_masks;
-    a.out_stats = out_stats ? out_stats + (uint64_t)cb * 4 : nullptr;
-    rc = run_batch(g, a, st);
-    if (rc) return rc;
-  }
+  ArraySource src;
+  src.proto = RunArgs{};
+  src.proto.d = d;
+  src.proto.planes = planes;
+  src.proto.dist_bytes = dist_bytes;
+  src.proto.C = n_clusters;
+  src.proto.direction = direction;
+  src.proto.out_dist = out_dist;
+  src.proto.out_masks = out_masks;
+  src.sources = sources;
+  src.sizes = sizes;
+  src.n_clusters = n_clusters;
+  src.out_stats = out_stats;
+  rc = run_batches(g, src, st);
+  if (rc) return rc;
   CBFS_CUDA(cudaStreamSynchronize(st));
   return CBFS_OK;
 }
 
 // A1 overlapped with A2-A8: the selection CTA runs on a side stream and
-// publishes each finished cluster through mapped host memory; batch b of the
-// traversal starts as soon as clusters [64b, 64b+64) exist.
+// publishes each finished cluster through mapped host memory; a batch of
+// LANES clusters is started as soon as its clusters exist.
+struct SelectSource : ArraySource {
+  volatile uint32_t* prog;
+  cudaStream_t side;
+  uint32_t r;
+  int next(RunArgs& a) override {
+    const uint32_t need = std::min<uint32_t>(r, next_c + LANES);
+    const uint32_t p = prog[0];
+    const bool done = prog[1] != 0;
+    if (p < need && !done) {
+      if (cudaStreamQuery(side) != cudaErrorNotReady && prog[0] < need && !prog[1]) return -1;  // selection died
+      return 0;
+    }
+    n_clusters = prog[0];
+    return ArraySource::next(a);
+  }
+};
+
 int cbfs_select_and_run(cbfs_graph* gh, uint32_t r, uint32_t k, uint32_t d, uint32_t root_policy, uint64_t seed,
                         uint32_t* out_sources, uint8_t* out_sizes, uint32_t* out_r, uint32_t dist_bytes,
                         void* out_dist, uint64_t* out_masks, uint32_t planes, uint64_t* out_stats,
@@ -799,48 +971,49 @@ int cbfs_select_and_run(cbfs_graph* gh, uint32_t r, uint32_t k, uint32_t d, uint
   const uint64_t C = r;
   if (out_dist) CBFS_CUDA(cudaMemsetAsync(out_dist, 0xFF, (uint64_t)g->n * C * dist_bytes, st));
   if (out_masks) CBFS_CUDA(cudaMemsetAsync(out_masks, 0, (uint64_t)planes * g->n * C * sizeof(uint64_t), st));
-  uint32_t produced = 0;
-  for (uint32_t cb = 0; cb < r; cb += LANES) {
-    const uint32_t need = std::min<uint32_t>(r, cb + LANES);
-    for (;;) {  // wait until the batch's clusters are published (or selection ended)
-      const uint32_t p = prog[0];
-      if (p >= need || prog[1]) break;
-      if (cudaStreamQuery(side[dv]) != cudaErrorNotReady && !(prog[0] >= need) && !prog[1]) {
-        CBFS_CUDA(cudaStreamSynchronize(side[dv]));
-        return fail(CBFS_ECUDA, "cluster selection ended without publishing");
-      }
-    }
-    produced = prog[0];
-    if (cb >= produced) break;
-    RunArgs a;
-    a.sources = out_sources + (uint64_t)cb * 64;
-    a.sizes = out_sizes + cb;
-    a.nb = std::min<uint32_t>(LANES, produced - cb);
-    a.d = d;
-    a.planes = planes;
-    a.dist_bytes = dist_bytes;
-    a.C = r;
-    a.cbase = cb;
-    a.direction = direction;
-    a.out_dist = out_dist;
-    a.out_masks = out_masks;
-    a.out_stats = out_stats ? out_stats + (uint64_t)cb * 4 : nullptr;
-    rc = run_batch(g, a, st);
-    if (rc) {
-      cudaStreamSynchronize(side[dv]);
-      return rc;
-    }
-  }
-  CBFS_CUDA(cudaStreamSynchronize(side[dv]));
+  SelectSource src;
+  src.proto = RunArgs{};
+  src.proto.d = d;
+  src.proto.planes = planes;
+  src.proto.dist_bytes = dist_bytes;
+  src.proto.C = r;
+  src.proto.direction = direction;
+  src.proto.out_dist = out_dist;
+  src.proto.out_masks = out_masks;
+  src.sources = out_sources;
+  src.sizes = out_sizes;
+  src.n_clusters = 0;
+  src.out_stats = out_stats;
+  src.prog = prog;
+  src.side = side[dv];
+  src.r = r;
+  rc = run_batches(g, src, st);
+  cudaError_t e2 = cudaStreamSynchronize(side[dv]);
+  if (rc) return rc;
+  if (e2 != cudaSuccess) return cuda_fail(e2, "cluster selection");
+  if (!prog[1]) return fail(CBFS_ECUDA, "cluster selection ended without publishing");
   CBFS_CUDA(cudaStreamSynchronize(st));
   *out_r = prog[0];
   return CBFS_OK;
 }
 
 int cbfs_profile_enable(int on) {
-  if (on && !g_prof.ev[0])
-    for (int k = 0; k < 4; ++k) CBFS_CUDA(cudaEventCreate(&g_prof.ev[k]));
   g_prof.on = on != 0;
+  return CBFS_OK;
+}
+
+int cbfs_set_concurrency(int batches) {
+  if (batches < 1 || batches > 16) return fail(CBFS_EINVAL, "concurrency must be 1..16");
+  for (int dv = 0; dv < MAX_DEV; ++dv) {  // re-size the slot sets lazily
+    std::lock_guard<std::mutex> lk(g_work_mu[dv]);
+    if ((int)g_dev[dv].slots.size() != batches && !g_dev[dv].slots.empty()) {
+      cudaSetDevice(dv);
+      for (Slot* w : g_dev[dv].slots) slot_free(w);
+      g_dev[dv].slots.clear();
+      g_dev[dv].cap = 0;
+    }
+  }
+  g_max_slots = batches;
   return CBFS_OK;
 }
 

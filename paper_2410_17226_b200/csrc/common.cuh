@@ -75,8 +75,8 @@ struct WorkLease {
   bool locked_ = false;
 };
 
-// one batch (<= 32 clusters) of cbfs_run; outputs use row stride C and start
-// at column cbase
+// one batch (<= LANES clusters) of cbfs_run; outputs use row stride C and
+// start at column cbase
 struct RunArgs {
   const uint32_t* sources;  // device, batch base ([nb][64])
   const uint8_t* sizes;     // device, batch base ([nb])
@@ -85,7 +85,28 @@ struct RunArgs {
   uint64_t* out_masks;      // device [planes][n][C] or null
   uint64_t* out_stats;      // device [nb][4] or null
 };
-int run_batch(Graph* g, const RunArgs& a, cudaStream_t st);
+// A producer of batches for run_batches (several batches run concurrently,
+// one per workspace slot, each on its own stream).
+struct BatchSource {
+  virtual ~BatchSource() = default;
+  // fill `a` with the next batch: 1 = got one, 0 = none available yet, -1 = exhausted
+  virtual int next(RunArgs& a) = 0;
+  // before the batch starts on slot `slot` (may redirect outputs to slot-local buffers on stream s)
+  virtual int bind(RunArgs& a, int slot, cudaStream_t s) { (void)a; (void)slot; (void)s; return CBFS_OK; }
+  // after the batch's last kernel has been queued on stream s
+  virtual int finished(const RunArgs& a, int slot, cudaStream_t s) { (void)a; (void)slot; (void)s; return CBFS_OK; }
+};
+// batches of an array of clusters in device memory
+struct ArraySource : BatchSource {
+  RunArgs proto{};
+  const uint32_t* sources = nullptr;
+  const uint8_t* sizes = nullptr;
+  uint32_t n_clusters = 0, next_c = 0;
+  uint64_t* out_stats = nullptr;
+  int next(RunArgs& a) override;
+};
+int run_batches(Graph* g, BatchSource& src, cudaStream_t st);
+int num_slots(const Graph* g);  // concurrent batches of the leased workspace
 int select_launch(const Graph* g, uint32_t r, uint32_t k, uint32_t d, uint32_t root_policy, uint64_t seed,
                   uint32_t* out_sources, uint8_t* out_sizes, uint32_t* d_count, volatile uint32_t* progress,
                   cudaStream_t st);

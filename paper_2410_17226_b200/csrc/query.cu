@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(256) k_query(uint32_t n, uint32_t C, uint32_t 
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mine = min(mine, __shfl_xor_sync(0xFFFFFFFFu, mine, o));
-    if (lane == 0 && mine < best[qi]) best[qi] = mine;
+    if (lane == 0 && mine < 0x7FFFFFFF) atomicMin(&best[qi], mine);  // concurrent batches min-merge
   }
 }
 
@@ -155,6 +155,30 @@ int cbfs_query_distance(uint32_t n, uint32_t C, uint32_t d, uint32_t planes, con
   return CBFS_OK;
 }
 
+// per-slot label staging; the query runs on the slot's stream when its batch ends
+struct QuerySource : ArraySource {
+  uint32_t n = 0, d = 0, planes = 0;
+  std::vector<uint16_t*> sd;
+  std::vector<uint64_t*> sm;
+  const uint32_t *s = nullptr, *t = nullptr;
+  uint64_t q = 0;
+  int32_t* best = nullptr;
+  int* bad = nullptr;
+  int bind(RunArgs& a, int slot, cudaStream_t st) override {
+    a.out_dist = sd[slot];
+    a.out_masks = sm[slot];
+    a.C = LANES;
+    a.cbase = 0;
+    CBFS_CUDA(cudaMemsetAsync(sd[slot], 0xFF, sizeof(uint16_t) * (uint64_t)n * LANES, st));
+    CBFS_CUDA(cudaMemsetAsync(sm[slot], 0, sizeof(uint64_t) * (uint64_t)planes * n * LANES, st));
+    return CBFS_OK;
+  }
+  int finished(const RunArgs& a, int slot, cudaStream_t st) override {
+    // lanes >= nb stay unreachable (dist 0xFFFF), so the query skips them
+    return launch_query(n, LANES, d, planes, sd[slot], 2, sm[slot], a.sizes, s, t, q, best, bad, st);
+  }
+};
+
 int cbfs_query_stream(cbfs_graph* gh, const uint32_t* sources, const uint8_t* sizes, uint32_t n_clusters, uint32_t d,
                       const uint32_t* s, const uint32_t* t, uint64_t q, int32_t* inout_best, uint64_t* out_stats,
                       cbfs_stream stream) {
@@ -168,40 +192,69 @@ int cbfs_query_stream(cbfs_graph* gh, const uint32_t* sources, const uint8_t* si
   if (lease.rc) return lease.rc;
   const uint32_t n = g->n;
   const uint32_t planes = d + 1;
-  uint16_t* bdist = nullptr;
-  uint64_t* bmasks = nullptr;
-  int* bad = nullptr;
-  CBFS_CUDA(cudaMallocAsync(&bdist, sizeof(uint16_t) * (uint64_t)n * LANES + 16, st));
-  CBFS_CUDA(cudaMallocAsync(&bmasks, sizeof(uint64_t) * (uint64_t)planes * n * LANES + 16, st));
-  CBFS_CUDA(cudaMallocAsync(&bad, sizeof(int), st));
-  CBFS_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
-  for (uint32_t cb = 0; cb < n_clusters && rc == CBFS_OK; cb += LANES) {
-    const uint32_t nb = std::min<uint32_t>(LANES, n_clusters - cb);
-    CBFS_CUDA(cudaMemsetAsync(bdist, 0xFF, sizeof(uint16_t) * (uint64_t)n * LANES, st));
-    CBFS_CUDA(cudaMemsetAsync(bmasks, 0, sizeof(uint64_t) * (uint64_t)planes * n * LANES, st));
-    RunArgs a;
-    a.sources = sources + (uint64_t)cb * 64;
-    a.sizes = sizes + cb;
-    a.nb = nb; a.d = d; a.planes = planes; a.dist_bytes = 2; a.C = LANES; a.cbase = 0;
-    a.direction = CBFS_DIR_AUTO;
-    a.out_dist = bdist;
-    a.out_masks = bmasks;
-    a.out_stats = out_stats ? out_stats + (uint64_t)cb * 4 : nullptr;
-    rc = run_batch(g, a, st);
-    if (rc) break;
-    // lanes >= nb stay unreachable (dist 0xFFFF), so the query skips them
-    rc = launch_query(n, LANES, d, planes, bdist, 2, bmasks, sizes + cb, s, t, q, inout_best, bad, st);
+  const int P = num_slots(g);
+  QuerySource src;
+  src.proto.d = d;
+  src.proto.planes = planes;
+  src.proto.dist_bytes = 2;
+  src.proto.direction = CBFS_DIR_AUTO;
+  src.sources = sources;
+  src.sizes = sizes;
+  src.n_clusters = n_clusters;
+  src.out_stats = out_stats;
+  src.n = n; src.d = d; src.planes = planes; src.s = s; src.t = t; src.q = q; src.best = inout_best;
+  src.sd.assign(P, nullptr);
+  src.sm.assign(P, nullptr);
+  for (int k = 0; k < P; ++k) {
+    CBFS_CUDA(cudaMallocAsync(&src.sd[k], sizeof(uint16_t) * (uint64_t)n * LANES + 16, st));
+    CBFS_CUDA(cudaMallocAsync(&src.sm[k], sizeof(uint64_t) * (uint64_t)planes * n * LANES + 16, st));
   }
+  CBFS_CUDA(cudaMallocAsync(&src.bad, sizeof(int), st));
+  CBFS_CUDA(cudaMemsetAsync(src.bad, 0, sizeof(int), st));
+  rc = run_batches(g, src, st);
   int hbad = 0;
-  CBFS_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
-  CBFS_CUDA(cudaFreeAsync(bdist, st));
-  CBFS_CUDA(cudaFreeAsync(bmasks, st));
-  CBFS_CUDA(cudaFreeAsync(bad, st));
+  CBFS_CUDA(cudaMemcpyAsync(&hbad, src.bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  for (int k = 0; k < P; ++k) {
+    CBFS_CUDA(cudaFreeAsync(src.sd[k], st));
+    CBFS_CUDA(cudaFreeAsync(src.sm[k], st));
+  }
+  CBFS_CUDA(cudaFreeAsync(src.bad, st));
   CBFS_CUDA(cudaStreamSynchronize(st));
   if (rc) return rc;
   if (hbad) return fail(CBFS_EINVAL, "query vertex id >= n");
   return CBFS_OK;
 }
+
+// per-slot output staging copied to the caller's host arrays when a batch ends
+struct HostSource : ArraySource {
+  uint32_t n = 0, planes = 0, dist_bytes = 0;
+  uint64_t C = 0;
+  void* h_dist = nullptr;
+  uint64_t* h_masks = nullptr;
+  std::vector<void*> sd;
+  std::vector<uint64_t*> sm;
+  int bind(RunArgs& a, int slot, cudaStream_t st) override {
+    a.out_dist = sd[slot];
+    a.out_masks = sm[slot];
+    a.C = LANES;
+    a.cbase = 0;
+    if (sd[slot]) CBFS_CUDA(cudaMemsetAsync(sd[slot], 0xFF, (uint64_t)n * LANES * dist_bytes, st));
+    if (sm[slot]) CBFS_CUDA(cudaMemsetAsync(sm[slot], 0, sizeof(uint64_t) * (uint64_t)planes * n * LANES, st));
+    return CBFS_OK;
+  }
+  int finished(const RunArgs& a, int slot, cudaStream_t st) override {
+    const uint64_t cb = (uint64_t)(a.sizes - sizes);  // first cluster of the batch
+    if (h_dist)
+      CBFS_CUDA(cudaMemcpy2DAsync((uint8_t*)h_dist + cb * dist_bytes, C * dist_bytes, sd[slot],
+                                  (uint64_t)LANES * dist_bytes, (uint64_t)a.nb * dist_bytes, n,
+                                  cudaMemcpyDeviceToHost, st));
+    if (h_masks)
+      CBFS_CUDA(cudaMemcpy2DAsync(h_masks + cb, C * sizeof(uint64_t), sm[slot], LANES * sizeof(uint64_t),
+                                  (uint64_t)a.nb * sizeof(uint64_t), (uint64_t)planes * n, cudaMemcpyDeviceToHost,
+                                  st));
+    return CBFS_OK;
+  }
+};
 
 int cbfs_run_host(cbfs_graph* gh, const uint32_t* sources, const uint8_t* sizes, uint32_t n_clusters, uint32_t d,
                   uint32_t dist_bytes, void* out_dist, uint64_t* out_masks, uint32_t planes, uint64_t* out_stats,
@@ -215,6 +268,7 @@ int cbfs_run_host(cbfs_graph* gh, const uint32_t* sources, const uint8_t* sizes,
   if (lease.rc) return lease.rc;
   const uint32_t n = g->n;
   const uint64_t C = n_clusters;
+  const int P = num_slots(g);
   uint32_t* dsrc = nullptr;
   uint8_t* dsz = nullptr;
   uint64_t* dstats = nullptr;
@@ -225,60 +279,35 @@ int cbfs_run_host(cbfs_graph* gh, const uint32_t* sources, const uint8_t* sizes,
     CBFS_CUDA(cudaMemcpyAsync(dsrc, sources, sizeof(uint32_t) * 64 * C, cudaMemcpyHostToDevice, st));
     CBFS_CUDA(cudaMemcpyAsync(dsz, sizes, C, cudaMemcpyHostToDevice, st));
   }
-  // double-buffered device staging for one batch: [n][32] dist, [planes][n][32] masks
-  cudaStream_t cp;
-  CBFS_CUDA(cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking));
-  void* sd[2] = {nullptr, nullptr};
-  uint64_t* sm[2] = {nullptr, nullptr};
-  cudaEvent_t done[2], copied[2];
-  for (int b = 0; b < 2; ++b) {
-    if (out_dist) CBFS_CUDA(cudaMallocAsync(&sd[b], (uint64_t)n * LANES * dist_bytes + 16, st));
-    if (out_masks) CBFS_CUDA(cudaMallocAsync(&sm[b], sizeof(uint64_t) * (uint64_t)planes * n * LANES + 16, st));
-    CBFS_CUDA(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming));
-    CBFS_CUDA(cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming));
-    CBFS_CUDA(cudaEventRecord(copied[b], cp));
+  HostSource src;
+  src.proto.d = d;
+  src.proto.planes = planes;
+  src.proto.dist_bytes = dist_bytes;
+  src.proto.direction = direction;
+  src.sources = dsrc;
+  src.sizes = dsz;
+  src.n_clusters = n_clusters;
+  src.out_stats = dstats;
+  src.n = n; src.planes = planes; src.dist_bytes = dist_bytes; src.C = C;
+  src.h_dist = out_dist;
+  src.h_masks = out_masks;
+  src.sd.assign(P, nullptr);
+  src.sm.assign(P, nullptr);
+  for (int k = 0; k < P; ++k) {
+    if (out_dist) CBFS_CUDA(cudaMallocAsync(&src.sd[k], (uint64_t)n * LANES * dist_bytes + 16, st));
+    if (out_masks) CBFS_CUDA(cudaMallocAsync(&src.sm[k], sizeof(uint64_t) * (uint64_t)planes * n * LANES + 16, st));
   }
-  int slot = 0;
-  for (uint32_t cb = 0; cb < n_clusters && rc == CBFS_OK; cb += LANES, slot ^= 1) {
-    const uint32_t nb = std::min<uint32_t>(LANES, n_clusters - cb);
-    CBFS_CUDA(cudaStreamWaitEvent(st, copied[slot], 0));  // staging slot free again
-    if (out_dist) CBFS_CUDA(cudaMemsetAsync(sd[slot], 0xFF, (uint64_t)n * LANES * dist_bytes, st));
-    if (out_masks) CBFS_CUDA(cudaMemsetAsync(sm[slot], 0, sizeof(uint64_t) * (uint64_t)planes * n * LANES, st));
-    RunArgs a;
-    a.sources = dsrc + (uint64_t)cb * 64;
-    a.sizes = dsz + cb;
-    a.nb = nb; a.d = d; a.planes = planes; a.dist_bytes = dist_bytes; a.C = LANES; a.cbase = 0;
-    a.direction = direction;
-    a.out_dist = sd[slot];
-    a.out_masks = sm[slot];
-    a.out_stats = dstats + (uint64_t)cb * 4;
-    rc = run_batch(g, a, st);
-    if (rc) break;
-    CBFS_CUDA(cudaEventRecord(done[slot], st));
-    CBFS_CUDA(cudaStreamWaitEvent(cp, done[slot], 0));
-    if (out_dist)
-      CBFS_CUDA(cudaMemcpy2DAsync((uint8_t*)out_dist + (uint64_t)cb * dist_bytes, C * dist_bytes, sd[slot],
-                                  (uint64_t)LANES * dist_bytes, (uint64_t)nb * dist_bytes, n, cudaMemcpyDeviceToHost,
-                                  cp));
-    if (out_masks)
-      CBFS_CUDA(cudaMemcpy2DAsync(out_masks + cb, C * sizeof(uint64_t), sm[slot], LANES * sizeof(uint64_t),
-                                  (uint64_t)nb * sizeof(uint64_t), (uint64_t)planes * n, cudaMemcpyDeviceToHost, cp));
-    CBFS_CUDA(cudaEventRecord(copied[slot], cp));
-  }
-  CBFS_CUDA(cudaStreamSynchronize(cp));
+  rc = run_batches(g, src, st);
   if (rc == CBFS_OK && out_stats && C)
     CBFS_CUDA(cudaMemcpyAsync(out_stats, dstats, sizeof(uint64_t) * 4 * C, cudaMemcpyDeviceToHost, st));
-  CBFS_CUDA(cudaStreamSynchronize(st));
-  for (int b = 0; b < 2; ++b) {
-    if (sd[b]) cudaFreeAsync(sd[b], st);
-    if (sm[b]) cudaFreeAsync(sm[b], st);
-    cudaEventDestroy(done[b]);
-    cudaEventDestroy(copied[b]);
+  for (int k = 0; k < P; ++k) {
+    if (src.sd[k]) CBFS_CUDA(cudaFreeAsync(src.sd[k], st));
+    if (src.sm[k]) CBFS_CUDA(cudaFreeAsync(src.sm[k], st));
   }
-  cudaStreamDestroy(cp);
-  cudaFreeAsync(dsrc, st);
-  cudaFreeAsync(dsz, st);
-  cudaFreeAsync(dstats, st);
+  CBFS_CUDA(cudaFreeAsync(dsrc, st));
+  CBFS_CUDA(cudaFreeAsync(dsz, st));
+  CBFS_CUDA(cudaFreeAsync(dstats, st));
+  CBFS_CUDA(cudaStreamSynchronize(st));
   return rc;
 }
 

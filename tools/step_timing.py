@@ -30,6 +30,7 @@ def step(parts):
     return t
 
 if os.environ.get("ALPHA"): cb.cbfs_set_direction_alpha(float(os.environ["ALPHA"]))
+if os.environ.get("CONC"): cb.cbfs_set_concurrency(int(os.environ["CONC"]))
 for it in range(3):
     step(None)
 for prof in (False, True, False):
