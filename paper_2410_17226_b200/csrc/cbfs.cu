@@ -338,25 +338,31 @@ __global__ void __launch_bounds__(256) k_push(const uint64_t* __restrict__ off, 
                                               uint64_t* __restrict__ bstats, unsigned long long* __restrict__ ctr,
                                               uint32_t i, uint32_t d) {
   __shared__ unsigned long long sF[LANES], sE[LANES], sM[LANES];
+  __shared__ uint32_t s_out[8][PUSH_CHUNK];  // per-warp claims of the current chunk
   for (uint32_t c = threadIdx.x; c < LANES; c += blockDim.x) sF[c] = sE[c] = sM[c] = 0;
   __syncthreads();
   const uint32_t lane = lane_id();
+  uint32_t* obuf = s_out[threadIdx.x >> 5];
+  const unsigned lt = (1u << lane) - 1;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
   unsigned long long degsum = 0, nu = 0;
   for (uint64_t w = warp; w * PUSH_CHUNK < total; w += nwarps) {
     const uint64_t start = w * PUSH_CHUNK;
     const uint64_t end = min(start + PUSH_CHUNK, total);
-    uint32_t idx = 0;
-    if (lane == 0) {  // largest idx with pre[idx] <= start
-      uint32_t lo = 0, hi = nF - 1;
-      while (lo < hi) {
-        uint32_t mid = (lo + hi + 1) >> 1;
-        if (pre[mid] <= start) lo = mid; else hi = mid - 1;
-      }
-      idx = lo;
+    // largest idx with pre[idx] <= start: 32-ary warp search (log32 steps)
+    uint32_t lo = 0, hi = nF;  // answer in [lo, hi)
+    while (hi - lo > 1) {
+      const uint32_t step = (hi - lo + 31) / 32;
+      const uint32_t pos = lo + lane * step;
+      const bool le = pos < hi && pre[pos] <= start;
+      const uint32_t cntle = __popc(__ballot_sync(FULLW, le));  // probes at or before the answer
+      const uint32_t nlo = lo + (cntle - 1) * step;
+      hi = min(nlo + step, hi);
+      lo = nlo;
     }
-    idx = __shfl_sync(FULLW, idx, 0);
+    uint32_t idx = lo;
+    uint32_t nout = 0;
     for (uint64_t p0 = start; p0 < end; p0 += 32) {
       const uint64_t p = p0 + lane;
       bool claim = false;
@@ -383,9 +389,20 @@ __global__ void __launch_bounds__(256) k_push(const uint64_t* __restrict__ off, 
           }
         }
       }
-      warp_append(claim, ev, out_list, &ctr[0]);
+      const unsigned cm = __ballot_sync(FULLW, claim);
+      if (claim) obuf[nout + __popc(cm & lt)] = ev;
+      nout += __popc(cm);
       nu += warp_set_bit(claim, v, ubits_next);
     }
+    // one global reservation per chunk
+    __syncwarp();
+    if (nout) {
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(&ctr[0], (unsigned long long)nout);
+      base = __shfl_sync(FULLW, base, 0);
+      for (uint32_t t = lane; t < nout; t += 32) out_list[base + t] = obuf[t];
+    }
+    __syncwarp();
   }
   degsum = warp_sum(degsum);
   nu = warp_sum(nu);
