@@ -46,7 +46,7 @@ UNIT = "source-edges/s"
 BYTES_PER_FRONTIER_ARC = 22     # 4 B column + 2 B Delta cap read + 16 B OR-update
 BYTES_PER_FRONTIER_ENTRY = 40   # offsets, frontier id w/r, next read, seen RMW
 BYTES_PER_ARC = 4                # batched pull: one u32 CSR column per arc per launch
-BYTES_PER_VROW = 64 * 2 + 64 * 8  # batched pull: a vertex's Delta row + S_seen row (64 clusters)
+BYTES_PER_VROW = 64 * 2 + 8      # batched pull: a vertex's Delta row (64 clusters) + its 64-bit "subset full" word
 BYTES_PER_ROW = 64 * 8           # batched pull: one 64-cluster bit-subset row
 
 

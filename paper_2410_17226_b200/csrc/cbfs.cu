@@ -48,6 +48,7 @@ struct Slot {
   unsigned long long* ctr = nullptr;    // [0] next count, [1] next E, [2] error bits, [3] |U_next|
   unsigned long long* h_ctr = nullptr;  // pinned mirror
   uint64_t* bstats = nullptr;           // [LANES][4]
+  uint64_t* fullm = nullptr;            // [n] bit c: S_seen[v][c] == S_c (maintained by the fold)
   void* scan_tmp = nullptr;
   size_t scan_bytes = 0;
   cudaStream_t s = nullptr;
@@ -99,6 +100,7 @@ static void slot_free(Slot* w) {
   cudaFree(w->seen); cudaFree(w->pend); cudaFree(w->dist); cudaFree(w->listA); cudaFree(w->listB);
   cudaFree(w->pre); cudaFree(w->ubits); cudaFree(w->ctr); cudaFreeHost(w->h_ctr); cudaFree(w->bstats);
   cudaFree(w->scan_tmp);
+  cudaFree(w->fullm);
   if (w->s) cudaStreamDestroy(w->s);
   if (w->ready) cudaEventDestroy(w->ready);
   for (int k = 0; k < 4; ++k)
@@ -125,6 +127,7 @@ static int slot_alloc(Slot* w, uint64_t cap) {
   CBFS_CUDA(cudaMalloc(&w->ctr, 4 * sizeof(unsigned long long)));
   CBFS_CUDA(cudaMallocHost(&w->h_ctr, 4 * sizeof(unsigned long long)));
   CBFS_CUDA(cudaMalloc(&w->bstats, LANES * 4 * sizeof(uint64_t)));
+  CBFS_CUDA(cudaMalloc(&w->fullm, (cap / LANES + 1) * sizeof(uint64_t)));
   CBFS_CUDA(cudaMemset(w->pend, 0, cap * sizeof(uint64_t)));  // zero-invariant from here on
   CBFS_CUDA(cudaMemset(w->ubits, 0, ubw * sizeof(uint32_t)));  // both bitmaps zero between batches
   CBFS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, w->scan_bytes, w->pre, w->pre, cap));
@@ -276,14 +279,17 @@ __global__ void __launch_bounds__(256) k_fold(const uint32_t* __restrict__ F, ui
                                               const uint32_t* __restrict__ perm, uint32_t n, uint32_t C,
                                               uint32_t cbase, uint32_t planes, void* __restrict__ out_dist,
                                               uint64_t* __restrict__ out_masks, uint64_t* __restrict__ pre,
-                                              int write_pre, unsigned long long* __restrict__ ctr) {
+                                              int write_pre, const uint8_t* __restrict__ sizes,
+                                              uint64_t* __restrict__ fullm, unsigned long long* __restrict__ ctr) {
   const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+  const uint32_t lane = lane_id();
   bool overflow = false;
   for (uint64_t t0 = tid; t0 < nF; t0 += nth * FOLD_ILP) {
     uint32_t e[FOLD_ILP];
     uint64_t nw[FOLD_ILP], sv[FOLD_ILP];
     uint32_t dv[FOLD_ILP];
+    uint32_t fvx[FOLD_ILP];  // vertex whose subset of cluster c just became full, else ~0
 #pragma unroll
     for (int q = 0; q < FOLD_ILP; ++q) {
       const uint64_t t = t0 + q * nth;
@@ -299,10 +305,12 @@ __global__ void __launch_bounds__(256) k_fold(const uint32_t* __restrict__ F, ui
     }
 #pragma unroll
     for (int q = 0; q < FOLD_ILP; ++q) {
+      fvx[q] = 0xFFFFFFFFu;
       if (e[q] == 0xFFFFFFFFu) continue;
       const uint32_t v = e[q] >> LSHIFT, c = e[q] & (LANES - 1);
       pend[e[q]] = 0;
       seen[e[q]] = sv[q] | nw[q];
+      if ((sv[q] | nw[q]) == full_mask(sizes[c])) fvx[q] = v;
       const bool first = dv[q] == INF16;
       if (first) { dv[q] = i; dist[e[q]] = (uint16_t)i; }
       if (write_pre) pre[t0 + q * nth] = off[v + 1] - off[v];
@@ -318,6 +326,18 @@ __global__ void __launch_bounds__(256) k_fold(const uint32_t* __restrict__ F, ui
       }
       const uint32_t oi = i - dv[q];
       if (out_masks && oi < planes) out_masks[(uint64_t)oi * n * C + col] = nw[q];
+    }
+    // per-vertex "subset full" bits (read by the dense pull instead of the
+    // whole S_seen row): one 64-bit atomic per distinct vertex in the warp
+    const unsigned am = __activemask();
+#pragma unroll
+    for (int q = 0; q < FOLD_ILP; ++q) {
+      const bool f = fvx[q] != 0xFFFFFFFFu;
+      const uint64_t bit = f ? (1ULL << (e[q] & (LANES - 1))) : 0ULL;
+      const unsigned grp = __match_any_sync(am, fvx[q]);
+      const uint32_t lo = __reduce_or_sync(grp, (uint32_t)bit), hi = __reduce_or_sync(grp, (uint32_t)(bit >> 32));
+      if (f && lane == (uint32_t)(__ffs(grp) - 1))
+        atomicOr((unsigned long long*)&fullm[fvx[q]], ((unsigned long long)hi << 32) | lo);
     }
   }
   if (overflow) atomicOr(&ctr[2], ERR_OVERFLOW);
@@ -470,7 +490,7 @@ __global__ void __launch_bounds__(PULL_WARPS * 32, CBFS_PULL_MINB) k_pull(
     uint64_t n_chunks, uint64_t m, uint32_t n, const uint64_t* __restrict__ seen, const uint16_t* __restrict__ dist,
     uint64_t* __restrict__ pend, const uint32_t* __restrict__ ubits, uint32_t* __restrict__ ubits_next,
     const uint8_t* __restrict__ sizes, uint32_t nb, uint32_t* __restrict__ out_list, uint64_t* __restrict__ bstats,
-    unsigned long long* __restrict__ ctr, uint32_t i, uint32_t d) {
+    unsigned long long* __restrict__ ctr, const uint64_t* __restrict__ fullm, uint32_t i, uint32_t d) {
   __shared__ uint32_t s_list[PULL_WARPS][PULL_CHUNK + 32];
   __shared__ uint32_t s_cnt[PULL_WARPS][32];
   __shared__ unsigned long long s_stat[PULL_WARPS][3][LANES];  // per-warp F / E / M per cluster
@@ -508,15 +528,15 @@ __global__ void __launch_bounds__(PULL_WARPS * 32, CBFS_PULL_MINB) k_pull(
       unsigned cap0 = 0, cap1 = 0, inf0 = 0, inf1 = 0, actv = 0;
       for (uint32_t j0 = 0; j0 < nv; j0 += 4) {
         uint32_t dq[4];
-        U2 sq[4];
+        uint64_t fq[4];  // "subset full" bits of the vertex (one broadcast load)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const uint32_t j = j0 + q;
           dq[q] = 0xFFFFFFFFu;
-          sq[q] = {0, 0};
+          fq[q] = ~0ULL;
           if (j < nv && ((hasarcs >> j) & 1u)) {
             dq[q] = dist2[(uint64_t)(v + j) * (LANES / 2)];
-            sq[q] = ld2(seen2 + (uint64_t)(v + j) * LANES);
+            fq[q] = fullm[v + j];
           }
         }
 #pragma unroll
@@ -524,8 +544,8 @@ __global__ void __launch_bounds__(PULL_WARPS * 32, CBFS_PULL_MINB) k_pull(
           const uint32_t j = j0 + q;
           if (j < nv && ((hasarcs >> j) & 1u)) {
             const uint32_t d0 = dq[q] & 0xFFFFu, d1 = dq[q] >> 16;
-            const bool k0 = full0 != 0 && (d0 == INF16 || (int)i - (int)d0 < (int)d) && sq[q].a != full0;
-            const bool k1 = full1 != 0 && (d1 == INF16 || (int)i - (int)d1 < (int)d) && sq[q].b != full1;
+            const bool k0 = full0 != 0 && (d0 == INF16 || (int)i - (int)d0 < (int)d) && !((fq[q] >> c0) & 1ULL);
+            const bool k1 = full1 != 0 && (d1 == INF16 || (int)i - (int)d1 < (int)d) && !((fq[q] >> c1) & 1ULL);
             cap0 |= (unsigned)k0 << j;
             cap1 |= (unsigned)k1 << j;
             inf0 |= (unsigned)(d0 == INF16) << j;
@@ -689,6 +709,7 @@ static int slot_start(Graph* g, Slot* w, const RunArgs& a) {
   CBFS_CUDA(cudaMemsetAsync(w->seen, 0, (uint64_t)(n + 1) * LANES * sizeof(uint64_t), st));
   CBFS_CUDA(cudaMemsetAsync(w->dist, 0xFF, (uint64_t)n * LANES * sizeof(uint16_t), st));
   CBFS_CUDA(cudaMemsetAsync(w->bstats, 0, LANES * 4 * sizeof(uint64_t), st));
+  CBFS_CUDA(cudaMemsetAsync(w->fullm, 0, (uint64_t)(n + 1) * sizeof(uint64_t), st));
   CBFS_CUDA(cudaMemsetAsync(w->ctr, 0, 4 * sizeof(unsigned long long), st));
   k_seed<<<(a.nb * 64 + 255) / 256, 256, 0, st>>>(a.sources, a.sizes, a.nb, n, g->inv, g->off, w->pend, w->listA,
                                                    w->ubits, w->bstats, w->ctr);
@@ -713,10 +734,12 @@ static int slot_round(Graph* g, Slot* w) {
   if (g_prof.on) CBFS_CUDA(cudaEventRecord(w->pe[0], st));
   if (a.dist_bytes == 1)
     k_fold<1><<<fb, 256, 0, st>>>(w->cur, (uint32_t)nF, i, w->seen, w->pend, w->dist, g->off, g->perm, n, a.C,
-                                  a.cbase, a.planes, a.out_dist, a.out_masks, w->pre, write_pre, w->ctr);
+                                  a.cbase, a.planes, a.out_dist, a.out_masks, w->pre, write_pre, a.sizes, w->fullm,
+                                  w->ctr);
   else
     k_fold<2><<<fb, 256, 0, st>>>(w->cur, (uint32_t)nF, i, w->seen, w->pend, w->dist, g->off, g->perm, n, a.C,
-                                  a.cbase, a.planes, a.out_dist, a.out_masks, w->pre, write_pre, w->ctr);
+                                  a.cbase, a.planes, a.out_dist, a.out_masks, w->pre, write_pre, a.sizes, w->fullm,
+                                  w->ctr);
   CBFS_LAUNCHED();
   if (g_prof.on) CBFS_CUDA(cudaEventRecord(w->pe[1], st));
   CBFS_CUDA(cudaMemsetAsync(w->ctr, 0, 2 * sizeof(unsigned long long), st));
@@ -727,7 +750,8 @@ static int slot_round(Graph* g, Slot* w) {
     if (g_prof.on) CBFS_CUDA(cudaEventRecord(w->pe[2], st));
     const unsigned pb = grid_for(g->n_chunks * 32, PULL_WARPS * 32, 148u * 8u);
     k_pull<<<pb, PULL_WARPS * 32, 0, st>>>(g->off, g->cols, g->chunk_v, g->n_chunks, g->m, n, w->seen, w->dist,
-                                           w->pend, ub_cur, ub_nxt, a.sizes, a.nb, w->nxt, w->bstats, w->ctr, i, a.d);
+                                           w->pend, ub_cur, ub_nxt, a.sizes, a.nb, w->nxt, w->bstats, w->ctr, w->fullm,
+                                           i, a.d);
     CBFS_LAUNCHED();
     if (g_prof.on) CBFS_CUDA(cudaEventRecord(w->pe[3], st));
   } else if (E > 0) {
