@@ -1,7 +1,7 @@
 """Run one BASELINE.json config at full size on the GPU and (optionally) check
 sampled clusters against the oracle.
 
-    python tools/run_config.py c4_grid [--check 8] [--first-batch-outputs]
+    python tests/run_config.py c4_grid [--check 8] [--first-batch-outputs]
 
 Prints one JSON line: timings of build / selection / C-BFS (outputs not
 materialised for the whole config when they do not fit; stats always),
