@@ -253,6 +253,8 @@ def run_ours(args, world, rank, local):
     stream = torch.cuda.current_stream()
     if args.alpha:
         cb.cbfs_set_direction_alpha(args.alpha)
+    if args.concurrency:
+        cb.cbfs_set_concurrency(args.concurrency)
 
     phase_ms = {"build": 0.0, "select": 0.0, "cbfs": 0.0}
 
@@ -452,6 +454,7 @@ def main():
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--separate-select", action="store_true", help="select, then run (no A1/A2-A8 overlap)")
     ap.add_argument("--clock-ms", type=int, default=500)
+    ap.add_argument("--concurrency", type=int, default=0, help="concurrent batches per GPU (0 = library default)")
     args = ap.parse_args()
     world, rank, local = dist_init()
     if args.impl == "reference":

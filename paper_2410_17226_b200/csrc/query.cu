@@ -62,7 +62,11 @@ __global__ void __launch_bounds__(256) k_query(uint32_t n, uint32_t C, uint32_t 
       if (lane == 0) *bad = 1;
       continue;
     }
-    int32_t mine = 0x7FFFFFFF;
+    // start from the answer so far (earlier batches / label shards): a
+    // cluster whose Delta sum cannot beat it is skipped before its subsets
+    // are read
+    const int32_t prev = best[qi];
+    int32_t mine = prev;
     for (uint32_t c = lane; c < C; c += 32) {
       const uint32_t da = load_dist<DB>(dist, (uint64_t)a * C + c);
       const uint32_t db = load_dist<DB>(dist, (uint64_t)b * C + c);
@@ -95,7 +99,7 @@ __global__ void __launch_bounds__(256) k_query(uint32_t n, uint32_t C, uint32_t 
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mine = min(mine, __shfl_xor_sync(0xFFFFFFFFu, mine, o));
-    if (lane == 0 && mine < 0x7FFFFFFF) atomicMin(&best[qi], mine);  // concurrent batches min-merge
+    if (lane == 0 && mine < prev) atomicMin(&best[qi], mine);  // concurrent batches min-merge
   }
 }
 

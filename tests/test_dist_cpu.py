@@ -65,3 +65,69 @@ def test_reference_arm_under_torchrun():
     j = json.loads(lines[0])
     assert j["impl"] == "reference" and j["unit"] == "source-edges/s" and j["value"] > 0
     assert j["cpu_baseline"]["kind"] == "oracle" and j["e2e"]["h2d_bytes_per_step"] == 0
+
+
+# ---------------------------------------------------------------- A12
+def _a12_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    sys.path.insert(0, ROOT)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import cbfs_inputs as ci
+    import oracle as orc
+    from paper_2410_17226_b200 import distributed as pd
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    el = ci.erdos_renyi(400, 900, seed=11)
+    g = orc.csr_from_edgelist(el)
+    d = 2
+    src, sz = orc.select_clusters(g, 11, 64, d, orc.ROOT_DEGREE, 0)  # 11 clusters: ragged over 2 ranks
+    C = len(sz)
+    s, t = ci.query_pairs(g.n, 500, seed=5)
+    # the rank's clusters (round-robin) -> its partial answers -> MIN all-reduce
+    idx = pd.cluster_shard(C, world, rank).numpy()
+    part = orc.query_stream(g, src[idx], sz[idx], d, s, t, threads=1) if len(idx) else \
+        np.full(len(s), orc.INT32_MAX, np.int32)
+    best = pd.min_reduce_answers(torch.from_numpy(part.copy()))
+    # label shards padded to shard_width columns with unreachable clusters, all-gathered
+    W = pd.shard_width(C, world)
+    r = orc.cluster_bfs_many(g, src[idx], sz[idx], d, threads=1)
+    dist_sh = np.full((W, g.n), 0xFFFF, np.uint16)
+    sub_sh = np.zeros((W, d + 1, g.n), np.uint64)
+    dist_sh[:len(idx)] = r["dist"]
+    sub_sh[:len(idx)] = r["sub"]
+    parts = pd.all_gather_shards([torch.from_numpy(dist_sh.view(np.int16)), torch.from_numpy(sub_sh.view(np.int64))])
+    merged = np.full(len(s), orc.INT32_MAX, np.int32)
+    for dp, mp_ in zip(*parts):
+        merged = np.minimum(merged, orc.query(dp.numpy().view(np.uint16), mp_.numpy().view(np.uint64), s, t))
+    full = orc.query_stream(g, src, sz, d, s, t, threads=1)
+    out.put((rank, idx.tolist(), bool(np.array_equal(best.numpy(), full)), bool(np.array_equal(merged, full)),
+             int((full < orc.INT32_MAX).sum())))
+    dist.destroy_process_group()
+
+
+def test_a12_shard_min_reduce_and_label_gather_gloo():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_a12_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=180) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0][1] == [0, 2, 4, 6, 8, 10] and res[1][1] == [1, 3, 5, 7, 9]
+    for _, _, ok_min, ok_gather, reached in res:
+        assert ok_min and ok_gather and reached > 0
+
+
+def test_cluster_shard_partition():
+    from paper_2410_17226_b200 import distributed as pd
+    for C in (0, 1, 7, 64, 1024, 1031):
+        for R in (1, 2, 3, 8):
+            parts = [pd.cluster_shard(C, R, r).tolist() for r in range(R)]
+            assert sorted(sum(parts, [])) == list(range(C))
+            assert max((len(p) for p in parts), default=0) <= pd.shard_width(C, R)
