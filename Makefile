@@ -6,12 +6,12 @@ NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -std=c++17 $(ARCH) -O3 -lineinfo -Xcompiler -fPIC -Xptxas -v
 CSRC := paper_2410_17226_b200/csrc
-SRCS := $(CSRC)/graph.cu $(CSRC)/cbfs.cu $(CSRC)/select.cu $(CSRC)/query.cu
+SRCS := $(CSRC)/graph.cu $(CSRC)/cbfs.cu $(CSRC)/sparse.cu $(CSRC)/select.cu $(CSRC)/query.cu
 OBJS := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
 
 all: paper_2410_17226_b200/libcbfs.so oracle/liboracle.so cbfs_inputs/libcbfsgen.so
 
-build/%.o: $(CSRC)/%.cu $(CSRC)/common.cuh include/cbfs.h
+build/%.o: $(CSRC)/%.cu $(CSRC)/common.cuh $(CSRC)/engine.cuh include/cbfs.h
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
 

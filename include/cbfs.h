@@ -69,6 +69,8 @@ enum { CBFS_RELABEL_DEGREE = 2, CBFS_INPUT_DEVICE = 4 };
 enum { CBFS_ROOT_DEGREE = 0, CBFS_ROOT_RANDOM = 1 };
 /* EdgeMap direction policy (R8: parity-neutral) */
 enum { CBFS_DIR_AUTO = 0, CBFS_DIR_PUSH = 1, CBFS_DIR_PULL = 2 };
+/* traversal engines (cbfs_set_engine; identical outputs, R8/R25) */
+enum { CBFS_ENGINE_AUTO = 0, CBFS_ENGINE_BATCHED = 1, CBFS_ENGINE_SPARSE = 2 };
 
 /* --------------------------------------------------------------- graph
  * cbfs_graph_create — build the device CSR of an UNDIRECTED graph from an
@@ -205,11 +207,23 @@ int cbfs_query_stream(cbfs_graph* g, const uint32_t* sources, const uint8_t* siz
  * exceeds batch_clusters * m / alpha (default 100; S:186 suggests 20 for a
  * single source; tunable, parity-neutral R8). */
 int cbfs_set_direction_alpha(double alpha);
+/* Traversal engine for later cbfs_run / cbfs_select_and_run / cbfs_run_host /
+ * cbfs_query_stream calls (process-wide):
+ *   CBFS_ENGINE_BATCHED — vertex-major state rows shared by the 64 clusters
+ *     of a batch, host-driven rounds, push/pull switch (low-diameter graphs);
+ *   CBFS_ENGINE_SPARSE  — cluster-major state, push-only rounds, the round
+ *     loop on the device (CUDA-graph while node) (high-diameter graphs);
+ *   CBFS_ENGINE_AUTO (default) — SPARSE when a BFS from the highest-degree
+ *     vertex is still running after 48 levels, else BATCHED (cached per graph).
+ * direction == CBFS_DIR_PULL always uses BATCHED.  Outputs are identical.
+ * Errors: EINVAL (unknown engine). */
+int cbfs_set_engine(int engine);
 /* Kernel-level timing of the C-BFS engine (process-wide, not thread-safe):
  * when enabled, CUDA events are recorded on the launching stream around every
  * fold / push / pull launch and read after the round's synchronisation.
- * cbfs_profile_read fills arrays of 3 entries indexed {0 fold, 1 push,
- * 2 pull}: total device ms, launches, frontier (cluster, arc) pairs,
+ * cbfs_profile_read fills arrays of 4 entries indexed {0 fold, 1 push,
+ * 2 pull, 3 sparse-engine round loop (one graph launch per batch; its
+ * "launches" count the kernels the loop ran)}: total device ms, launches, frontier (cluster, arc) pairs,
  * frontier (vertex, cluster) entries, distinct frontier vertices |U_i| and
  * distinct vertices claimed for the next frontier |U_{i+1}| summed over the
  * launches (host pointers, any may be NULL). */

@@ -75,6 +75,8 @@ def lib():
                                u32p, i32p]
         L.or_query_stream.argtypes = [ctypes.c_uint32, u64p, u32p, u32p, u8p, ctypes.c_uint32, ctypes.c_uint32,
                                       ctypes.c_uint64, u32p, u32p, ctypes.c_int, i32p]
+        L.or_csr_build.restype = ctypes.c_int64
+        L.or_csr_build.argtypes = [ctypes.c_uint32, ctypes.c_uint64, u32p, u32p, ctypes.c_int, u32p, u64p]
         L.or_record_bytes.restype = ctypes.c_int64
         L.or_record_bytes.argtypes = [ctypes.c_uint32, ctypes.c_uint32]
         L.or_budget_to_clusters.restype = ctypes.c_int64
@@ -129,7 +131,24 @@ def csr_from_edges(n: int, src: np.ndarray, dst: np.ndarray) -> CSR:
     return CSR(n, off, np.ascontiguousarray(cols))
 
 
+def csr_from_edges_c(n: int, src: np.ndarray, dst: np.ndarray, threads: int | None = None) -> CSR:
+    """Same normalisation in C (oracle.c or_csr_build: per-row sort + dedup),
+    for edge lists too large for numpy's unique (config 3: 537M pairs)."""
+    src = np.ascontiguousarray(src, dtype=np.uint32)
+    dst = np.ascontiguousarray(dst, dtype=np.uint32)
+    work = np.empty(max(1, 2 * len(src)), np.uint32)
+    off = np.zeros(n + 1, np.uint64)
+    m = lib().or_csr_build(n, len(src), _p(src, ctypes.c_uint32), _p(dst, ctypes.c_uint32),
+                           threads or default_threads(), _p(work, ctypes.c_uint32), _p(off, ctypes.c_uint64))
+    if m < 0:
+        raise ValueError("vertex id out of range")
+    cols = work[:m].copy() if m < len(work) // 2 else work[:m]
+    return CSR(n, off, cols)
+
+
 def csr_from_edgelist(el) -> CSR:
+    if len(el.src) > (8 << 20):
+        return csr_from_edges_c(el.n, el.src, el.dst)
     return csr_from_edges(el.n, el.src, el.dst)
 
 

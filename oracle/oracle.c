@@ -415,3 +415,75 @@ int64_t or_budget_to_clusters(uint64_t t, uint32_t w, uint32_t d) {
   if ((int64_t)t < rb) return -1;
   return (int64_t)t / rb;
 }
+
+/* ---------------------------------------------------------------------
+ * csr_build — graph normalisation (R17) for edge lists too large
+ * for numpy's unique: every pair {u,v} with u != v becomes arcs u->v and
+ * v->u, each row is sorted and its duplicates dropped.  Same result as
+ * csr_from_edges in oracle/__init__.py (pinned against scipy there).
+ *   work : [2 * P] uint32 scratch; on return work[0..m) holds the columns
+ *   off  : [n+1] uint64 row offsets.  Returns m, or -1 on an id >= n.
+ * Rows are sorted by `threads` threads (qsort per row).
+ * ------------------------------------------------------------------- */
+static int cmp_u32(const void* a, const void* b) {
+  uint32_t x = *(const uint32_t*)a, y = *(const uint32_t*)b;
+  return (x > y) - (x < y);
+}
+
+typedef struct { uint32_t lo, hi; uint64_t* start; uint32_t* work; uint64_t* kept; } csr_job;
+
+static void* csr_sort_rows(void* p) {
+  csr_job* J = (csr_job*)p;
+  for (uint32_t v = J->lo; v < J->hi; ++v) {
+    uint32_t* row = J->work + J->start[v];
+    uint64_t len = J->start[v + 1] - J->start[v];
+    qsort(row, len, sizeof(uint32_t), cmp_u32);
+    uint64_t k = 0;
+    for (uint64_t e = 0; e < len; ++e)
+      if (k == 0 || row[e] != row[k - 1]) row[k++] = row[e];
+    J->kept[v] = k;
+  }
+  return NULL;
+}
+
+int64_t or_csr_build(uint32_t n, uint64_t P, const uint32_t* src, const uint32_t* dst, int threads, uint32_t* work,
+                     uint64_t* off) {
+  uint64_t* start = (uint64_t*)calloc((size_t)n + 1, sizeof(uint64_t));
+  uint64_t* kept = (uint64_t*)calloc((size_t)n + 1, sizeof(uint64_t));
+  for (uint64_t e = 0; e < P; ++e) {
+    if (src[e] >= n || dst[e] >= n) { free(start); free(kept); return -1; }
+    if (src[e] == dst[e]) continue;  /* self loops dropped */
+    start[src[e] + 1]++;
+    start[dst[e] + 1]++;
+  }
+  for (uint32_t v = 0; v < n; ++v) start[v + 1] += start[v];
+  uint64_t* fill = (uint64_t*)malloc(sizeof(uint64_t) * ((size_t)n + 1));
+  memcpy(fill, start, sizeof(uint64_t) * ((size_t)n + 1));
+  for (uint64_t e = 0; e < P; ++e) {
+    uint32_t u = src[e], v = dst[e];
+    if (u == v) continue;
+    work[fill[u]++] = v;
+    work[fill[v]++] = u;
+  }
+  free(fill);
+  if (threads < 1) threads = 1;
+  pthread_t* th = (pthread_t*)calloc((size_t)threads, sizeof(pthread_t));
+  csr_job* jobs = (csr_job*)calloc((size_t)threads, sizeof(csr_job));
+  for (int t = 0; t < threads; ++t) {
+    jobs[t].lo = (uint32_t)((uint64_t)n * t / threads);
+    jobs[t].hi = (uint32_t)((uint64_t)n * (t + 1) / threads);
+    jobs[t].start = start; jobs[t].work = work; jobs[t].kept = kept;
+    pthread_create(&th[t], NULL, csr_sort_rows, &jobs[t]);
+  }
+  for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
+  free(th); free(jobs);
+  /* compact the deduplicated rows to the front of work */
+  off[0] = 0;
+  for (uint32_t v = 0; v < n; ++v) {
+    memmove(work + off[v], work + start[v], sizeof(uint32_t) * kept[v]);
+    off[v + 1] = off[v] + kept[v];
+  }
+  int64_t m = (int64_t)off[n];
+  free(start); free(kept);
+  return m;
+}

@@ -31,6 +31,7 @@ CBFS_QUERY_UNREACHED = 0x7FFFFFFF
 CBFS_RELABEL_DEGREE, CBFS_INPUT_DEVICE = 2, 4
 CBFS_ROOT_DEGREE, CBFS_ROOT_RANDOM = 0, 1
 CBFS_DIR_AUTO, CBFS_DIR_PUSH, CBFS_DIR_PULL = 0, 1, 2
+CBFS_ENGINE_AUTO, CBFS_ENGINE_BATCHED, CBFS_ENGINE_SPARSE = 0, 1, 2
 
 _vp, _u32, _u64, _i32 = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int
 
@@ -57,6 +58,7 @@ _sig("cbfs_query_distance", [_u32, _u32, _u32, _u32, _vp, _u32, _vp, _vp, _vp, _
 _sig("cbfs_query_stream", [_vp, _vp, _vp, _u32, _u32, _vp, _vp, _u64, _vp, _vp, _vp])
 _sig("cbfs_set_direction_alpha", [ctypes.c_double])
 _sig("cbfs_set_concurrency", [_i32])
+_sig("cbfs_set_engine", [_i32])
 _sig("cbfs_profile_enable", [_i32])
 _sig("cbfs_profile_read", [_vp, _vp, _vp, _vp, _vp, _vp, _i32])
 _sig("cbfs_graph_nonisolated", [_vp, ctypes.POINTER(_u32)])
@@ -185,17 +187,21 @@ def cbfs_set_concurrency(batches: int):
     _check(_lib.cbfs_set_concurrency(batches))
 
 
+def cbfs_set_engine(engine: int):
+    _check(_lib.cbfs_set_engine(engine))
+
+
 def cbfs_profile_enable(on: bool = True):
     _check(_lib.cbfs_profile_enable(int(on)))
 
 
 def cbfs_profile_read(reset: bool = False) -> dict:
-    ms = np.zeros(3, np.float64)
-    la, arcs, ent, ui, uo = (np.zeros(3, np.uint64) for _ in range(5))
+    ms = np.zeros(4, np.float64)
+    la, arcs, ent, ui, uo = (np.zeros(4, np.uint64) for _ in range(5))
     _check(_lib.cbfs_profile_read(_ptr(ms), _ptr(la), _ptr(arcs), _ptr(ent), _ptr(ui), _ptr(uo), int(reset)))
     return {name: dict(ms=float(ms[i]), launches=int(la[i]), arcs=int(arcs[i]), entries=int(ent[i]),
                        u_in=int(ui[i]), u_out=int(uo[i]))
-            for i, name in enumerate(("fold", "push", "pull"))}
+            for i, name in enumerate(("fold", "push", "pull", "sparse"))}
 
 
 def cbfs_graph_nonisolated(h) -> int:

@@ -28,47 +28,9 @@
 #include <thread>
 #include <vector>
 
-#include "common.cuh"
+#include "engine.cuh"
 
 namespace cbfs {
-
-// One in-flight batch of LANES clusters: its workspace, its stream, and the
-// state of its round loop.  Several slots run concurrently (run_batches), so
-// the small rounds and the latency-bound dense rounds of different batches
-// overlap on the GPU.
-struct Slot {
-  uint64_t cap = 0;                     // n * LANES entries
-  uint64_t* seen = nullptr;             // [n+1][64] S_seen (row n stays zero)
-  uint64_t* pend = nullptr;             // [n][64] S_next \ S_seen (pending)
-  uint16_t* dist = nullptr;             // [n][64] Delta
-  uint32_t* listA = nullptr;            // frontier lists (packed v*64+c)
-  uint32_t* listB = nullptr;
-  uint64_t* pre = nullptr;              // [cap + 1] degrees -> exclusive prefix (push)
-  uint32_t* ubits = nullptr;            // 2 x [n/32 + 1]: union frontier U_i, U_{i+1}
-  unsigned long long* ctr = nullptr;    // [0] next count, [1] next E, [2] error bits, [3] |U_next|
-  unsigned long long* h_ctr = nullptr;  // pinned mirror
-  uint64_t* bstats = nullptr;           // [LANES][4]
-  uint64_t* fullm = nullptr;            // [n] bit c: S_seen[v][c] == S_c (maintained by the fold)
-  void* scan_tmp = nullptr;
-  size_t scan_bytes = 0;
-  cudaStream_t s = nullptr;
-  cudaEvent_t ready = nullptr;  // counters of the last queued round are on the host
-  cudaEvent_t pe[4] = {nullptr, nullptr, nullptr, nullptr};  // profiling
-  // round-loop state
-  bool busy = false;
-  bool seeding = false;
-  RunArgs a{};
-  uint32_t i = 0;
-  uint64_t nF = 0, E = 0, U = 0;
-  uint32_t *cur = nullptr, *nxt = nullptr;
-  int kind = -1;
-  bool overflow = false;
-};
-
-struct DevSlots {
-  std::vector<Slot*> slots;
-  uint64_t cap = 0;
-};
 
 static double g_alpha = 100.0;
 static int g_max_slots = 4;
@@ -77,7 +39,7 @@ static int g_max_slots = 4;
 // the launching stream around each fold / push / pull launch; read after the
 // round's counters arrive, so no extra sync is added.  With concurrent
 // batches a launch's time includes the time it shares the GPU.
-enum { PK_FOLD = 0, PK_PUSH = 1, PK_PULL = 2, PK_N = 4 };
+enum { PK_FOLD = 0, PK_PUSH = 1, PK_PULL = 2, PK_SPARSE = 3, PK_N = 4 };
 struct Prof {
   bool on = false;
   double ms[PK_N] = {0, 0, 0, 0};
@@ -101,6 +63,7 @@ static void slot_free(Slot* w) {
   cudaFree(w->pre); cudaFree(w->ubits); cudaFree(w->ctr); cudaFreeHost(w->h_ctr); cudaFree(w->bstats);
   cudaFree(w->scan_tmp);
   cudaFree(w->fullm);
+  sparse_free(w);
   if (w->s) cudaStreamDestroy(w->s);
   if (w->ready) cudaEventDestroy(w->ready);
   for (int k = 0; k < 4; ++k)
@@ -135,7 +98,7 @@ static int slot_alloc(Slot* w, uint64_t cap) {
   CBFS_CUDA(cudaStreamCreateWithFlags(&w->s, cudaStreamNonBlocking));
   CBFS_CUDA(cudaEventCreateWithFlags(&w->ready, cudaEventDisableTiming));
   for (int k = 0; k < 4; ++k) CBFS_CUDA(cudaEventCreate(&w->pe[k]));
-  return CBFS_OK;
+  return sparse_alloc(w);
 }
 
 static int work_grow(DevSlots& D, uint32_t n) {
@@ -171,13 +134,8 @@ WorkLease::~WorkLease() {
   if (locked_) g_work_mu[g_->device].unlock();
 }
 
-enum : unsigned long long { ERR_BAD_SOURCE = 1, ERR_DUP_SOURCE = 2, ERR_BAD_SIZE = 4, ERR_OVERFLOW = 8 };
-
-constexpr unsigned FULLW = 0xFFFFFFFFu;
 constexpr uint32_t LSHIFT = 6;  // log2(LANES)
 static_assert((1u << LSHIFT) == LANES, "LANES must be 64");
-
-__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 
 // warp-aggregated append of `e` for lanes with `flag`
 __device__ __forceinline__ void warp_append(bool flag, uint32_t e, uint32_t* __restrict__ list,
@@ -190,12 +148,6 @@ __device__ __forceinline__ void warp_append(bool flag, uint32_t e, uint32_t* __r
   if ((int)lane == leader) base = atomicAdd(count, (unsigned long long)__popc(mask));
   base = __shfl_sync(FULLW, base, leader);
   if (flag) list[base + __popc(mask & ((1u << lane) - 1))] = e;
-}
-
-__device__ __forceinline__ unsigned long long warp_sum(unsigned long long x) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULLW, x, o);
-  return x;
 }
 
 // union-frontier bit of vertex v, one atomic per distinct word in the warp
@@ -704,6 +656,8 @@ static int slot_start(Graph* g, Slot* w, const RunArgs& a) {
   w->seeding = true;
   w->overflow = false;
   w->i = 0;
+  w->engine = a.engine;
+  if (a.engine == ENGINE_SPARSE) return sparse_start(g, w, a);
   w->cur = w->listA;
   w->nxt = w->listB;
   CBFS_CUDA(cudaMemsetAsync(w->seen, 0, (uint64_t)(n + 1) * LANES * sizeof(uint64_t), st));
@@ -756,6 +710,7 @@ static int slot_round(Graph* g, Slot* w) {
     if (g_prof.on) CBFS_CUDA(cudaEventRecord(w->pe[3], st));
   } else if (E > 0) {
     w->kind = PK_PUSH;
+    w->pre_zero = false;
     CBFS_CUDA(cub::DeviceScan::ExclusiveSum(w->scan_tmp, w->scan_bytes, w->pre, w->pre, nF, st));
     count_launch(2);
     k_set_u64<<<1, 1, 0, st>>>(w->pre + nF, E);
@@ -774,7 +729,58 @@ static int slot_round(Graph* g, Slot* w) {
 
 // The slot's counters arrived: account the finished round, then queue the
 // next one or finish the batch.  Returns 1 when the batch finished.
+static int finish_batch(Slot* w, BatchSource& src, int slot, int* err) {
+  if (w->a.out_stats)
+    CBFS_CUDA(cudaMemcpyAsync(w->a.out_stats, w->bstats, (uint64_t)w->a.nb * 4 * sizeof(uint64_t),
+                              cudaMemcpyDeviceToDevice, w->s));
+  int rc = src.finished(w->a, slot, w->s);
+  w->busy = false;
+  if (rc) *err = rc;
+  if (w->overflow && !*err) *err = fail(CBFS_EOVERFLOW, "a distance exceeds 254 with dist_bytes == 1");
+  return 1;
+}
+
+static int seed_error(Slot* w, unsigned long long bits, int* err) {
+  w->busy = false;
+  if (bits & ERR_BAD_SIZE) *err = fail(CBFS_EINVAL, "cluster size must be 1..64");
+  else if (bits & ERR_BAD_SOURCE) *err = fail(CBFS_EINVAL, "source id >= n");
+  else *err = fail(CBFS_EINVAL, "duplicate source in a cluster");
+  return 1;
+}
+
+// sparse engine: seeding checked -> the device-side round loop -> done
+static int sparse_step(Graph* g, Slot* w, BatchSource& src, int slot, int* err) {
+  const SpCtl& h = *w->sp_ctl_h;
+  if (w->seeding) {
+    w->seeding = false;
+    if (h.err) {  // bad sources: restore the zero invariant of the first pending buffer, report
+      CBFS_CUDA(cudaMemsetAsync(w->pend, 0, (uint64_t)g->n * LANES * sizeof(uint64_t), w->s));
+      CBFS_CUDA(cudaStreamSynchronize(w->s));
+      return seed_error(w, h.err, err);
+    }
+    int rc = sparse_launch(w);
+    if (rc) { *err = rc; w->busy = false; return 1; }
+    return 0;
+  }
+  count_launch(3 * h.i);  // fold + push + tail per round, launched by the graph
+  if (g_prof.on) {
+    float ms = 0;
+    CBFS_CUDA(cudaEventElapsedTime(&ms, w->sp_t0, w->sp_t1));
+    g_prof.ms[PK_SPARSE] += ms; g_prof.launches[PK_SPARSE] += 3 * h.i;
+  }
+  w->i = (uint32_t)h.i;
+  if (h.err & ERR_ROUNDS) {
+    w->busy = false;
+    w->pre_zero = false;  // pending entries of the last round are left; the caller's error path clears them
+    *err = fail(CBFS_EOVERFLOW, "more than 65534 rounds");
+    return 1;
+  }
+  if (h.err & ERR_OVERFLOW) w->overflow = true;
+  return finish_batch(w, src, slot, err);
+}
+
 static int slot_step(Graph* g, Slot* w, BatchSource& src, int slot, int* err) {
+  if (w->engine == ENGINE_SPARSE) return sparse_step(g, w, src, slot, err);
   const uint32_t n = g->n;
   if (w->seeding) {
     w->seeding = false;
@@ -782,11 +788,7 @@ static int slot_step(Graph* g, Slot* w, BatchSource& src, int slot, int* err) {
       CBFS_CUDA(cudaMemsetAsync(w->pend, 0, (uint64_t)n * LANES * sizeof(uint64_t), w->s));
       CBFS_CUDA(cudaMemsetAsync(w->ubits, 0, 2 * ((n >> 5) + 1) * sizeof(uint32_t), w->s));
       CBFS_CUDA(cudaStreamSynchronize(w->s));
-      w->busy = false;
-      if (w->h_ctr[2] & ERR_BAD_SIZE) *err = fail(CBFS_EINVAL, "cluster size must be 1..64");
-      else if (w->h_ctr[2] & ERR_BAD_SOURCE) *err = fail(CBFS_EINVAL, "source id >= n");
-      else *err = fail(CBFS_EINVAL, "duplicate source in a cluster");
-      return 1;
+      return seed_error(w, w->h_ctr[2], err);
     }
   } else {
     if (g_prof.on) {
@@ -806,17 +808,9 @@ static int slot_step(Graph* g, Slot* w, BatchSource& src, int slot, int* err) {
   w->nF = w->h_ctr[0];
   w->E = w->h_ctr[1];
   w->U = w->h_ctr[3];
-  if (w->nF == 0) {  // batch done
-    if (w->a.out_stats)
-      CBFS_CUDA(cudaMemcpyAsync(w->a.out_stats, w->bstats, (uint64_t)w->a.nb * 4 * sizeof(uint64_t),
-                                cudaMemcpyDeviceToDevice, w->s));
-    int rc = src.finished(w->a, slot, w->s);
-    w->busy = false;
-    if (rc) *err = rc;
-    if (w->overflow && !*err) *err = fail(CBFS_EOVERFLOW, "a distance exceeds 254 with dist_bytes == 1");
-    return 1;
-  }
+  if (w->nF == 0) return finish_batch(w, src, slot, err);  // batch done
   if (w->i >= 0xFFFEu) {
+    w->busy = false;
     *err = fail(CBFS_EOVERFLOW, "more than 65534 rounds");
     return 1;  // pend is left non-zero only for this slot's pending entries; cleared below
   }
@@ -882,6 +876,7 @@ int run_batches(Graph* g, BatchSource& src, cudaStream_t st) {
       CBFS_CUDA(cudaMemset(w->pend, 0, D.cap * sizeof(uint64_t)));
       CBFS_CUDA(cudaMemset(w->ubits, 0, 2 * ((D.cap / LANES >> 5) + 1) * sizeof(uint32_t)));
       w->busy = false;
+      w->pre_zero = false;
     }
   }
   return err;
@@ -938,6 +933,8 @@ int cbfs_run(cbfs_graph* gh, const uint32_t* sources, const uint8_t* sizes, uint
   src.proto.dist_bytes = dist_bytes;
   src.proto.C = n_clusters;
   src.proto.direction = direction;
+  src.proto.engine = choose_engine(g, direction);
+  if (src.proto.engine < 0) return CBFS_ECUDA;
   src.proto.out_dist = out_dist;
   src.proto.out_masks = out_masks;
   src.sources = sources;
@@ -1019,6 +1016,8 @@ int cbfs_select_and_run(cbfs_graph* gh, uint32_t r, uint32_t k, uint32_t d, uint
   src.proto.dist_bytes = dist_bytes;
   src.proto.C = r;
   src.proto.direction = direction;
+  src.proto.engine = choose_engine(g, direction);
+  if (src.proto.engine < 0) return CBFS_ECUDA;
   src.proto.out_dist = out_dist;
   src.proto.out_masks = out_masks;
   src.sources = out_sources;
@@ -1060,7 +1059,7 @@ int cbfs_set_concurrency(int batches) {
 
 int cbfs_profile_read(double* ms, uint64_t* launches, uint64_t* arcs, uint64_t* entries, uint64_t* u_in,
                       uint64_t* u_out, int reset) {
-  for (int k = 0; k < 3; ++k) {
+  for (int k = 0; k < PK_N; ++k) {
     if (ms) ms[k] = g_prof.ms[k];
     if (launches) launches[k] = g_prof.launches[k];
     if (arcs) arcs[k] = g_prof.arcs[k];

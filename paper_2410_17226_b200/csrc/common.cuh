@@ -54,6 +54,8 @@ struct Graph {
   // pull-kernel chunk table: first vertex of every PULL_CHUNK arcs
   uint32_t* chunk_v = nullptr;
   uint64_t n_chunks = 0;
+  // diameter class for the engine choice (-1 unknown, 0 low, 1 high; sparse.cu)
+  int high_diameter = -1;
   // traversal workspace (lazily allocated, sized n*LANES)
   struct Work* work = nullptr;
 };
@@ -81,6 +83,7 @@ struct RunArgs {
   const uint32_t* sources;  // device, batch base ([nb][64])
   const uint8_t* sizes;     // device, batch base ([nb])
   uint32_t nb, d, planes, dist_bytes, C, cbase, direction;
+  int engine;               // ENGINE_BATCHED / ENGINE_SPARSE (engine.cuh)
   void* out_dist;           // device [n][C] or null
   uint64_t* out_masks;      // device [planes][n][C] or null
   uint64_t* out_stats;      // device [nb][4] or null

@@ -1,0 +1,110 @@
+// engine.cuh — internals shared by the two C-BFS engines of libcbfs.so:
+//  * the BATCHED engine (cbfs.cu): vertex-major state rows of 64 clusters,
+//    host-driven rounds with a push/pull switch — for low-diameter graphs,
+//    where the 64 clusters' frontiers overlap round by round;
+//  * the SPARSE engine (sparse.cu): cluster-major state, push-only rounds,
+//    the whole round loop on the device (CUDA-graph while-node) — for
+//    high-diameter graphs, where the clusters' wavefronts are disjoint.
+// Both run Alg. 1 and produce identical outputs (R8, R25).
+#pragma once
+#include <vector>
+
+#include "common.cuh"
+
+namespace cbfs {
+
+enum : unsigned long long { ERR_BAD_SOURCE = 1, ERR_DUP_SOURCE = 2, ERR_BAD_SIZE = 4, ERR_OVERFLOW = 8,
+                            ERR_ROUNDS = 16 };
+enum { ENGINE_BATCHED = 0, ENGINE_SPARSE = 1 };
+
+constexpr unsigned FULLW = 0xFFFFFFFFu;
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+
+__device__ __forceinline__ unsigned long long warp_sum(unsigned long long x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULLW, x, o);
+  return x;
+}
+
+// Device-resident description of the batch a sparse-engine slot runs: the
+// instantiated CUDA graph reads everything that changes per batch from here,
+// so one graph per slot serves every batch and every graph handle.
+struct SpDesc {
+  const uint64_t* off;
+  const uint32_t* cols;
+  const uint32_t* perm;      // internal -> original id (null: identity)
+  const uint32_t* inv;       // original -> internal id (null: identity)
+  const uint32_t* sources;   // [nb][64]
+  const uint8_t* sizes;      // [nb]
+  void* out_dist;            // [n][C] or null
+  uint64_t* out_masks;       // [planes][n][C] or null
+  uint64_t C, cbase;
+  uint32_t n, nb, d, planes, dist_bytes, pad;
+};
+// Round state of a sparse-engine batch (device-resident).
+struct SpCtl {
+  unsigned long long nF[2];  // frontier list sizes: list (i & 1) holds F_i
+  unsigned long long err;    // ERR_* bits
+  unsigned long long i;      // current round
+};
+
+// One in-flight batch of LANES clusters: its workspace, its stream, and the
+// state of its round loop.  Several slots run concurrently (run_batches), so
+// the small rounds and the latency-bound dense rounds of different batches
+// overlap on the GPU.  The sparse engine reuses the same arrays with a
+// cluster-major layout (see sparse.cu).
+struct Slot {
+  uint64_t cap = 0;                     // n * LANES entries
+  uint64_t* seen = nullptr;             // [n+1][64] S_seen (row n stays zero)
+  uint64_t* pend = nullptr;             // [n][64] S_next \ S_seen (pending)
+  uint16_t* dist = nullptr;             // [n][64] Delta
+  uint32_t* listA = nullptr;            // frontier lists (packed v*64+c)
+  uint32_t* listB = nullptr;
+  uint64_t* pre = nullptr;              // [cap + 1] degrees -> exclusive prefix (push)
+  uint32_t* ubits = nullptr;            // 2 x [n/32 + 1]: union frontier U_i, U_{i+1}
+  unsigned long long* ctr = nullptr;    // [0] next count, [1] next E, [2] error bits, [3] |U_next|
+  unsigned long long* h_ctr = nullptr;  // pinned mirror
+  uint64_t* bstats = nullptr;           // [LANES][4]
+  uint64_t* fullm = nullptr;            // [n] bit c: S_seen[v][c] == S_c (maintained by the fold)
+  void* scan_tmp = nullptr;
+  size_t scan_bytes = 0;
+  cudaStream_t s = nullptr;
+  cudaEvent_t ready = nullptr;  // counters of the last queued round are on the host
+  cudaEvent_t pe[4] = {nullptr, nullptr, nullptr, nullptr};  // profiling
+  // round-loop state
+  bool busy = false;
+  bool seeding = false;
+  RunArgs a{};
+  uint32_t i = 0;
+  uint64_t nF = 0, E = 0, U = 0;
+  uint32_t *cur = nullptr, *nxt = nullptr;
+  int kind = -1;
+  bool overflow = false;
+  // sparse engine
+  int engine = ENGINE_BATCHED;  // engine of the batch in flight
+  bool pre_zero = false;        // `pre` is all zero (it is the sparse engine's second pending buffer)
+  SpDesc* sp_desc = nullptr;    // device
+  SpDesc* sp_desc_h = nullptr;  // pinned staging
+  SpCtl* sp_ctl = nullptr;      // device
+  SpCtl* sp_ctl_h = nullptr;    // pinned mirror
+  cudaGraph_t sp_graph = nullptr;
+  cudaGraphExec_t sp_exec = nullptr;
+  cudaEvent_t sp_t0 = nullptr, sp_t1 = nullptr;  // profiling
+  uint32_t sp_db = 0;                             // dist_bytes the graph was built for
+};
+
+struct DevSlots {
+  std::vector<Slot*> slots;
+  uint64_t cap = 0;
+};
+
+// sparse.cu
+int sparse_alloc(Slot* w);
+void sparse_free(Slot* w);
+int sparse_start(const Graph* g, Slot* w, const RunArgs& a);  // queue init + seeding + counters readback
+int sparse_launch(Slot* w);                                    // queue the whole round loop + readback
+int choose_engine(Graph* g, uint32_t direction);               // ENGINE_* for this graph and direction
+extern int g_engine_policy;                                    // CBFS_ENGINE_*
+
+}  // namespace cbfs

@@ -5,7 +5,7 @@
 #include <algorithm>
 #include <vector>
 
-#include "common.cuh"
+#include "engine.cuh"
 
 namespace cbfs {
 
@@ -202,6 +202,8 @@ int cbfs_query_stream(cbfs_graph* gh, const uint32_t* sources, const uint8_t* si
   src.proto.planes = planes;
   src.proto.dist_bytes = 2;
   src.proto.direction = CBFS_DIR_AUTO;
+  src.proto.engine = choose_engine(g, CBFS_DIR_AUTO);
+  if (src.proto.engine < 0) return CBFS_ECUDA;
   src.sources = sources;
   src.sizes = sizes;
   src.n_clusters = n_clusters;
@@ -288,6 +290,8 @@ int cbfs_run_host(cbfs_graph* gh, const uint32_t* sources, const uint8_t* sizes,
   src.proto.planes = planes;
   src.proto.dist_bytes = dist_bytes;
   src.proto.direction = direction;
+  src.proto.engine = choose_engine(g, direction);
+  if (src.proto.engine < 0) return CBFS_ECUDA;
   src.sources = dsrc;
   src.sizes = dsz;
   src.n_clusters = n_clusters;

@@ -1,0 +1,502 @@
+// sparse.cu — the SPARSE C-BFS engine: Alg. 1 for a batch of
+// LANES = 64 clusters on graphs whose clusters' wavefronts do not overlap
+// (high diameter: the road-like grid and the k-NN graph of BASELINE.json
+// configs 4 and 5).
+//
+// Why a second engine: in the BATCHED engine (cbfs.cu) the 64 clusters of a
+// batch share one 512-byte state row per vertex, which pays off when their
+// frontiers cover the same vertices in the same round (social/web graphs).
+// On a 4096^2 grid the 64 clusters' frontiers are 64 disjoint rings, so each
+// 32-byte sector of a row carries one useful 8-byte word, and the ~7,400
+// rounds each cost a host round trip.  Here:
+//  * state is CLUSTER-major: S_seen[c][v], Delta[c][v] and two pending
+//    buffers P[2][c][v] (P = S_next \ S_seen); a cluster's frontier band is
+//    contiguous along rows of the grid / along the relabelled order;
+//  * rounds are push-only (EdgeMap-Sparse): per frontier entry
+//    (c, v) the bits S_new[v] are pushed to the neighbours (R7a: older bits of
+//    S_seen[v] reached them in earlier rounds), 64-bit atomicOr into the NEXT
+//    pending buffer; the first setter claims the entry (R4);
+//  * the round loop runs on the device: one CUDA graph per slot whose
+//    conditional WHILE node repeats {fold, push, tail} until the next
+//    frontier is empty — no host synchronisation per round.
+// Phase order (H9): the fold of round i completes (kernel boundary) before
+// the push of round i reads S_seen / Delta of its neighbours, and the push
+// writes only the other pending buffer, so the cap (R3) and the
+// claim see exactly Alg. 1's post-fold state.
+#include "engine.cuh"
+
+namespace cbfs {
+
+int g_engine_policy = CBFS_ENGINE_AUTO;
+
+constexpr uint32_t VBITS = 26;  // list entry = c << 26 | v  (n <= CBFS_MAX_N = 2^26)
+constexpr uint32_t VMASK = (1u << VBITS) - 1;
+constexpr int SP_THREADS = 256;
+constexpr int SP_WARPS = SP_THREADS / 32;
+constexpr uint32_t SP_SMALL = 32;    // entries of higher degree are pushed by the whole warp
+constexpr uint32_t SP_OUTBUF = 256;  // per-warp claim buffer (entries)
+constexpr unsigned SP_GRID = 148u * 8u;
+
+// ------------------------------------------------------------------ seeding
+// R1 (S_next[s_j] = {j}, F_0 = S) in the cluster-major layout.
+__global__ void k_sp_seed(const uint32_t* __restrict__ sources, const uint8_t* __restrict__ sizes, uint32_t nb,
+                          uint32_t n, const uint32_t* __restrict__ inv, uint64_t* __restrict__ pend0,
+                          uint32_t* __restrict__ list0, SpCtl* __restrict__ ctl) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;  // 64 threads per cluster
+  const uint32_t c = t >> 6, j = t & 63;
+  bool claim = false;
+  uint32_t e = 0;
+  if (c < nb) {
+    const uint32_t k = sizes[c];
+    if (k == 0 || k > 64) {
+      if (j == 0) atomicOr(&ctl->err, ERR_BAD_SIZE);
+    } else if (j < k) {
+      const uint32_t s = sources[(uint64_t)c * 64 + j];
+      if (s >= n) {
+        atomicOr(&ctl->err, ERR_BAD_SOURCE);
+      } else {
+        const uint32_t x = inv ? inv[s] : s;
+        const unsigned long long old = atomicOr((unsigned long long*)&pend0[(uint64_t)c * n + x], 1ULL << j);
+        if (old != 0) atomicOr(&ctl->err, ERR_DUP_SOURCE);  // R2
+        else { claim = true; e = (c << VBITS) | x; }
+      }
+    }
+  }
+  const unsigned m = __ballot_sync(FULLW, claim);
+  if (!m) return;
+  unsigned long long base = 0;
+  const int leader = __ffs(m) - 1;
+  if ((int)lane_id() == leader) base = atomicAdd(&ctl->nF[0], (unsigned long long)__popc(m));
+  base = __shfl_sync(FULLW, base, leader);
+  if (claim) list0[base + __popc(m & ((1u << lane_id()) - 1))] = e;
+}
+
+// ------------------------------------------------------------------ fold
+// Vertex phase of round i for every entry of F_i: S_new =
+// P_i[c][v] \ S_seen[c][v]; Delta on first visit; S_v[i - Delta] = S_new;
+// S_seen |= S_new; the output writes; per-cluster statistics.  P_i keeps
+// S_new for the push of the same round.
+template <int DB>
+__global__ void __launch_bounds__(SP_THREADS) k_sp_fold(const SpDesc* __restrict__ D, SpCtl* __restrict__ ctl,
+                                                        uint64_t* __restrict__ seen, uint16_t* __restrict__ dist,
+                                                        uint64_t* __restrict__ pend0, uint64_t* __restrict__ pend1,
+                                                        const uint32_t* __restrict__ list0,
+                                                        const uint32_t* __restrict__ list1,
+                                                        uint64_t* __restrict__ bstats) {
+  __shared__ unsigned long long sF[LANES], sE[LANES], sM[LANES];
+  for (uint32_t c = threadIdx.x; c < LANES; c += blockDim.x) sF[c] = sE[c] = sM[c] = 0;
+  __syncthreads();
+  const uint32_t i = (uint32_t)ctl->i;
+  const uint32_t cur = i & 1;
+  const uint32_t* __restrict__ L = cur ? list1 : list0;
+  uint64_t* __restrict__ P = cur ? pend1 : pend0;
+  const uint64_t nF = ctl->nF[cur];
+  const uint32_t n = D->n, planes = D->planes;
+  const uint64_t C = D->C, cbase = D->cbase;
+  const uint64_t* __restrict__ off = D->off;
+  const uint32_t* __restrict__ perm = D->perm;
+  void* __restrict__ out_dist = D->out_dist;
+  uint64_t* __restrict__ out_masks = D->out_masks;
+  const uint32_t lane = lane_id();
+  bool overflow = false;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t b = warp * 32; b < nF; b += nwarps * 32) {
+    const uint64_t t = b + lane;
+    uint32_t c = LANES, deg = 0;
+    bool act = false, first = false;
+    if (t < nF) {
+      const uint32_t e = L[t];
+      c = e >> VBITS;
+      const uint32_t v = e & VMASK;
+      const uint64_t idx = (uint64_t)c * n + v;
+      const uint64_t p = P[idx], s = seen[idx];
+      const uint64_t nw = p & ~s;
+      if (nw != p) P[idx] = nw;
+      if (nw) {
+        act = true;
+        seen[idx] = s | nw;
+        uint32_t dv = dist[idx];
+        first = dv == INF16;
+        if (first) { dv = i; dist[idx] = (uint16_t)i; }
+        deg = (uint32_t)(off[v + 1] - off[v]);
+        const uint32_t orig = perm ? perm[v] : v;
+        const uint64_t col = (uint64_t)orig * C + cbase + c;
+        if (first && out_dist) {
+          if (DB == 1) {
+            overflow |= i > 254;
+            ((uint8_t*)out_dist)[col] = (uint8_t)(i > 254 ? 254 : i);
+          } else {
+            ((uint16_t*)out_dist)[col] = (uint16_t)i;
+          }
+        }
+        const uint32_t oi = i - dv;
+        if (out_masks && oi < planes) out_masks[(uint64_t)oi * n * C + col] = nw;
+      }
+    }
+    // per-cluster statistics, one shared atomic per distinct cluster in the warp
+    const unsigned grp = __match_any_sync(FULLW, act ? c : 0xFFFFFFFFu);
+    const uint32_t fsum = __reduce_add_sync(grp, act ? 1u : 0u);
+    const uint32_t esum = __reduce_add_sync(grp, act ? deg : 0u);
+    const uint32_t msum = __reduce_add_sync(grp, act && first ? deg : 0u);
+    if (act && lane == (uint32_t)(__ffs(grp) - 1)) {
+      atomicAdd(&sF[c], (unsigned long long)fsum);
+      atomicAdd(&sE[c], (unsigned long long)esum);
+      if (msum) atomicAdd(&sM[c], (unsigned long long)msum);
+    }
+  }
+  if (overflow) atomicOr(&ctl->err, ERR_OVERFLOW);
+  __syncthreads();
+  for (uint32_t c = threadIdx.x; c < LANES; c += blockDim.x) {
+    if (!sF[c]) continue;
+    atomicAdd((unsigned long long*)&bstats[c * 4 + 1], sF[c]);
+    atomicAdd((unsigned long long*)&bstats[c * 4 + 2], sE[c]);
+    if (sM[c]) atomicAdd((unsigned long long*)&bstats[c * 4 + 3], sM[c]);
+    atomicMax((unsigned long long*)&bstats[c * 4 + 0], (unsigned long long)(i + 1));
+  }
+}
+
+// ------------------------------------------------------------------ push
+// Edge phase of round i: for every entry (c, v) of F_i and u in
+// N(v) with cap(u) (Delta_u = inf or i - Delta_u < d, R3): x =
+// S_new[v] \ S_seen[u]; if x != 0, atomicOr(P_{i+1}[c][u], x); the op that
+// turns P_{i+1}[c][u] non-zero appends (c, u) to F_{i+1} (R4).  P_i[c][v] is
+// cleared once read, so both pending buffers are zero between batches.
+__device__ __forceinline__ bool sp_try(uint64_t cn, uint32_t u, uint64_t nw, uint32_t i, uint32_t d,
+                                       const uint64_t* __restrict__ seen, const uint16_t* __restrict__ dist,
+                                       uint64_t* __restrict__ Pn) {
+  const uint64_t ui = cn + u;
+  const uint32_t du = dist[ui];
+  if (du != INF16 && (int)i - (int)du >= (int)d) return false;
+  const uint64_t x = nw & ~seen[ui];
+  if (!x) return false;
+  return atomicOr((unsigned long long*)&Pn[ui], (unsigned long long)x) == 0ULL;
+}
+
+__global__ void __launch_bounds__(SP_THREADS) k_sp_push(const SpDesc* __restrict__ D, SpCtl* __restrict__ ctl,
+                                                        const uint64_t* __restrict__ seen,
+                                                        const uint16_t* __restrict__ dist, uint64_t* __restrict__ pend0,
+                                                        uint64_t* __restrict__ pend1, uint32_t* __restrict__ list0,
+                                                        uint32_t* __restrict__ list1) {
+  __shared__ uint32_t s_out[SP_WARPS][SP_OUTBUF];
+  const uint32_t i = (uint32_t)ctl->i;
+  const uint32_t cur = i & 1;
+  const uint32_t* __restrict__ L = cur ? list1 : list0;
+  uint32_t* __restrict__ Ln = cur ? list0 : list1;
+  uint64_t* __restrict__ P = cur ? pend1 : pend0;
+  uint64_t* __restrict__ Pn = cur ? pend0 : pend1;
+  unsigned long long* cnt = &ctl->nF[cur ^ 1];
+  const uint64_t nF = ctl->nF[cur];
+  const uint32_t n = D->n, d = D->d;
+  const uint64_t* __restrict__ off = D->off;
+  const uint32_t* __restrict__ cols = D->cols;
+  const uint32_t lane = lane_id();
+  const unsigned lt = (1u << lane) - 1;
+  uint32_t* obuf = s_out[threadIdx.x >> 5];
+  uint32_t nout = 0;
+  auto emit = [&](bool claim, uint32_t val) {
+    const unsigned m = __ballot_sync(FULLW, claim);
+    if (claim) obuf[nout + __popc(m & lt)] = val;
+    nout += __popc(m);
+    if (nout > SP_OUTBUF - 32) {
+      __syncwarp();
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(cnt, (unsigned long long)nout);
+      base = __shfl_sync(FULLW, base, 0);
+      for (uint32_t q = lane; q < nout; q += 32) Ln[base + q] = obuf[q];
+      __syncwarp();
+      nout = 0;
+    }
+  };
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t b = warp * 32; b < nF; b += nwarps * 32) {
+    const uint64_t t = b + lane;
+    uint32_t c = 0, v = 0;
+    uint64_t nw = 0, beg = 0, end = 0;
+    if (t < nF) {
+      const uint32_t e = L[t];
+      c = e >> VBITS;
+      v = e & VMASK;
+      const uint64_t idx = (uint64_t)c * n + v;
+      nw = P[idx];
+      if (nw) {
+        P[idx] = 0;
+        beg = off[v];
+        end = off[v + 1];
+      }
+    }
+    const uint64_t cn = (uint64_t)c * n;
+    const uint64_t deg = end - beg;
+    const bool big = deg > SP_SMALL;
+    // entries of small degree: every lane walks its own neighbour list
+    const uint32_t sdeg = big ? 0u : (uint32_t)deg;
+    const uint32_t maxd = __reduce_max_sync(FULLW, sdeg);
+    for (uint32_t k = 0; k < maxd; ++k) {
+      bool claim = false;
+      uint32_t u = 0;
+      if (k < sdeg) {
+        u = cols[beg + k];
+        claim = sp_try(cn, u, nw, i, d, seen, dist, Pn);
+      }
+      emit(claim, (c << VBITS) | u);
+    }
+    // entries of large degree: the whole warp walks one list at a time
+    unsigned bigm = __ballot_sync(FULLW, big);
+    while (bigm) {
+      const int j = __ffs(bigm) - 1;
+      bigm &= bigm - 1;
+      const uint32_t cj = __shfl_sync(FULLW, c, j);
+      const uint64_t bj = __shfl_sync(FULLW, beg, j), ej = __shfl_sync(FULLW, end, j);
+      const uint64_t nwj = __shfl_sync(FULLW, nw, j);
+      const uint64_t cnj = (uint64_t)cj * n;
+      for (uint64_t a0 = bj; a0 < ej; a0 += 32) {
+        const uint64_t a = a0 + lane;
+        bool claim = false;
+        uint32_t u = 0;
+        if (a < ej) {
+          u = cols[a];
+          claim = sp_try(cnj, u, nwj, i, d, seen, dist, Pn);
+        }
+        emit(claim, (cj << VBITS) | u);
+      }
+    }
+  }
+  __syncwarp();
+  if (nout) {
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(cnt, (unsigned long long)nout);
+    base = __shfl_sync(FULLW, base, 0);
+    for (uint32_t q = lane; q < nout; q += 32) Ln[base + q] = obuf[q];
+  }
+}
+
+// ------------------------------------------------------------------ tail
+// End of round i: F_i is consumed, i advances, and the WHILE node repeats
+// while F_{i+1} is non-empty (Alg. 1's loop).
+__global__ void k_sp_tail(SpCtl* __restrict__ ctl, cudaGraphConditionalHandle h) {
+  const unsigned long long i = ctl->i;
+  const uint32_t cur = i & 1;
+  ctl->nF[cur] = 0;
+  const unsigned long long nn = ctl->nF[cur ^ 1];
+  ctl->i = i + 1;
+  bool go = nn > 0;
+  if (go && i + 1 >= 0xFFFEull) {
+    atomicOr(&ctl->err, ERR_ROUNDS);
+    go = false;
+  }
+  cudaGraphSetConditional(h, go ? 1u : 0u);
+}
+
+// ------------------------------------------------------------------ host
+static int sp_add_kernel(cudaGraph_t body, cudaGraphNode_t* node, const cudaGraphNode_t* dep, void* fn, unsigned grid,
+                         unsigned block, void** args) {
+  cudaKernelNodeParams kp = {};
+  kp.func = fn;
+  kp.gridDim = dim3(grid);
+  kp.blockDim = dim3(block);
+  kp.sharedMemBytes = 0;
+  kp.kernelParams = args;
+  CBFS_CUDA(cudaGraphAddKernelNode(node, body, dep, dep ? 1 : 0, &kp));
+  return CBFS_OK;
+}
+
+// The per-slot round-loop graph: WHILE (F_i non-empty) { fold; push; tail }.
+// Two graphs per slot would be needed for the two Delta output widths; the
+// fold instance is chosen by dist_bytes when the graph is (re)built.
+static int sp_build(Slot* w, uint32_t dist_bytes) {
+  if (w->sp_exec) {
+    CBFS_CUDA(cudaGraphExecDestroy(w->sp_exec));
+    w->sp_exec = nullptr;
+  }
+  if (w->sp_graph) {
+    CBFS_CUDA(cudaGraphDestroy(w->sp_graph));
+    w->sp_graph = nullptr;
+  }
+  cudaGraph_t g;
+  CBFS_CUDA(cudaGraphCreate(&g, 0));
+  w->sp_graph = g;
+  cudaGraphConditionalHandle h;
+  CBFS_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t cond;
+  CBFS_CUDA(cudaGraphAddNode(&cond, g, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  SpDesc* D = w->sp_desc;
+  SpCtl* ctl = w->sp_ctl;
+  uint64_t* pend0 = w->pend;
+  uint64_t* pend1 = w->pre;
+  uint32_t* l0 = w->listA;
+  uint32_t* l1 = w->listB;
+  void* fa[] = {&D, &ctl, &w->seen, &w->dist, &pend0, &pend1, &l0, &l1, &w->bstats};
+  void* pa[] = {&D, &ctl, &w->seen, &w->dist, &pend0, &pend1, &l0, &l1};
+  void* ta[] = {&ctl, &h};
+  cudaGraphNode_t nf, np, nt;
+  int rc = sp_add_kernel(body, &nf, nullptr, dist_bytes == 1 ? (void*)k_sp_fold<1> : (void*)k_sp_fold<2>, SP_GRID,
+                         SP_THREADS, fa);
+  if (rc) return rc;
+  rc = sp_add_kernel(body, &np, &nf, (void*)k_sp_push, SP_GRID, SP_THREADS, pa);
+  if (rc) return rc;
+  rc = sp_add_kernel(body, &nt, &np, (void*)k_sp_tail, 1, 1, ta);
+  if (rc) return rc;
+  CBFS_CUDA(cudaGraphInstantiate(&w->sp_exec, g, 0));
+  w->sp_db = dist_bytes;
+  return CBFS_OK;
+}
+
+int sparse_alloc(Slot* w) {
+  CBFS_CUDA(cudaMalloc(&w->sp_desc, sizeof(SpDesc)));
+  CBFS_CUDA(cudaMallocHost(&w->sp_desc_h, sizeof(SpDesc)));
+  CBFS_CUDA(cudaMalloc(&w->sp_ctl, sizeof(SpCtl)));
+  CBFS_CUDA(cudaMallocHost(&w->sp_ctl_h, sizeof(SpCtl)));
+  CBFS_CUDA(cudaEventCreate(&w->sp_t0));
+  CBFS_CUDA(cudaEventCreate(&w->sp_t1));
+  return CBFS_OK;
+}
+
+void sparse_free(Slot* w) {
+  if (w->sp_exec) cudaGraphExecDestroy(w->sp_exec);
+  if (w->sp_graph) cudaGraphDestroy(w->sp_graph);
+  cudaFree(w->sp_desc);
+  cudaFreeHost(w->sp_desc_h);
+  cudaFree(w->sp_ctl);
+  cudaFreeHost(w->sp_ctl_h);
+  if (w->sp_t0) cudaEventDestroy(w->sp_t0);
+  if (w->sp_t1) cudaEventDestroy(w->sp_t1);
+}
+
+int sparse_start(const Graph* g, Slot* w, const RunArgs& a) {
+  const uint32_t n = g->n;
+  cudaStream_t st = w->s;
+  if (!w->sp_exec || w->sp_db != a.dist_bytes) {
+    int rc = sp_build(w, a.dist_bytes);
+    if (rc) return rc;
+  }
+  SpDesc* h = w->sp_desc_h;  // the slot's previous batch (and its copy) finished before this one starts
+  h->off = g->off;
+  h->cols = g->cols;
+  h->perm = g->perm;
+  h->inv = g->inv;
+  h->sources = a.sources;
+  h->sizes = a.sizes;
+  h->out_dist = a.out_dist;
+  h->out_masks = a.out_masks;
+  h->C = a.C;
+  h->cbase = a.cbase;
+  h->n = n;
+  h->nb = a.nb;
+  h->d = a.d;
+  h->planes = a.planes;
+  h->dist_bytes = a.dist_bytes;
+  h->pad = 0;
+  CBFS_CUDA(cudaMemcpyAsync(w->sp_desc, h, sizeof(SpDesc), cudaMemcpyHostToDevice, st));
+  const uint64_t cells = (uint64_t)n * LANES;
+  CBFS_CUDA(cudaMemsetAsync(w->seen, 0, cells * sizeof(uint64_t), st));
+  CBFS_CUDA(cudaMemsetAsync(w->dist, 0xFF, cells * sizeof(uint16_t), st));
+  if (!w->pre_zero) {
+    CBFS_CUDA(cudaMemsetAsync(w->pre, 0, cells * sizeof(uint64_t), st));
+    w->pre_zero = true;
+  }
+  CBFS_CUDA(cudaMemsetAsync(w->bstats, 0, LANES * 4 * sizeof(uint64_t), st));
+  CBFS_CUDA(cudaMemsetAsync(w->sp_ctl, 0, sizeof(SpCtl), st));
+  k_sp_seed<<<(a.nb * 64 + 255) / 256, 256, 0, st>>>(a.sources, a.sizes, a.nb, n, g->inv, w->pend, w->listA,
+                                                     w->sp_ctl);
+  CBFS_LAUNCHED();
+  CBFS_CUDA(cudaMemcpyAsync(w->sp_ctl_h, w->sp_ctl, sizeof(SpCtl), cudaMemcpyDeviceToHost, st));
+  CBFS_CUDA(cudaEventRecord(w->ready, st));
+  return CBFS_OK;
+}
+
+int sparse_launch(Slot* w) {
+  cudaStream_t st = w->s;
+  CBFS_CUDA(cudaEventRecord(w->sp_t0, st));
+  CBFS_CUDA(cudaGraphLaunch(w->sp_exec, st));
+  CBFS_CUDA(cudaEventRecord(w->sp_t1, st));
+  CBFS_CUDA(cudaMemcpyAsync(w->sp_ctl_h, w->sp_ctl, sizeof(SpCtl), cudaMemcpyDeviceToHost, st));
+  CBFS_CUDA(cudaEventRecord(w->ready, st));
+  return CBFS_OK;
+}
+
+// ------------------------------------------------------------------ engine choice
+// AUTO: a plain BFS from the highest-degree vertex; if it is still running
+// after PROBE_ROUNDS levels the graph is "high diameter" and the clusters'
+// wavefronts will not share state rows -> SPARSE, else BATCHED.  Cached per
+// graph handle.  Parity-neutral: both engines compute Alg. 1 exactly.
+constexpr uint32_t PROBE_ROUNDS = 48;
+
+__global__ void k_probe_level(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cols,
+                              const uint32_t* __restrict__ q, uint32_t nq, uint32_t* __restrict__ level,
+                              uint32_t lvl, uint32_t* __restrict__ qn, unsigned long long* __restrict__ cnt) {
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < nq; t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = q[t];
+    for (uint64_t a = off[v]; a < off[v + 1]; ++a) {
+      const uint32_t u = cols[a];
+      if (level[u] == 0xFFFFFFFFu && atomicCAS(&level[u], 0xFFFFFFFFu, lvl + 1) == 0xFFFFFFFFu)
+        qn[atomicAdd(cnt, 1ULL)] = u;
+    }
+  }
+}
+
+static int probe_high_diameter(Graph* g, int* out) {
+  const uint32_t n = g->n;
+  *out = 0;
+  if (n == 0 || g->m == 0) return CBFS_OK;
+  cudaStream_t st;
+  CBFS_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  uint32_t *level = nullptr, *qa = nullptr, *qb = nullptr;
+  unsigned long long* cnt = nullptr;
+  CBFS_CUDA(cudaMallocAsync(&level, sizeof(uint32_t) * n, st));
+  CBFS_CUDA(cudaMallocAsync(&qa, sizeof(uint32_t) * n, st));
+  CBFS_CUDA(cudaMallocAsync(&qb, sizeof(uint32_t) * n, st));
+  CBFS_CUDA(cudaMallocAsync(&cnt, sizeof(unsigned long long), st));
+  CBFS_CUDA(cudaMemsetAsync(level, 0xFF, sizeof(uint32_t) * n, st));
+  uint32_t root = 0;
+  CBFS_CUDA(cudaMemcpyAsync(&root, g->order, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  CBFS_CUDA(cudaStreamSynchronize(st));
+  const uint32_t zero = 0;
+  CBFS_CUDA(cudaMemcpyAsync(level + root, &zero, sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+  CBFS_CUDA(cudaMemcpyAsync(qa, &root, sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+  unsigned long long nq = 1, h = 0;
+  uint32_t lvl = 0;
+  for (; nq && lvl < PROBE_ROUNDS; ++lvl) {
+    CBFS_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st));
+    k_probe_level<<<grid_for(nq, 256), 256, 0, st>>>(g->off, g->cols, qa, (uint32_t)nq, level, lvl, qb, cnt);
+    CBFS_LAUNCHED();
+    CBFS_CUDA(cudaMemcpyAsync(&h, cnt, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CBFS_CUDA(cudaStreamSynchronize(st));
+    nq = h;
+    std::swap(qa, qb);
+  }
+  *out = nq > 0 ? 1 : 0;
+  CBFS_CUDA(cudaFreeAsync(level, st));
+  CBFS_CUDA(cudaFreeAsync(qa, st));
+  CBFS_CUDA(cudaFreeAsync(qb, st));
+  CBFS_CUDA(cudaFreeAsync(cnt, st));
+  CBFS_CUDA(cudaStreamSynchronize(st));
+  CBFS_CUDA(cudaStreamDestroy(st));
+  return CBFS_OK;
+}
+
+int choose_engine(Graph* g, uint32_t direction) {
+  if (direction == CBFS_DIR_PULL) return ENGINE_BATCHED;  // pull exists in the batched engine only
+  if (g_engine_policy == CBFS_ENGINE_BATCHED) return ENGINE_BATCHED;
+  if (g_engine_policy == CBFS_ENGINE_SPARSE) return ENGINE_SPARSE;
+  if (g->high_diameter < 0) {
+    int hd = 0;
+    if (probe_high_diameter(g, &hd) != CBFS_OK) return -1;
+    g->high_diameter = hd;
+  }
+  return g->high_diameter ? ENGINE_SPARSE : ENGINE_BATCHED;
+}
+
+}  // namespace cbfs
+
+extern "C" int cbfs_set_engine(int engine) {
+  if (engine < CBFS_ENGINE_AUTO || engine > CBFS_ENGINE_SPARSE) return cbfs::fail(CBFS_EINVAL, "bad engine");
+  cbfs::g_engine_policy = engine;
+  return CBFS_OK;
+}

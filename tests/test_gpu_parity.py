@@ -15,6 +15,29 @@ from gpu_util import gpu_graph, np_u16, np_u32, np_u64, run_clusters, to_dev_u32
 
 pytestmark = pytest.mark.gpu
 
+ENGINES = [cb.CBFS_ENGINE_BATCHED, cb.CBFS_ENGINE_SPARSE]
+
+
+@pytest.fixture(params=ENGINES, ids=["batched", "sparse"])
+def engine(request):
+    """Run the test under each traversal engine (identical outputs, R8/R25)."""
+    cb.cbfs_set_engine(request.param)
+    yield request.param
+    cb.cbfs_set_engine(cb.CBFS_ENGINE_AUTO)
+
+
+@pytest.fixture(autouse=True)
+def _reset_engine():
+    yield
+    cb.cbfs_set_engine(cb.CBFS_ENGINE_AUTO)
+
+
+def each_mode():
+    """(engine, direction) pairs: batched push / pull / auto and the sparse engine."""
+    return [(cb.CBFS_ENGINE_BATCHED, cb.CBFS_DIR_AUTO), (cb.CBFS_ENGINE_BATCHED, cb.CBFS_DIR_PUSH),
+            (cb.CBFS_ENGINE_BATCHED, cb.CBFS_DIR_PULL), (cb.CBFS_ENGINE_SPARSE, cb.CBFS_DIR_AUTO),
+            (cb.CBFS_ENGINE_AUTO, cb.CBFS_DIR_AUTO)]
+
 
 def random_el(seed, n, kind):
     rng = np.random.default_rng(seed)
@@ -133,7 +156,7 @@ def compare_many(g, ref, src, sz, d, **kw):
 
 @pytest.mark.parametrize("direction", [cb.CBFS_DIR_AUTO, cb.CBFS_DIR_PUSH, cb.CBFS_DIR_PULL])
 @pytest.mark.parametrize("relabel", [False, True])
-def test_c1_full_parity(direction, relabel):
+def test_c1_full_parity(direction, relabel, engine):
     cfg = ci.CONFIGS["c1_er"]
     el = ci.make_graph("c1_er")
     ref = orc.csr_from_edgelist(el)
@@ -157,7 +180,8 @@ def test_random_graphs_parity(seed):
     C = [1, 5, 31, 32, 33, 70][seed % 6]  # ragged batches
     src, sz = ball_clusters(ref, rng, C, d, [1, 7, 64][seed % 3] if d else 1)
     g = gpu_graph(el, relabel=bool(seed % 2))
-    for direction in (cb.CBFS_DIR_AUTO, cb.CBFS_DIR_PUSH, cb.CBFS_DIR_PULL):
+    for eng, direction in each_mode():
+        cb.cbfs_set_engine(eng)
         compare_many(g, ref, src, sz, d, direction=direction)
 
 
@@ -177,11 +201,12 @@ def test_diameter_exceeds_d_parity(seed):
         src[c, :k] = S; sz[c] = k
     d = [1, 2, 3][seed % 3]
     g = gpu_graph(el, relabel=bool(seed % 2))
-    for direction in (cb.CBFS_DIR_PUSH, cb.CBFS_DIR_PULL, cb.CBFS_DIR_AUTO):
+    for eng, direction in each_mode():
+        cb.cbfs_set_engine(eng)
         compare_many(g, ref, src, sz, d, direction=direction)
 
 
-def test_label_planes_and_u8_dist():
+def test_label_planes_and_u8_dist(engine):
     el = random_el(77, 2500, "rmat")
     ref = orc.csr_from_edgelist(el)
     src, sz = orc.select_clusters(ref, 40, 64, 2)
@@ -189,7 +214,7 @@ def test_label_planes_and_u8_dist():
     compare_many(g, ref, src, sz, 2, planes=2, dist_bytes=1)
 
 
-def test_edge_cases():
+def test_edge_cases(engine):
     # isolated source; graph without edges; single-vertex cluster on a path with d=0 (plain BFS)
     el = ci.EdgeList(6, np.array([1, 2], np.uint32), np.array([2, 3], np.uint32))
     ref = orc.csr_from_edgelist(el)
@@ -205,7 +230,7 @@ def test_edge_cases():
     cb.cbfs_run(g.h, to_dev_u32(src), to_dev_u8(sz), 0, 2, 2, None, None, 3)
 
 
-def test_invalid_sources_rejected():
+def test_invalid_sources_rejected(engine):
     el = random_el(3, 500, "er")
     g = gpu_graph(el)
     for S, k in (([1, 1], 2), ([600], 1), ([0], 0)):
@@ -219,7 +244,7 @@ def test_invalid_sources_rejected():
     compare_many(g, ref, src, sz, 2)
 
 
-def test_overflow_u8():
+def test_overflow_u8(engine):
     n = 600
     el = random_el(0, n, "path")
     g = gpu_graph(el)
@@ -231,7 +256,7 @@ def test_overflow_u8():
     compare_many(g, ref, src, np.array([1], np.uint8), 0)  # u16 is fine
 
 
-def test_run_host_equals_device():
+def test_run_host_equals_device(engine):
     el = random_el(8, 3000, "rmat")
     ref = orc.csr_from_edgelist(el)
     src, sz = orc.select_clusters(ref, 45, 64, 2)
@@ -265,7 +290,7 @@ def test_decode_parity():
 
 # ------------------------------------------------------------------ A10/A11 labels and queries
 @pytest.mark.parametrize("d,planes,dist_bytes", [(2, 2, 1), (2, 3, 2), (4, 4, 2), (6, 6, 2)])
-def test_query_parity(d, planes, dist_bytes):
+def test_query_parity(d, planes, dist_bytes, engine):
     el = random_el(31 + d, 3000, "rmat" if d == 2 else "grid")
     ref = orc.csr_from_edgelist(el)
     src, sz = orc.select_clusters(ref, 70, 64, d)
@@ -334,7 +359,7 @@ def test_c2_full_size_sampled():
 
 
 @pytest.mark.parametrize("policy,r", [(0, 150), (1, 70), (0, 5000)])
-def test_select_and_run_equals_separate_calls(policy, r):
+def test_select_and_run_equals_separate_calls(policy, r, engine):
     """A1 overlapped with A2-A8 (cbfs_select_and_run) == cbfs_select_clusters + cbfs_run == oracle."""
     el = random_el(91, 5000, "rmat")
     ref = orc.csr_from_edgelist(el)
@@ -357,3 +382,42 @@ def test_select_and_run_equals_separate_calls(policy, r):
     assert np.array_equal(stats.cpu().numpy().view(np.uint64)[:got], om["stats"])
     if got < r:  # columns past the selected clusters stay unreached
         assert np.all(gd.T[got:] == 0xFFFF) and not np.any(np_u64(masks).transpose(2, 0, 1)[got:])
+
+
+# ------------------------------------------------------------------ engines
+def test_auto_engine_choice_and_equivalence():
+    """AUTO picks SPARSE on a high-diameter grid and BATCHED on an RMAT graph;
+    every engine gives the oracle's output on both (R8/R25)."""
+    for el, d in ((ci.grid(200, 0.05, 0.001, 7), 4), (ci.rmat(13, 16, 0.57, 0.19, 0.19, seed=7), 2)):
+        ref = orc.csr_from_edgelist(el)
+        src, sz = orc.select_clusters(ref, 100, 64, d)
+        g = gpu_graph(el)
+        for eng in (cb.CBFS_ENGINE_AUTO, cb.CBFS_ENGINE_BATCHED, cb.CBFS_ENGINE_SPARSE):
+            cb.cbfs_set_engine(eng)
+            cb.cbfs_profile_enable(True)
+            cb.cbfs_profile_read(reset=True)
+            compare_many(g, ref, src, sz, d)
+            prof = cb.cbfs_profile_read(reset=True)
+            cb.cbfs_profile_enable(False)
+            used_sparse = prof["sparse"]["launches"] > 0
+            if eng == cb.CBFS_ENGINE_AUTO:
+                assert used_sparse == (d == 4), (el.name, prof)
+            else:
+                assert used_sparse == (eng == cb.CBFS_ENGINE_SPARSE)
+
+
+def test_sparse_engine_round_cap_and_recovery():
+    """A path longer than 65534 rounds: EOVERFLOW from the device-side loop;
+    the workspace is usable afterwards."""
+    n = 70000
+    el = random_el(0, n, "path")
+    g = gpu_graph(el)
+    cb.cbfs_set_engine(cb.CBFS_ENGINE_SPARSE)
+    src = np.full((1, 64), orc.PAD, np.uint32); src[0, 0] = 0
+    with pytest.raises(cb.CbfsError) as e:
+        g.run(to_dev_u32(src), to_dev_u8(np.array([1], np.uint8)), 0)
+    assert e.value.code == cb.CBFS_EOVERFLOW
+    el2 = random_el(5, 2000, "grid")
+    ref2 = orc.csr_from_edgelist(el2)
+    src2, sz2 = orc.select_clusters(ref2, 20, 64, 2)
+    compare_many(gpu_graph(el2), ref2, src2, sz2, 2)

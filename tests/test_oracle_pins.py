@@ -95,6 +95,29 @@ def test_csr_matches_scipy():
         assert np.all(np.diff(row.astype(np.int64)) > 0) and v not in row
 
 
+@pytest.mark.parametrize("seed", range(3))
+def test_csr_c_builder_matches_scipy(seed):
+    """The C normaliser used for large edge lists (or_csr_build) gives scipy's
+    symmetrised, self-loop-free, deduplicated sorted CSR (and numpy's)."""
+    n = [300, 1000, 5000][seed]
+    rng = np.random.default_rng(100 + seed)
+    P = 6 * n
+    s = rng.integers(0, n, P).astype(np.uint32); t = rng.integers(0, n, P).astype(np.uint32)
+    s[:50] = t[:50]  # self loops
+    s[50:60] = s[60:70]; t[50:60] = t[60:70]  # duplicates
+    g = orc.csr_from_edges_c(n, s, t, threads=3)
+    A = sp.coo_matrix((np.ones(P), (s.astype(np.int64), t.astype(np.int64))), shape=(n, n))
+    A = ((A + A.T) > 0).astype(np.int8).tolil()
+    A.setdiag(0)
+    A = A.tocsr(); A.eliminate_zeros(); A.sort_indices()
+    assert np.array_equal(g.off.astype(np.int64), A.indptr.astype(np.int64))
+    assert np.array_equal(g.cols.astype(np.int64), A.indices.astype(np.int64))
+    g2 = orc.csr_from_edges(n, s, t)
+    assert np.array_equal(g.off, g2.off) and np.array_equal(g.cols, g2.cols)
+    with pytest.raises(ValueError):
+        orc.csr_from_edges_c(3, np.array([0], np.uint32), np.array([3], np.uint32))
+
+
 def test_csr_empty_and_isolated():
     g = orc.csr_from_edges(5, np.array([], np.uint32), np.array([], np.uint32))
     assert g.m == 0 and g.off.tolist() == [0] * 6
