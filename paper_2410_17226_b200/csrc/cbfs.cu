@@ -710,7 +710,7 @@ static int slot_round(Graph* g, Slot* w) {
     if (g_prof.on) CBFS_CUDA(cudaEventRecord(w->pe[3], st));
   } else if (E > 0) {
     w->kind = PK_PUSH;
-    w->pre_zero = false;
+    w->pre_zero_cells = 0;
     CBFS_CUDA(cub::DeviceScan::ExclusiveSum(w->scan_tmp, w->scan_bytes, w->pre, w->pre, nF, st));
     count_launch(2);
     k_set_u64<<<1, 1, 0, st>>>(w->pre + nF, E);
@@ -771,7 +771,7 @@ static int sparse_step(Graph* g, Slot* w, BatchSource& src, int slot, int* err) 
   w->i = (uint32_t)h.i;
   if (h.err & ERR_ROUNDS) {
     w->busy = false;
-    w->pre_zero = false;  // pending entries of the last round are left; the caller's error path clears them
+    w->pre_zero_cells = 0;  // pending entries of the last round are left; the caller's error path clears them
     *err = fail(CBFS_EOVERFLOW, "more than 65534 rounds");
     return 1;
   }
@@ -876,7 +876,7 @@ int run_batches(Graph* g, BatchSource& src, cudaStream_t st) {
       CBFS_CUDA(cudaMemset(w->pend, 0, D.cap * sizeof(uint64_t)));
       CBFS_CUDA(cudaMemset(w->ubits, 0, 2 * ((D.cap / LANES >> 5) + 1) * sizeof(uint32_t)));
       w->busy = false;
-      w->pre_zero = false;
+      w->pre_zero_cells = 0;
     }
   }
   return err;

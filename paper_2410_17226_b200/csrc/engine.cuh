@@ -83,7 +83,7 @@ struct Slot {
   bool overflow = false;
   // sparse engine
   int engine = ENGINE_BATCHED;  // engine of the batch in flight
-  bool pre_zero = false;        // `pre` is all zero (it is the sparse engine's second pending buffer)
+  uint64_t pre_zero_cells = 0;  // `pre` is zero over [0, pre_zero_cells) (the sparse engine's 2nd pending buffer)
   SpDesc* sp_desc = nullptr;    // device
   SpDesc* sp_desc_h = nullptr;  // pinned staging
   SpCtl* sp_ctl = nullptr;      // device

@@ -397,9 +397,9 @@ int sparse_start(const Graph* g, Slot* w, const RunArgs& a) {
   const uint64_t cells = (uint64_t)n * LANES;
   CBFS_CUDA(cudaMemsetAsync(w->seen, 0, cells * sizeof(uint64_t), st));
   CBFS_CUDA(cudaMemsetAsync(w->dist, 0xFF, cells * sizeof(uint16_t), st));
-  if (!w->pre_zero) {
-    CBFS_CUDA(cudaMemsetAsync(w->pre, 0, cells * sizeof(uint64_t), st));
-    w->pre_zero = true;
+  if (w->pre_zero_cells < cells) {  // the second pending buffer must be zero over this graph's cells
+    CBFS_CUDA(cudaMemsetAsync(w->pre + w->pre_zero_cells, 0, (cells - w->pre_zero_cells) * sizeof(uint64_t), st));
+    w->pre_zero_cells = cells;
   }
   CBFS_CUDA(cudaMemsetAsync(w->bstats, 0, LANES * 4 * sizeof(uint64_t), st));
   CBFS_CUDA(cudaMemsetAsync(w->sp_ctl, 0, sizeof(SpCtl), st));
