@@ -59,8 +59,8 @@ static DevSlots g_dev[MAX_DEV];
 static std::mutex g_work_mu[MAX_DEV];
 
 static void slot_free(Slot* w) {
-  cudaFree(w->seen); cudaFree(w->pend); cudaFree(w->dist); cudaFree(w->listA); cudaFree(w->listB);
-  cudaFree(w->pre); cudaFree(w->ubits); cudaFree(w->ctr); cudaFreeHost(w->h_ctr); cudaFree(w->bstats);
+  cudaFree(w->blk); cudaFree(w->listA); cudaFree(w->listB);
+  cudaFree(w->ubits); cudaFree(w->ctr); cudaFreeHost(w->h_ctr); cudaFree(w->bstats);
   cudaFree(w->scan_tmp);
   cudaFree(w->fullm);
   sparse_free(w);
@@ -73,25 +73,33 @@ static void slot_free(Slot* w) {
 
 void work_free(Graph* g) { g->work = nullptr; }  // the cache outlives graphs
 
-static uint64_t slot_bytes(uint64_t cap) {
-  return (cap + LANES) * 8 + cap * 8 + cap * 2 + cap * 8 + (cap + 1) * 8 + cap / 4;
+// One block per slot holds the per-cell state of either engine: the batched
+// engine's seen [cap + 64] | pend [cap] | pre [cap + 1] (u64) | dist [cap]
+// (u16), or the sparse engine's 32-byte cells (sparse.cu).
+static uint64_t blk_bytes(uint64_t cap) {
+  const uint64_t batched = (cap + LANES) * 8 + cap * 8 + (cap + 1) * 8 + cap * 2;
+  return std::max<uint64_t>(batched, cap * SPARSE_CELL_BYTES);
 }
+
+static uint64_t slot_bytes(uint64_t cap) { return blk_bytes(cap) + cap * 4 * 2 + cap / 4 + cap / 8; }
 
 static int slot_alloc(Slot* w, uint64_t cap) {
   w->cap = cap;
   const uint64_t ubw = 2 * ((cap / LANES >> 5) + 1);
-  CBFS_CUDA(cudaMalloc(&w->seen, (cap + LANES) * sizeof(uint64_t)));  // + all-zero row n
-  CBFS_CUDA(cudaMalloc(&w->pend, cap * sizeof(uint64_t)));
-  CBFS_CUDA(cudaMalloc(&w->dist, cap * sizeof(uint16_t)));
+  CBFS_CUDA(cudaMalloc(&w->blk, blk_bytes(cap)));
+  w->seen = reinterpret_cast<uint64_t*>(w->blk);  // [cap + LANES]: + all-zero row n
+  w->pend = w->seen + cap + LANES;
+  w->pre = w->pend + cap;
+  w->dist = reinterpret_cast<uint16_t*>(w->pre + cap + 1);
   CBFS_CUDA(cudaMalloc(&w->listA, cap * sizeof(uint32_t)));
   CBFS_CUDA(cudaMalloc(&w->listB, cap * sizeof(uint32_t)));
-  CBFS_CUDA(cudaMalloc(&w->pre, (cap + 1) * sizeof(uint64_t)));
   CBFS_CUDA(cudaMalloc(&w->ubits, ubw * sizeof(uint32_t)));
   CBFS_CUDA(cudaMalloc(&w->ctr, 4 * sizeof(unsigned long long)));
   CBFS_CUDA(cudaMallocHost(&w->h_ctr, 4 * sizeof(unsigned long long)));
   CBFS_CUDA(cudaMalloc(&w->bstats, LANES * 4 * sizeof(uint64_t)));
   CBFS_CUDA(cudaMalloc(&w->fullm, (cap / LANES + 1) * sizeof(uint64_t)));
   CBFS_CUDA(cudaMemset(w->pend, 0, cap * sizeof(uint64_t)));  // zero-invariant from here on
+  w->pend_clean_cells = cap;
   CBFS_CUDA(cudaMemset(w->ubits, 0, ubw * sizeof(uint32_t)));  // both bitmaps zero between batches
   CBFS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, w->scan_bytes, w->pre, w->pre, cap));
   CBFS_CUDA(cudaMalloc(&w->scan_tmp, w->scan_bytes ? w->scan_bytes : 1));
@@ -657,7 +665,15 @@ static int slot_start(Graph* g, Slot* w, const RunArgs& a) {
   w->overflow = false;
   w->i = 0;
   w->engine = a.engine;
-  if (a.engine == ENGINE_SPARSE) return sparse_start(g, w, a);
+  if (a.engine == ENGINE_SPARSE) {
+    w->pend_clean_cells = 0;  // the 32-byte cells overwrite the batched arrays
+    return sparse_start(g, w, a);
+  }
+  const uint64_t cells = (uint64_t)n * LANES;
+  if (w->pend_clean_cells < cells) {  // pend must be zero over this graph's cells
+    CBFS_CUDA(cudaMemsetAsync(w->pend, 0, cells * sizeof(uint64_t), st));
+    w->pend_clean_cells = cells;
+  }
   w->cur = w->listA;
   w->nxt = w->listB;
   CBFS_CUDA(cudaMemsetAsync(w->seen, 0, (uint64_t)(n + 1) * LANES * sizeof(uint64_t), st));
@@ -710,7 +726,6 @@ static int slot_round(Graph* g, Slot* w) {
     if (g_prof.on) CBFS_CUDA(cudaEventRecord(w->pe[3], st));
   } else if (E > 0) {
     w->kind = PK_PUSH;
-    w->pre_zero_cells = 0;
     CBFS_CUDA(cub::DeviceScan::ExclusiveSum(w->scan_tmp, w->scan_bytes, w->pre, w->pre, nF, st));
     count_launch(2);
     k_set_u64<<<1, 1, 0, st>>>(w->pre + nF, E);
@@ -753,25 +768,22 @@ static int sparse_step(Graph* g, Slot* w, BatchSource& src, int slot, int* err) 
   const SpCtl& h = *w->sp_ctl_h;
   if (w->seeding) {
     w->seeding = false;
-    if (h.err) {  // bad sources: restore the zero invariant of the first pending buffer, report
-      CBFS_CUDA(cudaMemsetAsync(w->pend, 0, (uint64_t)g->n * LANES * sizeof(uint64_t), w->s));
-      CBFS_CUDA(cudaStreamSynchronize(w->s));
-      return seed_error(w, h.err, err);
-    }
+    if (h.err) return seed_error(w, h.err, err);  // bad sources (every batch re-initialises its cells)
     int rc = sparse_launch(w);
     if (rc) { *err = rc; w->busy = false; return 1; }
     return 0;
   }
-  count_launch(3 * h.i);  // fold + push + tail per round, launched by the graph
+  const uint64_t per_round = w->sp_fused ? 2 : 3;  // (fold +) push + tail per round, launched by the graph
+  count_launch(per_round * h.i);
   if (g_prof.on) {
     float ms = 0;
     CBFS_CUDA(cudaEventElapsedTime(&ms, w->sp_t0, w->sp_t1));
-    g_prof.ms[PK_SPARSE] += ms; g_prof.launches[PK_SPARSE] += 3 * h.i;
+    g_prof.ms[PK_SPARSE] += ms; g_prof.launches[PK_SPARSE] += per_round * h.i;
+    g_prof.entries[PK_SPARSE] += h.listed;
   }
   w->i = (uint32_t)h.i;
   if (h.err & ERR_ROUNDS) {
     w->busy = false;
-    w->pre_zero_cells = 0;  // pending entries of the last round are left; the caller's error path clears them
     *err = fail(CBFS_EOVERFLOW, "more than 65534 rounds");
     return 1;
   }
@@ -876,8 +888,7 @@ int run_batches(Graph* g, BatchSource& src, cudaStream_t st) {
       CBFS_CUDA(cudaMemset(w->pend, 0, D.cap * sizeof(uint64_t)));
       CBFS_CUDA(cudaMemset(w->ubits, 0, 2 * ((D.cap / LANES >> 5) + 1) * sizeof(uint32_t)));
       w->busy = false;
-      w->pre_zero_cells = 0;
-    }
+      }
   }
   return err;
 }

@@ -27,6 +27,19 @@ __device__ __forceinline__ unsigned long long warp_sum(unsigned long long x) {
   return x;
 }
 
+// Sparse-engine state of one (cluster, vertex) cell: S_seen, Delta and the
+// two pending buffers P_i / P_{i+1} (S_next \ S_seen) in one 32-byte sector,
+// so the push touches one sector per arc (the cap test and the atomicOr hit
+// the same sector).
+struct __align__(32) SpCell {
+  uint64_t seen;
+  uint32_t dist;  // Delta, INF16 = unreached
+  uint32_t pad;
+  uint64_t p[2];
+};
+constexpr uint64_t SPARSE_CELL_BYTES = sizeof(SpCell);
+static_assert(sizeof(SpCell) == 32, "one sector per cell");
+
 // Device-resident description of the batch a sparse-engine slot runs: the
 // instantiated CUDA graph reads everything that changes per batch from here,
 // so one graph per slot serves every batch and every graph handle.
@@ -47,6 +60,7 @@ struct SpCtl {
   unsigned long long nF[2];  // frontier list sizes: list (i & 1) holds F_i
   unsigned long long err;    // ERR_* bits
   unsigned long long i;      // current round
+  unsigned long long listed; // frontier list entries processed (incl. entries whose S_new came out empty)
 };
 
 // One in-flight batch of LANES clusters: its workspace, its stream, and the
@@ -56,6 +70,7 @@ struct SpCtl {
 // cluster-major layout (see sparse.cu).
 struct Slot {
   uint64_t cap = 0;                     // n * LANES entries
+  void* blk = nullptr;                  // per-cell state of either engine (seen/pend/pre/dist or sparse cells)
   uint64_t* seen = nullptr;             // [n+1][64] S_seen (row n stays zero)
   uint64_t* pend = nullptr;             // [n][64] S_next \ S_seen (pending)
   uint16_t* dist = nullptr;             // [n][64] Delta
@@ -83,7 +98,7 @@ struct Slot {
   bool overflow = false;
   // sparse engine
   int engine = ENGINE_BATCHED;  // engine of the batch in flight
-  uint64_t pre_zero_cells = 0;  // `pre` is zero over [0, pre_zero_cells) (the sparse engine's 2nd pending buffer)
+  uint64_t pend_clean_cells = 0;  // the batched `pend` is zero over [0, pend_clean_cells)
   SpDesc* sp_desc = nullptr;    // device
   SpDesc* sp_desc_h = nullptr;  // pinned staging
   SpCtl* sp_ctl = nullptr;      // device
@@ -92,6 +107,7 @@ struct Slot {
   cudaGraphExec_t sp_exec = nullptr;
   cudaEvent_t sp_t0 = nullptr, sp_t1 = nullptr;  // profiling
   uint32_t sp_db = 0;                             // dist_bytes the graph was built for
+  bool sp_fused = false;                          // fold fused into the push (d >= 1)
 };
 
 struct DevSlots {

@@ -9,9 +9,9 @@
 // On a 4096^2 grid the 64 clusters' frontiers are 64 disjoint rings, so each
 // 32-byte sector of a row carries one useful 8-byte word, and the ~7,400
 // rounds each cost a host round trip.  Here:
-//  * state is CLUSTER-major: S_seen[c][v], Delta[c][v] and two pending
-//    buffers P[2][c][v] (P = S_next \ S_seen); a cluster's frontier band is
-//    contiguous along rows of the grid / along the relabelled order;
+//  * state is CLUSTER-major: cell[c][v] = {S_seen, Delta, P_0, P_1} in one
+//    32-byte sector (P = S_next \ S_seen, double-buffered by round parity);
+//    a cluster's frontier band is contiguous along rows of the grid;
 //  * rounds are push-only (EdgeMap-Sparse): per frontier entry
 //    (c, v) the bits S_new[v] are pushed to the neighbours (R7a: older bits of
 //    S_seen[v] reached them in earlier rounds), 64-bit atomicOr into the NEXT
@@ -23,6 +23,8 @@
 // the push of round i reads S_seen / Delta of its neighbours, and the push
 // writes only the other pending buffer, so the cap (R3) and the
 // claim see exactly Alg. 1's post-fold state.
+#include <cstdlib>
+
 #include "engine.cuh"
 
 namespace cbfs {
@@ -33,14 +35,27 @@ constexpr uint32_t VBITS = 26;  // list entry = c << 26 | v  (n <= CBFS_MAX_N = 
 constexpr uint32_t VMASK = (1u << VBITS) - 1;
 constexpr int SP_THREADS = 256;
 constexpr int SP_WARPS = SP_THREADS / 32;
-constexpr uint32_t SP_SMALL = 32;    // entries of higher degree are pushed by the whole warp
 constexpr uint32_t SP_OUTBUF = 256;  // per-warp claim buffer (entries)
+constexpr int SP_ILP = 4;            // neighbours per lane in flight (push)
+constexpr int SP_FOLD_ILP = 4;       // frontier entries per lane in flight (fold)
 constexpr unsigned SP_GRID = 148u * 8u;
 
+// ------------------------------------------------------------------ init
+// Per batch: every cell = {S_seen = 0, Delta = inf, P_0 = P_1 = 0} (A2).
+__global__ void k_sp_init(SpCell* __restrict__ cells, uint64_t count) {
+  const ulonglong2 a = make_ulonglong2(0ULL, (unsigned long long)INF16), z = make_ulonglong2(0ULL, 0ULL);
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < count;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    ulonglong2* p = reinterpret_cast<ulonglong2*>(cells + t);
+    p[0] = a;
+    p[1] = z;
+  }
+}
+
 // ------------------------------------------------------------------ seeding
-// R1 (S_next[s_j] = {j}, F_0 = S) in the cluster-major layout.
+// R1 (S_next[s_j] = {j}, F_0 = S): P_0 of cell (c, s_j) = bit j.
 __global__ void k_sp_seed(const uint32_t* __restrict__ sources, const uint8_t* __restrict__ sizes, uint32_t nb,
-                          uint32_t n, const uint32_t* __restrict__ inv, uint64_t* __restrict__ pend0,
+                          uint32_t n, const uint32_t* __restrict__ inv, SpCell* __restrict__ cells,
                           uint32_t* __restrict__ list0, SpCtl* __restrict__ ctl) {
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;  // 64 threads per cluster
   const uint32_t c = t >> 6, j = t & 63;
@@ -56,7 +71,8 @@ __global__ void k_sp_seed(const uint32_t* __restrict__ sources, const uint8_t* _
         atomicOr(&ctl->err, ERR_BAD_SOURCE);
       } else {
         const uint32_t x = inv ? inv[s] : s;
-        const unsigned long long old = atomicOr((unsigned long long*)&pend0[(uint64_t)c * n + x], 1ULL << j);
+        const unsigned long long old =
+            atomicOr((unsigned long long*)&cells[(uint64_t)c * n + x].p[0], 1ULL << j);
         if (old != 0) atomicOr(&ctl->err, ERR_DUP_SOURCE);  // R2
         else { claim = true; e = (c << VBITS) | x; }
       }
@@ -73,13 +89,12 @@ __global__ void k_sp_seed(const uint32_t* __restrict__ sources, const uint8_t* _
 
 // ------------------------------------------------------------------ fold
 // Vertex phase of round i for every entry of F_i: S_new =
-// P_i[c][v] \ S_seen[c][v]; Delta on first visit; S_v[i - Delta] = S_new;
-// S_seen |= S_new; the output writes; per-cluster statistics.  P_i keeps
-// S_new for the push of the same round.
+// P_i \ S_seen; Delta on first visit; S_v[i - Delta] = S_new; S_seen |=
+// S_new; the output writes; per-cluster statistics.  P_i keeps S_new for the
+// push of the same round.
 template <int DB>
 __global__ void __launch_bounds__(SP_THREADS) k_sp_fold(const SpDesc* __restrict__ D, SpCtl* __restrict__ ctl,
-                                                        uint64_t* __restrict__ seen, uint16_t* __restrict__ dist,
-                                                        uint64_t* __restrict__ pend0, uint64_t* __restrict__ pend1,
+                                                        SpCell* __restrict__ cells,
                                                         const uint32_t* __restrict__ list0,
                                                         const uint32_t* __restrict__ list1,
                                                         uint64_t* __restrict__ bstats) {
@@ -89,7 +104,6 @@ __global__ void __launch_bounds__(SP_THREADS) k_sp_fold(const SpDesc* __restrict
   const uint32_t i = (uint32_t)ctl->i;
   const uint32_t cur = i & 1;
   const uint32_t* __restrict__ L = cur ? list1 : list0;
-  uint64_t* __restrict__ P = cur ? pend1 : pend0;
   const uint64_t nF = ctl->nF[cur];
   const uint32_t n = D->n, planes = D->planes;
   const uint64_t C = D->C, cbase = D->cbase;
@@ -101,48 +115,67 @@ __global__ void __launch_bounds__(SP_THREADS) k_sp_fold(const SpDesc* __restrict
   bool overflow = false;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t b = warp * 32; b < nF; b += nwarps * 32) {
-    const uint64_t t = b + lane;
-    uint32_t c = LANES, deg = 0;
-    bool act = false, first = false;
-    if (t < nF) {
-      const uint32_t e = L[t];
-      c = e >> VBITS;
-      const uint32_t v = e & VMASK;
-      const uint64_t idx = (uint64_t)c * n + v;
-      const uint64_t p = P[idx], s = seen[idx];
-      const uint64_t nw = p & ~s;
-      if (nw != p) P[idx] = nw;
-      if (nw) {
-        act = true;
-        seen[idx] = s | nw;
-        uint32_t dv = dist[idx];
-        first = dv == INF16;
-        if (first) { dv = i; dist[idx] = (uint16_t)i; }
-        deg = (uint32_t)(off[v + 1] - off[v]);
-        const uint32_t orig = perm ? perm[v] : v;
-        const uint64_t col = (uint64_t)orig * C + cbase + c;
-        if (first && out_dist) {
-          if (DB == 1) {
-            overflow |= i > 254;
-            ((uint8_t*)out_dist)[col] = (uint8_t)(i > 254 ? 254 : i);
-          } else {
-            ((uint16_t*)out_dist)[col] = (uint16_t)i;
-          }
-        }
-        const uint32_t oi = i - dv;
-        if (out_masks && oi < planes) out_masks[(uint64_t)oi * n * C + col] = nw;
-      }
+  for (uint64_t b = warp * 32 * SP_FOLD_ILP; b < nF; b += nwarps * 32 * SP_FOLD_ILP) {
+    // SP_FOLD_ILP entries per lane: all their loads are issued before any is used
+    uint32_t e[SP_FOLD_ILP];
+    ulonglong2 sd[SP_FOLD_ILP];
+    uint64_t p[SP_FOLD_ILP], o0[SP_FOLD_ILP], o1[SP_FOLD_ILP];
+#pragma unroll
+    for (int q = 0; q < SP_FOLD_ILP; ++q) {
+      const uint64_t t = b + q * 32 + lane;
+      e[q] = t < nF ? L[t] : 0xFFFFFFFFu;
     }
-    // per-cluster statistics, one shared atomic per distinct cluster in the warp
-    const unsigned grp = __match_any_sync(FULLW, act ? c : 0xFFFFFFFFu);
-    const uint32_t fsum = __reduce_add_sync(grp, act ? 1u : 0u);
-    const uint32_t esum = __reduce_add_sync(grp, act ? deg : 0u);
-    const uint32_t msum = __reduce_add_sync(grp, act && first ? deg : 0u);
-    if (act && lane == (uint32_t)(__ffs(grp) - 1)) {
-      atomicAdd(&sF[c], (unsigned long long)fsum);
-      atomicAdd(&sE[c], (unsigned long long)esum);
-      if (msum) atomicAdd(&sM[c], (unsigned long long)msum);
+#pragma unroll
+    for (int q = 0; q < SP_FOLD_ILP; ++q) {
+      if (e[q] == 0xFFFFFFFFu) continue;
+      const uint32_t v = e[q] & VMASK;
+      const SpCell* cell = cells + (uint64_t)(e[q] >> VBITS) * n + v;
+      sd[q] = *reinterpret_cast<const ulonglong2*>(cell);  // {S_seen, Delta}
+      p[q] = cell->p[cur];
+      o0[q] = off[v];
+      o1[q] = off[v + 1];
+    }
+#pragma unroll
+    for (int q = 0; q < SP_FOLD_ILP; ++q) {
+      uint32_t c = LANES, deg = 0;
+      bool act = false, first = false;
+      if (e[q] != 0xFFFFFFFFu) {
+        c = e[q] >> VBITS;
+        const uint32_t v = e[q] & VMASK;
+        SpCell* cell = cells + (uint64_t)c * n + v;
+        const uint64_t nw = p[q] & ~sd[q].x;
+        if (nw != p[q]) cell->p[cur] = nw;
+        if (nw) {
+          act = true;
+          uint32_t dv = (uint32_t)sd[q].y;
+          first = dv == INF16;
+          if (first) dv = i;
+          *reinterpret_cast<ulonglong2*>(cell) = make_ulonglong2(sd[q].x | nw, (unsigned long long)dv);
+          deg = (uint32_t)(o1[q] - o0[q]);
+          const uint32_t orig = perm ? perm[v] : v;
+          const uint64_t col = (uint64_t)orig * C + cbase + c;
+          if (first && out_dist) {
+            if (DB == 1) {
+              overflow |= i > 254;
+              ((uint8_t*)out_dist)[col] = (uint8_t)(i > 254 ? 254 : i);
+            } else {
+              ((uint16_t*)out_dist)[col] = (uint16_t)i;
+            }
+          }
+          const uint32_t oi = i - dv;
+          if (out_masks && oi < planes) out_masks[(uint64_t)oi * n * C + col] = nw;
+        }
+      }
+      // per-cluster statistics, one shared atomic per distinct cluster in the warp
+      const unsigned grp = __match_any_sync(FULLW, act ? c : 0xFFFFFFFFu);
+      const uint32_t fsum = __reduce_add_sync(grp, act ? 1u : 0u);
+      const uint32_t esum = __reduce_add_sync(grp, act ? deg : 0u);
+      const uint32_t msum = __reduce_add_sync(grp, act && first ? deg : 0u);
+      if (act && lane == (uint32_t)(__ffs(grp) - 1)) {
+        atomicAdd(&sF[c], (unsigned long long)fsum);
+        atomicAdd(&sE[c], (unsigned long long)esum);
+        if (msum) atomicAdd(&sM[c], (unsigned long long)msum);
+      }
     }
   }
   if (overflow) atomicOr(&ctl->err, ERR_OVERFLOW);
@@ -161,38 +194,62 @@ __global__ void __launch_bounds__(SP_THREADS) k_sp_fold(const SpDesc* __restrict
 // N(v) with cap(u) (Delta_u = inf or i - Delta_u < d, R3): x =
 // S_new[v] \ S_seen[u]; if x != 0, atomicOr(P_{i+1}[c][u], x); the op that
 // turns P_{i+1}[c][u] non-zero appends (c, u) to F_{i+1} (R4).  P_i[c][v] is
-// cleared once read, so both pending buffers are zero between batches.
-__device__ __forceinline__ bool sp_try(uint64_t cn, uint32_t u, uint64_t nw, uint32_t i, uint32_t d,
-                                       const uint64_t* __restrict__ seen, const uint16_t* __restrict__ dist,
-                                       uint64_t* __restrict__ Pn) {
-  const uint64_t ui = cn + u;
-  const uint32_t du = dist[ui];
-  if (du != INF16 && (int)i - (int)du >= (int)d) return false;
-  const uint64_t x = nw & ~seen[ui];
-  if (!x) return false;
-  return atomicOr((unsigned long long*)&Pn[ui], (unsigned long long)x) == 0ULL;
-}
+// cleared once read, so both pending buffers are zero when the batch ends.
+// S_seen and Delta are not written during the push: read-only loads.
+// The warp takes SP_EPL * 32 frontier entries at a time, loads their S_new
+// and degree ranges together, and then walks the concatenation of their
+// neighbour lists SP_ILP * 32 arcs at a time (each lane finds its arcs'
+// entries by a binary search over the warp's degree prefix in shared memory),
+// so every lane keeps several independent memory operations in flight and
+// hubs and degree-4 grid vertices are balanced alike.
+constexpr int SP_EPL = 4;  // frontier entries per lane per warp step
+#ifndef CBFS_SP_MINB
+#define CBFS_SP_MINB 3
+#endif
 
-__global__ void __launch_bounds__(SP_THREADS) k_sp_push(const SpDesc* __restrict__ D, SpCtl* __restrict__ ctl,
-                                                        const uint64_t* __restrict__ seen,
-                                                        const uint16_t* __restrict__ dist, uint64_t* __restrict__ pend0,
-                                                        uint64_t* __restrict__ pend1, uint32_t* __restrict__ list0,
-                                                        uint32_t* __restrict__ list1) {
+//
+// FUSED (d >= 1): the fold of each entry runs in the same thread right before
+// its push, so a round is one kernel.  A pusher may then read a neighbour's
+// {S_seen, Delta} before that neighbour's own fold of this round: a stale
+// Delta = inf passes the cap exactly like the post-fold Delta = i does when d
+// >= 1 (H9), and bits the neighbour is folding this round may be pushed into
+// its P_{i+1} again — they are masked by the next fold (S_new = P \ S_seen),
+// and an entry whose S_new comes out empty is skipped (no output, statistic
+// or push), so outputs and round statistics are exactly Alg. 1's.  d = 0 uses
+// the separate fold kernel (there the post-fold cap differs).
+template <int DB, bool FUSED>
+__global__ void __launch_bounds__(SP_THREADS, CBFS_SP_MINB) k_sp_push(const SpDesc* __restrict__ D, SpCtl* __restrict__ ctl,
+                                                        SpCell* __restrict__ cells, uint32_t* __restrict__ list0,
+                                                        uint32_t* __restrict__ list1, uint64_t* __restrict__ bstats) {
+  constexpr int W = 32 * SP_EPL;  // entries per warp step
+  __shared__ unsigned long long sF[FUSED ? LANES : 1], sE[FUSED ? LANES : 1], sM[FUSED ? LANES : 1];
+  if (FUSED) {
+    for (uint32_t c = threadIdx.x; c < LANES; c += blockDim.x) sF[c] = sE[c] = sM[c] = 0;
+    __syncthreads();
+  }
+  bool overflow = false;
   __shared__ uint32_t s_out[SP_WARPS][SP_OUTBUF];
+  __shared__ uint32_t s_pre[SP_WARPS][W + 1];
+  __shared__ uint32_t s_c[SP_WARPS][W];
+  __shared__ uint64_t s_beg[SP_WARPS][W];
+  __shared__ uint64_t s_nw[SP_WARPS][W];
+  const uint32_t wib = threadIdx.x >> 5;
+  uint32_t* pre = s_pre[wib];
+  uint32_t* sc = s_c[wib];
+  uint64_t* sbeg = s_beg[wib];
+  uint64_t* snw = s_nw[wib];
   const uint32_t i = (uint32_t)ctl->i;
-  const uint32_t cur = i & 1;
+  const uint32_t cur = i & 1, nxt = cur ^ 1;
   const uint32_t* __restrict__ L = cur ? list1 : list0;
   uint32_t* __restrict__ Ln = cur ? list0 : list1;
-  uint64_t* __restrict__ P = cur ? pend1 : pend0;
-  uint64_t* __restrict__ Pn = cur ? pend0 : pend1;
-  unsigned long long* cnt = &ctl->nF[cur ^ 1];
+  unsigned long long* cnt = &ctl->nF[nxt];
   const uint64_t nF = ctl->nF[cur];
   const uint32_t n = D->n, d = D->d;
   const uint64_t* __restrict__ off = D->off;
   const uint32_t* __restrict__ cols = D->cols;
   const uint32_t lane = lane_id();
   const unsigned lt = (1u << lane) - 1;
-  uint32_t* obuf = s_out[threadIdx.x >> 5];
+  uint32_t* obuf = s_out[wib];
   uint32_t nout = 0;
   auto emit = [&](bool claim, uint32_t val) {
     const unsigned m = __ballot_sync(FULLW, claim);
@@ -210,57 +267,132 @@ __global__ void __launch_bounds__(SP_THREADS) k_sp_push(const SpDesc* __restrict
   };
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t b = warp * 32; b < nF; b += nwarps * 32) {
-    const uint64_t t = b + lane;
-    uint32_t c = 0, v = 0;
-    uint64_t nw = 0, beg = 0, end = 0;
-    if (t < nF) {
-      const uint32_t e = L[t];
-      c = e >> VBITS;
-      v = e & VMASK;
-      const uint64_t idx = (uint64_t)c * n + v;
-      nw = P[idx];
-      if (nw) {
-        P[idx] = 0;
-        beg = off[v];
-        end = off[v + 1];
+  for (uint64_t b = warp * W; b < nF; b += nwarps * W) {
+    // ---- the step's entries: S_new (cleared once read) and neighbour ranges
+    uint32_t e[SP_EPL];
+    uint64_t nw[SP_EPL], o0[SP_EPL], o1[SP_EPL];
+#pragma unroll
+    for (int q = 0; q < SP_EPL; ++q) {
+      const uint64_t t = b + q * 32 + lane;
+      e[q] = t < nF ? L[t] : 0xFFFFFFFFu;
+    }
+    ulonglong2 sd0[SP_EPL];
+#pragma unroll
+    for (int q = 0; q < SP_EPL; ++q) {
+      nw[q] = 0;
+      o0[q] = o1[q] = 0;
+      if (e[q] != 0xFFFFFFFFu) {
+        const uint32_t v = e[q] & VMASK;
+        const SpCell* cell = cells + (uint64_t)(e[q] >> VBITS) * n + v;
+        nw[q] = cell->p[cur];
+        if (FUSED) sd0[q] = *reinterpret_cast<const ulonglong2*>(cell);  // {S_seen, Delta}
+        o0[q] = off[v];
+        o1[q] = off[v + 1];
       }
     }
-    const uint64_t cn = (uint64_t)c * n;
-    const uint64_t deg = end - beg;
-    const bool big = deg > SP_SMALL;
-    // entries of small degree: every lane walks its own neighbour list
-    const uint32_t sdeg = big ? 0u : (uint32_t)deg;
-    const uint32_t maxd = __reduce_max_sync(FULLW, sdeg);
-    for (uint32_t k = 0; k < maxd; ++k) {
-      bool claim = false;
-      uint32_t u = 0;
-      if (k < sdeg) {
-        u = cols[beg + k];
-        claim = sp_try(cn, u, nw, i, d, seen, dist, Pn);
-      }
-      emit(claim, (c << VBITS) | u);
-    }
-    // entries of large degree: the whole warp walks one list at a time
-    unsigned bigm = __ballot_sync(FULLW, big);
-    while (bigm) {
-      const int j = __ffs(bigm) - 1;
-      bigm &= bigm - 1;
-      const uint32_t cj = __shfl_sync(FULLW, c, j);
-      const uint64_t bj = __shfl_sync(FULLW, beg, j), ej = __shfl_sync(FULLW, end, j);
-      const uint64_t nwj = __shfl_sync(FULLW, nw, j);
-      const uint64_t cnj = (uint64_t)cj * n;
-      for (uint64_t a0 = bj; a0 < ej; a0 += 32) {
-        const uint64_t a = a0 + lane;
-        bool claim = false;
-        uint32_t u = 0;
-        if (a < ej) {
-          u = cols[a];
-          claim = sp_try(cnj, u, nwj, i, d, seen, dist, Pn);
+    if (FUSED) {  // the fold of the step's entries
+#pragma unroll
+      for (int q = 0; q < SP_EPL; ++q) {
+        uint32_t c = LANES, deg = 0;
+        bool act = false, first = false;
+        if (e[q] != 0xFFFFFFFFu) {
+          c = e[q] >> VBITS;
+          const uint32_t v = e[q] & VMASK;
+          SpCell* cell = cells + (uint64_t)c * n + v;
+          const uint64_t p = nw[q];
+          nw[q] = p & ~sd0[q].x;
+          if (nw[q]) {
+            act = true;
+            uint32_t dv = (uint32_t)sd0[q].y;
+            first = dv == INF16;
+            if (first) dv = i;
+            *reinterpret_cast<ulonglong2*>(cell) = make_ulonglong2(sd0[q].x | nw[q], (unsigned long long)dv);
+            deg = (uint32_t)(o1[q] - o0[q]);
+            const uint32_t orig = D->perm ? D->perm[v] : v;
+            const uint64_t col = (uint64_t)orig * D->C + D->cbase + c;
+            if (first && D->out_dist) {
+              if (DB == 1) {
+                overflow |= i > 254;
+                ((uint8_t*)D->out_dist)[col] = (uint8_t)(i > 254 ? 254 : i);
+              } else {
+                ((uint16_t*)D->out_dist)[col] = (uint16_t)i;
+              }
+            }
+            const uint32_t oi = i - dv;
+            if (D->out_masks && oi < D->planes) D->out_masks[(uint64_t)oi * n * D->C + col] = nw[q];
+          }
+          if (p) cell->p[cur] = 0;
         }
-        emit(claim, (cj << VBITS) | u);
+        const unsigned grp = __match_any_sync(FULLW, act ? c : 0xFFFFFFFFu);
+        const uint32_t fsum = __reduce_add_sync(grp, act ? 1u : 0u);
+        const uint32_t esum = __reduce_add_sync(grp, act ? deg : 0u);
+        const uint32_t msum = __reduce_add_sync(grp, act && first ? deg : 0u);
+        if (act && lane == (uint32_t)(__ffs(grp) - 1)) {
+          atomicAdd(&sF[c], (unsigned long long)fsum);
+          atomicAdd(&sE[c], (unsigned long long)esum);
+          if (msum) atomicAdd(&sM[c], (unsigned long long)msum);
+        }
       }
     }
+    uint32_t base = 0;
+#pragma unroll
+    for (int q = 0; q < SP_EPL; ++q) {
+      if (!FUSED && nw[q]) cells[(uint64_t)(e[q] >> VBITS) * n + (e[q] & VMASK)].p[cur] = 0;
+      const uint32_t deg = nw[q] ? (uint32_t)(o1[q] - o0[q]) : 0u;
+      uint32_t inc = deg;  // inclusive warp scan of the degrees
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULLW, inc, o);
+        if (lane >= (uint32_t)o) inc += y;
+      }
+      const int idx = q * 32 + lane;
+      pre[idx] = base + inc - deg;
+      sc[idx] = e[q] >> VBITS;
+      sbeg[idx] = o0[q];
+      snw[idx] = nw[q];
+      base += __shfl_sync(FULLW, inc, 31);
+    }
+    if (lane == 0) pre[W] = base;
+    __syncwarp();
+    // ---- the step's arcs, SP_ILP * 32 at a time
+    for (uint32_t a0 = 0; a0 < base; a0 += 32 * SP_ILP) {
+      uint32_t u[SP_ILP], cq[SP_ILP];
+      uint64_t nq[SP_ILP];
+      ulonglong2 sd[SP_ILP];
+      bool claim[SP_ILP];
+#pragma unroll
+      for (int r = 0; r < SP_ILP; ++r) {
+        const uint32_t a = a0 + r * 32 + lane;
+        u[r] = 0xFFFFFFFFu;
+        if (a < base) {
+          int lo = 0, hi = W;  // largest idx with pre[idx] <= a
+          while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (pre[mid] <= a) lo = mid; else hi = mid;
+          }
+          cq[r] = sc[lo];
+          nq[r] = snw[lo];
+          u[r] = cols[sbeg[lo] + (a - pre[lo])];
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < SP_ILP; ++r)
+        if (u[r] != 0xFFFFFFFFu) sd[r] = __ldg(reinterpret_cast<const ulonglong2*>(cells + (uint64_t)cq[r] * n + u[r]));
+#pragma unroll
+      for (int r = 0; r < SP_ILP; ++r) {
+        claim[r] = false;
+        if (u[r] == 0xFFFFFFFFu) continue;
+        const uint32_t du = (uint32_t)sd[r].y;
+        if (du != INF16 && (int)i - (int)du >= (int)d) continue;  // cap, R3
+        const uint64_t x = nq[r] & ~sd[r].x;
+        if (x)
+          claim[r] = atomicOr((unsigned long long*)&cells[(uint64_t)cq[r] * n + u[r]].p[nxt],
+                              (unsigned long long)x) == 0ULL;
+      }
+#pragma unroll
+      for (int r = 0; r < SP_ILP; ++r) emit(claim[r], claim[r] ? ((cq[r] << VBITS) | u[r]) : 0u);
+    }
+    __syncwarp();
   }
   __syncwarp();
   if (nout) {
@@ -268,6 +400,17 @@ __global__ void __launch_bounds__(SP_THREADS) k_sp_push(const SpDesc* __restrict
     if (lane == 0) base = atomicAdd(cnt, (unsigned long long)nout);
     base = __shfl_sync(FULLW, base, 0);
     for (uint32_t q = lane; q < nout; q += 32) Ln[base + q] = obuf[q];
+  }
+  if (FUSED) {
+    if (overflow) atomicOr(&ctl->err, ERR_OVERFLOW);
+    __syncthreads();
+    for (uint32_t c = threadIdx.x; c < LANES; c += blockDim.x) {
+      if (!sF[c]) continue;
+      atomicAdd((unsigned long long*)&bstats[c * 4 + 1], sF[c]);
+      atomicAdd((unsigned long long*)&bstats[c * 4 + 2], sE[c]);
+      if (sM[c]) atomicAdd((unsigned long long*)&bstats[c * 4 + 3], sM[c]);
+      atomicMax((unsigned long long*)&bstats[c * 4 + 0], (unsigned long long)(i + 1));
+    }
   }
 }
 
@@ -277,6 +420,7 @@ __global__ void __launch_bounds__(SP_THREADS) k_sp_push(const SpDesc* __restrict
 __global__ void k_sp_tail(SpCtl* __restrict__ ctl, cudaGraphConditionalHandle h) {
   const unsigned long long i = ctl->i;
   const uint32_t cur = i & 1;
+  ctl->listed += ctl->nF[cur];
   ctl->nF[cur] = 0;
   const unsigned long long nn = ctl->nF[cur ^ 1];
   ctl->i = i + 1;
@@ -285,7 +429,7 @@ __global__ void k_sp_tail(SpCtl* __restrict__ ctl, cudaGraphConditionalHandle h)
     atomicOr(&ctl->err, ERR_ROUNDS);
     go = false;
   }
-  cudaGraphSetConditional(h, go ? 1u : 0u);
+  if (h) cudaGraphSetConditional(h, go ? 1u : 0u);  // h == 0: host-driven loop (profiling mode)
 }
 
 // ------------------------------------------------------------------ host
@@ -304,7 +448,7 @@ static int sp_add_kernel(cudaGraph_t body, cudaGraphNode_t* node, const cudaGrap
 // The per-slot round-loop graph: WHILE (F_i non-empty) { fold; push; tail }.
 // Two graphs per slot would be needed for the two Delta output widths; the
 // fold instance is chosen by dist_bytes when the graph is (re)built.
-static int sp_build(Slot* w, uint32_t dist_bytes) {
+static int sp_build(Slot* w, uint32_t dist_bytes, bool fused) {
   if (w->sp_exec) {
     CBFS_CUDA(cudaGraphExecDestroy(w->sp_exec));
     w->sp_exec = nullptr;
@@ -328,23 +472,29 @@ static int sp_build(Slot* w, uint32_t dist_bytes) {
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   SpDesc* D = w->sp_desc;
   SpCtl* ctl = w->sp_ctl;
-  uint64_t* pend0 = w->pend;
-  uint64_t* pend1 = w->pre;
+  SpCell* cells = reinterpret_cast<SpCell*>(w->blk);
   uint32_t* l0 = w->listA;
   uint32_t* l1 = w->listB;
-  void* fa[] = {&D, &ctl, &w->seen, &w->dist, &pend0, &pend1, &l0, &l1, &w->bstats};
-  void* pa[] = {&D, &ctl, &w->seen, &w->dist, &pend0, &pend1, &l0, &l1};
+  void* fa[] = {&D, &ctl, &cells, &l0, &l1, &w->bstats};
   void* ta[] = {&ctl, &h};
   cudaGraphNode_t nf, np, nt;
-  int rc = sp_add_kernel(body, &nf, nullptr, dist_bytes == 1 ? (void*)k_sp_fold<1> : (void*)k_sp_fold<2>, SP_GRID,
-                         SP_THREADS, fa);
-  if (rc) return rc;
-  rc = sp_add_kernel(body, &np, &nf, (void*)k_sp_push, SP_GRID, SP_THREADS, pa);
-  if (rc) return rc;
+  int rc;
+  if (fused) {  // d >= 1: one kernel per round
+    rc = sp_add_kernel(body, &np, nullptr, dist_bytes == 1 ? (void*)k_sp_push<1, true> : (void*)k_sp_push<2, true>,
+                       SP_GRID, SP_THREADS, fa);
+    if (rc) return rc;
+  } else {
+    rc = sp_add_kernel(body, &nf, nullptr, dist_bytes == 1 ? (void*)k_sp_fold<1> : (void*)k_sp_fold<2>, SP_GRID,
+                       SP_THREADS, fa);
+    if (rc) return rc;
+    rc = sp_add_kernel(body, &np, &nf, (void*)k_sp_push<2, false>, SP_GRID, SP_THREADS, fa);
+    if (rc) return rc;
+  }
   rc = sp_add_kernel(body, &nt, &np, (void*)k_sp_tail, 1, 1, ta);
   if (rc) return rc;
   CBFS_CUDA(cudaGraphInstantiate(&w->sp_exec, g, 0));
   w->sp_db = dist_bytes;
+  w->sp_fused = fused;
   return CBFS_OK;
 }
 
@@ -372,8 +522,9 @@ void sparse_free(Slot* w) {
 int sparse_start(const Graph* g, Slot* w, const RunArgs& a) {
   const uint32_t n = g->n;
   cudaStream_t st = w->s;
-  if (!w->sp_exec || w->sp_db != a.dist_bytes) {
-    int rc = sp_build(w, a.dist_bytes);
+  const bool fused = a.d >= 1;
+  if (!w->sp_exec || w->sp_db != a.dist_bytes || w->sp_fused != fused) {
+    int rc = sp_build(w, a.dist_bytes, fused);
     if (rc) return rc;
   }
   SpDesc* h = w->sp_desc_h;  // the slot's previous batch (and its copy) finished before this one starts
@@ -394,24 +545,64 @@ int sparse_start(const Graph* g, Slot* w, const RunArgs& a) {
   h->dist_bytes = a.dist_bytes;
   h->pad = 0;
   CBFS_CUDA(cudaMemcpyAsync(w->sp_desc, h, sizeof(SpDesc), cudaMemcpyHostToDevice, st));
-  const uint64_t cells = (uint64_t)n * LANES;
-  CBFS_CUDA(cudaMemsetAsync(w->seen, 0, cells * sizeof(uint64_t), st));
-  CBFS_CUDA(cudaMemsetAsync(w->dist, 0xFF, cells * sizeof(uint16_t), st));
-  if (w->pre_zero_cells < cells) {  // the second pending buffer must be zero over this graph's cells
-    CBFS_CUDA(cudaMemsetAsync(w->pre + w->pre_zero_cells, 0, (cells - w->pre_zero_cells) * sizeof(uint64_t), st));
-    w->pre_zero_cells = cells;
-  }
+  const uint64_t ncell = (uint64_t)n * LANES;
+  k_sp_init<<<grid_for(ncell, 256, 148u * 16u), 256, 0, st>>>(reinterpret_cast<SpCell*>(w->blk), ncell);
+  CBFS_LAUNCHED();
   CBFS_CUDA(cudaMemsetAsync(w->bstats, 0, LANES * 4 * sizeof(uint64_t), st));
   CBFS_CUDA(cudaMemsetAsync(w->sp_ctl, 0, sizeof(SpCtl), st));
-  k_sp_seed<<<(a.nb * 64 + 255) / 256, 256, 0, st>>>(a.sources, a.sizes, a.nb, n, g->inv, w->pend, w->listA,
-                                                     w->sp_ctl);
+  k_sp_seed<<<(a.nb * 64 + 255) / 256, 256, 0, st>>>(a.sources, a.sizes, a.nb, n, g->inv,
+                                                     reinterpret_cast<SpCell*>(w->blk), w->listA, w->sp_ctl);
   CBFS_LAUNCHED();
   CBFS_CUDA(cudaMemcpyAsync(w->sp_ctl_h, w->sp_ctl, sizeof(SpCtl), cudaMemcpyDeviceToHost, st));
   CBFS_CUDA(cudaEventRecord(w->ready, st));
   return CBFS_OK;
 }
 
+// Profiling aid (env CBFS_SPARSE_HOSTLOOP=1): the same kernels launched one
+// by one with a host round trip per round, so that ncu (which cannot profile
+// kernel nodes of graphs with conditional nodes) sees them.  Synchronous.
+static int sparse_hostloop(Slot* w) {
+  cudaStream_t st = w->s;
+  SpDesc* D = w->sp_desc;
+  SpCtl* ctl = w->sp_ctl;
+  CBFS_CUDA(cudaEventRecord(w->sp_t0, st));
+  for (;;) {
+    SpCell* cells = reinterpret_cast<SpCell*>(w->blk);
+    if (w->sp_fused) {
+      if (w->sp_db == 1)
+        k_sp_push<1, true><<<SP_GRID, SP_THREADS, 0, st>>>(D, ctl, cells, w->listA, w->listB, w->bstats);
+      else
+        k_sp_push<2, true><<<SP_GRID, SP_THREADS, 0, st>>>(D, ctl, cells, w->listA, w->listB, w->bstats);
+    } else {
+      if (w->sp_db == 1)
+        k_sp_fold<1><<<SP_GRID, SP_THREADS, 0, st>>>(D, ctl, cells, w->listA, w->listB, w->bstats);
+      else
+        k_sp_fold<2><<<SP_GRID, SP_THREADS, 0, st>>>(D, ctl, cells, w->listA, w->listB, w->bstats);
+      k_sp_push<2, false><<<SP_GRID, SP_THREADS, 0, st>>>(D, ctl, cells, w->listA, w->listB, w->bstats);
+    }
+    k_sp_tail<<<1, 1, 0, st>>>(ctl, 0);
+    CBFS_CUDA(cudaGetLastError());
+    CBFS_CUDA(cudaMemcpyAsync(w->sp_ctl_h, ctl, sizeof(SpCtl), cudaMemcpyDeviceToHost, st));
+    CBFS_CUDA(cudaStreamSynchronize(st));
+    const SpCtl& h = *w->sp_ctl_h;
+    if (h.nF[h.i & 1] == 0 || h.i >= 0xFFFEull) {
+      if (h.nF[h.i & 1] && h.i >= 0xFFFEull) {
+        SpCtl c = h;
+        c.err |= ERR_ROUNDS;
+        CBFS_CUDA(cudaMemcpyAsync(ctl, &c, sizeof(SpCtl), cudaMemcpyHostToDevice, st));
+      }
+      break;
+    }
+  }
+  CBFS_CUDA(cudaEventRecord(w->sp_t1, st));
+  CBFS_CUDA(cudaMemcpyAsync(w->sp_ctl_h, ctl, sizeof(SpCtl), cudaMemcpyDeviceToHost, st));
+  CBFS_CUDA(cudaEventRecord(w->ready, st));
+  return CBFS_OK;
+}
+
 int sparse_launch(Slot* w) {
+  static const bool hostloop = getenv("CBFS_SPARSE_HOSTLOOP") != nullptr;
+  if (hostloop) return sparse_hostloop(w);
   cudaStream_t st = w->s;
   CBFS_CUDA(cudaEventRecord(w->sp_t0, st));
   CBFS_CUDA(cudaGraphLaunch(w->sp_exec, st));
