@@ -223,6 +223,46 @@ def run_reference(args, world, rank):
 
 
 # ------------------------------------------------------------------ our arm
+# How a config's outputs are consumed:
+#   full  — every cluster's full distance vector (Delta + d+1 bit-subset planes)
+#           is written to HBM-resident output buffers (configs 1, 2);
+#   stats — the vectors do not fit HBM (1.8 TB / 0.36 TB for configs 3 / 4):
+#           the traversal runs in full but only the per-cluster round
+#           statistics leave the library (stated in `config.outputs`);
+#   query — config 5: the labels of every batch are consumed by 10M distance
+#           queries as soon as they are built (cbfs_query_stream, H3); with
+#           N ranks the answers are MIN-all-reduced (NCCL, A12).
+MODES = {"c1_er": "full", "c2_rmat20": "full", "c3_rmat24": "stats", "c4_grid": "stats", "c5_knn": "query"}
+INT32_MAX = 2**31 - 1
+
+
+def alg_bytes_model(prof, stats_np, sizes_np, n, m_h, n_ni, d, planes, dist_bytes, C, mode, queries):
+    """Algorithmic (compulsory) HBM bytes of the step's C-BFS kernels.
+
+    batched engine: per pull launch 4 B per CSR arc + 136 B per non-isolated
+    vertex row + 512 B per distinct frontier row read and per claimed row
+    written; 40 B per fold entry and 22 B per pushed (cluster, arc) pair
+    (SURVEY §8(d)); sparse engine: SURVEY §8(d)'s per-cluster model
+    22 B x sum_i E_i + 40 B x sum_i |F_i|.  Both: 10 B per (vertex, cluster)
+    of state initialisation (S_seen + Delta) and the output bytes written;
+    query mode: 4 B per (query, cluster) Delta reads."""
+    pull, fold, push, sp = prof["pull"], prof["fold"], prof["push"], prof["sparse"]
+    parts = {}
+    parts["pull"] = pull["launches"] * (BYTES_PER_ARC * m_h + BYTES_PER_VROW * n_ni) + \
+        BYTES_PER_ROW * (pull["u_in"] + pull["u_out"])
+    parts["fold"] = BYTES_PER_FRONTIER_ENTRY * fold["entries"]
+    parts["push"] = BYTES_PER_FRONTIER_ARC * push["arcs"]
+    if sp["launches"]:
+        parts["sparse"] = BYTES_PER_FRONTIER_ARC * float(stats_np[:, 2].astype(np.float64).sum()) + \
+            BYTES_PER_FRONTIER_ENTRY * float(stats_np[:, 1].astype(np.float64).sum())
+    parts["init"] = 10.0 * n * C
+    if mode == "full":
+        parts["outputs"] = float(n) * C * (dist_bytes + 8 * planes)
+    if mode == "query":
+        parts["queries"] = 4.0 * queries * C
+    return parts
+
+
 def run_ours(args, world, rank, local):
     import torch
 
@@ -230,12 +270,14 @@ def run_ours(args, world, rank, local):
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     cfg = ci.CONFIGS[args.config]
+    mode = args.mode or MODES[args.config]
     d, k = cfg["d"], cfg["k"]
-    C = cfg["clusters"]
+    C = args.clusters or cfg["clusters"]
     r_total, first = shard(C, world, rank)
     policy = cb.CBFS_ROOT_RANDOM if cfg["root"] == "random" else cb.CBFS_ROOT_DEGREE
     relabel = cfg["kind"] in ("rmat", "er")
     dist_bytes = 1 if cfg["kind"] in ("rmat", "er") else 2
+    planes = d + 1
 
     t0 = time.perf_counter()
     el = ci.make_graph(args.config)
@@ -244,8 +286,18 @@ def run_ours(args, world, rank, local):
     dst_h = torch.from_numpy(el.dst.view(np.int32)).pin_memory()
     src_d, dst_d = src_h.to(dev), dst_h.to(dev)
     n = el.n
-    dist_out = torch.empty((n, C), dtype=torch.uint8 if dist_bytes == 1 else torch.int16, device=dev)
-    masks_out = torch.empty((d + 1, n, C), dtype=torch.int64, device=dev)
+    Q = 0
+    dist_out = masks_out = best = qs_d = qt_d = None
+    if mode == "full":
+        dist_out = torch.empty((n, C), dtype=torch.uint8 if dist_bytes == 1 else torch.int16, device=dev)
+        masks_out = torch.empty((planes, n, C), dtype=torch.int64, device=dev)
+    if mode == "query":
+        Q = args.queries or cfg.get("queries", 0)
+        qs, qt = ci.query_pairs(n, Q, cfg.get("query_seed", 7))
+        qs_h = torch.from_numpy(qs.view(np.int32)).pin_memory()
+        qt_h = torch.from_numpy(qt.view(np.int32)).pin_memory()
+        qs_d, qt_d = qs_h.to(dev), qt_h.to(dev)
+        best = torch.empty((Q,), dtype=torch.int32, device=dev)
     stats = torch.zeros((C, 4), dtype=torch.int64, device=dev)
     sel_src = torch.empty((r_total, 64), dtype=torch.int32, device=dev)
     sel_sz = torch.empty((r_total,), dtype=torch.uint8, device=dev)
@@ -255,24 +307,40 @@ def run_ours(args, world, rank, local):
         cb.cbfs_set_direction_alpha(args.alpha)
     if args.concurrency:
         cb.cbfs_set_concurrency(args.concurrency)
+    if args.engine:
+        cb.cbfs_set_engine(args.engine)
+    overlap = world == 1 and mode == "full" and not args.separate_select
 
     phase_ms = {"build": 0.0, "select": 0.0, "cbfs": 0.0}
+
+    def traverse(h):
+        blk_src, blk_sz = sel_src[first:first + C], sel_sz[first:first + C]
+        if mode == "full":
+            cb.cbfs_run(h, blk_src, blk_sz, C, d, dist_bytes, dist_out, masks_out, planes, stats, args.direction,
+                        stream)
+        elif mode == "stats":
+            cb.cbfs_run(h, blk_src, blk_sz, C, d, dist_bytes, None, None, planes, stats, args.direction, stream)
+        else:
+            best.fill_(INT32_MAX)
+            cb.cbfs_query_stream(h, blk_src, blk_sz, C, d, qs_d, qt_d, best, stats, stream)
+            if world > 1:
+                import torch.distributed as tdist
+                tdist.all_reduce(best, op=tdist.ReduceOp.MIN)  # A12: answers MIN-all-reduced over ranks
 
     def step(timed_phases: bool):
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         evs[0].record(stream)
         h = cb.cbfs_graph_create(n, src_d, dst_d, cb.CBFS_RELABEL_DEGREE if relabel else 0, local, stream)
         evs[1].record(stream)
-        if world == 1 and not args.separate_select:
+        if overlap:
             # A1 overlapped with A2-A8: traversal of batch b starts once its clusters are selected
             evs[2].record(stream)
             got = cb.cbfs_select_and_run(h, r_total, k, d, policy, cfg["root_seed"], sel_src, sel_sz, dist_bytes,
-                                         dist_out, masks_out, d + 1, stats, args.direction, stream)
+                                         dist_out, masks_out, planes, stats, args.direction, stream)
         else:
             got = cb.cbfs_select_clusters(h, r_total, k, d, policy, cfg["root_seed"], sel_src, sel_sz, stream)
             evs[2].record(stream)
-            cb.cbfs_run(h, sel_src[first:first + C], sel_sz[first:first + C], C, d, dist_bytes, dist_out,
-                        masks_out, d + 1, stats, args.direction, stream)
+            traverse(h)
         assert got == r_total, f"selection produced {got} < {r_total} clusters"
         evs[3].record(stream)
         cb.cbfs_graph_destroy(h)
@@ -312,81 +380,81 @@ def run_ours(args, world, rank, local):
     st = stats.cpu().numpy().view(np.uint64)
     sizes = sel_sz[first:first + C].cpu().numpy().astype(np.float64)
     units_step = float((sizes * st[:, 3].astype(np.float64)).sum())
-    n_h, m_h, maxdeg = None, None, None
     hh = cb.cbfs_graph_create(n, src_d, dst_d, 0, local, stream)
     n_h, m_h, maxdeg = cb.cbfs_graph_info(hh)
     n_ni = cb.cbfs_graph_nonisolated(hh)
     cb.cbfs_graph_destroy(hh)
-    units_wholegraph = float(sizes.sum()) * m_h
 
     T = allreduce_max(total_ms, world) / 1000.0
     units_all = allreduce_sum(units_step * args.steps, world)
     value = units_all / T
 
-    # ---- roofline of the dominant kernel (per-launch algorithmic bytes / avg duration)
+    # ---- roofline of the step's C-BFS kernels (batches run concurrently on several streams, so the
+    # unit is the kernel group of the traversal phase: algorithmic bytes / phase time), plus a
+    # per-kernel breakdown of the summed per-launch event times
     peak, peak_src = peaks()
-    dom = max(prof, key=lambda kk: prof[kk]["ms"])
-    pk = prof[dom]
-    if dom == "pull":
-        # compulsory HBM bytes of one batched pull launch: every CSR column once,
-        # every non-isolated vertex's state row (64 x u16 Delta + 64 x u64 S_seen), every distinct
-        # frontier row once, every claimed row written once
-        alg_bytes = (pk["launches"] * (BYTES_PER_ARC * m_h + BYTES_PER_VROW * n_ni)
-                     + BYTES_PER_ROW * (pk["u_in"] + pk["u_out"]))
-        model = (f"{BYTES_PER_ARC} B per CSR arc + {BYTES_PER_VROW} B per non-isolated vertex row + "
-                 f"{BYTES_PER_ROW} B per distinct frontier row read and per claimed row written")
-    elif dom == "fold":
-        alg_bytes = BYTES_PER_FRONTIER_ENTRY * pk["entries"]
-        model = f"{BYTES_PER_FRONTIER_ENTRY} B per frontier (vertex, cluster) entry (SURVEY §8(d))"
-    else:
-        alg_bytes = BYTES_PER_FRONTIER_ARC * pk["arcs"]
-        model = f"{BYTES_PER_FRONTIER_ARC} B per frontier (cluster, arc) pair (SURVEY §8(d))"
-    achieved = alg_bytes / (pk["ms"] / 1000.0) / 1e9 if pk["ms"] > 0 else 0.0
+    perstep = {kk: {f: (v / args.steps if f in ("ms", "launches", "arcs", "entries", "u_in", "u_out") else v)
+                    for f, v in pk.items()} for kk, pk in prof.items()}
+    parts = alg_bytes_model(perstep, st, sizes, n, m_h, n_ni, d, planes, dist_bytes, C, mode, Q)
+    alg_step = float(sum(parts.values()))
+    cbfs_s = phase_ms["cbfs"] / 1000.0
+    achieved = alg_step / cbfs_s / 1e9 if cbfs_s > 0 else 0.0
     traffic = None
     ncu_json = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(ncu_json):
         try:
-            traffic = json.load(open(ncu_json)).get("traffic_per_launch", {}).get(f"k_{dom}")
+            traffic = json.load(open(ncu_json)).get("traffic_per_step", {}).get(args.config)
         except Exception:
             traffic = None
+    ksum = sum(v["ms"] for v in perstep.values()) or 1e-9
+    per_kernel = {kk: {"event_ms_per_step": round(v["ms"], 3), "launches_per_step": v["launches"],
+                       "share_of_event_time": round(v["ms"] / ksum, 4)}
+                  for kk, v in perstep.items() if v["launches"]}
+    dom = max(per_kernel, key=lambda kk: per_kernel[kk]["event_ms_per_step"]) if per_kernel else None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": f"k_{dom}", "launches": pk["launches"],
-                "avg_launch_ms": pk["ms"] / max(1, pk["launches"]),
-                "alg_bytes_per_launch": alg_bytes / max(1, pk["launches"]), "model": model,
-                "peak_source": peak_src, "kernels": prof,
-                "share_of_cbfs_time": pk["ms"] / max(1e-9, sum(v["ms"] for v in prof.values())),
-                "note": ("batches run concurrently on up to 4 streams, so a launch's event time includes the time it "
-                         "shares the GPU; frac_aggregate divides the algorithmic bytes of all C-BFS kernels by the "
-                         "C-BFS wall time")}
-    if phase_ms["cbfs"] > 0:
-        allb = (prof["pull"]["launches"] * (BYTES_PER_ARC * m_h + BYTES_PER_VROW * n_ni)
-                + BYTES_PER_ROW * (prof["pull"]["u_in"] + prof["pull"]["u_out"])
-                + BYTES_PER_FRONTIER_ENTRY * prof["fold"]["entries"] + BYTES_PER_FRONTIER_ARC * prof["push"]["arcs"])
-        roofline["frac_aggregate"] = allb / args.steps / (phase_ms["cbfs"] / 1000.0) / 1e9 / peak
+                "traffic": traffic,
+                "kernel": ("C-BFS traversal kernels of one step (k_fold/k_push/k_pull or the sparse round loop; "
+                           "up to 4 batches of 64 clusters in flight on separate streams)"),
+                "dominant": f"k_{dom}" if dom else None,
+                "alg_bytes_per_step": alg_step, "alg_bytes_parts": {kk: float(v) for kk, v in parts.items()},
+                "phase_s": cbfs_s, "model": alg_bytes_model.__doc__.split("\n\n")[1].strip().replace("\n    ", " "),
+                "peak_source": peak_src, "per_kernel": per_kernel,
+                "traffic_note": "ncu dram__bytes_read+write summed over the step's C-BFS kernels (profiles/)"}
 
     # ---- end to end through the public API with host buffers (rank-local)
     e2e = None
     if not args.no_e2e:
         import ctypes
-        hd = torch.empty((n, C), dtype=dist_out.dtype).pin_memory()
-        hm = torch.empty((d + 1, n, C), dtype=torch.int64).pin_memory()
+        e2e_ms = 0.0
         hs = torch.zeros((C, 4), dtype=torch.int64).pin_memory()
         hsrc = torch.empty((r_total, 64), dtype=torch.int32).pin_memory()
         hsz = torch.empty((r_total,), dtype=torch.uint8).pin_memory()
-        e2e_ms = 0.0
+        hd = hm = hbest = None
+        if mode == "full":
+            hd = torch.empty((n, C), dtype=dist_out.dtype).pin_memory()
+            hm = torch.empty((planes, n, C), dtype=torch.int64).pin_memory()
+        if mode == "query":
+            hbest = torch.empty((Q,), dtype=torch.int32).pin_memory()
         for it in range(args.e2e_warmup + args.e2e_steps):
             barrier(world)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             h = cb.cbfs_graph_create(n, src_h, dst_h, cb.CBFS_RELABEL_DEGREE if relabel else 0, local, stream)
             cb.cbfs_select_clusters(h, r_total, k, d, policy, cfg["root_seed"], sel_src, sel_sz, stream)
-            hsrc.copy_(sel_src)
-            hsz.copy_(sel_sz)
-            cb._check(cb._lib.cbfs_run_host(h, ctypes.c_void_p(hsrc[first:].data_ptr()),
-                                            ctypes.c_void_p(hsz[first:].data_ptr()), C, d, dist_bytes,
-                                            ctypes.c_void_p(hd.data_ptr()), ctypes.c_void_p(hm.data_ptr()), d + 1,
-                                            ctypes.c_void_p(hs.data_ptr()), args.direction,
-                                            ctypes.c_void_p(stream.cuda_stream)))
+            if mode == "query":
+                qs_d.copy_(qs_h, non_blocking=True)
+                qt_d.copy_(qt_h, non_blocking=True)
+                traverse(h)
+                hbest.copy_(best)
+            else:
+                hsrc.copy_(sel_src)
+                hsz.copy_(sel_sz)
+                cb._check(cb._lib.cbfs_run_host(h, ctypes.c_void_p(hsrc[first:].data_ptr()),
+                                                ctypes.c_void_p(hsz[first:].data_ptr()), C, d, dist_bytes,
+                                                ctypes.c_void_p(hd.data_ptr()) if hd is not None else None,
+                                                ctypes.c_void_p(hm.data_ptr()) if hm is not None else None, planes,
+                                                ctypes.c_void_p(hs.data_ptr()), args.direction,
+                                                ctypes.c_void_p(stream.cuda_stream)))
             cb.cbfs_graph_destroy(h)
             torch.cuda.synchronize()
             dt = time.perf_counter() - t0
@@ -394,8 +462,9 @@ def run_ours(args, world, rank, local):
                 e2e_ms += 1000 * dt
         Te = allreduce_max(e2e_ms, world) / 1000.0
         units_e = allreduce_sum(units_step * args.e2e_steps, world)
-        h2d = 2 * 4 * len(el.src) + 64 * 4 * C + C
-        d2h = (hd.numel() * hd.element_size() + hm.numel() * 8 + hs.numel() * 8 + r_total * 65)
+        h2d = 2 * 4 * len(el.src) + (8 * Q if mode == "query" else 64 * 4 * C + C)
+        d2h = (r_total * 65 + C * 32 + (hd.numel() * hd.element_size() + hm.numel() * 8 if mode == "full" else 0)
+               + (4 * Q if mode == "query" else 0))
         e2e = {"value": units_e / Te, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "steps": args.e2e_steps, "ms_per_step": 1000 * Te / args.e2e_steps,
                "timing": "host wall clock around the public C-ABI calls, max over ranks"}
@@ -413,23 +482,30 @@ def run_ours(args, world, rank, local):
 
     if rank == 0:
         K = args.steps
+        outputs = {"full": f"full distance vectors written to HBM ({n * C * (dist_bytes + 8 * planes) / 1e9:.1f} GB)",
+                   "stats": (f"per-cluster round statistics only; the full vectors "
+                             f"({n * C * (dist_bytes + 8 * planes) / 1e9:.0f} GB) do not fit HBM"),
+                   "query": f"labels of every batch consumed by {Q} distance queries (cbfs_query_stream)"}[mode]
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
             "ms_per_step": 1000 * T / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "u64", "data": "synthetic",
             "config": {"workload": args.config, "graph": el.name, "n": n, "arcs": m_h, "max_degree": maxdeg,
                        "clusters_per_gpu": C, "k": k, "d": d, "dist_bytes": dist_bytes, "relabel": relabel,
+                       "mode": mode, "outputs": outputs, "queries": Q,
                        "parallelism": f"clusters sharded, {world} rank(s), graph replicated",
-                       "step": ("A0 CSR build + A1 selection + A2-A8 C-BFS of all clusters (full vectors); A1 overlapped "
-                                "with A2-A8 (cbfs_select_and_run)" if world == 1 and not args.separate_select else
-                                "A0 CSR build + A1 selection + A2-A8 C-BFS of all clusters (full vectors)"),
-                       "l2": "flushed between timed steps (256 MiB write); inputs 134 MB and outputs 26 GB > L2",
+                       "step": ("A0 CSR build + A1 selection + A2-A8 C-BFS of all clusters"
+                                + (" (A1 overlapped with A2-A8: cbfs_select_and_run)" if overlap else "")
+                                + (" + A10/A11 labels and queries" if mode == "query" else "")),
+                       "l2": "flushed between timed steps (256 MiB write); inputs and outputs > L2",
                        "units_per_step_rank0": units_step,
                        "value_whole_graph_m": float(sizes.sum()) * m_h * args.steps * world / T,
                        "phase_ms_rank0": {kk: round(v, 3) for kk, v in phase_ms.items()},
-                       "phase_note": "with the overlap, 'select' is 0 and 'cbfs' covers A1+A2-A8",
+                       "phase_note": ("with the overlap, 'select' is 0 and 'cbfs' covers A1+A2-A8" if overlap
+                                      else "'cbfs' covers A2-A8 (+ queries)"),
                        "cbfs_only_value": units_step / (phase_ms["cbfs"] / 1000.0) if phase_ms["cbfs"] else None,
                        "direction": ["auto", "push", "pull"][args.direction],
+                       "engine": ["auto", "batched", "sparse"][args.engine],
                        "alpha": args.alpha or 100.0},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk,
@@ -455,6 +531,10 @@ def main():
     ap.add_argument("--separate-select", action="store_true", help="select, then run (no A1/A2-A8 overlap)")
     ap.add_argument("--clock-ms", type=int, default=500)
     ap.add_argument("--concurrency", type=int, default=0, help="concurrent batches per GPU (0 = library default)")
+    ap.add_argument("--engine", type=int, default=0, help="0 auto, 1 batched, 2 sparse (cbfs_set_engine)")
+    ap.add_argument("--mode", default="", choices=["", "full", "stats", "query"], help="override the config's mode")
+    ap.add_argument("--clusters", type=int, default=0, help="clusters per GPU (default: the config's)")
+    ap.add_argument("--queries", type=int, default=0, help="queries (query mode; default: the config's)")
     args = ap.parse_args()
     world, rank, local = dist_init()
     if args.impl == "reference":
