@@ -213,8 +213,10 @@ int cbfs_set_direction_alpha(double alpha);
  *     of a batch, host-driven rounds, push/pull switch (low-diameter graphs);
  *   CBFS_ENGINE_SPARSE  — cluster-major state, push-only rounds, the round
  *     loop on the device (CUDA-graph while node) (high-diameter graphs);
- *   CBFS_ENGINE_AUTO (default) — SPARSE when a BFS from the highest-degree
- *     vertex is still running after 48 levels, else BATCHED (cached per graph).
+ *   CBFS_ENGINE_AUTO (default) — BATCHED when some vertex has degree > 256
+ *     (hubs: low diameter); otherwise SPARSE when a BFS from the
+ *     highest-degree vertex is still running after 48 levels, else BATCHED
+ *     (cached per graph).
  * direction == CBFS_DIR_PULL always uses BATCHED.  Outputs are identical.
  * Errors: EINVAL (unknown engine). */
 int cbfs_set_engine(int engine);

@@ -77,7 +77,7 @@ void work_free(Graph* g) { g->work = nullptr; }  // the cache outlives graphs
 // engine's seen [cap + 64] | pend [cap] | pre [cap + 1] (u64) | dist [cap]
 // (u16), or the sparse engine's 32-byte cells (sparse.cu).
 static uint64_t blk_bytes(uint64_t cap) {
-  const uint64_t batched = (cap + LANES) * 8 + cap * 8 + (cap + 1) * 8 + cap * 2;
+  const uint64_t batched = (cap + LANES) * 8 + cap * 8 + (cap + LANES) * 8 + cap * 2;
   return std::max<uint64_t>(batched, cap * SPARSE_CELL_BYTES);
 }
 
@@ -90,7 +90,7 @@ static int slot_alloc(Slot* w, uint64_t cap) {
   w->seen = reinterpret_cast<uint64_t*>(w->blk);  // [cap + LANES]: + all-zero row n
   w->pend = w->seen + cap + LANES;
   w->pre = w->pend + cap;
-  w->dist = reinterpret_cast<uint16_t*>(w->pre + cap + 1);
+  w->dist = reinterpret_cast<uint16_t*>(w->pre + cap + LANES);  // 512-byte aligned rows
   CBFS_CUDA(cudaMalloc(&w->listA, cap * sizeof(uint32_t)));
   CBFS_CUDA(cudaMalloc(&w->listB, cap * sizeof(uint32_t)));
   CBFS_CUDA(cudaMalloc(&w->ubits, ubw * sizeof(uint32_t)));

@@ -613,23 +613,32 @@ int sparse_launch(Slot* w) {
 }
 
 // ------------------------------------------------------------------ engine choice
-// AUTO: a plain BFS from the highest-degree vertex; if it is still running
-// after PROBE_ROUNDS levels the graph is "high diameter" and the clusters'
-// wavefronts will not share state rows -> SPARSE, else BATCHED.  Cached per
-// graph handle.  Parity-neutral: both engines compute Alg. 1 exactly.
+// AUTO: a graph with a vertex of degree > PROBE_MAX_DEGREE is taken as low
+// diameter (BATCHED); otherwise a plain BFS from the highest-degree vertex
+// decides: if it is still running after PROBE_ROUNDS levels the graph is
+// "high diameter" and the clusters' wavefronts will not share state rows ->
+// SPARSE, else BATCHED.  Cached per graph handle.  Parity-neutral: both
+// engines compute Alg. 1 exactly.
 constexpr uint32_t PROBE_ROUNDS = 48;
+constexpr uint32_t PROBE_MAX_DEGREE = 256;
 
-__global__ void k_probe_level(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cols,
-                              const uint32_t* __restrict__ q, uint32_t nq, uint32_t* __restrict__ level,
-                              uint32_t lvl, uint32_t* __restrict__ qn, unsigned long long* __restrict__ cnt) {
-  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < nq; t += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t v = q[t];
-    for (uint64_t a = off[v]; a < off[v + 1]; ++a) {
-      const uint32_t u = cols[a];
-      if (level[u] == 0xFFFFFFFFu && atomicCAS(&level[u], 0xFFFFFFFFu, lvl + 1) == 0xFFFFFFFFu)
-        qn[atomicAdd(cnt, 1ULL)] = u;
-    }
+// One bottom-up BFS level (P:1769-1782 for a single source): every
+// unvisited vertex looks for a neighbour on level `lvl` (first hit wins), so
+// no thread walks a hub's whole neighbour list.
+__global__ void k_probe_level(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cols, uint32_t n,
+                              uint8_t* __restrict__ level, uint32_t lvl, unsigned long long* __restrict__ cnt) {
+  uint32_t found = 0;
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
+    if (level[v] != 0xFF) continue;
+    for (uint64_t a = off[v]; a < off[v + 1]; ++a)
+      if (level[cols[a]] == lvl) {
+        level[v] = (uint8_t)(lvl + 1);  // read only as "== lvl" in this launch: no race
+        ++found;
+        break;
+      }
   }
+  const unsigned long long s = warp_sum(found);
+  if (lane_id() == 0 && s) atomicAdd(cnt, s);
 }
 
 static int probe_high_diameter(Graph* g, int* out) {
@@ -638,36 +647,33 @@ static int probe_high_diameter(Graph* g, int* out) {
   if (n == 0 || g->m == 0) return CBFS_OK;
   cudaStream_t st;
   CBFS_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  uint32_t *level = nullptr, *qa = nullptr, *qb = nullptr;
+  uint8_t* level = nullptr;
   unsigned long long* cnt = nullptr;
-  CBFS_CUDA(cudaMallocAsync(&level, sizeof(uint32_t) * n, st));
-  CBFS_CUDA(cudaMallocAsync(&qa, sizeof(uint32_t) * n, st));
-  CBFS_CUDA(cudaMallocAsync(&qb, sizeof(uint32_t) * n, st));
+  unsigned long long* h = nullptr;
+  CBFS_CUDA(cudaMallocAsync(&level, n, st));
   CBFS_CUDA(cudaMallocAsync(&cnt, sizeof(unsigned long long), st));
-  CBFS_CUDA(cudaMemsetAsync(level, 0xFF, sizeof(uint32_t) * n, st));
-  uint32_t root = 0;
-  CBFS_CUDA(cudaMemcpyAsync(&root, g->order, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  CBFS_CUDA(cudaMallocHost(&h, sizeof(unsigned long long)));
+  CBFS_CUDA(cudaMemsetAsync(level, 0xFF, n, st));
+  // root: the highest-degree vertex (position 0 of the degree order), level 0
+  CBFS_CUDA(cudaMemcpyAsync(h, g->order, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   CBFS_CUDA(cudaStreamSynchronize(st));
-  const uint32_t zero = 0;
-  CBFS_CUDA(cudaMemcpyAsync(level + root, &zero, sizeof(uint32_t), cudaMemcpyHostToDevice, st));
-  CBFS_CUDA(cudaMemcpyAsync(qa, &root, sizeof(uint32_t), cudaMemcpyHostToDevice, st));
-  unsigned long long nq = 1, h = 0;
+  const uint32_t root = (uint32_t)(*h & 0xFFFFFFFFu);
+  CBFS_CUDA(cudaMemsetAsync(level + root, 0, 1, st));
+  unsigned long long found = 1;
   uint32_t lvl = 0;
-  for (; nq && lvl < PROBE_ROUNDS; ++lvl) {
+  for (; found && lvl < PROBE_ROUNDS; ++lvl) {
     CBFS_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st));
-    k_probe_level<<<grid_for(nq, 256), 256, 0, st>>>(g->off, g->cols, qa, (uint32_t)nq, level, lvl, qb, cnt);
+    k_probe_level<<<grid_for(n, 256), 256, 0, st>>>(g->off, g->cols, n, level, lvl, cnt);
     CBFS_LAUNCHED();
-    CBFS_CUDA(cudaMemcpyAsync(&h, cnt, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CBFS_CUDA(cudaMemcpyAsync(h, cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     CBFS_CUDA(cudaStreamSynchronize(st));
-    nq = h;
-    std::swap(qa, qb);
+    found = *h;
   }
-  *out = nq > 0 ? 1 : 0;
+  *out = found > 0 ? 1 : 0;  // still growing after PROBE_ROUNDS levels
   CBFS_CUDA(cudaFreeAsync(level, st));
-  CBFS_CUDA(cudaFreeAsync(qa, st));
-  CBFS_CUDA(cudaFreeAsync(qb, st));
   CBFS_CUDA(cudaFreeAsync(cnt, st));
   CBFS_CUDA(cudaStreamSynchronize(st));
+  CBFS_CUDA(cudaFreeHost(h));
   CBFS_CUDA(cudaStreamDestroy(st));
   return CBFS_OK;
 }
@@ -678,7 +684,9 @@ int choose_engine(Graph* g, uint32_t direction) {
   if (g_engine_policy == CBFS_ENGINE_SPARSE) return ENGINE_SPARSE;
   if (g->high_diameter < 0) {
     int hd = 0;
-    if (probe_high_diameter(g, &hd) != CBFS_OK) return -1;
+    // graphs with hubs (power-law degree tails: social / web) have low
+    // diameter; only hub-free graphs (meshes, roads, k-NN) pay for the probe
+    if (g->max_degree <= PROBE_MAX_DEGREE && probe_high_diameter(g, &hd) != CBFS_OK) return -1;
     g->high_diameter = hd;
   }
   return g->high_diameter ? ENGINE_SPARSE : ENGINE_BATCHED;
