@@ -458,6 +458,8 @@ def run_ours(args, world, rank, local):
             cb.cbfs_graph_destroy(h)
             torch.cuda.synchronize()
             dt = time.perf_counter() - t0
+            if os.environ.get("CBFS_BENCH_DEBUG"):
+                log(f"[e2e] iteration {it}: {1000 * dt:.1f} ms, device free {torch.cuda.mem_get_info()[0] / 1e9:.1f} GB")
             if it >= args.e2e_warmup:
                 e2e_ms += 1000 * dt
         Te = allreduce_max(e2e_ms, world) / 1000.0

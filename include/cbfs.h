@@ -160,9 +160,11 @@ int cbfs_select_and_run(cbfs_graph* g, uint32_t r, uint32_t k, uint32_t d, uint3
                         uint32_t direction, cbfs_stream stream);
 
 /* Same computation with HOST buffers (sources, sizes, out_dist, out_masks,
- * out_stats all host memory, pinned recommended): inputs are copied in, each
- * batch of 32 clusters is traversed into device staging and copied out while
- * the next batch runs (batches of 64 clusters).  Used for the end-to-end measurement. */
+ * out_stats all host memory, pinned recommended): inputs are copied in; when
+ * the whole output fits in free device memory it is built there and copied
+ * out with one DMA per array, otherwise each batch of 64 clusters is
+ * traversed into device staging and copied out while the next batch runs.
+ * Used for the end-to-end measurement. */
 int cbfs_run_host(cbfs_graph* g, const uint32_t* sources, const uint8_t* sizes, uint32_t n_clusters, uint32_t d,
                   uint32_t dist_bytes, void* out_dist, uint64_t* out_masks, uint32_t planes, uint64_t* out_stats,
                   uint32_t direction, cbfs_stream stream);

@@ -3,6 +3,7 @@
 // used when the label store cannot be resident (H3), and the host-buffer
 // variant of cbfs_run used for end-to-end timing.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "engine.cuh"
@@ -285,13 +286,58 @@ int cbfs_run_host(cbfs_graph* gh, const uint32_t* sources, const uint8_t* sizes,
     CBFS_CUDA(cudaMemcpyAsync(dsrc, sources, sizeof(uint32_t) * 64 * C, cudaMemcpyHostToDevice, st));
     CBFS_CUDA(cudaMemcpyAsync(dsz, sizes, C, cudaMemcpyHostToDevice, st));
   }
+  const int engine = choose_engine(g, direction);
+  if (engine < 0) return CBFS_ECUDA;
+  // When the whole output fits next to the workspace, traverse into a
+  // device-resident [n][C] store and copy it out with one contiguous DMA per
+  // array (the per-batch path below copies 64-column strips: 64..512-byte
+  // rows, far below PCIe efficiency).
+  const uint64_t dbytes = out_dist ? (uint64_t)n * C * dist_bytes : 0;
+  const uint64_t mbytes = out_masks ? (uint64_t)planes * n * C * sizeof(uint64_t) : 0;
+  size_t fr = 0, tot = 0;
+  CBFS_CUDA(cudaMemGetInfo(&fr, &tot));
+  const bool force_staging = getenv("CBFS_HOST_STAGING") != nullptr;  // tests: exercise the per-batch path
+  if (!force_staging && C && (dbytes + mbytes) > 0 && dbytes + mbytes + (2ull << 30) < fr) {
+    void* dd = nullptr;
+    uint64_t* dm = nullptr;
+    if (dbytes) CBFS_CUDA(cudaMallocAsync(&dd, dbytes, st));
+    if (mbytes) CBFS_CUDA(cudaMallocAsync(&dm, mbytes, st));
+    if (dd) CBFS_CUDA(cudaMemsetAsync(dd, 0xFF, dbytes, st));
+    if (dm) CBFS_CUDA(cudaMemsetAsync(dm, 0, mbytes, st));
+    ArraySource as;
+    as.proto = RunArgs{};
+    as.proto.d = d;
+    as.proto.planes = planes;
+    as.proto.dist_bytes = dist_bytes;
+    as.proto.C = n_clusters;
+    as.proto.direction = direction;
+    as.proto.engine = engine;
+    as.proto.out_dist = dd;
+    as.proto.out_masks = dm;
+    as.sources = dsrc;
+    as.sizes = dsz;
+    as.n_clusters = n_clusters;
+    as.out_stats = dstats;
+    rc = run_batches(g, as, st);
+    if (rc == CBFS_OK) {
+      if (dd) CBFS_CUDA(cudaMemcpyAsync(out_dist, dd, dbytes, cudaMemcpyDeviceToHost, st));
+      if (dm) CBFS_CUDA(cudaMemcpyAsync(out_masks, dm, mbytes, cudaMemcpyDeviceToHost, st));
+      if (out_stats) CBFS_CUDA(cudaMemcpyAsync(out_stats, dstats, sizeof(uint64_t) * 4 * C, cudaMemcpyDeviceToHost, st));
+    }
+    if (dd) CBFS_CUDA(cudaFreeAsync(dd, st));
+    if (dm) CBFS_CUDA(cudaFreeAsync(dm, st));
+    CBFS_CUDA(cudaFreeAsync(dsrc, st));
+    CBFS_CUDA(cudaFreeAsync(dsz, st));
+    CBFS_CUDA(cudaFreeAsync(dstats, st));
+    CBFS_CUDA(cudaStreamSynchronize(st));
+    return rc;
+  }
   HostSource src;
   src.proto.d = d;
   src.proto.planes = planes;
   src.proto.dist_bytes = dist_bytes;
   src.proto.direction = direction;
-  src.proto.engine = choose_engine(g, direction);
-  if (src.proto.engine < 0) return CBFS_ECUDA;
+  src.proto.engine = engine;
   src.sources = dsrc;
   src.sizes = dsz;
   src.n_clusters = n_clusters;

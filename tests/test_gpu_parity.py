@@ -256,7 +256,11 @@ def test_overflow_u8(engine):
     compare_many(g, ref, src, np.array([1], np.uint8), 0)  # u16 is fine
 
 
-def test_run_host_equals_device(engine):
+@pytest.mark.parametrize("staging", [False, True])
+def test_run_host_equals_device(engine, staging, monkeypatch):
+    """cbfs_run_host: device-resident output + one DMA, and (forced) per-batch staging."""
+    if staging:
+        monkeypatch.setenv("CBFS_HOST_STAGING", "1")
     el = random_el(8, 3000, "rmat")
     ref = orc.csr_from_edgelist(el)
     src, sz = orc.select_clusters(ref, 45, 64, 2)
