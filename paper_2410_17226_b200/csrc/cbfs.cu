@@ -773,7 +773,7 @@ static int sparse_step(Graph* g, Slot* w, BatchSource& src, int slot, int* err) 
     if (rc) { *err = rc; w->busy = false; return 1; }
     return 0;
   }
-  const uint64_t per_round = w->sp_fused ? 2 : 3;  // (fold +) push + tail per round, launched by the graph
+  const uint64_t per_round = w->sp_fused ? 1 : 2;  // (fold +) push per round, launched by the graph
   count_launch(per_round * h.i);
   if (g_prof.on) {
     float ms = 0;

@@ -61,6 +61,9 @@ struct SpCtl {
   unsigned long long err;    // ERR_* bits
   unsigned long long i;      // current round
   unsigned long long listed; // frontier list entries processed (incl. entries whose S_new came out empty)
+  unsigned long long go;     // the round loop continues (set at the end of each round)
+  unsigned done;             // blocks of the round's push that finished
+  unsigned pad;
 };
 
 // One in-flight batch of LANES clusters: its workspace, its stream, and the

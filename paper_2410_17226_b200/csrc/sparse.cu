@@ -36,9 +36,15 @@ constexpr uint32_t VMASK = (1u << VBITS) - 1;
 constexpr int SP_THREADS = 256;
 constexpr int SP_WARPS = SP_THREADS / 32;
 constexpr uint32_t SP_OUTBUF = 256;  // per-warp claim buffer (entries)
-constexpr int SP_ILP = 4;            // neighbours per lane in flight (push)
+#ifndef CBFS_SP_ILP
+#define CBFS_SP_ILP 4
+#endif
+#ifndef CBFS_SP_GRID_PER_SM
+#define CBFS_SP_GRID_PER_SM 8
+#endif
+constexpr int SP_ILP = CBFS_SP_ILP;  // neighbours per lane in flight (push)
 constexpr int SP_FOLD_ILP = 4;       // frontier entries per lane in flight (fold)
-constexpr unsigned SP_GRID = 148u * 8u;
+constexpr unsigned SP_GRID = 148u * CBFS_SP_GRID_PER_SM;
 
 // ------------------------------------------------------------------ init
 // Per batch: every cell = {S_seen = 0, Delta = inf, P_0 = P_1 = 0} (A2).
@@ -189,6 +195,34 @@ __global__ void __launch_bounds__(SP_THREADS) k_sp_fold(const SpDesc* __restrict
   }
 }
 
+// ------------------------------------------------------------------ round end
+// End of round i, run by the last block of the push to finish (no separate
+// tail kernel): F_i is consumed, i advances, and the graph's WHILE node
+// repeats while F_{i+1} is non-empty (Alg. 1's loop).
+__device__ __forceinline__ void sp_round_end(SpCtl* __restrict__ ctl, cudaGraphConditionalHandle h) {
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  __threadfence();
+  const unsigned prev = atomicAdd(&ctl->done, 1u);
+  if (prev != gridDim.x - 1) return;
+  __threadfence();
+  volatile SpCtl* v = ctl;
+  const unsigned long long i = v->i;
+  const uint32_t cur = i & 1;
+  v->listed = v->listed + v->nF[cur];
+  v->nF[cur] = 0;
+  const unsigned long long nn = v->nF[cur ^ 1];
+  v->i = i + 1;
+  v->done = 0;
+  bool go = nn > 0;
+  if (go && i + 1 >= 0xFFFEull) {
+    atomicOr(&ctl->err, ERR_ROUNDS);
+    go = false;
+  }
+  v->go = go;
+  if (h) cudaGraphSetConditional(h, go ? 1u : 0u);  // h == 0: host-driven loop (profiling mode)
+}
+
 // ------------------------------------------------------------------ push
 // Edge phase of round i: for every entry (c, v) of F_i and u in
 // N(v) with cap(u) (Delta_u = inf or i - Delta_u < d, R3): x =
@@ -202,7 +236,10 @@ __global__ void __launch_bounds__(SP_THREADS) k_sp_fold(const SpDesc* __restrict
 // entries by a binary search over the warp's degree prefix in shared memory),
 // so every lane keeps several independent memory operations in flight and
 // hubs and degree-4 grid vertices are balanced alike.
-constexpr int SP_EPL = 4;  // frontier entries per lane per warp step
+#ifndef CBFS_SP_EPL
+#define CBFS_SP_EPL 2
+#endif
+constexpr int SP_EPL = CBFS_SP_EPL;  // frontier entries per lane per warp step
 #ifndef CBFS_SP_MINB
 #define CBFS_SP_MINB 3
 #endif
@@ -220,7 +257,8 @@ constexpr int SP_EPL = 4;  // frontier entries per lane per warp step
 template <int DB, bool FUSED>
 __global__ void __launch_bounds__(SP_THREADS, CBFS_SP_MINB) k_sp_push(const SpDesc* __restrict__ D, SpCtl* __restrict__ ctl,
                                                         SpCell* __restrict__ cells, uint32_t* __restrict__ list0,
-                                                        uint32_t* __restrict__ list1, uint64_t* __restrict__ bstats) {
+                                                        uint32_t* __restrict__ list1, uint64_t* __restrict__ bstats,
+                                                        cudaGraphConditionalHandle hcond) {
   constexpr int W = 32 * SP_EPL;  // entries per warp step
   __shared__ unsigned long long sF[FUSED ? LANES : 1], sE[FUSED ? LANES : 1], sM[FUSED ? LANES : 1];
   if (FUSED) {
@@ -412,24 +450,7 @@ __global__ void __launch_bounds__(SP_THREADS, CBFS_SP_MINB) k_sp_push(const SpDe
       atomicMax((unsigned long long*)&bstats[c * 4 + 0], (unsigned long long)(i + 1));
     }
   }
-}
-
-// ------------------------------------------------------------------ tail
-// End of round i: F_i is consumed, i advances, and the WHILE node repeats
-// while F_{i+1} is non-empty (Alg. 1's loop).
-__global__ void k_sp_tail(SpCtl* __restrict__ ctl, cudaGraphConditionalHandle h) {
-  const unsigned long long i = ctl->i;
-  const uint32_t cur = i & 1;
-  ctl->listed += ctl->nF[cur];
-  ctl->nF[cur] = 0;
-  const unsigned long long nn = ctl->nF[cur ^ 1];
-  ctl->i = i + 1;
-  bool go = nn > 0;
-  if (go && i + 1 >= 0xFFFEull) {
-    atomicOr(&ctl->err, ERR_ROUNDS);
-    go = false;
-  }
-  if (h) cudaGraphSetConditional(h, go ? 1u : 0u);  // h == 0: host-driven loop (profiling mode)
+  sp_round_end(ctl, hcond);
 }
 
 // ------------------------------------------------------------------ host
@@ -445,7 +466,8 @@ static int sp_add_kernel(cudaGraph_t body, cudaGraphNode_t* node, const cudaGrap
   return CBFS_OK;
 }
 
-// The per-slot round-loop graph: WHILE (F_i non-empty) { fold; push; tail }.
+// The per-slot round-loop graph: WHILE (F_i non-empty) { [fold;] push } (the
+// push's last block ends the round).
 // Two graphs per slot would be needed for the two Delta output widths; the
 // fold instance is chosen by dist_bytes when the graph is (re)built.
 static int sp_build(Slot* w, uint32_t dist_bytes, bool fused) {
@@ -476,22 +498,20 @@ static int sp_build(Slot* w, uint32_t dist_bytes, bool fused) {
   uint32_t* l0 = w->listA;
   uint32_t* l1 = w->listB;
   void* fa[] = {&D, &ctl, &cells, &l0, &l1, &w->bstats};
-  void* ta[] = {&ctl, &h};
-  cudaGraphNode_t nf, np, nt;
+  void* pa[] = {&D, &ctl, &cells, &l0, &l1, &w->bstats, &h};
+  cudaGraphNode_t nf, np;
   int rc;
   if (fused) {  // d >= 1: one kernel per round
     rc = sp_add_kernel(body, &np, nullptr, dist_bytes == 1 ? (void*)k_sp_push<1, true> : (void*)k_sp_push<2, true>,
-                       SP_GRID, SP_THREADS, fa);
+                       SP_GRID, SP_THREADS, pa);
     if (rc) return rc;
   } else {
     rc = sp_add_kernel(body, &nf, nullptr, dist_bytes == 1 ? (void*)k_sp_fold<1> : (void*)k_sp_fold<2>, SP_GRID,
                        SP_THREADS, fa);
     if (rc) return rc;
-    rc = sp_add_kernel(body, &np, &nf, (void*)k_sp_push<2, false>, SP_GRID, SP_THREADS, fa);
+    rc = sp_add_kernel(body, &np, &nf, (void*)k_sp_push<2, false>, SP_GRID, SP_THREADS, pa);
     if (rc) return rc;
   }
-  rc = sp_add_kernel(body, &nt, &np, (void*)k_sp_tail, 1, 1, ta);
-  if (rc) return rc;
   CBFS_CUDA(cudaGraphInstantiate(&w->sp_exec, g, 0));
   w->sp_db = dist_bytes;
   w->sp_fused = fused;
@@ -570,29 +590,20 @@ static int sparse_hostloop(Slot* w) {
     SpCell* cells = reinterpret_cast<SpCell*>(w->blk);
     if (w->sp_fused) {
       if (w->sp_db == 1)
-        k_sp_push<1, true><<<SP_GRID, SP_THREADS, 0, st>>>(D, ctl, cells, w->listA, w->listB, w->bstats);
+        k_sp_push<1, true><<<SP_GRID, SP_THREADS, 0, st>>>(D, ctl, cells, w->listA, w->listB, w->bstats, 0);
       else
-        k_sp_push<2, true><<<SP_GRID, SP_THREADS, 0, st>>>(D, ctl, cells, w->listA, w->listB, w->bstats);
+        k_sp_push<2, true><<<SP_GRID, SP_THREADS, 0, st>>>(D, ctl, cells, w->listA, w->listB, w->bstats, 0);
     } else {
       if (w->sp_db == 1)
         k_sp_fold<1><<<SP_GRID, SP_THREADS, 0, st>>>(D, ctl, cells, w->listA, w->listB, w->bstats);
       else
         k_sp_fold<2><<<SP_GRID, SP_THREADS, 0, st>>>(D, ctl, cells, w->listA, w->listB, w->bstats);
-      k_sp_push<2, false><<<SP_GRID, SP_THREADS, 0, st>>>(D, ctl, cells, w->listA, w->listB, w->bstats);
+      k_sp_push<2, false><<<SP_GRID, SP_THREADS, 0, st>>>(D, ctl, cells, w->listA, w->listB, w->bstats, 0);
     }
-    k_sp_tail<<<1, 1, 0, st>>>(ctl, 0);
     CBFS_CUDA(cudaGetLastError());
     CBFS_CUDA(cudaMemcpyAsync(w->sp_ctl_h, ctl, sizeof(SpCtl), cudaMemcpyDeviceToHost, st));
     CBFS_CUDA(cudaStreamSynchronize(st));
-    const SpCtl& h = *w->sp_ctl_h;
-    if (h.nF[h.i & 1] == 0 || h.i >= 0xFFFEull) {
-      if (h.nF[h.i & 1] && h.i >= 0xFFFEull) {
-        SpCtl c = h;
-        c.err |= ERR_ROUNDS;
-        CBFS_CUDA(cudaMemcpyAsync(ctl, &c, sizeof(SpCtl), cudaMemcpyHostToDevice, st));
-      }
-      break;
-    }
+    if (!w->sp_ctl_h->go) break;
   }
   CBFS_CUDA(cudaEventRecord(w->sp_t1, st));
   CBFS_CUDA(cudaMemcpyAsync(w->sp_ctl_h, ctl, sizeof(SpCtl), cudaMemcpyDeviceToHost, st));
