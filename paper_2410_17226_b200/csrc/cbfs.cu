@@ -468,6 +468,7 @@ __global__ void __launch_bounds__(PULL_WARPS * 32, CBFS_PULL_MINB) k_pull(
   unsigned long long(*stat)[LANES] = s_stat[wib];
   stat[0][c0] = stat[0][c1] = stat[1][c0] = stat[1][c1] = stat[2][c0] = stat[2][c1] = 0;
   const uint64_t* seen2 = seen + 2 * lane;  // lane's word pair of row 0
+  const ulonglong2* rows2 = reinterpret_cast<const ulonglong2*>(seen) + lane;
   const uint32_t* dist2 = reinterpret_cast<const uint32_t*>(dist) + lane;
 
   for (uint64_t w = warp; w < n_chunks; w += nwarps) {
@@ -515,7 +516,7 @@ __global__ void __launch_bounds__(PULL_WARPS * 32, CBFS_PULL_MINB) k_pull(
         }
       }
       if (actv) {
-        // ---- (3) pass A: compact useful neighbours as (vertex << 27 | u),
+        // ---- (3) pass A: compact useful neighbours (ids u, grouped by vertex),
         // sorted by vertex, and count them per vertex
         cnt[lane] = 0;
         __syncwarp();
@@ -533,7 +534,7 @@ __global__ void __launch_bounds__(PULL_WARPS * 32, CBFS_PULL_MINB) k_pull(
           }
           const bool want = inr && ((actv >> jv) & 1u) && ((__ldg(&ubits[u >> 5]) >> (u & 31)) & 1u);
           const unsigned fm = __ballot_sync(FULLW, want);
-          if (want) list[nl + __popc(fm & lt)] = (jv << 27) | u;
+          if (want) list[nl + __popc(fm & lt)] = u;  // segments are contiguous per vertex (arc order)
           const unsigned grp = __match_any_sync(FULLW, want ? jv : 0xFFFFFFFFu);
           if (want && lane == (uint32_t)(__ffs(grp) - 1)) cnt[jv] += __popc(grp);
           nl += __popc(fm);
@@ -570,7 +571,8 @@ __global__ void __launch_bounds__(PULL_WARPS * 32, CBFS_PULL_MINB) k_pull(
 #pragma unroll
             for (int r = 0; r < PULL_MLP; ++r) {
               const uint32_t x = q + r < s1 ? list[q + r] : n;  // past the segment: the zero row
-              g[r] = ld2(seen2 + (uint64_t)(x & 0x7FFFFFFu) * LANES);
+              const ulonglong2 y = __ldg(rows2 + x * (LANES / 2));    // 32-bit index: x * 32 < 2^31
+              g[r] = {y.x, y.y};
             }
 #pragma unroll
             for (int r = 0; r < PULL_MLP; ++r) { acc0 |= g[r].a; acc1 |= g[r].b; }
