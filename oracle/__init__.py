@@ -75,6 +75,7 @@ def lib():
                                u32p, i32p]
         L.or_query_stream.argtypes = [ctypes.c_uint32, u64p, u32p, u32p, u8p, ctypes.c_uint32, ctypes.c_uint32,
                                       ctypes.c_uint64, u32p, u32p, ctypes.c_int, i32p]
+        L.or_bidir_refine.argtypes = [ctypes.c_uint32, u64p, u32p, ctypes.c_uint64, u32p, u32p, ctypes.c_uint32, i32p]
         L.or_csr_build.restype = ctypes.c_int64
         L.or_csr_build.argtypes = [ctypes.c_uint32, ctypes.c_uint64, u32p, u32p, ctypes.c_int, u32p, u64p]
         L.or_record_bytes.restype = ctypes.c_int64
@@ -284,6 +285,20 @@ def query_stream(g: CSR, sources, sizes, d: int, s, t, threads: int | None = Non
                                _p(out, ctypes.c_int32))
     if rc:
         raise ValueError("bad stream query")
+    return out
+
+
+def bidir_refine(g: CSR, s, t, tau: int) -> np.ndarray:
+    """Appendix B with reading R27: tau vertices visited from
+    each side in BFS order over the sorted CSR, min over common vertices of
+    dist_s + dist_t; INT32_MAX when disjoint."""
+    s = np.ascontiguousarray(s, dtype=np.uint32)
+    t = np.ascontiguousarray(t, dtype=np.uint32)
+    out = np.empty(len(s), np.int32)
+    rc = lib().or_bidir_refine(g.n, _p(g.off, ctypes.c_uint64), _p(g.cols, ctypes.c_uint32), len(s),
+                               _p(s, ctypes.c_uint32), _p(t, ctypes.c_uint32), tau, _p(out, ctypes.c_int32))
+    if rc:
+        raise ValueError("query vertex out of range")
     return out
 
 

@@ -487,3 +487,54 @@ int64_t or_csr_build(uint32_t n, uint64_t P, const uint32_t* src, const uint32_t
   free(start); free(kept);
   return m;
 }
+
+/* ---------------------------------------------------------------------
+ * bidir_refine — the fixed-size bi-directional search of Appendix B
+ * (P:1790-1800): "search tau vertices from each side by a BFS order, and take
+ * an intersection to find the minimum distance among them".  Reading R27
+ * (DESIGN.md §2): from each endpoint a queue BFS over the sorted CSR visits
+ * vertices in discovery order (the endpoint first) and stops once tau
+ * vertices are visited; the answer is min over x visited by both sides of
+ * dist_s(x) + dist_t(x), INT32_MAX when the two visited sets are disjoint
+ * (tau = 0: nothing visited).  Sequential, one pair at a time.
+ * ------------------------------------------------------------------- */
+static uint32_t bidir_side(uint32_t n, const uint64_t* off, const uint32_t* cols, uint32_t src, uint32_t tau,
+                           uint32_t* mark, uint32_t stamp, uint32_t* dist, uint32_t* order) {
+  if (tau == 0) return 0;
+  uint32_t cnt = 0, head = 0;
+  mark[src] = stamp; dist[src] = 0; order[cnt++] = src;
+  while (head < cnt && cnt < tau) {
+    uint32_t x = order[head++];
+    for (uint64_t e = off[x]; e < off[x + 1] && cnt < tau; ++e) {
+      uint32_t u = cols[e];
+      if (mark[u] != stamp) { mark[u] = stamp; dist[u] = dist[x] + 1; order[cnt++] = u; }
+    }
+  }
+  (void)n;
+  return cnt;
+}
+
+int or_bidir_refine(uint32_t n, const uint64_t* off, const uint32_t* cols, uint64_t q, const uint32_t* s,
+                    const uint32_t* t, uint32_t tau, int32_t* out) {
+  for (uint64_t j = 0; j < q; ++j) if (s[j] >= n || t[j] >= n) return -1;
+  uint32_t* mark_s = (uint32_t*)calloc(n ? n : 1, sizeof(uint32_t));
+  uint32_t* dist_s = (uint32_t*)malloc(sizeof(uint32_t) * (n ? n : 1));
+  uint32_t* ord_s = (uint32_t*)malloc(sizeof(uint32_t) * (n ? n : 1));
+  uint32_t* mark_t = (uint32_t*)calloc(n ? n : 1, sizeof(uint32_t));
+  uint32_t* dist_t = (uint32_t*)malloc(sizeof(uint32_t) * (n ? n : 1));
+  uint32_t* ord_t = (uint32_t*)malloc(sizeof(uint32_t) * (n ? n : 1));
+  for (uint64_t j = 0; j < q; ++j) {
+    const uint32_t stamp = (uint32_t)(j + 1);  /* fresh marks per pair */
+    uint32_t cs = bidir_side(n, off, cols, s[j], tau, mark_s, stamp, dist_s, ord_s);
+    uint32_t ct = bidir_side(n, off, cols, t[j], tau, mark_t, stamp, dist_t, ord_t);
+    int64_t best = INT32_MAX;
+    for (uint32_t a = 0; a < cs; ++a) {
+      uint32_t x = ord_s[a];
+      if (mark_t[x] == stamp && (int64_t)dist_s[x] + dist_t[x] < best) best = (int64_t)dist_s[x] + dist_t[x];
+    }
+    (void)ct;
+    out[j] = (int32_t)best;
+  }
+  free(mark_s); free(dist_s); free(ord_s); free(mark_t); free(dist_t); free(ord_t);
+  return 0;
+}

@@ -448,3 +448,37 @@ def test_query_empty_index_unreachable():
     assert a.tolist() == [1, orc.INT32_MAX]
     a = orc.query(many["dist"][:0], many["sub"][:0], np.array([0], np.uint32), np.array([1], np.uint32))
     assert a.tolist() == [orc.INT32_MAX]
+
+
+# ------------------------------------------------------------------ NEXT-2 bidirectional refinement
+def test_bidir_refine_pins():
+    """Appendix B, reading R27: tau >= n gives the exact distance
+    (scipy BFS); tau = 0 gives nothing; tau = 1 only meets at u = v; the
+    answer never undercuts delta and never grows with tau; hand-worked path."""
+    rng = np.random.default_rng(5)
+    g = random_graph(rng, 300, "er")
+    D = scipy_dist(g, np.arange(g.n))
+    s = rng.integers(0, g.n, 400).astype(np.uint32)
+    t = rng.integers(0, g.n, 400).astype(np.uint32)
+    exact = orc.bidir_refine(g, s, t, g.n)
+    ref = D[s.astype(int), t.astype(int)].astype(np.float64)
+    ref[ref < 0] = np.inf
+    reach = np.isfinite(ref)
+    assert reach.any() and np.array_equal(exact[reach], ref[reach].astype(np.int32))
+    assert np.all(exact[~reach] == orc.INT32_MAX)
+    assert np.all(orc.bidir_refine(g, s, t, 0) == orc.INT32_MAX)
+    one = orc.bidir_refine(g, s, t, 1)
+    assert np.all(one[s == t] == 0) and np.all(one[s != t] == orc.INT32_MAX)
+    prev = None
+    for tau in (2, 4, 16, 64, 300):
+        cur = orc.bidir_refine(g, s, t, tau)
+        fin = cur < orc.INT32_MAX
+        assert np.all(cur[fin] >= ref[fin])  # one-sided
+        if prev is not None:
+            assert np.all(cur <= prev)  # more search never hurts
+        prev = cur
+    # path 0-1-2-...-9: BFS from 0 visits 0,1,2,.. ; from 9 visits 9,8,...
+    p = orc.csr_from_edges(10, np.arange(9, dtype=np.uint32), np.arange(1, 10, dtype=np.uint32))
+    a = np.array([0], np.uint32); b = np.array([9], np.uint32)
+    assert orc.bidir_refine(p, a, b, 5)[0] == orc.INT32_MAX  # {0..4} and {5..9} are disjoint
+    assert orc.bidir_refine(p, a, b, 6)[0] == 9               # they meet at 4 and 5
