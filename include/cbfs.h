@@ -62,6 +62,7 @@ enum cbfs_status {
 #define CBFS_UNREACHED_U16 0xFFFFu     /* Delta sentinel, dist_bytes == 2    */
 #define CBFS_UNREACHED_U8 0xFFu        /* Delta sentinel, dist_bytes == 1    */
 #define CBFS_QUERY_UNREACHED 0x7FFFFFFF /* query answer when no cluster reaches both ends */
+#define CBFS_BIDIR_MAX_TAU 1024u        /* vertices visited per side by cbfs_query_bidir */
 
 /* graph flags */
 enum { CBFS_RELABEL_DEGREE = 2, CBFS_INPUT_DEVICE = 4 };
@@ -203,6 +204,21 @@ int cbfs_query_distance(uint32_t n, uint32_t C, uint32_t d, uint32_t planes, con
 int cbfs_query_stream(cbfs_graph* g, const uint32_t* sources, const uint8_t* sizes, uint32_t n_clusters, uint32_t d,
                       const uint32_t* s, const uint32_t* t, uint64_t q, int32_t* inout_best, uint64_t* out_stats,
                       cbfs_stream stream);
+
+/* cbfs_query_bidir — the fixed-size bi-directional search of Appendix B
+ * (P:1790-1800), reading R27: from each endpoint a BFS over the sorted
+ * original-id CSR visits vertices in discovery order (the endpoint first)
+ * until tau are visited; the answer is min over vertices visited by both
+ * sides of dist_s + dist_t, min-merged into inout_best (so calling it after
+ * cbfs_query_distance gives the combined query, "the minimum distance
+ * obtained by the index and bi-directional search").  Disjoint visited sets
+ * (or tau = 0) leave the answer unchanged.
+ *   s, t : device [q] uint32 original ids; inout_best : device [q] int32
+ *   tau  : 0..CBFS_BIDIR_MAX_TAU
+ * Errors: EINVAL (null pointers, ids >= n: the call returns after the
+ * kernel), EUNSUPPORTED (tau too large).  Synchronises. */
+int cbfs_query_bidir(cbfs_graph* g, const uint32_t* s, const uint32_t* t, uint64_t q, uint32_t tau,
+                     int32_t* inout_best, cbfs_stream stream);
 
 /* --------------------------------------------------------------- misc */
 /* Direction switch: pull when the frontier's (cluster, arc) pair count

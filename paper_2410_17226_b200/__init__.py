@@ -28,6 +28,7 @@ CBFS_MAX_K, CBFS_MAX_D, CBFS_MAX_N = 64, 31, 1 << 26
 CBFS_PAD = 0xFFFFFFFF
 CBFS_UNREACHED_U16, CBFS_UNREACHED_U8 = 0xFFFF, 0xFF
 CBFS_QUERY_UNREACHED = 0x7FFFFFFF
+CBFS_BIDIR_MAX_TAU = 1024
 CBFS_RELABEL_DEGREE, CBFS_INPUT_DEVICE = 2, 4
 CBFS_ROOT_DEGREE, CBFS_ROOT_RANDOM = 0, 1
 CBFS_DIR_AUTO, CBFS_DIR_PUSH, CBFS_DIR_PULL = 0, 1, 2
@@ -56,6 +57,7 @@ _sig("cbfs_run_host", [_vp, _vp, _vp, _u32, _u32, _u32, _vp, _vp, _u32, _vp, _u3
 _sig("cbfs_decode", [_u32, _u32, _u32, _u32, _vp, _u32, _vp, _u32, _u32, _vp, _vp])
 _sig("cbfs_query_distance", [_u32, _u32, _u32, _u32, _vp, _u32, _vp, _vp, _vp, _vp, _u64, _vp, _vp])
 _sig("cbfs_query_stream", [_vp, _vp, _vp, _u32, _u32, _vp, _vp, _u64, _vp, _vp, _vp])
+_sig("cbfs_query_bidir", [_vp, _vp, _vp, _u64, _u32, _vp, _vp])
 _sig("cbfs_set_direction_alpha", [ctypes.c_double])
 _sig("cbfs_set_concurrency", [_i32])
 _sig("cbfs_set_engine", [_i32])
@@ -177,6 +179,10 @@ def cbfs_query_distance(n, C, d, planes, dist, dist_bytes, masks, sizes, s, t, i
 def cbfs_query_stream(h, sources, sizes, n_clusters, d, s, t, inout_best, out_stats=None, stream=None):
     _check(_lib.cbfs_query_stream(h, _ptr(sources), _ptr(sizes), n_clusters, d, _ptr(s), _ptr(t), len(s),
                                   _ptr(inout_best), _ptr(out_stats), _stream(stream)))
+
+
+def cbfs_query_bidir(h, s, t, tau, inout_best, stream=None):
+    _check(_lib.cbfs_query_bidir(h, _ptr(s), _ptr(t), len(s), tau, _ptr(inout_best), _stream(stream)))
 
 
 def cbfs_set_direction_alpha(alpha: float):

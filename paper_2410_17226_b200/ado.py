@@ -20,7 +20,8 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from . import (CBFS_QUERY_UNREACHED, CBFS_ROOT_DEGREE, cbfs_query_distance, cbfs_run, cbfs_select_clusters)
+from . import (CBFS_QUERY_UNREACHED, CBFS_ROOT_DEGREE, cbfs_query_bidir, cbfs_query_distance, cbfs_run,
+               cbfs_select_clusters)
 
 UNREACHED16 = 0xFFFF
 
@@ -43,12 +44,16 @@ class LandmarkIndex:
         if got:
             cbfs_run(graph.h, self.sources, self.sizes, got, d, 2, self.dist, self.masks, self.planes, None)
 
-    def query(self, s: torch.Tensor, t: torch.Tensor) -> torch.Tensor:
-        """int32 answers, CBFS_QUERY_UNREACHED where no cluster reaches both ends."""
+    def query(self, s: torch.Tensor, t: torch.Tensor, tau: int = 0) -> torch.Tensor:
+        """int32 answers, CBFS_QUERY_UNREACHED where no cluster reaches both
+        ends; tau > 0 adds the Appendix B bi-directional search:
+        the answer is the minimum of the index's and the search's."""
         best = torch.full((int(s.shape[0]),), CBFS_QUERY_UNREACHED, dtype=torch.int32, device=s.device)
         if self.r:
             cbfs_query_distance(self.graph.n, self.r, self.d, self.planes, self.dist, 2, self.masks, self.sizes,
                                 s, t, best)
+        if tau:
+            cbfs_query_bidir(self.graph.h, s, t, tau, best)
         return best
 
 

@@ -10,6 +10,8 @@
 
 namespace cbfs {
 
+constexpr unsigned FULLW_Q = 0xFFFFFFFFu;
+
 
 template <int DB>
 __device__ __forceinline__ uint32_t load_dist(const void* p, uint64_t idx) {
@@ -117,6 +119,113 @@ static int launch_query(uint32_t n, uint32_t C, uint32_t d, uint32_t planes, con
   return CBFS_OK;
 }
 
+// ------------------------------------------------------------------ bidirectional refinement
+// Appendix B, reading R27: from each endpoint a BFS in the
+// order of the sorted ORIGINAL-id CSR visits vertices in discovery order (the
+// endpoint first) until tau are visited; the answer is min over vertices
+// visited by both sides of dist_s + dist_t, min-merged into best.  One warp
+// per query pair; each side keeps its visited list (id, hop) and an
+// open-addressing hash of the visited ids in shared memory.  A neighbour
+// chunk of 32 arcs is tested by 32 lanes at once and the new vertices are
+// appended in arc order (ballot prefix), so the visited sets are exactly the
+// sequential BFS's.
+constexpr uint32_t BIDIR_EMPTY = 0xFFFFFFFFu;
+
+struct BidirSide {
+  uint32_t* ids;   // [tau] visited, discovery order
+  uint32_t* hop;   // [tau]
+  uint32_t* keys;  // [H] hash keys
+  uint32_t* pos;   // [H] position in ids
+};
+
+__device__ __forceinline__ uint32_t bidir_hash(uint32_t x, uint32_t mask) { return (x * 0x9E3779B1u) & mask; }
+
+__device__ __forceinline__ int bidir_find(const BidirSide& S, uint32_t x, uint32_t mask) {
+  for (uint32_t h = bidir_hash(x, mask);; h = (h + 1) & mask) {
+    const uint32_t k = S.keys[h];
+    if (k == x) return (int)S.pos[h];
+    if (k == BIDIR_EMPTY) return -1;
+  }
+}
+
+__device__ __forceinline__ void bidir_insert(const BidirSide& S, uint32_t x, uint32_t p, uint32_t mask) {
+  for (uint32_t h = bidir_hash(x, mask);; h = (h + 1) & mask) {
+    if (atomicCAS(&S.keys[h], BIDIR_EMPTY, x) == BIDIR_EMPTY) {
+      S.pos[h] = p;
+      return;
+    }
+  }
+}
+
+// visits up to tau vertices from src; returns how many
+__device__ uint32_t bidir_bfs(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cols, uint32_t src,
+                              uint32_t tau, const BidirSide& S, uint32_t H) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t mask = H - 1;
+  for (uint32_t h = lane; h < H; h += 32) S.keys[h] = BIDIR_EMPTY;
+  __syncwarp();
+  if (tau == 0) return 0;
+  if (lane == 0) {
+    S.ids[0] = src;
+    S.hop[0] = 0;
+    bidir_insert(S, src, 0, mask);
+  }
+  __syncwarp();
+  uint32_t cnt = 1, head = 0;
+  while (head < cnt && cnt < tau) {
+    const uint32_t x = S.ids[head], hx = S.hop[head];
+    ++head;
+    const uint64_t e1 = off[x + 1];
+    for (uint64_t a0 = off[x]; a0 < e1 && cnt < tau; a0 += 32) {
+      const uint64_t a = a0 + lane;
+      const uint32_t u = a < e1 ? cols[a] : 0u;
+      const bool isnew = a < e1 && bidir_find(S, u, mask) < 0;
+      const unsigned m = __ballot_sync(FULLW_Q, isnew);
+      const uint32_t rank = __popc(m & ((1u << lane) - 1));
+      if (isnew && cnt + rank < tau) {
+        S.ids[cnt + rank] = u;
+        S.hop[cnt + rank] = hx + 1;
+        bidir_insert(S, u, cnt + rank, mask);
+      }
+      cnt = min(cnt + (uint32_t)__popc(m), tau);
+      __syncwarp();
+    }
+  }
+  return cnt;
+}
+
+__global__ void k_bidir(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cols, uint32_t n,
+                        const uint32_t* __restrict__ s, const uint32_t* __restrict__ t, uint64_t q, uint32_t tau,
+                        uint32_t H, int32_t* __restrict__ best, int* __restrict__ bad) {
+  extern __shared__ uint32_t smem[];
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint32_t per_side = 2 * tau + 2 * H;
+  uint32_t* base = smem + (uint64_t)wib * 2 * per_side;
+  BidirSide A{base, base + tau, base + 2 * tau, base + 2 * tau + H};
+  uint32_t* b2 = base + per_side;
+  BidirSide B{b2, b2 + tau, b2 + 2 * tau, b2 + 2 * tau + H};
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t qi = warp; qi < q; qi += nwarps) {
+    const uint32_t a = s[qi], b = t[qi];
+    if (a >= n || b >= n) {
+      if (lane == 0) *bad = 1;
+      continue;
+    }
+    const uint32_t ca = bidir_bfs(off, cols, a, tau, A, H);
+    bidir_bfs(off, cols, b, tau, B, H);
+    int32_t mine = 0x7FFFFFFF;
+    for (uint32_t p = lane; p < ca; p += 32) {
+      const int k = bidir_find(B, A.ids[p], H - 1);
+      if (k >= 0) mine = min(mine, (int32_t)(A.hop[p] + B.hop[k]));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mine = min(mine, __shfl_xor_sync(FULLW_Q, mine, o));
+    if (lane == 0 && mine < best[qi]) atomicMin(&best[qi], mine);
+    __syncwarp();
+  }
+}
+
 }  // namespace cbfs
 
 using namespace cbfs;
@@ -136,6 +245,34 @@ int cbfs_decode(uint32_t n, uint32_t C, uint32_t d, uint32_t planes, const void*
   else
     k_decode<2><<<grid_for(n, 256), 256, 0, st>>>(n, C, d, planes, dist, masks, c, k, out);
   CBFS_LAUNCHED();
+  return CBFS_OK;
+}
+
+int cbfs_query_bidir(cbfs_graph* gh, const uint32_t* s, const uint32_t* t, uint64_t q, uint32_t tau,
+                     int32_t* inout_best, cbfs_stream stream) {
+  Graph* g = reinterpret_cast<Graph*>(gh);
+  if (!g) return fail(CBFS_EINVAL, "null graph");
+  if (q && (!s || !t || !inout_best)) return fail(CBFS_EINVAL, "null query arrays");
+  if (tau > CBFS_BIDIR_MAX_TAU) return fail(CBFS_EUNSUPPORTED, "tau > CBFS_BIDIR_MAX_TAU");
+  if (q == 0 || tau == 0) return CBFS_OK;
+  CBFS_CUDA(cudaSetDevice(g->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  uint32_t H = 1;
+  while (H < 2 * tau) H <<= 1;
+  const uint32_t warps = 4;
+  const size_t smem = (size_t)warps * 2 * (2 * tau + 2 * H) * sizeof(uint32_t);
+  CBFS_CUDA(cudaFuncSetAttribute(k_bidir, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int* bad = nullptr;
+  CBFS_CUDA(cudaMallocAsync(&bad, sizeof(int), st));
+  CBFS_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+  const unsigned blocks = grid_for(q * 32, warps * 32, 148u * 16u);
+  k_bidir<<<blocks, warps * 32, smem, st>>>(g->off_orig, g->cols_orig, g->n, s, t, q, tau, H, inout_best, bad);
+  CBFS_LAUNCHED();
+  int hbad = 0;
+  CBFS_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CBFS_CUDA(cudaFreeAsync(bad, st));
+  CBFS_CUDA(cudaStreamSynchronize(st));
+  if (hbad) return fail(CBFS_EINVAL, "query vertex id >= n");
   return CBFS_OK;
 }
 

@@ -46,3 +46,32 @@ def test_distortion_matches_oracle(kind, d):
     psi = expect[expect < orc.INT32_MAX] / dd[expect < orc.INT32_MAX].astype(np.float64)
     assert res["epsilon_pct"] == pytest.approx(100.0 * (psi.mean() - 1.0), abs=0, rel=1e-12)
     g.close()
+
+
+# ------------------------------------------------------------------ NEXT-2: bidirectional refinement
+@pytest.mark.parametrize("kind,relabel", [("rmat", True), ("rmat", False), ("grid", False)])
+def test_bidir_refine_parity(kind, relabel):
+    """cbfs_query_bidir == the oracle's Appendix B search (reading R27) for
+    several tau, and after the landmark query it gives min(index, search)."""
+    import paper_2410_17226_b200 as cb
+    el = ci.rmat(11, 8, 0.57, 0.19, 0.19, seed=31) if kind == "rmat" else ci.grid(50, 0.05, 0.01, 31)
+    ref = orc.csr_from_edgelist(el)
+    g = gpu_graph(el, relabel=relabel)
+    s, t = ci.query_pairs(el.n, 3000, seed=8, stream=6)
+    s[:20] = t[:20]  # u = v
+    sd = torch.from_numpy(s.view(np.int32)).cuda()
+    td = torch.from_numpy(t.view(np.int32)).cuda()
+    for tau in (0, 1, 2, 5, 64, 1024):
+        best = torch.full((len(s),), cb.CBFS_QUERY_UNREACHED, dtype=torch.int32, device="cuda")
+        cb.cbfs_query_bidir(g.h, sd, td, tau, best)
+        assert np.array_equal(best.cpu().numpy(), orc.bidir_refine(ref, s, t, tau)), tau
+    # combined query: landmark labels, then the refinement min-merged
+    idx = ado.LandmarkIndex(g, 12, 64, 2)
+    osrc, osz = orc.select_clusters(ref, 12, 64, 2)
+    best = idx.query(sd, td)
+    cb.cbfs_query_bidir(g.h, sd, td, 32, best)
+    expect = np.minimum(orc.query_stream(ref, osrc, osz, 2, s, t), orc.bidir_refine(ref, s, t, 32))
+    assert np.array_equal(best.cpu().numpy(), expect)
+    with pytest.raises(cb.CbfsError):
+        cb.cbfs_query_bidir(g.h, sd, td, cb.CBFS_BIDIR_MAX_TAU + 1, best)
+    g.close()

@@ -48,12 +48,17 @@ while have < pairs and stream < 40:  # candidate draws until enough distinct, mu
     stream += 1
 s, t, dd = (np.concatenate([p[i] for p in parts]) for i in range(3))
 t_exact = time.perf_counter() - t0
-torch.cuda.synchronize()
-t0 = time.perf_counter()
-ans = idx.query(torch.from_numpy(s.view(np.int32)).to(dev), torch.from_numpy(t.view(np.int32)).to(dev))
-torch.cuda.synchronize()
-t_query = time.perf_counter() - t0
-res = ado.distortion(ans.cpu().numpy(), dd)
-res.update({"config": name, "budget_bytes_per_vertex": budget, "record_bytes": record, "clusters": idx.r, "d": d,
-            "index_s": t_index, "query_s": t_query, "exact_s": t_exact, "mean_delta": float(dd.mean())})
-print(json.dumps(res), flush=True)
+taus = [int(x) for x in os.environ.get("TAUS", "0").split(",")]
+sd, td = torch.from_numpy(s.view(np.int32)).to(dev), torch.from_numpy(t.view(np.int32)).to(dev)
+for tau in taus:  # Appendix B: tau vertices visited per side by the bi-directional search (0 = index only)
+    idx.query(sd, td, tau)  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ans = idx.query(sd, td, tau)
+    torch.cuda.synchronize()
+    t_query = time.perf_counter() - t0
+    res = ado.distortion(ans.cpu().numpy(), dd)
+    res.update({"config": name, "budget_bytes_per_vertex": budget, "record_bytes": record, "clusters": idx.r, "d": d,
+                "tau": tau, "index_s": t_index, "query_s": t_query, "exact_s": t_exact,
+                "mean_delta": float(dd.mean())})
+    print(json.dumps(res), flush=True)
