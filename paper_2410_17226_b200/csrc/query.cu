@@ -333,7 +333,9 @@ int cbfs_query_stream(cbfs_graph* gh, const uint32_t* sources, const uint8_t* si
   WorkLease lease(g);
   if (lease.rc) return lease.rc;
   const uint32_t n = g->n;
-  const uint32_t planes = d + 1;
+  // label records keep S_v[0..d-1] only (R14): S_v[d] is rebuilt
+  // by the query from the cluster size; d = 0 keeps its single subset
+  const uint32_t planes = d > 0 ? d : 1;
   const int P = num_slots(g);
   QuerySource src;
   src.proto.d = d;
