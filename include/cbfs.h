@@ -9,7 +9,9 @@
  *   C-BFS, Alg. 1, direction-optimised EdgeMap,
  *     batched over clusters      -> cbfs_run
  *   distance decode  -> cbfs_decode
- *   landmark labels -> cbfs_run with planes = d
+ *   landmark labels -> cbfs_run with planes = d,
+ *                                  or the cbfs_labels_* handle (build, export
+ *                                  / import for the multi-GPU gather, query)
  *   landmark query  -> cbfs_query_distance
  *   fused build + query (streaming index)      -> cbfs_query_stream
  *
@@ -44,6 +46,7 @@ extern "C" {
 #endif
 
 typedef struct cbfs_graph cbfs_graph;
+typedef struct cbfs_labels cbfs_labels; /* opaque, device-resident landmark label store */
 typedef void* cbfs_stream; /* cudaStream_t */
 
 enum cbfs_status {
@@ -204,6 +207,32 @@ int cbfs_query_distance(uint32_t n, uint32_t C, uint32_t d, uint32_t planes, con
 int cbfs_query_stream(cbfs_graph* g, const uint32_t* sources, const uint8_t* sizes, uint32_t n_clusters, uint32_t d,
                       const uint32_t* s, const uint32_t* t, uint64_t q, int32_t* inout_best, uint64_t* out_stats,
                       cbfs_stream stream);
+
+/* --------------------------------------------------------------- label store handles
+ * cbfs_labels_build — the landmark labels of n_clusters clusters (A10,
+ * P:1001-1012 and P:1438-1447): one cbfs_run with planes = d (records Delta +
+ * S_v[0..d-1], R14; d = 0 keeps S_v[0]) into a library-owned device image.
+ *   sources, sizes : as cbfs_run (device);  dist_bytes : 1 or 2
+ * Errors: as cbfs_run, ENOMEM.  Synchronises.
+ * cbfs_labels_info — n, clusters, d, dist_bytes and the image size in bytes.
+ * cbfs_labels_export — copy the flat image (64-byte header, sizes, Delta
+ *   rows, subset planes) to buf (device or host, >= image bytes): the unit
+ *   an NCCL all-gather moves between ranks (A12).  EINVAL if buf is small.
+ * cbfs_labels_import — a new handle on g's device from an exported image
+ *   (device or host); EINVAL if the header is not a label image of a graph
+ *   with g's n.
+ * cbfs_labels_query — cbfs_query_distance over the store (min-merged into
+ *   inout_best, device [q] int32; s, t device [q] uint32 original ids).
+ * cbfs_labels_destroy — free the handle. */
+int cbfs_labels_build(cbfs_graph* g, const uint32_t* sources, const uint8_t* sizes, uint32_t n_clusters, uint32_t d,
+                      uint32_t dist_bytes, cbfs_labels** out, cbfs_stream stream);
+int cbfs_labels_info(const cbfs_labels* l, uint32_t* n, uint32_t* n_clusters, uint32_t* d, uint32_t* dist_bytes,
+                     uint64_t* image_bytes);
+int cbfs_labels_export(const cbfs_labels* l, void* buf, uint64_t bytes);
+int cbfs_labels_import(cbfs_graph* g, const void* buf, uint64_t bytes, cbfs_labels** out);
+int cbfs_labels_query(const cbfs_labels* l, const uint32_t* s, const uint32_t* t, uint64_t q, int32_t* inout_best,
+                      cbfs_stream stream);
+int cbfs_labels_destroy(cbfs_labels* l);
 
 /* cbfs_query_bidir — the fixed-size bi-directional search of Appendix B
  * (P:1790-1800), reading R27: from each endpoint a BFS over the sorted

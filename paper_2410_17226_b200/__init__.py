@@ -58,6 +58,13 @@ _sig("cbfs_decode", [_u32, _u32, _u32, _u32, _vp, _u32, _vp, _u32, _u32, _vp, _v
 _sig("cbfs_query_distance", [_u32, _u32, _u32, _u32, _vp, _u32, _vp, _vp, _vp, _vp, _u64, _vp, _vp])
 _sig("cbfs_query_stream", [_vp, _vp, _vp, _u32, _u32, _vp, _vp, _u64, _vp, _vp, _vp])
 _sig("cbfs_query_bidir", [_vp, _vp, _vp, _u64, _u32, _vp, _vp])
+_sig("cbfs_labels_build", [_vp, _vp, _vp, _u32, _u32, _u32, ctypes.POINTER(_vp), _vp])
+_sig("cbfs_labels_info", [_vp, ctypes.POINTER(_u32), ctypes.POINTER(_u32), ctypes.POINTER(_u32), ctypes.POINTER(_u32),
+                          ctypes.POINTER(_u64)])
+_sig("cbfs_labels_export", [_vp, _vp, _u64])
+_sig("cbfs_labels_import", [_vp, _vp, _u64, ctypes.POINTER(_vp)])
+_sig("cbfs_labels_query", [_vp, _vp, _vp, _u64, _vp, _vp])
+_sig("cbfs_labels_destroy", [_vp])
 _sig("cbfs_set_direction_alpha", [ctypes.c_double])
 _sig("cbfs_set_concurrency", [_i32])
 _sig("cbfs_set_engine", [_i32])
@@ -183,6 +190,40 @@ def cbfs_query_stream(h, sources, sizes, n_clusters, d, s, t, inout_best, out_st
 
 def cbfs_query_bidir(h, s, t, tau, inout_best, stream=None):
     _check(_lib.cbfs_query_bidir(h, _ptr(s), _ptr(t), len(s), tau, _ptr(inout_best), _stream(stream)))
+
+
+def cbfs_labels_build(g, sources, sizes, n_clusters, d, dist_bytes=2, stream=None):
+    h = _vp()
+    _check(_lib.cbfs_labels_build(g, _ptr(sources), _ptr(sizes), n_clusters, d, dist_bytes, ctypes.byref(h),
+                                  _stream(stream)))
+    return h
+
+
+def cbfs_labels_info(lh):
+    n, C, d, db, b = _u32(), _u32(), _u32(), _u32(), _u64()
+    _check(_lib.cbfs_labels_info(lh, ctypes.byref(n), ctypes.byref(C), ctypes.byref(d), ctypes.byref(db),
+                                 ctypes.byref(b)))
+    return dict(n=n.value, clusters=C.value, d=d.value, dist_bytes=db.value, image_bytes=b.value)
+
+
+def cbfs_labels_export(lh, buf):
+    nbytes = buf.nbytes if isinstance(buf, np.ndarray) else buf.numel() * buf.element_size()
+    _check(_lib.cbfs_labels_export(lh, _ptr(buf), nbytes))
+
+
+def cbfs_labels_import(g, buf):
+    h = _vp()
+    nbytes = buf.nbytes if isinstance(buf, np.ndarray) else buf.numel() * buf.element_size()
+    _check(_lib.cbfs_labels_import(g, _ptr(buf), nbytes, ctypes.byref(h)))
+    return h
+
+
+def cbfs_labels_query(lh, s, t, inout_best, stream=None):
+    _check(_lib.cbfs_labels_query(lh, _ptr(s), _ptr(t), len(s), _ptr(inout_best), _stream(stream)))
+
+
+def cbfs_labels_destroy(lh):
+    _check(_lib.cbfs_labels_destroy(lh))
 
 
 def cbfs_set_direction_alpha(alpha: float):

@@ -7,7 +7,10 @@ cluster c goes to rank c mod R (round-robin balances the degree-ordered
 selection, whose early clusters are the largest).  NCCL (torch.distributed)
 is used only at the end, in one of two ways:
 
-  * gather_labels — the label store fits every GPU (configs 1/2): each rank
+  * gather_label_images — the boundary's way: each rank builds
+    a cbfs_labels handle of its clusters, exports its flat image, the images
+    are all-gathered and imported as one handle per rank;
+  * gather_labels — the same with raw tensors: each rank
     builds the labels of its clusters with cbfs_run (planes = d, P:1438-1447,
     R14) and the shards are all-gathered; a gathered store is R shards of the
     cbfs_run layout, and cbfs_query_distance min-merges over them one by one
@@ -27,7 +30,8 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
-from . import (CBFS_QUERY_UNREACHED, CBFS_UNREACHED_U8, CBFS_UNREACHED_U16, cbfs_query_distance, cbfs_query_stream,
+from . import (CBFS_QUERY_UNREACHED, CBFS_UNREACHED_U8, CBFS_UNREACHED_U16, cbfs_labels_build, cbfs_labels_export,
+               cbfs_labels_import, cbfs_labels_info, cbfs_labels_query, cbfs_query_distance, cbfs_query_stream,
                cbfs_run)
 
 
@@ -116,6 +120,38 @@ def query_gathered(stores, d: int, s: torch.Tensor, t: torch.Tensor, dist_bytes:
     return best
 
 
+def build_local_labels(graph, sources: torch.Tensor, sizes: torch.Tensor, d: int, dist_bytes: int = 2, group=None):
+    """This rank's label store as a cbfs_labels handle (cbfs_labels_build over
+    its round-robin clusters)."""
+    src_r, sz_r = local_clusters(sources, sizes, group)
+    return cbfs_labels_build(graph.h, src_r, sz_r, int(sz_r.shape[0]), d, dist_bytes)
+
+
+def gather_label_images(graph, labels, group=None):
+    """cbfs_labels_export -> NCCL all_gather of the flat
+    images (padded to the largest; the header carries each image's size) ->
+    cbfs_labels_import.  Returns one handle per rank, rank order."""
+    world, _ = _world(group)
+    size = cbfs_labels_info(labels)["image_bytes"]
+    dev = torch.device(f"cuda:{graph.device}") if torch.cuda.is_available() else torch.device("cpu")
+    sizes = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
+    dist.all_gather(sizes, torch.tensor([size], dtype=torch.int64, device=dev), group=group)
+    top = int(max(int(x.item()) for x in sizes))
+    img = torch.zeros(top, dtype=torch.uint8, device=dev)
+    cbfs_labels_export(labels, img[:size])
+    parts = [torch.empty_like(img) for _ in range(world)]
+    dist.all_gather(parts, img, group=group)
+    return [cbfs_labels_import(graph.h, p[:int(sz.item())]) for p, sz in zip(parts, sizes)]
+
+
+def query_label_handles(handles, s: torch.Tensor, t: torch.Tensor) -> torch.Tensor:
+    """cbfs_labels_query over every gathered store, min-merged (R15, R16)."""
+    best = torch.full((int(s.shape[0]),), CBFS_QUERY_UNREACHED, dtype=torch.int32, device=s.device)
+    for h in handles:
+        cbfs_labels_query(h, s, t, best)
+    return best
+
+
 def min_reduce_answers(best: torch.Tensor, group=None) -> torch.Tensor:
     """MIN all-reduce of per-rank partial answers (int32, CBFS_QUERY_UNREACHED =
     no cluster reached both ends), in place."""
@@ -135,5 +171,5 @@ def query_stream_sharded(graph, sources: torch.Tensor, sizes: torch.Tensor, d: i
 
 
 __all__ = ["cluster_shard", "shard_width", "local_clusters", "build_label_shard", "all_gather_shards",
-           "gather_labels", "query_gathered", "min_reduce_answers", "query_stream_sharded",
-           "CBFS_UNREACHED_U16"]
+           "gather_labels", "query_gathered", "build_local_labels", "gather_label_images", "query_label_handles",
+           "min_reduce_answers", "query_stream_sharded", "CBFS_UNREACHED_U16"]

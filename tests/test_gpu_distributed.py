@@ -63,3 +63,38 @@ def test_query_stream_sharded(nccl_group):
     expect = orc.query_stream(ref, src, sz, d, s, t)
     assert np.array_equal(best.cpu().numpy(), expect)
     g.close()
+
+
+@pytest.mark.parametrize("d,dist_bytes", [(2, 1), (0, 2), (6, 2)])
+def test_label_images_gather_and_query(nccl_group, d, dist_bytes):
+    """cbfs_labels_build -> export -> NCCL all_gather -> import -> query ==
+    the oracle; host-buffer export/import round trip; bad images rejected."""
+    import paper_2410_17226_b200 as cb
+    el = ci.rmat(12, 8, 0.57, 0.19, 0.19, seed=44) if d <= 2 else ci.grid(50, 0.05, 0.01, 44)
+    ref = orc.csr_from_edgelist(el)
+    src, sz = orc.select_clusters(ref, 70, 64, max(d, 1) if d else 2)
+    if d == 0:  # d = 0 labels: single-source clusters (plain BFS landmarks)
+        src = src.copy(); src[:, 1:] = orc.PAD; sz = np.ones_like(sz)
+    g = gpu_graph(el, relabel=(d == 2))
+    h = pd.build_local_labels(g, to_dev_u32(src), to_dev_u8(sz), d, dist_bytes)
+    info = cb.cbfs_labels_info(h)
+    assert info["clusters"] == len(sz) and info["d"] == d and info["n"] == g.n
+    handles = pd.gather_label_images(g, h)
+    s, t = ci.query_pairs(g.n, 20000, seed=12)
+    best = pd.query_label_handles(handles, to_dev_u32(s), to_dev_u32(t))
+    expect = orc.query_stream(ref, src, sz, d, s, t)
+    assert np.array_equal(best.cpu().numpy(), expect)
+    img = np.zeros(info["image_bytes"], np.uint8)  # host round trip
+    cb.cbfs_labels_export(h, img)
+    h2 = cb.cbfs_labels_import(g.h, img)
+    best2 = torch.full((len(s),), cb.CBFS_QUERY_UNREACHED, dtype=torch.int32, device="cuda:0")
+    cb.cbfs_labels_query(h2, to_dev_u32(s), to_dev_u32(t), best2)
+    assert np.array_equal(best2.cpu().numpy(), expect)
+    bad = img.copy(); bad[0] ^= 0xFF
+    with pytest.raises(cb.CbfsError):
+        cb.cbfs_labels_import(g.h, bad)
+    with pytest.raises(cb.CbfsError):
+        cb.cbfs_labels_export(h, np.zeros(16, np.uint8))
+    for x in handles + [h, h2]:
+        cb.cbfs_labels_destroy(x)
+    g.close()
