@@ -10,7 +10,7 @@ full cluster distance vectors (u8 Delta + 3 u64 bit-subset planes per
 vertex per cluster).  Synthetic seeded input (cbfs_inputs, seed 2).
 
 One step = the whole hot path over the resident edge list: A0 CSR build
-(symmetrise, dedup, degree relabel) -> A1 cluster selection -> A2-A8 C-BFS of
+(symmetrise, dedup, relabel) -> A1 cluster selection -> A2-A8 C-BFS of
 every cluster -> output vectors in HBM.  `value` = sum_c |S_c| * m_c / T,
 m_c = arcs whose tail is reachable from S_c, T = device time
 of the K steps (CUDA events on the launching stream, max over ranks).
@@ -275,7 +275,8 @@ def run_ours(args, world, rank, local):
     C = args.clusters or cfg["clusters"]
     r_total, first = shard(C, world, rank)
     policy = cb.CBFS_ROOT_RANDOM if cfg["root"] == "random" else cb.CBFS_ROOT_DEGREE
-    relabel = cfg["kind"] in ("rmat", "er")
+    relabel = cfg.get("relabel", "none")
+    rflags = cb.Graph.relabel_flags(relabel)
     dist_bytes = 1 if cfg["kind"] in ("rmat", "er") else 2
     planes = d + 1
 
@@ -330,7 +331,7 @@ def run_ours(args, world, rank, local):
     def step(timed_phases: bool):
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         evs[0].record(stream)
-        h = cb.cbfs_graph_create(n, src_d, dst_d, cb.CBFS_RELABEL_DEGREE if relabel else 0, local, stream)
+        h = cb.cbfs_graph_create(n, src_d, dst_d, rflags, local, stream)
         evs[1].record(stream)
         if overlap:
             # A1 overlapped with A2-A8: traversal of batch b starts once its clusters are selected
@@ -439,7 +440,7 @@ def run_ours(args, world, rank, local):
             barrier(world)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            h = cb.cbfs_graph_create(n, src_h, dst_h, cb.CBFS_RELABEL_DEGREE if relabel else 0, local, stream)
+            h = cb.cbfs_graph_create(n, src_h, dst_h, rflags, local, stream)
             cb.cbfs_select_clusters(h, r_total, k, d, policy, cfg["root_seed"], sel_src, sel_sz, stream)
             if mode == "query":
                 qs_d.copy_(qs_h, non_blocking=True)

@@ -121,19 +121,23 @@ def query_pairs(n: int, q: int, seed: int, stream: int = 2):
 
 
 # --------------------------------------------------------------------------
-# BASELINE.json configs (seeds per SURVEY.md R22).  `scale_down` shrinks a
+# BASELINE.json configs (seeds per SURVEY.md R22).  `relabel` is the internal
+# vertex order the CUDA path is asked for (outputs are in original ids, R18):
+# hubs first for the power-law graphs, BFS locality for the k-NN graph; the
+# grid's row-major ids are already local.  `scale_down` shrinks a
 # config for quick tests while keeping its generator family and parameters.
 # --------------------------------------------------------------------------
 CONFIGS = {
-    "c1_er": dict(kind="er", n=4096, pairs=32768, seed=1, clusters=8, k=64, d=2, root="random", root_seed=1),
+    "c1_er": dict(kind="er", n=4096, pairs=32768, seed=1, clusters=8, k=64, d=2, root="random", root_seed=1,
+                  relabel="degree"),
     "c2_rmat20": dict(kind="rmat", scale=20, ef=16, abc=(0.57, 0.19, 0.19), seed=2, clusters=1024, k=64, d=2,
-                      root="degree", root_seed=0),
+                      root="degree", root_seed=0, relabel="degree"),
     "c3_rmat24": dict(kind="rmat", scale=24, ef=32, abc=(0.6, 0.15, 0.15), seed=3, clusters=4096, k=64, d=2,
-                      root="degree", root_seed=0),
+                      root="degree", root_seed=0, relabel="degree"),
     "c4_grid": dict(kind="grid", side=4096, p_delete=0.05, p_diag=0.001, seed=4, clusters=512, k=64, d=4,
-                    root="random", root_seed=4),
+                    root="random", root_seed=4, relabel="none"),
     "c5_knn": dict(kind="knn", n=10_000_000, knn=10, seed=7, clusters=8192, k=64, d=6, root="degree",
-                   root_seed=0, queries=10_000_000, query_seed=7),
+                   root_seed=0, queries=10_000_000, query_seed=7, relabel="locality"),
 }
 
 

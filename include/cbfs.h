@@ -68,7 +68,7 @@ enum cbfs_status {
 #define CBFS_BIDIR_MAX_TAU 1024u        /* vertices visited per side by cbfs_query_bidir */
 
 /* graph flags */
-enum { CBFS_RELABEL_DEGREE = 2, CBFS_INPUT_DEVICE = 4 };
+enum { CBFS_RELABEL_DEGREE = 2, CBFS_INPUT_DEVICE = 4, CBFS_RELABEL_LOCALITY = 8 };
 /* cluster root policies (R12) */
 enum { CBFS_ROOT_DEGREE = 0, CBFS_ROOT_RANDOM = 1 };
 /* EdgeMap direction policy (R8: parity-neutral) */
@@ -83,7 +83,12 @@ enum { CBFS_ENGINE_AUTO = 0, CBFS_ENGINE_BATCHED = 1, CBFS_ENGINE_SPARSE = 2 };
  * removed, neighbour lists sorted.  n vertices, ids in [0, n).
  *   src, dst : [n_pairs] uint32 — host, or device if flags & CBFS_INPUT_DEVICE
  *   flags    : CBFS_RELABEL_DEGREE (internal degree-descending order,
- *              ties by id) | CBFS_INPUT_DEVICE
+ *              ties by id: hubs packed, for power-law graphs) or
+ *              CBFS_RELABEL_LOCALITY (internal BFS order from the highest-
+ *              degree vertex, each level sorted by its first parent's
+ *              position then id, other components appended by id: graph
+ *              neighbours get nearby ids, for meshes / k-NN graphs; DEGREE
+ *              wins if both are set) | CBFS_INPUT_DEVICE
  *   device   : CUDA ordinal; the handle lives there.
  * Errors: EINVAL (null out, id >= n), EUNSUPPORTED (n > CBFS_MAX_N or more
  * than 2^32-1 arcs), ENOMEM, ECUDA.  Synchronises. */

@@ -29,7 +29,7 @@ CBFS_PAD = 0xFFFFFFFF
 CBFS_UNREACHED_U16, CBFS_UNREACHED_U8 = 0xFFFF, 0xFF
 CBFS_QUERY_UNREACHED = 0x7FFFFFFF
 CBFS_BIDIR_MAX_TAU = 1024
-CBFS_RELABEL_DEGREE, CBFS_INPUT_DEVICE = 2, 4
+CBFS_RELABEL_DEGREE, CBFS_INPUT_DEVICE, CBFS_RELABEL_LOCALITY = 2, 4, 8
 CBFS_ROOT_DEGREE, CBFS_ROOT_RANDOM = 0, 1
 CBFS_DIR_AUTO, CBFS_DIR_PUSH, CBFS_DIR_PULL = 0, 1, 2
 CBFS_ENGINE_AUTO, CBFS_ENGINE_BATCHED, CBFS_ENGINE_SPARSE = 0, 1, 2
@@ -274,14 +274,24 @@ class Graph:
         self.device = device
         self.n, self.m, self.max_degree = cbfs_graph_info(handle)
 
+    @staticmethod
+    def relabel_flags(relabel) -> int:
+        """False / None -> 0; True / "degree" -> CBFS_RELABEL_DEGREE; "locality" -> CBFS_RELABEL_LOCALITY."""
+        if relabel in (False, None, "none"):
+            return 0
+        if relabel in (True, "degree"):
+            return CBFS_RELABEL_DEGREE
+        if relabel == "locality":
+            return CBFS_RELABEL_LOCALITY
+        raise ValueError(f"unknown relabel {relabel!r}")
+
     @classmethod
     def from_edges(cls, n, src, dst, relabel=False, device=0, stream=None):
-        return cls(cbfs_graph_create(n, src, dst, CBFS_RELABEL_DEGREE if relabel else 0, device, stream), device)
+        return cls(cbfs_graph_create(n, src, dst, cls.relabel_flags(relabel), device, stream), device)
 
     @classmethod
     def from_csr(cls, n, offsets, cols, relabel=False, device=0, stream=None):
-        return cls(cbfs_graph_create_csr(n, offsets, cols, CBFS_RELABEL_DEGREE if relabel else 0, device, stream),
-                   device)
+        return cls(cbfs_graph_create_csr(n, offsets, cols, cls.relabel_flags(relabel), device, stream), device)
 
     def export_csr(self):
         return cbfs_graph_export_csr(self.h)

@@ -127,6 +127,63 @@ __global__ void k_relabel_keys(const uint64_t* __restrict__ arcs, uint64_t m, co
   }
 }
 
+// ---- locality order (CBFS_RELABEL_LOCALITY): a deterministic
+// Cuthill-McKee-like BFS order.  Level L+1 is sorted by (smallest position of
+// a parent in level L, original id), so vertices near each other in the graph
+// get nearby ids and a cluster's wavefront touches contiguous state.
+__global__ void k_bfsord_expand(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cols,
+                                const uint32_t* __restrict__ order, uint32_t lo, uint32_t hi,
+                                const uint32_t* __restrict__ pos, uint32_t* __restrict__ key,
+                                uint32_t* __restrict__ flag, uint64_t* __restrict__ next,
+                                unsigned long long* __restrict__ cnt) {
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < hi - lo;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t p = lo + (uint32_t)t, u = order[p];
+    for (uint64_t a = off[u]; a < off[u + 1]; ++a) {
+      const uint32_t v = cols[a];
+      if (pos[v] != 0xFFFFFFFFu) continue;
+      atomicMin(&key[v], p);
+      if (atomicCAS(&flag[v], 0u, 1u) == 0u) next[atomicAdd(cnt, 1ULL)] = v;
+    }
+  }
+}
+__global__ void k_bfsord_keys(uint64_t* __restrict__ next, uint64_t c, const uint32_t* __restrict__ key) {
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < c; t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = (uint32_t)next[t];
+    next[t] = ((uint64_t)key[v] << 32) | v;
+  }
+}
+__global__ void k_bfsord_place(const uint64_t* __restrict__ sorted, uint64_t c, uint32_t base,
+                               uint32_t* __restrict__ order, uint32_t* __restrict__ pos) {
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < c; t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = (uint32_t)sorted[t];
+    order[base + t] = v;
+    pos[v] = base + (uint32_t)t;
+  }
+}
+// vertices the BFS did not reach (other components), appended in id order
+__global__ void k_bfsord_flags(const uint32_t* __restrict__ pos, uint32_t n, uint32_t* __restrict__ f) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x)
+    f[v] = pos[v] == 0xFFFFFFFFu ? 1u : 0u;
+}
+__global__ void k_bfsord_rest(const uint32_t* __restrict__ f, const uint32_t* __restrict__ x, uint32_t n,
+                              uint32_t base, uint32_t* __restrict__ order, uint32_t* __restrict__ pos) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x)
+    if (f[v]) {
+      order[base + x[v]] = (uint32_t)v;
+      pos[v] = base + x[v];
+    }
+}
+// degree order (sorted keys of original ids) expressed in internal ids
+__global__ void k_order_map(const uint64_t* __restrict__ keys, uint32_t n, const uint32_t* __restrict__ inv,
+                            uint32_t* __restrict__ order, uint32_t* __restrict__ rank) {
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n; p += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t x = inv[(uint32_t)keys[p]];
+    order[p] = x;
+    rank[x] = (uint32_t)p;
+  }
+}
+
 __global__ void k_identity(uint32_t* a, uint32_t n) {
   for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x)
     a[v] = (uint32_t)v;
@@ -217,6 +274,75 @@ int graph_free(Graph* g) {
   return CBFS_OK;
 }
 
+// perm (internal -> original) = the locality order from `root`, inv = its inverse
+static int locality_order(const uint64_t* off, const uint32_t* cols, uint32_t n, uint32_t root, cudaStream_t st,
+                          uint32_t* perm, uint32_t* inv) {
+  uint32_t *key = nullptr, *flag = nullptr;
+  uint64_t *next = nullptr, *alt = nullptr;
+  unsigned long long *cnt = nullptr, *hcnt = nullptr;
+  CBFS_CUDA(cudaMallocAsync(&key, sizeof(uint32_t) * n, st));
+  CBFS_CUDA(cudaMallocAsync(&flag, sizeof(uint32_t) * n, st));
+  CBFS_CUDA(cudaMallocAsync(&next, sizeof(uint64_t) * n, st));
+  CBFS_CUDA(cudaMallocAsync(&alt, sizeof(uint64_t) * n, st));
+  CBFS_CUDA(cudaMallocAsync(&cnt, sizeof(unsigned long long), st));
+  CBFS_CUDA(cudaMallocHost(&hcnt, sizeof(unsigned long long)));
+  CBFS_CUDA(cudaMemsetAsync(inv, 0xFF, sizeof(uint32_t) * n, st));  // pos = inv
+  CBFS_CUDA(cudaMemsetAsync(key, 0xFF, sizeof(uint32_t) * n, st));
+  CBFS_CUDA(cudaMemsetAsync(flag, 0, sizeof(uint32_t) * n, st));
+  const uint32_t zero = 0;
+  CBFS_CUDA(cudaMemcpyAsync(perm, &root, sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+  CBFS_CUDA(cudaMemcpyAsync(inv + root, &zero, sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+  CBFS_CUDA(cudaMemsetAsync(flag + root, 1, 1, st));
+  size_t tb = 0;
+  cub::DoubleBuffer<uint64_t> probe(next, alt);
+  CBFS_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, probe, (uint64_t)n, 0, 64, st));
+  void* tmp = nullptr;
+  CBFS_CUDA(cudaMallocAsync(&tmp, tb ? tb : 1, st));
+  uint32_t lo = 0, hi = 1;
+  while (hi > lo) {
+    CBFS_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st));
+    k_bfsord_expand<<<grid_for(hi - lo, 256), 256, 0, st>>>(off, cols, perm, lo, hi, inv, key, flag, next, cnt);
+    CBFS_LAUNCHED();
+    CBFS_CUDA(cudaMemcpyAsync(hcnt, cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CBFS_CUDA(cudaStreamSynchronize(st));
+    const uint64_t c = *hcnt;
+    if (c) {
+      k_bfsord_keys<<<grid_for(c, 256), 256, 0, st>>>(next, c, key);
+      CBFS_LAUNCHED();
+      cub::DoubleBuffer<uint64_t> db(next, alt);
+      CBFS_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, db, c, 0, 64, st));
+      count_launch(8);
+      k_bfsord_place<<<grid_for(c, 256), 256, 0, st>>>(db.Current(), c, hi, perm, inv);
+      CBFS_LAUNCHED();
+    }
+    lo = hi;
+    hi = hi + (uint32_t)c;
+  }
+  if (hi < n) {  // unreached vertices (other components, isolated) in id order
+    uint32_t *f = key, *x = flag;  // reuse as scratch
+    k_bfsord_flags<<<grid_for(n, 256), 256, 0, st>>>(inv, n, f);
+    CBFS_LAUNCHED();
+    size_t sb = 0;
+    CBFS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, sb, f, x, n, st));
+    void* stmp = nullptr;
+    CBFS_CUDA(cudaMallocAsync(&stmp, sb ? sb : 1, st));
+    CBFS_CUDA(cub::DeviceScan::ExclusiveSum(stmp, sb, f, x, n, st));
+    count_launch(2);
+    k_bfsord_rest<<<grid_for(n, 256), 256, 0, st>>>(f, x, n, hi, perm, inv);
+    CBFS_LAUNCHED();
+    CBFS_CUDA(cudaFreeAsync(stmp, st));
+  }
+  CBFS_CUDA(cudaFreeAsync(tmp, st));
+  CBFS_CUDA(cudaFreeAsync(key, st));
+  CBFS_CUDA(cudaFreeAsync(flag, st));
+  CBFS_CUDA(cudaFreeAsync(next, st));
+  CBFS_CUDA(cudaFreeAsync(alt, st));
+  CBFS_CUDA(cudaFreeAsync(cnt, st));
+  CBFS_CUDA(cudaStreamSynchronize(st));
+  CBFS_CUDA(cudaFreeHost(hcnt));
+  return CBFS_OK;
+}
+
 // build from device keys buffer (length L = 2 * pairs), consumes `keys`
 static int build_from_keys(uint64_t* keys, uint64_t L, uint32_t n, uint32_t flags, int device, cudaStream_t st,
                            cbfs_graph** out) {
@@ -250,12 +376,21 @@ static int build_from_keys(uint64_t* keys, uint64_t L, uint32_t n, uint32_t flag
     CBFS_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, db, (uint64_t)n, 0, 64, st));
     count_launch(8);
     CBFS_CUDA(cudaFreeAsync(tmp, st));
-    if (flags & CBFS_RELABEL_DEGREE) {
-      // perm = order (internal x -> original), inv = rank
+    const bool by_degree = (flags & CBFS_RELABEL_DEGREE) != 0;
+    const bool by_locality = !by_degree && (flags & CBFS_RELABEL_LOCALITY) != 0 && g->m > 0;
+    if (by_degree || by_locality) {
       CBFS_CUDA(cudaMallocAsync(&g->perm, sizeof(uint32_t) * n, st));
       CBFS_CUDA(cudaMallocAsync(&g->inv, sizeof(uint32_t) * n, st));
-      k_order_from_keys<<<grid_for(n, 256), 256, 0, st>>>(db.Current(), n, g->perm, g->inv);
-      CBFS_LAUNCHED();
+      if (by_degree) {  // perm = degree order (internal x -> original), inv = rank
+        k_order_from_keys<<<grid_for(n, 256), 256, 0, st>>>(db.Current(), n, g->perm, g->inv);
+        CBFS_LAUNCHED();
+      } else {  // perm = BFS order from the highest-degree vertex
+        uint64_t k0 = 0;
+        CBFS_CUDA(cudaMemcpyAsync(&k0, db.Current(), sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+        CBFS_CUDA(cudaStreamSynchronize(st));
+        int rcl = locality_order(g->off, g->cols, n, (uint32_t)k0, st, g->perm, g->inv);
+        if (rcl) return rcl;
+      }
       // internal CSR: keys (inv[u] << 32 | inv[v]) sorted; the original
       // arc keys' buffer is reused as the sort's alternate buffer
       uint64_t* rk = nullptr;
@@ -282,11 +417,15 @@ static int build_from_keys(uint64_t* keys, uint64_t L, uint32_t n, uint32_t flag
       if (rc2) return rc2;
       CBFS_CUDA(cudaFreeAsync(rk, st));
       CBFS_CUDA(cudaFreeAsync(ralt, st));
-      // in internal ids the degree order is the identity
-      k_identity<<<grid_for(n, 256), 256, 0, st>>>(g->rank, n);
-      CBFS_LAUNCHED();
-      k_identity<<<grid_for(n, 256), 256, 0, st>>>(g->order, n);
-      CBFS_LAUNCHED();
+      if (by_degree) {  // in internal ids the degree order is the identity
+        k_identity<<<grid_for(n, 256), 256, 0, st>>>(g->rank, n);
+        CBFS_LAUNCHED();
+        k_identity<<<grid_for(n, 256), 256, 0, st>>>(g->order, n);
+        CBFS_LAUNCHED();
+      } else {  // the degree order (ties by original id, R12/R18) mapped to internal ids
+        k_order_map<<<grid_for(n, 256), 256, 0, st>>>(db.Current(), n, g->inv, g->order, g->rank);
+        CBFS_LAUNCHED();
+      }
       g->relabeled = true;
     } else {
       k_order_from_keys<<<grid_for(n, 256), 256, 0, st>>>(db.Current(), n, g->order, g->rank);

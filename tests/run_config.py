@@ -39,7 +39,7 @@ def main():
     el = ci.make_graph(args.config)
     t_gen = time.perf_counter() - t0
     n = el.n
-    relabel = (cfg["kind"] in ("rmat", "er")) if args.relabel < 0 else bool(args.relabel)
+    relabel = cb.Graph.relabel_flags(cfg.get("relabel", "none")) if args.relabel < 0 else args.relabel
     src_d = torch.from_numpy(el.src.view(np.int32)).to(dev)
     dst_d = torch.from_numpy(el.dst.view(np.int32)).to(dev)
     C = args.clusters or cfg["clusters"]
@@ -54,7 +54,7 @@ def main():
     for rep in range(args.reps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        h = cb.cbfs_graph_create(n, src_d, dst_d, cb.CBFS_RELABEL_DEGREE if relabel else 0, 0, st)
+        h = cb.cbfs_graph_create(n, src_d, dst_d, relabel, 0, st)
         torch.cuda.synchronize()
         t_build = time.perf_counter() - t0
         _, m, maxdeg = cb.cbfs_graph_info(h)

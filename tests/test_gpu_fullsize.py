@@ -25,10 +25,10 @@ DEV = "cuda:0"
 def _graph(name):
     cfg = ci.CONFIGS[name]
     el = ci.make_graph(name)
-    relabel = cfg["kind"] in ("rmat", "er")
+    relabel = cb.Graph.relabel_flags(cfg.get("relabel", "none"))
     src_d = torch.from_numpy(el.src.view(np.int32)).to(DEV)
     dst_d = torch.from_numpy(el.dst.view(np.int32)).to(DEV)
-    g = cb.Graph(cb.cbfs_graph_create(el.n, src_d, dst_d, cb.CBFS_RELABEL_DEGREE if relabel else 0, 0), 0)
+    g = cb.Graph(cb.cbfs_graph_create(el.n, src_d, dst_d, relabel, 0), 0)
     del src_d, dst_d
     return cfg, el, g
 

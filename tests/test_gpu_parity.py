@@ -72,7 +72,7 @@ def ball_clusters(g: orc.CSR, rng, C, d, kmax):
 
 
 # ------------------------------------------------------------------ A0 CSR build
-@pytest.mark.parametrize("relabel", [False, True])
+@pytest.mark.parametrize("relabel", [False, True, "locality"])
 @pytest.mark.parametrize("case", ["c1", "er", "rmat", "grid", "empty"])
 def test_csr_build_parity(case, relabel):
     if case == "c1":
@@ -107,7 +107,7 @@ def test_csr_build_rejects_bad_ids():
 
 
 # ------------------------------------------------------------------ A1 selection
-@pytest.mark.parametrize("relabel", [False, True])
+@pytest.mark.parametrize("relabel", [False, True, "locality"])
 @pytest.mark.parametrize("policy,d,k", [(0, 2, 64), (1, 2, 64), (0, 4, 13), (1, 4, 64), (0, 6, 64), (0, 3, 5),
                                         (0, 0, 1), (1, 1, 64)])
 def test_selection_parity(policy, d, k, relabel):
@@ -179,7 +179,7 @@ def test_random_graphs_parity(seed):
     d = [0, 1, 2, 3, 4, 6][seed % 6]
     C = [1, 5, 31, 32, 33, 70][seed % 6]  # ragged batches
     src, sz = ball_clusters(ref, rng, C, d, [1, 7, 64][seed % 3] if d else 1)
-    g = gpu_graph(el, relabel=bool(seed % 2))
+    g = gpu_graph(el, relabel=[False, True, "locality"][seed % 3])
     for eng, direction in each_mode():
         cb.cbfs_set_engine(eng)
         compare_many(g, ref, src, sz, d, direction=direction)
@@ -200,7 +200,7 @@ def test_diameter_exceeds_d_parity(seed):
         S = rng.choice(el.n, size=k, replace=False)
         src[c, :k] = S; sz[c] = k
     d = [1, 2, 3][seed % 3]
-    g = gpu_graph(el, relabel=bool(seed % 2))
+    g = gpu_graph(el, relabel=[False, True, "locality"][seed % 3])
     for eng, direction in each_mode():
         cb.cbfs_set_engine(eng)
         compare_many(g, ref, src, sz, d, direction=direction)

@@ -32,7 +32,7 @@ r = budget // record
 el = ci.make_graph(name)
 dev = torch.device("cuda:0")
 g = cb.Graph.from_edges(el.n, torch.from_numpy(el.src.view(np.int32)).to(dev),
-                        torch.from_numpy(el.dst.view(np.int32)).to(dev), relabel=cfg["kind"] in ("rmat", "er"))
+                        torch.from_numpy(el.dst.view(np.int32)).to(dev), relabel=cfg.get("relabel", "none"))
 torch.cuda.synchronize()
 t0 = time.perf_counter()
 idx = ado.LandmarkIndex(g, r, w, d, cb.CBFS_ROOT_RANDOM if cfg["root"] == "random" else cb.CBFS_ROOT_DEGREE,

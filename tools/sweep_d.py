@@ -23,12 +23,12 @@ name = sys.argv[1] if len(sys.argv) > 1 else "c2_rmat20"
 C = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
 cfg = ci.CONFIGS[name]
 el = ci.make_graph(name)
-relabel = cfg["kind"] in ("rmat", "er")
+relabel = cb.Graph.relabel_flags(cfg.get("relabel", "none"))
 dev = torch.device("cuda:0")
 st = torch.cuda.current_stream()
 h = cb.cbfs_graph_create(el.n, torch.from_numpy(el.src.view(np.int32)).to(dev),
                          torch.from_numpy(el.dst.view(np.int32)).to(dev),
-                         cb.CBFS_RELABEL_DEGREE if relabel else 0, 0, st)
+                         relabel, 0, st)
 policy = cb.CBFS_ROOT_RANDOM if cfg["root"] == "random" else cb.CBFS_ROOT_DEGREE
 for d in range(2, 7):
     ss = torch.empty((C, 64), dtype=torch.int32, device=dev)
