@@ -705,11 +705,11 @@ static int slot_round(Graph* g, Slot* w) {
   const unsigned fb = grid_for((nF + FOLD_ILP - 1) / FOLD_ILP, 256);
   if (g_prof.on) CBFS_CUDA(cudaEventRecord(w->pe[0], st));
   if (a.dist_bytes == 1)
-    k_fold<1><<<fb, 256, 0, st>>>(w->cur, (uint32_t)nF, i, w->seen, w->pend, w->dist, g->off, g->perm, n, a.C,
+    k_fold<1><<<fb, 256, 0, st>>>(w->cur, (uint32_t)nF, i, w->seen, w->pend, w->dist, g->off, a.out_internal ? nullptr : g->perm, n, a.C,
                                   a.cbase, a.planes, a.out_dist, a.out_masks, w->pre, write_pre, a.sizes, w->fullm,
                                   w->ctr);
   else
-    k_fold<2><<<fb, 256, 0, st>>>(w->cur, (uint32_t)nF, i, w->seen, w->pend, w->dist, g->off, g->perm, n, a.C,
+    k_fold<2><<<fb, 256, 0, st>>>(w->cur, (uint32_t)nF, i, w->seen, w->pend, w->dist, g->off, a.out_internal ? nullptr : g->perm, n, a.C,
                                   a.cbase, a.planes, a.out_dist, a.out_masks, w->pre, write_pre, a.sizes, w->fullm,
                                   w->ctr);
   CBFS_LAUNCHED();

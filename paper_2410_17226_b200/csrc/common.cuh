@@ -84,6 +84,7 @@ struct RunArgs {
   const uint8_t* sizes;     // device, batch base ([nb])
   uint32_t nb, d, planes, dist_bytes, C, cbase, direction;
   int engine;               // ENGINE_BATCHED / ENGINE_SPARSE (engine.cuh)
+  int out_internal;         // output rows are internal ids (library-internal staging), not original ids
   void* out_dist;           // device [n][C] or null
   uint64_t* out_masks;      // device [planes][n][C] or null
   uint64_t* out_stats;      // device [nb][4] or null

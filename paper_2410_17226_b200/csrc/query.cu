@@ -55,15 +55,20 @@ __global__ void __launch_bounds__(256) k_query(uint32_t n, uint32_t C, uint32_t 
                                                const void* __restrict__ dist, const uint64_t* __restrict__ masks,
                                                const uint8_t* __restrict__ sizes, const uint32_t* __restrict__ s,
                                                const uint32_t* __restrict__ t, uint64_t q,
-                                               int32_t* __restrict__ best, int* __restrict__ bad) {
+                                               int32_t* __restrict__ best, int* __restrict__ bad,
+                                               const uint32_t* __restrict__ inv) {
   const int lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
   for (uint64_t qi = warp; qi < q; qi += nwarps) {
-    const uint32_t a = s[qi], b = t[qi];
+    uint32_t a = s[qi], b = t[qi];
     if (a >= n || b >= n) {
       if (lane == 0) *bad = 1;
       continue;
+    }
+    if (inv) {  // label rows in internal ids (the streaming store)
+      a = inv[a];
+      b = inv[b];
     }
     // start from the answer so far (earlier batches / label shards): a
     // cluster whose Delta sum cannot beat it is skipped before its subsets
@@ -108,13 +113,13 @@ __global__ void __launch_bounds__(256) k_query(uint32_t n, uint32_t C, uint32_t 
 
 static int launch_query(uint32_t n, uint32_t C, uint32_t d, uint32_t planes, const void* dist, uint32_t dist_bytes,
                         const uint64_t* masks, const uint8_t* sizes, const uint32_t* s, const uint32_t* t, uint64_t q,
-                        int32_t* best, int* bad, cudaStream_t st) {
+                        int32_t* best, int* bad, cudaStream_t st, const uint32_t* inv = nullptr) {
   if (q == 0 || C == 0) return CBFS_OK;
   const unsigned blocks = grid_for(q * 32, 256, 148u * 8u * 8u);
   if (dist_bytes == 1)
-    k_query<1><<<blocks, 256, 0, st>>>(n, C, d, planes, dist, masks, sizes, s, t, q, best, bad);
+    k_query<1><<<blocks, 256, 0, st>>>(n, C, d, planes, dist, masks, sizes, s, t, q, best, bad, inv);
   else
-    k_query<2><<<blocks, 256, 0, st>>>(n, C, d, planes, dist, masks, sizes, s, t, q, best, bad);
+    k_query<2><<<blocks, 256, 0, st>>>(n, C, d, planes, dist, masks, sizes, s, t, q, best, bad, inv);
   CBFS_LAUNCHED();
   return CBFS_OK;
 }
@@ -306,18 +311,20 @@ struct QuerySource : ArraySource {
   uint64_t q = 0;
   int32_t* best = nullptr;
   int* bad = nullptr;
+  const uint32_t* inv = nullptr;  // the graph's original -> internal map (label rows are internal ids)
   int bind(RunArgs& a, int slot, cudaStream_t st) override {
     a.out_dist = sd[slot];
     a.out_masks = sm[slot];
     a.C = LANES;
     a.cbase = 0;
+    a.out_internal = 1;  // rows by internal id: the fold's writes follow the traversal's locality
     CBFS_CUDA(cudaMemsetAsync(sd[slot], 0xFF, sizeof(uint16_t) * (uint64_t)n * LANES, st));
     CBFS_CUDA(cudaMemsetAsync(sm[slot], 0, sizeof(uint64_t) * (uint64_t)planes * n * LANES, st));
     return CBFS_OK;
   }
   int finished(const RunArgs& a, int slot, cudaStream_t st) override {
     // lanes >= nb stay unreachable (dist 0xFFFF), so the query skips them
-    return launch_query(n, LANES, d, planes, sd[slot], 2, sm[slot], a.sizes, s, t, q, best, bad, st);
+    return launch_query(n, LANES, d, planes, sd[slot], 2, sm[slot], a.sizes, s, t, q, best, bad, st, inv);
   }
 };
 
@@ -349,6 +356,7 @@ int cbfs_query_stream(cbfs_graph* gh, const uint32_t* sources, const uint8_t* si
   src.n_clusters = n_clusters;
   src.out_stats = out_stats;
   src.n = n; src.d = d; src.planes = planes; src.s = s; src.t = t; src.q = q; src.best = inout_best;
+  src.inv = g->inv;
   src.sd.assign(P, nullptr);
   src.sm.assign(P, nullptr);
   for (int k = 0; k < P; ++k) {

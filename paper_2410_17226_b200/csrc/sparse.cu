@@ -550,7 +550,7 @@ int sparse_start(const Graph* g, Slot* w, const RunArgs& a) {
   SpDesc* h = w->sp_desc_h;  // the slot's previous batch (and its copy) finished before this one starts
   h->off = g->off;
   h->cols = g->cols;
-  h->perm = g->perm;
+  h->perm = a.out_internal ? nullptr : g->perm;  // output rows: original ids unless library staging
   h->inv = g->inv;
   h->sources = a.sources;
   h->sizes = a.sizes;
