@@ -156,8 +156,10 @@ def barrier(world: int):
 
 
 def shard(n_clusters_per_rank: int, world: int, rank: int):
-    """Weak scaling: an N*C-cluster selection, rank r owns the block [r*C, (r+1)*C)."""
-    return n_clusters_per_rank * world, rank * n_clusters_per_rank
+    """Weak scaling: an N*C-cluster selection; rank r owns the clusters
+    r, r + N, r + 2N, ... (round-robin balances the degree-ordered
+    selection).  Returns (selection size, rank's first cluster; stride N)."""
+    return n_clusters_per_rank * world, rank
 
 
 # ------------------------------------------------------------------ CPU oracle sample
@@ -310,12 +312,13 @@ def run_ours(args, world, rank, local):
         cb.cbfs_set_concurrency(args.concurrency)
     if args.engine:
         cb.cbfs_set_engine(args.engine)
-    overlap = world == 1 and mode == "full" and not args.separate_select
+    overlap = mode == "full" and not args.separate_select
 
     phase_ms = {"build": 0.0, "select": 0.0, "cbfs": 0.0}
 
     def traverse(h):
-        blk_src, blk_sz = sel_src[first:first + C], sel_sz[first:first + C]
+        blk_src = sel_src[first::world].contiguous()  # this rank's clusters (round-robin)
+        blk_sz = sel_sz[first::world].contiguous()
         if mode == "full":
             cb.cbfs_run(h, blk_src, blk_sz, C, d, dist_bytes, dist_out, masks_out, planes, stats, args.direction,
                         stream)
@@ -336,8 +339,9 @@ def run_ours(args, world, rank, local):
         if overlap:
             # A1 overlapped with A2-A8: traversal of batch b starts once its clusters are selected
             evs[2].record(stream)
-            got = cb.cbfs_select_and_run(h, r_total, k, d, policy, cfg["root_seed"], sel_src, sel_sz, dist_bytes,
-                                         dist_out, masks_out, planes, stats, args.direction, stream)
+            got = cb.cbfs_select_and_run_shard(h, r_total, k, d, policy, cfg["root_seed"], world, rank, sel_src,
+                                               sel_sz, dist_bytes, dist_out, masks_out, planes, stats,
+                                               args.direction, stream)
         else:
             got = cb.cbfs_select_clusters(h, r_total, k, d, policy, cfg["root_seed"], sel_src, sel_sz, stream)
             evs[2].record(stream)
@@ -379,7 +383,7 @@ def run_ours(args, world, rank, local):
     clk = clocks.stop()
     phase_ms = {kk: v / args.steps for kk, v in phase_ms.items()}  # per timed step
     st = stats.cpu().numpy().view(np.uint64)
-    sizes = sel_sz[first:first + C].cpu().numpy().astype(np.float64)
+    sizes = sel_sz[first::world].cpu().numpy().astype(np.float64)
     units_step = float((sizes * st[:, 3].astype(np.float64)).sum())
     hh = cb.cbfs_graph_create(n, src_d, dst_d, 0, local, stream)
     n_h, m_h, maxdeg = cb.cbfs_graph_info(hh)
@@ -428,8 +432,8 @@ def run_ours(args, world, rank, local):
         import ctypes
         e2e_ms = 0.0
         hs = torch.zeros((C, 4), dtype=torch.int64).pin_memory()
-        hsrc = torch.empty((r_total, 64), dtype=torch.int32).pin_memory()
-        hsz = torch.empty((r_total,), dtype=torch.uint8).pin_memory()
+        hsrc = torch.empty((C, 64), dtype=torch.int32).pin_memory()
+        hsz = torch.empty((C,), dtype=torch.uint8).pin_memory()
         hd = hm = hbest = None
         if mode == "full":
             hd = torch.empty((n, C), dtype=dist_out.dtype).pin_memory()
@@ -448,10 +452,10 @@ def run_ours(args, world, rank, local):
                 traverse(h)
                 hbest.copy_(best)
             else:
-                hsrc.copy_(sel_src)
-                hsz.copy_(sel_sz)
-                cb._check(cb._lib.cbfs_run_host(h, ctypes.c_void_p(hsrc[first:].data_ptr()),
-                                                ctypes.c_void_p(hsz[first:].data_ptr()), C, d, dist_bytes,
+                hsrc.copy_(sel_src[first::world])
+                hsz.copy_(sel_sz[first::world])
+                cb._check(cb._lib.cbfs_run_host(h, ctypes.c_void_p(hsrc.data_ptr()),
+                                                ctypes.c_void_p(hsz.data_ptr()), C, d, dist_bytes,
                                                 ctypes.c_void_p(hd.data_ptr()) if hd is not None else None,
                                                 ctypes.c_void_p(hm.data_ptr()) if hm is not None else None, planes,
                                                 ctypes.c_void_p(hs.data_ptr()), args.direction,
@@ -496,9 +500,9 @@ def run_ours(args, world, rank, local):
             "config": {"workload": args.config, "graph": el.name, "n": n, "arcs": m_h, "max_degree": maxdeg,
                        "clusters_per_gpu": C, "k": k, "d": d, "dist_bytes": dist_bytes, "relabel": relabel,
                        "mode": mode, "outputs": outputs, "queries": Q,
-                       "parallelism": f"clusters sharded, {world} rank(s), graph replicated",
-                       "step": ("A0 CSR build + A1 selection + A2-A8 C-BFS of all clusters"
-                                + (" (A1 overlapped with A2-A8: cbfs_select_and_run)" if overlap else "")
+                       "parallelism": f"clusters round-robin over {world} rank(s), graph replicated",
+                       "step": ("A0 CSR build + A1 selection + A2-A8 C-BFS of the rank's clusters"
+                                + (" (A1 overlapped with A2-A8: cbfs_select_and_run_shard)" if overlap else "")
                                 + (" + A10/A11 labels and queries" if mode == "query" else "")),
                        "l2": "flushed between timed steps (256 MiB write); inputs and outputs > L2",
                        "units_per_step_rank0": units_step,

@@ -168,6 +168,21 @@ int cbfs_select_and_run(cbfs_graph* g, uint32_t r, uint32_t k, uint32_t d, uint3
                         void* out_dist, uint64_t* out_masks, uint32_t planes, uint64_t* out_stats,
                         uint32_t direction, cbfs_stream stream);
 
+/* cbfs_select_and_run_shard — the same for rank `rank` of `world` ranks
+ * (cluster c belongs to rank c mod world): every rank runs the
+ * whole (deterministic, sequential) selection of r clusters on a side stream
+ * into out_sources / out_sizes ([r][64] / [r], device) and traverses its own
+ * clusters c = rank, rank + world, ... as soon as each batch of 64 of them
+ * exists.  Outputs use this rank's columns: C_rank = ceil((r - rank) /
+ * world), out_dist [n][C_rank], out_masks [planes][n][C_rank], out_stats
+ * [C_rank][4], column j = global cluster rank + j * world.  world = 1 is
+ * cbfs_select_and_run.  Errors: EINVAL (rank >= world) and as above. */
+int cbfs_select_and_run_shard(cbfs_graph* g, uint32_t r, uint32_t k, uint32_t d, uint32_t root_policy,
+                              uint64_t seed, uint32_t world, uint32_t rank, uint32_t* out_sources,
+                              uint8_t* out_sizes, uint32_t* out_r, uint32_t dist_bytes, void* out_dist,
+                              uint64_t* out_masks, uint32_t planes, uint64_t* out_stats, uint32_t direction,
+                              cbfs_stream stream);
+
 /* Same computation with HOST buffers (sources, sizes, out_dist, out_masks,
  * out_stats all host memory, pinned recommended): inputs are copied in; when
  * the whole output fits in free device memory it is built there and copied

@@ -53,6 +53,8 @@ _sig("cbfs_select_clusters", [_vp, _u32, _u32, _u32, _u32, _u64, _vp, _vp, ctype
 _sig("cbfs_run", [_vp, _vp, _vp, _u32, _u32, _u32, _vp, _vp, _u32, _vp, _u32, _vp])
 _sig("cbfs_select_and_run", [_vp, _u32, _u32, _u32, _u32, _u64, _vp, _vp, ctypes.POINTER(_u32), _u32, _vp, _vp,
                               _u32, _vp, _u32, _vp])
+_sig("cbfs_select_and_run_shard", [_vp, _u32, _u32, _u32, _u32, _u64, _u32, _u32, _vp, _vp, ctypes.POINTER(_u32), _u32,
+                                    _vp, _vp, _u32, _vp, _u32, _vp])
 _sig("cbfs_run_host", [_vp, _vp, _vp, _u32, _u32, _u32, _vp, _vp, _u32, _vp, _u32, _vp])
 _sig("cbfs_decode", [_u32, _u32, _u32, _u32, _vp, _u32, _vp, _u32, _u32, _vp, _vp])
 _sig("cbfs_query_distance", [_u32, _u32, _u32, _u32, _vp, _u32, _vp, _vp, _vp, _vp, _u64, _vp, _vp])
@@ -165,6 +167,15 @@ def cbfs_select_and_run(h, r, k, d, root_policy, seed, out_sources, out_sizes, d
     _check(_lib.cbfs_select_and_run(h, r, k, d, root_policy, seed, _ptr(out_sources), _ptr(out_sizes),
                                     ctypes.byref(got), dist_bytes, _ptr(out_dist), _ptr(out_masks), planes,
                                     _ptr(out_stats), direction, _stream(stream)))
+    return got.value
+
+
+def cbfs_select_and_run_shard(h, r, k, d, root_policy, seed, world, rank, out_sources, out_sizes, dist_bytes, out_dist,
+                              out_masks, planes, out_stats=None, direction=CBFS_DIR_AUTO, stream=None) -> int:
+    got = _u32()
+    _check(_lib.cbfs_select_and_run_shard(h, r, k, d, root_policy, seed, world, rank, _ptr(out_sources),
+                                          _ptr(out_sizes), ctypes.byref(got), dist_bytes, _ptr(out_dist),
+                                          _ptr(out_masks), planes, _ptr(out_stats), direction, _stream(stream)))
     return got.value
 
 

@@ -962,29 +962,60 @@ int cbfs_run(cbfs_graph* gh, const uint32_t* sources, const uint8_t* sizes, uint
 
 // A1 overlapped with A2-A8: the selection CTA runs on a side stream and
 // publishes each finished cluster through mapped host memory; a batch of
-// LANES clusters is started as soon as its clusters exist.
+// LANES clusters is started as soon as its clusters exist.  With world > 1
+// the caller's rank owns the clusters c = rank, rank + world, ... (SURVEY
+// §8(e)); a batch's rows are gathered into slot-local contiguous buffers.
 struct SelectSource : ArraySource {
   volatile uint32_t* prog;
   cudaStream_t side;
   uint32_t r;
+  uint32_t world = 1, rank = 0;
+  std::vector<uint32_t*> slot_src;
+  std::vector<uint8_t*> slot_sz;
+  uint32_t local_of(uint32_t global_count) const {  // this rank's clusters among the first global_count
+    return global_count > rank ? (global_count - rank + world - 1) / world : 0;
+  }
   int next(RunArgs& a) override {
-    const uint32_t need = std::min<uint32_t>(r, next_c + LANES);
+    const uint32_t total = local_of(r);
+    if (next_c >= total) return -1;
+    const uint32_t want_end = std::min<uint32_t>(total, next_c + LANES);
+    const uint32_t need = rank + world * (want_end - 1) + 1;  // global clusters that must exist
     const uint32_t p = prog[0];
     const bool done = prog[1] != 0;
     if (p < need && !done) {
       if (cudaStreamQuery(side) != cudaErrorNotReady && prog[0] < need && !prog[1]) return -1;  // selection died
       return 0;
     }
-    n_clusters = prog[0];
-    return ArraySource::next(a);
+    const uint32_t avail = local_of(std::min<uint32_t>((uint32_t)prog[0], r));
+    if (next_c >= avail) return -1;  // the selection ran out of vertices
+    a = proto;
+    a.nb = std::min<uint32_t>(LANES, avail - next_c);
+    const uint64_t g0 = rank + (uint64_t)world * next_c;  // global index of the batch's first cluster
+    a.sources = sources + g0 * 64;
+    a.sizes = sizes + g0;
+    a.cbase = proto.cbase + next_c;
+    a.out_stats = out_stats ? out_stats + (uint64_t)next_c * 4 : nullptr;
+    next_c += a.nb;
+    return 1;
+  }
+  int bind(RunArgs& a, int slot, cudaStream_t st) override {
+    if (world == 1) return CBFS_OK;
+    CBFS_CUDA(cudaMemcpy2DAsync(slot_src[slot], 64 * sizeof(uint32_t), a.sources, (uint64_t)world * 64 * sizeof(uint32_t),
+                                64 * sizeof(uint32_t), a.nb, cudaMemcpyDeviceToDevice, st));
+    CBFS_CUDA(cudaMemcpy2DAsync(slot_sz[slot], 1, a.sizes, world, 1, a.nb, cudaMemcpyDeviceToDevice, st));
+    a.sources = slot_src[slot];
+    a.sizes = slot_sz[slot];
+    return CBFS_OK;
   }
 };
 
-int cbfs_select_and_run(cbfs_graph* gh, uint32_t r, uint32_t k, uint32_t d, uint32_t root_policy, uint64_t seed,
-                        uint32_t* out_sources, uint8_t* out_sizes, uint32_t* out_r, uint32_t dist_bytes,
-                        void* out_dist, uint64_t* out_masks, uint32_t planes, uint64_t* out_stats,
-                        uint32_t direction, cbfs_stream stream) {
+int cbfs_select_and_run_shard(cbfs_graph* gh, uint32_t r, uint32_t k, uint32_t d, uint32_t root_policy,
+                              uint64_t seed, uint32_t world, uint32_t rank, uint32_t* out_sources,
+                              uint8_t* out_sizes, uint32_t* out_r, uint32_t dist_bytes, void* out_dist,
+                              uint64_t* out_masks, uint32_t planes, uint64_t* out_stats, uint32_t direction,
+                              cbfs_stream stream) {
   Graph* g = reinterpret_cast<Graph*>(gh);
+  if (world == 0 || rank >= world) return fail(CBFS_EINVAL, "rank must be < world");
   int rc = check_select_args(g, r, k, d, root_policy, out_sources, out_sizes);
   if (rc) return rc;
   rc = check_run_args(g, out_sources, out_sizes, r, d, dist_bytes, planes, direction);
@@ -1019,15 +1050,17 @@ int cbfs_select_and_run(cbfs_graph* gh, uint32_t r, uint32_t k, uint32_t d, uint
   CBFS_CUDA(cudaEventDestroy(ready));
   rc = select_launch(g, r, k, d, root_policy, seed, out_sources, out_sizes, count_d[dv], prog_d[dv], side[dv]);
   if (rc) return rc;
-  const uint64_t C = r;
+  SelectSource src;
+  src.world = world;
+  src.rank = rank;
+  const uint64_t C = src.local_of(r);  // this rank's output columns
   if (out_dist) CBFS_CUDA(cudaMemsetAsync(out_dist, 0xFF, (uint64_t)g->n * C * dist_bytes, st));
   if (out_masks) CBFS_CUDA(cudaMemsetAsync(out_masks, 0, (uint64_t)planes * g->n * C * sizeof(uint64_t), st));
-  SelectSource src;
   src.proto = RunArgs{};
   src.proto.d = d;
   src.proto.planes = planes;
   src.proto.dist_bytes = dist_bytes;
-  src.proto.C = r;
+  src.proto.C = (uint32_t)C;
   src.proto.direction = direction;
   src.proto.engine = choose_engine(g, direction);
   if (src.proto.engine < 0) return CBFS_ECUDA;
@@ -1040,14 +1073,35 @@ int cbfs_select_and_run(cbfs_graph* gh, uint32_t r, uint32_t k, uint32_t d, uint
   src.prog = prog;
   src.side = side[dv];
   src.r = r;
+  const int P = num_slots(g);
+  if (world > 1) {
+    src.slot_src.assign(P, nullptr);
+    src.slot_sz.assign(P, nullptr);
+    for (int q = 0; q < P; ++q) {
+      CBFS_CUDA(cudaMallocAsync(&src.slot_src[q], LANES * 64 * sizeof(uint32_t), st));
+      CBFS_CUDA(cudaMallocAsync(&src.slot_sz[q], LANES, st));
+    }
+  }
   rc = run_batches(g, src, st);
   cudaError_t e2 = cudaStreamSynchronize(side[dv]);
+  for (int q = 0; q < (int)src.slot_src.size(); ++q) {
+    cudaFreeAsync(src.slot_src[q], st);
+    cudaFreeAsync(src.slot_sz[q], st);
+  }
   if (rc) return rc;
   if (e2 != cudaSuccess) return cuda_fail(e2, "cluster selection");
   if (!prog[1]) return fail(CBFS_ECUDA, "cluster selection ended without publishing");
   CBFS_CUDA(cudaStreamSynchronize(st));
   *out_r = prog[0];
   return CBFS_OK;
+}
+
+int cbfs_select_and_run(cbfs_graph* gh, uint32_t r, uint32_t k, uint32_t d, uint32_t root_policy, uint64_t seed,
+                        uint32_t* out_sources, uint8_t* out_sizes, uint32_t* out_r, uint32_t dist_bytes,
+                        void* out_dist, uint64_t* out_masks, uint32_t planes, uint64_t* out_stats,
+                        uint32_t direction, cbfs_stream stream) {
+  return cbfs_select_and_run_shard(gh, r, k, d, root_policy, seed, 1, 0, out_sources, out_sizes, out_r, dist_bytes,
+                                   out_dist, out_masks, planes, out_stats, direction, stream);
 }
 
 int cbfs_profile_enable(int on) {

@@ -14,6 +14,7 @@
 namespace cbfs {
 
 constexpr int SEL_THREADS = 1024;
+constexpr uint32_t SEL_PUBLISH = 8;
 
 struct SelScratch {
   uint8_t* marked;
@@ -123,15 +124,30 @@ k_select(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cols, co
           if ((rk & pm) == pre) atomicAdd(&hist[(rk >> shift) & 255u], 1u);
         }
         __syncthreads();
-        if (tid == 0) {
-          unsigned cum = 0, need = s_need, b = 0;
-          for (; b < 256; ++b) {
-            if (cum + hist[b] >= need) break;
-            cum += hist[b];
+        if (tid < 32) {  // the bucket holding the need-th smallest: warp prefix over 8 buckets per lane
+          unsigned loc[8], sum = 0;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) { loc[q] = hist[tid * 8 + q]; sum += loc[q]; }
+          unsigned incl = sum;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (tid >= (unsigned)o) incl += y;
           }
-          s_need = need - cum;
-          s_prefix = pre | (b << shift);
-          s_pmask = pm | (255u << shift);
+          const unsigned need = s_need;
+          unsigned cum = incl - sum;  // buckets before this lane's
+          const bool mine = cum < need && incl >= need;
+          if (mine) {
+            unsigned b = tid * 8;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              if (cum + loc[q] >= need) { b = tid * 8 + q; break; }
+              cum += loc[q];
+            }
+            s_need = need - cum;
+            s_prefix = pre | (b << shift);
+            s_pmask = pm | (255u << shift);
+          }
         }
         __syncthreads();
       }
@@ -170,9 +186,13 @@ k_select(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cols, co
     }
     if (dec) atomicAdd(&s_avail, (unsigned long long)0 - dec);  // subtract
     ++produced;
-    if (progress) __threadfence();
+    // publish to a concurrent traversal (cbfs_select_and_run*) every
+    // SEL_PUBLISH clusters (a system-scope fence per cluster costs more than
+    // the batches, which need 64 clusters at a time, can use)
+    const bool publish = progress && (produced % SEL_PUBLISH) == 0;
+    if (publish) __threadfence();
     __syncthreads();
-    if (progress && tid == 0) {  // publish cluster c to a concurrent traversal (cbfs_select_and_run)
+    if (publish && tid == 0) {
       __threadfence_system();
       progress[0] = produced;
     }

@@ -49,7 +49,7 @@ def test_gloo_reductions_and_shards():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert res[0][1:] == (11.0, 3.0, 2048, 0)
-    assert res[1][1:] == (11.0, 3.0, 2048, 1024)
+    assert res[1][1:] == (11.0, 3.0, 2048, 1)  # round-robin: rank 1 owns clusters 1, 3, 5, ...
 
 
 def test_reference_arm_under_torchrun():

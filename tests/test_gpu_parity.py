@@ -432,3 +432,31 @@ def test_sparse_engine_round_cap_and_recovery():
     ref2 = orc.csr_from_edgelist(el2)
     src2, sz2 = orc.select_clusters(ref2, 20, 64, 2)
     compare_many(gpu_graph(el2), ref2, src2, sz2, 2)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_select_and_run_shard_round_robin(world, engine):
+    """cbfs_select_and_run_shard: rank r's outputs are exactly the oracle's for
+    clusters r, r + world, ... of the full selection."""
+    el = random_el(93, 4000, "rmat")
+    ref = orc.csr_from_edgelist(el)
+    g = gpu_graph(el, relabel=True)
+    d, r = 2, 200
+    osrc, osz = orc.select_clusters(ref, r, 64, d, 0, seed=0)
+    om = orc.cluster_bfs_many(ref, osrc, osz, d)
+    for rank in range(world):
+        Cr = (r - rank + world - 1) // world
+        src = torch.empty((r, 64), dtype=torch.int32, device="cuda:0")
+        sz = torch.empty((r,), dtype=torch.uint8, device="cuda:0")
+        dist = torch.empty((g.n, Cr), dtype=torch.uint8, device="cuda:0")
+        masks = torch.empty((d + 1, g.n, Cr), dtype=torch.int64, device="cuda:0")
+        stats = torch.zeros((Cr, 4), dtype=torch.int64, device="cuda:0")
+        got = cb.cbfs_select_and_run_shard(g.h, r, 64, d, 0, 0, world, rank, src, sz, 1, dist, masks, d + 1, stats)
+        assert got == len(osz) == r
+        assert np.array_equal(np_u32(src), osrc)
+        idx = np.arange(rank, r, world)
+        gd = dist.cpu().numpy().astype(np.uint16)
+        gd[gd == 0xFF] = 0xFFFF
+        assert np.array_equal(gd.T, om["dist"][idx])
+        assert np.array_equal(np_u64(masks).transpose(2, 0, 1), om["sub"][idx])
+        assert np.array_equal(stats.cpu().numpy().view(np.uint64), om["stats"][idx])
