@@ -15,10 +15,14 @@ every cluster -> output vectors in HBM.  `value` = sum_c |S_c| * m_c / T,
 m_c = arcs whose tail is reachable from S_c, T = device time
 of the K steps (CUDA events on the launching stream, max over ranks).
 
-N>1 (torchrun, one rank per GPU, NCCL): weak scaling — rank r runs its own
-block of 1,024 clusters of an N*1,024-cluster selection over the replicated
-graph; no data-path collective (clusters are independent); only the
-timing MAX and the unit totals are all-reduced.
+N>1 (torchrun, one rank per GPU, NCCL): strong scaling by default — the
+config's 1,024 clusters are split round-robin over the ranks (rank r owns
+clusters r, r+N, ...), the graph is replicated, every rank
+runs the deterministic selection overlapped with its traversal
+(cbfs_select_and_run_shard); no data-path collective (clusters are
+independent) except the MIN all-reduce of query answers in query
+mode; the timing MAX and the unit totals are all-reduced.  `--scaling weak`
+gives every rank C clusters of an N x C selection instead.
 
 `--impl reference` times the CPU oracle (oracle/, sequential Alg. 1 per
 cluster, clusters over all host cores) on a bounded sample of the same
@@ -155,11 +159,15 @@ def barrier(world: int):
         dist.barrier()
 
 
-def shard(n_clusters_per_rank: int, world: int, rank: int):
-    """Weak scaling: an N*C-cluster selection; rank r owns the clusters
-    r, r + N, r + 2N, ... (round-robin balances the degree-ordered
-    selection).  Returns (selection size, rank's first cluster; stride N)."""
-    return n_clusters_per_rank * world, rank
+def shard(n_clusters: int, world: int, rank: int, strong: bool = True):
+    """Rank r owns clusters r, r + N, r + 2N, ... of the selection (SURVEY
+    §8(e): round-robin balances the degree-ordered selection).  Strong scaling
+    (default, SURVEY §8(e) "per-rank work is r/R clusters"): the config's
+    selection is split over the N ranks; weak: an N x C selection, C per rank.
+    Returns (selection size, rank's first cluster, rank's cluster count);
+    the stride is N."""
+    total = n_clusters if strong else n_clusters * world
+    return total, rank, len(range(rank, total, world))
 
 
 # ------------------------------------------------------------------ CPU oracle sample
@@ -173,7 +181,7 @@ def oracle_sample(cfg_name: str, el, threads: int, n_sample: int, world: int = 1
     t_build = time.perf_counter() - t0
     t0 = time.perf_counter()
     pol = orc.ROOT_RANDOM if cfg["root"] == "random" else orc.ROOT_DEGREE
-    src, sz = orc.select_clusters(g, cfg["clusters"] * world, cfg["k"], cfg["d"], pol, cfg["root_seed"])
+    src, sz = orc.select_clusters(g, cfg["clusters"], cfg["k"], cfg["d"], pol, cfg["root_seed"])
     t_sel = time.perf_counter() - t0
     C = len(sz)
     idx = np.linspace(0, C - 1, min(n_sample, C)).round().astype(int)
@@ -274,8 +282,9 @@ def run_ours(args, world, rank, local):
     cfg = ci.CONFIGS[args.config]
     mode = args.mode or MODES[args.config]
     d, k = cfg["d"], cfg["k"]
-    C = args.clusters or cfg["clusters"]
-    r_total, first = shard(C, world, rank)
+    C_cfg = args.clusters or cfg["clusters"]
+    strong = args.scaling == "strong"
+    r_total, first, C = shard(C_cfg, world, rank, strong)  # C = this rank's clusters
     policy = cb.CBFS_ROOT_RANDOM if cfg["root"] == "random" else cb.CBFS_ROOT_DEGREE
     relabel = cfg.get("relabel", "none")
     rflags = cb.Graph.relabel_flags(relabel)
@@ -495,10 +504,11 @@ def run_ours(args, world, rank, local):
                    "query": f"labels of every batch consumed by {Q} distance queries (cbfs_query_stream)"}[mode]
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
-            "ms_per_step": 1000 * T / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": 1000 * T / K, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "u64", "data": "synthetic",
             "config": {"workload": args.config, "graph": el.name, "n": n, "arcs": m_h, "max_degree": maxdeg,
-                       "clusters_per_gpu": C, "k": k, "d": d, "dist_bytes": dist_bytes, "relabel": relabel,
+                       "clusters": r_total, "clusters_rank0": C, "k": k, "d": d, "dist_bytes": dist_bytes,
+                       "relabel": relabel,
                        "mode": mode, "outputs": outputs, "queries": Q,
                        "parallelism": f"clusters round-robin over {world} rank(s), graph replicated",
                        "step": ("A0 CSR build + A1 selection + A2-A8 C-BFS of the rank's clusters"
@@ -539,6 +549,8 @@ def main():
     ap.add_argument("--clock-ms", type=int, default=500)
     ap.add_argument("--concurrency", type=int, default=0, help="concurrent batches per GPU (0 = library default)")
     ap.add_argument("--engine", type=int, default=0, help="0 auto, 1 batched, 2 sparse (cbfs_set_engine)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the config's clusters split over the ranks; weak: C clusters per rank")
     ap.add_argument("--mode", default="", choices=["", "full", "stats", "query"], help="override the config's mode")
     ap.add_argument("--clusters", type=int, default=0, help="clusters per GPU (default: the config's)")
     ap.add_argument("--queries", type=int, default=0, help="queries (query mode; default: the config's)")

@@ -3,10 +3,13 @@
 //
 // The greedy rule is inherently sequential (each cluster's marks constrain
 // the next), so one 1024-thread CTA runs the cluster loop and parallelises
-// inside a cluster: the root scan over the (degree desc, id asc) order, the
-// floor(d/2)-hop ball expansion, and a 4-pass block radix select of the k-1
-// best candidates (rank = position in that order; ranks are unique, so the
-// (k-1)-th smallest rank is an exact threshold).
+// inside a cluster: the root scan over the (degree desc, id asc) order (warp
+// 0, 32 positions per step), the floor(d/2)-hop ball expansion, and the k-1
+// best candidates (rank = position in that order; ranks are unique): up to
+// 1024 candidates each thread counts the candidates ranked before its own,
+// which is its position; beyond that a block radix select of the (k-1)-th
+// smallest rank gives an exact threshold.  About three block barriers per
+// cluster: the loop is barrier-latency bound.
 #include <algorithm>
 
 #include "common.cuh"
@@ -30,66 +33,74 @@ k_select(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cols, co
          uint32_t n, uint32_t r, uint32_t k, uint32_t d, uint32_t policy, uint64_t seed, SelScratch S,
          uint32_t* __restrict__ out_sources, uint8_t* __restrict__ out_sizes, uint32_t* __restrict__ out_count,
          volatile uint32_t* progress) {
-  __shared__ unsigned s_best, s_na, s_nb, s_nc, s_nsel, s_done, s_root;
-  __shared__ unsigned long long s_avail, s_cursor, s_tdraw;
+  __shared__ unsigned s_na, s_nb, s_nc, s_nsel, s_root;
+  __shared__ unsigned long long s_avail;
   __shared__ unsigned hist[256];
   __shared__ unsigned s_need, s_prefix, s_pmask;
   __shared__ unsigned sel[64];
-  const unsigned tid = threadIdx.x;
+  __shared__ unsigned s_cand[SEL_THREADS];  // the first SEL_THREADS candidate ranks (the common case)
+  const unsigned tid = threadIdx.x, lane = tid & 31;
   const uint32_t h = d / 2;
+  const unsigned want = k - 1;
+  const int rank_bits = max(1, 32 - __clz((int)max(n, 2u) - 1));  // ranks < n
   // available = unmarked non-isolated vertices
-  if (tid == 0) { s_avail = 0; s_cursor = 0; s_tdraw = 0; }
+  if (tid == 0) s_avail = 0;
   __syncthreads();
   unsigned long long loc = 0;
   for (uint32_t v = tid; v < n; v += SEL_THREADS) loc += off[v + 1] > off[v];
   atomicAdd(&s_avail, loc);
   __syncthreads();
   uint32_t produced = 0;
+  unsigned long long cursor = 0, tdraw = 0;  // warp 0's root-scan state
+  uint32_t* fa = S.fa;
+  uint32_t* fb = S.fb;
   for (uint32_t c = 0; c < r; ++c) {
-    // ---- root (R12)
-    if (tid == 0) { s_done = 0; s_root = 0xFFFFFFFFu; if (s_avail == 0) s_done = 1; }
-    __syncthreads();
-    if (s_done) break;
-    if (policy == CBFS_ROOT_DEGREE) {
-      for (;;) {
-        if (tid == 0) s_best = 0xFFFFFFFFu;
-        __syncthreads();
-        const unsigned long long p = s_cursor + tid;
-        if (p < n) {
-          const uint32_t x = order[p];
-          if (!S.marked[x] && off[x + 1] > off[x]) atomicMin(&s_best, (unsigned)tid);
-        }
-        __syncthreads();
-        if (s_best != 0xFFFFFFFFu) {
-          if (tid == 0) { s_cursor += s_best; s_root = order[s_cursor]; }
-          __syncthreads();
-          break;
-        }
-        if (tid == 0) s_cursor += SEL_THREADS;
-        __syncthreads();
-        if (s_cursor >= n) break;
-      }
-    } else {
-      if (tid == 0) {
-        for (;;) {
-          const uint32_t v = (uint32_t)bounded(crand(seed, 1, s_tdraw++), n);
-          const uint32_t x = inv ? inv[v] : v;
-          if (!S.marked[x] && off[x + 1] > off[x]) { s_root = x; break; }
-        }
-      }
-      __syncthreads();
-    }
-    if (s_root == 0xFFFFFFFFu) break;
-    const uint32_t root = s_root;
     const uint32_t tag = c + 1;
-    // ---- floor(d/2)-hop ball through all vertices; unmarked ones are candidates (P:1066)
-    if (tid == 0) { s_na = 1; s_nc = 0; S.fa[0] = root; S.stamp[root] = tag; }
+    // ---- root (R12), by warp 0; the ball's first level is set up with it
+    if (tid < 32) {
+      uint32_t root = 0xFFFFFFFFu;
+      if (s_avail != 0) {
+        if (policy == CBFS_ROOT_DEGREE) {
+          while (cursor < n) {  // next unmarked non-isolated vertex in (degree desc, id asc) order
+            const unsigned long long p = cursor + lane;
+            bool ok = false;
+            if (p < n) {
+              const uint32_t x = order[p];
+              ok = !S.marked[x] && off[x + 1] > off[x];
+            }
+            const unsigned m = __ballot_sync(0xFFFFFFFFu, ok);
+            if (m) {
+              cursor += __ffs(m) - 1;
+              root = order[cursor];
+              break;
+            }
+            cursor += 32;
+          }
+        } else if (lane == 0) {
+          for (;;) {
+            const uint32_t v = (uint32_t)bounded(crand(seed, 1, tdraw++), n);
+            const uint32_t x = inv ? inv[v] : v;
+            if (!S.marked[x] && off[x + 1] > off[x]) { root = x; break; }
+          }
+        }
+      }
+      if (lane == 0) {
+        s_root = root;
+        s_na = 1;
+        s_nb = 0;
+        s_nc = 0;
+        s_nsel = 0;
+        if (root != 0xFFFFFFFFu) {
+          fa[0] = root;
+          S.stamp[root] = tag;
+        }
+      }
+    }
     __syncthreads();
-    uint32_t* fa = S.fa;
-    uint32_t* fb = S.fb;
+    const uint32_t root = s_root;
+    if (root == 0xFFFFFFFFu) break;
+    // ---- floor(d/2)-hop ball through all vertices; unmarked ones are candidates (P:1066)
     for (uint32_t lev = 1; lev <= h; ++lev) {
-      if (tid == 0) s_nb = 0;
-      __syncthreads();
       const unsigned na = s_na;
       for (unsigned q = 0; q < na; ++q) {
         const uint32_t u = fa[q];
@@ -98,24 +109,48 @@ k_select(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cols, co
           const uint32_t v = cols[t];
           if (atomicExch(&S.stamp[v], tag) != tag) {
             if (lev < h) fb[atomicAdd(&s_nb, 1u)] = v;
-            if (!S.marked[v]) S.cand[atomicAdd(&s_nc, 1u)] = rank[v];
+            if (!S.marked[v]) {
+              const unsigned ci = atomicAdd(&s_nc, 1u);
+              const unsigned rk = rank[v];
+              S.cand[ci] = rk;
+              if (ci < SEL_THREADS) s_cand[ci] = rk;
+            }
           }
         }
       }
-      __syncthreads();
-      if (tid == 0) s_na = s_nb;
       uint32_t* tmp = fa; fa = fb; fb = tmp;
       __syncthreads();
+      if (lev < h) {
+        if (tid == 0) { s_na = s_nb; s_nb = 0; }
+        __syncthreads();
+      }
     }
-    // ---- best k-1 candidates by rank (degree desc, id asc)
+    // ---- the best k-1 candidates by rank (degree desc, id asc), in rank order
     const unsigned nc = s_nc;
-    const unsigned want = k - 1;
-    if (tid == 0) { s_nsel = 0; s_need = want; s_prefix = 0; s_pmask = 0; }
-    __syncthreads();
-    unsigned thr = 0xFFFFFFFFu;
-    if (want > 0 && nc > want) {
-      for (int pass = 0; pass < 4; ++pass) {
-        const int shift = 24 - 8 * pass;
+    const unsigned ns = min(nc, want);
+    uint32_t* outS = out_sources + (uint64_t)c * 64;
+    unsigned long long dec = 0;
+    if (nc <= SEL_THREADS) {
+      // rank by counting (ranks are unique): candidate t is selected iff fewer
+      // than `want` candidates precede it, and that count is its position
+      if (tid < nc) {
+        const unsigned rk = s_cand[tid];
+        unsigned pos = 0;
+        for (unsigned j = 0; j < nc && pos < want; ++j) pos += s_cand[j] < rk;
+        if (pos < want) {
+          const uint32_t x = order[rk];
+          outS[1 + pos] = perm ? perm[x] : x;
+          S.marked[x] = 1;
+          dec += off[x + 1] > off[x];
+        }
+      }
+    } else {
+      // radix select of the want-th smallest rank (8-bit digits over the rank bits)
+      if (tid == 0) { s_need = want; s_prefix = 0; s_pmask = 0; }
+      __syncthreads();
+      const int passes = (rank_bits + 7) / 8;
+      for (int pass = 0; pass < passes; ++pass) {
+        const int shift = 8 * (passes - 1 - pass);
         for (unsigned b = tid; b < 256; b += SEL_THREADS) hist[b] = 0;
         __syncthreads();
         const unsigned pre = s_prefix, pm = s_pmask;
@@ -125,9 +160,9 @@ k_select(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cols, co
         }
         __syncthreads();
         if (tid < 32) {  // the bucket holding the need-th smallest: warp prefix over 8 buckets per lane
-          unsigned loc[8], sum = 0;
+          unsigned lc[8], sum = 0;
 #pragma unroll
-          for (int q = 0; q < 8; ++q) { loc[q] = hist[tid * 8 + q]; sum += loc[q]; }
+          for (int q = 0; q < 8; ++q) { lc[q] = hist[tid * 8 + q]; sum += lc[q]; }
           unsigned incl = sum;
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
@@ -135,14 +170,13 @@ k_select(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cols, co
             if (tid >= (unsigned)o) incl += y;
           }
           const unsigned need = s_need;
-          unsigned cum = incl - sum;  // buckets before this lane's
-          const bool mine = cum < need && incl >= need;
-          if (mine) {
+          unsigned cum = incl - sum;
+          if (cum < need && incl >= need) {
             unsigned b = tid * 8;
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-              if (cum + loc[q] >= need) { b = tid * 8 + q; break; }
-              cum += loc[q];
+              if (cum + lc[q] >= need) { b = tid * 8 + q; break; }
+              cum += lc[q];
             }
             s_need = need - cum;
             s_prefix = pre | (b << shift);
@@ -151,35 +185,24 @@ k_select(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cols, co
         }
         __syncthreads();
       }
-      thr = s_prefix;  // the want-th smallest rank
-    }
-    if (want > 0) {
+      const unsigned thr = s_prefix;  // the want-th smallest rank
       for (unsigned t = tid; t < nc; t += SEL_THREADS) {
         const unsigned rk = S.cand[t];
         if (rk <= thr) sel[atomicAdd(&s_nsel, 1u)] = rk;
       }
-    }
-    __syncthreads();
-    const unsigned ns = s_nsel;
-    // order the selected members by rank; write the cluster in original ids
-    uint32_t* outS = out_sources + (uint64_t)c * 64;
-    if (tid < 64) {
-      uint32_t val = 0xFFFFFFFFu;
-      if (tid == 0) val = perm ? perm[root] : root;
-      outS[tid] = val;
-    }
-    __syncthreads();
-    unsigned long long dec = 0;
-    if (tid < ns) {
-      const unsigned rk = sel[tid];
-      unsigned pos = 0;
-      for (unsigned j = 0; j < ns; ++j) pos += sel[j] < rk;
-      const uint32_t x = order[rk];
-      outS[1 + pos] = perm ? perm[x] : x;
-      S.marked[x] = 1;
-      dec += off[x + 1] > off[x];
+      __syncthreads();
+      if (tid < ns) {
+        const unsigned rk = sel[tid];
+        unsigned pos = 0;
+        for (unsigned j = 0; j < ns; ++j) pos += sel[j] < rk;
+        const uint32_t x = order[rk];
+        outS[1 + pos] = perm ? perm[x] : x;
+        S.marked[x] = 1;
+        dec += off[x + 1] > off[x];
+      }
     }
     if (tid == 0) {
+      outS[0] = perm ? perm[root] : root;
       S.marked[root] = 1;
       dec += 1;  // root is non-isolated
       out_sizes[c] = (uint8_t)(1 + ns);

@@ -30,9 +30,10 @@ def _worker(rank, world, port, out):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     mx = bench.allreduce_max(float(10 + rank), world)
     sm = bench.allreduce_sum(float(1 + rank), world)
-    total, first = bench.shard(1024, world, rank)
+    total, first, mine = bench.shard(1024, world, rank)
+    wtotal, wfirst, wmine = bench.shard(1024, world, rank, strong=False)
     bench.barrier(world)
-    out.put((rank, mx, sm, total, first))
+    out.put((rank, mx, sm, total, first, mine, wtotal, wmine))
     dist.destroy_process_group()
 
 
@@ -48,8 +49,9 @@ def test_gloo_reductions_and_shards():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    assert res[0][1:] == (11.0, 3.0, 2048, 0)
-    assert res[1][1:] == (11.0, 3.0, 2048, 1)  # round-robin: rank 1 owns clusters 1, 3, 5, ...
+    # round-robin: rank 1 owns clusters 1, 3, 5, ... of the config's 1,024 (strong) or of 2,048 (weak)
+    assert res[0][1:] == (11.0, 3.0, 1024, 0, 512, 2048, 1024)
+    assert res[1][1:] == (11.0, 3.0, 1024, 1, 512, 2048, 1024)
 
 
 def test_reference_arm_under_torchrun():

@@ -1,4 +1,4 @@
-"""Predicted weak-scaling step time: one GPU doing rank (world-1)'s share of a
+"""Predicted scaling step time: one GPU doing rank (world-1)'s share of a
 world x 1,024-cluster C2 step (graph build + overlapped selection + its
 clusters' C-BFS) -- what every GPU of a world-rank run does, with no
 inter-rank waiting in the data path."""
@@ -13,8 +13,9 @@ st = torch.cuda.current_stream()
 C = 1024
 dist = torch.empty((n, C), dtype=torch.uint8, device="cuda"); masks = torch.empty((d + 1, n, C), dtype=torch.int64, device="cuda")
 stats = torch.zeros((C, 4), dtype=torch.int64, device="cuda")
+strong = (sys.argv[1] if len(sys.argv) > 1 else "strong") == "strong"
 for world in (1, 2, 4, 8):
-    r = C * world
+    r = C if strong else C * world
     src = torch.empty((r, 64), dtype=torch.int32, device="cuda"); sz = torch.empty((r,), dtype=torch.uint8, device="cuda")
     times = []
     for rep in range(4):
@@ -29,4 +30,8 @@ for world in (1, 2, 4, 8):
         cb.cbfs_graph_destroy(h)
         if rep: times.append((e0.elapsed_time(e1), e1.elapsed_time(e2)))
     b, s = np.mean(times, axis=0)
-    print(f"world {world}: build {b:.1f} ms, select+C-BFS {s:.1f} ms, step {b + s:.1f} ms", flush=True)
+    Cr = len(range(world - 1, r, world))
+    st_np = stats[:Cr].cpu().numpy()
+    units = float((sz[world - 1::world][:Cr].cpu().numpy().astype(np.float64) * st_np[:, 3]).sum())
+    print(f"{'strong' if strong else 'weak'} world {world}: build {b:.1f} ms, select+C-BFS {s:.1f} ms, "
+          f"step {b + s:.1f} ms, rank units/s {units / ((b + s) / 1e3):.3e}", flush=True)
