@@ -440,6 +440,40 @@ extern "C" int cbfs_debug_read(unsigned long long* out) {
 struct U2 {
   uint64_t a, b;
 };
+
+// ---- TMA (cp.async.bulk) row staging for the dense pull's gathers (build
+// with -DCBFS_PULL_TMA=1).  Measured on config 2: the step takes 75 ms with
+// 8 rows staged per bulk batch and 82 ms with 16, against 68.8 ms for the
+// default 16-byte-per-lane register gathers (8 rows in flight per warp): one
+// lane issuing 512-byte bulk copies and the mbarrier round trip add latency
+// to a loop that is latency-bound already.  Off by default; parity-tested.
+#ifndef CBFS_PULL_TMA
+#define CBFS_PULL_TMA 0
+#endif
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 __device__ __forceinline__ U2 ld2(const uint64_t* p) {
   const ulonglong2 x = __ldg(reinterpret_cast<const ulonglong2*>(p));
   return {x.x, x.y};
@@ -454,6 +488,14 @@ __global__ void __launch_bounds__(PULL_WARPS * 32, CBFS_PULL_MINB) k_pull(
   __shared__ uint32_t s_list[PULL_WARPS][PULL_CHUNK + 32];
   __shared__ uint32_t s_cnt[PULL_WARPS][32];
   __shared__ unsigned long long s_stat[PULL_WARPS][3][LANES];  // per-warp F / E / M per cluster
+#if CBFS_PULL_TMA
+  __shared__ __align__(128) ulonglong2 s_rows[PULL_WARPS][PULL_MLP][LANES / 2];  // staged neighbour rows
+  __shared__ __align__(8) uint64_t s_bar[PULL_WARPS];
+  uint32_t tma_phase = 0;
+  if (lane_id() == 0) mbar_init(&s_bar[threadIdx.x >> 5], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+#endif
   const uint32_t lane = lane_id();
   const uint32_t wib = threadIdx.x >> 5;
   uint32_t* list = s_list[wib];
@@ -567,6 +609,26 @@ __global__ void __launch_bounds__(PULL_WARPS * 32, CBFS_PULL_MINB) k_pull(
           const bool k0 = (cap0 >> j) & 1u, k1 = (cap1 >> j) & 1u;
           uint64_t acc0 = 0, acc1 = 0;
           for (uint32_t q = s0; q < s1; q += PULL_MLP) {
+#if CBFS_PULL_TMA
+            // one lane stages up to PULL_MLP neighbour rows (512 B each) into
+            // shared memory with bulk copies; the warp ORs them from there
+            const uint32_t nr = min((uint32_t)PULL_MLP, s1 - q);
+            ulonglong2(*rows_s)[LANES / 2] = s_rows[wib];
+            if (lane == 0) {
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of the buffer
+              mbar_expect_tx(&s_bar[wib], nr * LANES * 8);
+              for (uint32_t r = 0; r < nr; ++r)
+                bulk_g2s(rows_s[r], seen + (uint64_t)list[q + r] * LANES, LANES * 8, &s_bar[wib]);
+            }
+            mbar_wait(&s_bar[wib], tma_phase);
+            tma_phase ^= 1;
+            for (uint32_t r = 0; r < nr; ++r) {
+              const ulonglong2 y = rows_s[r][lane];
+              acc0 |= y.x;
+              acc1 |= y.y;
+            }
+            __syncwarp();
+#else
             U2 g[PULL_MLP];
 #pragma unroll
             for (int r = 0; r < PULL_MLP; ++r) {
@@ -576,6 +638,7 @@ __global__ void __launch_bounds__(PULL_WARPS * 32, CBFS_PULL_MINB) k_pull(
             }
 #pragma unroll
             for (int r = 0; r < PULL_MLP; ++r) { acc0 |= g[r].a; acc1 |= g[r].b; }
+#endif
             // R7: stop once every capped lane holds its full subset
             if (q + PULL_MLP < s1 &&
                 !__ballot_sync(FULLW, (k0 && ((acc0 | sv.a) & full0) != full0) ||
