@@ -12,7 +12,7 @@ def create():
     torch.cuda.synchronize(); t0 = time.perf_counter()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
-    h = cb.cbfs_graph_create(n, src_d, dst_d, 0, 0, st)
+    h = cb.cbfs_graph_create(n, src_d, dst_d, int(sys.argv[2]) if len(sys.argv) > 2 else 0, 0, st)
     e1.record(st); torch.cuda.synchronize()
     print(f"create: host {1000*(time.perf_counter()-t0):.1f} ms, events {e0.elapsed_time(e1):.1f} ms", flush=True)
     return h
