@@ -210,7 +210,8 @@ int cbfs_decode(uint32_t n, uint32_t C, uint32_t d, uint32_t planes, const void*
  *          Delta_s + Delta_t + min{ i+j : S_s[i] & S_t[j] != 0 },
  * min-merged into inout_best[q] (initialise to CBFS_QUERY_UNREACHED).
  *   n, C, d, planes, dist, dist_bytes, masks : a label store in the
- *         cbfs_run layout (planes = d or d+1)
+ *         cbfs_run layout (planes = d or d+1; planes = d = 0 with a null
+ *         masks is a plain landmark store of single-source clusters)
  *   sizes : device [C] uint8 (needed for S_v[d] = FULL & ~U when planes == d)
  *   s, t  : device [q] uint32 original ids;  inout_best : device [q] int32
  * Errors: EINVAL (null pointers, planes not d or d+1).  Ids >= n: the
@@ -234,6 +235,16 @@ int cbfs_query_stream(cbfs_graph* g, const uint32_t* sources, const uint8_t* siz
  * S_v[0..d-1], R14; d = 0 keeps S_v[0]) into a library-owned device image.
  *   sources, sizes : as cbfs_run (device);  dist_bytes : 1 or 2
  * Errors: as cbfs_run, ENOMEM.  Synchronises.
+ * cbfs_labels_build_w — the same with the store's word size w = word_bits
+ *   (8, 16, 32 or 64; the paper's w, P:1447 and Tables 4/8 at P:1379-1414 and
+ *   P:1821-1848): each bit-subset is stored in w bits, so a record is
+ *   dist_bytes + d * w / 8 bytes (3 B at w = 8, d = 2, u8 Delta; 17 B at
+ *   w = 64).  Every cluster must have <= w sources (EINVAL otherwise; sizes
+ *   are read back to the host for that check).  word_bits = 0 is the
+ *   paper's plain landmark labeling: d = 0 and single-source
+ *   clusters (EINVAL otherwise), records are Delta alone.  cbfs_labels_build
+ *   is w = 64.
+ * cbfs_labels_word_bits — the store's w.
  * cbfs_labels_info — n, clusters, d, dist_bytes and the image size in bytes.
  * cbfs_labels_export — copy the flat image (64-byte header, sizes, Delta
  *   rows, subset planes) to buf (device or host, >= image bytes): the unit
@@ -246,6 +257,9 @@ int cbfs_query_stream(cbfs_graph* g, const uint32_t* sources, const uint8_t* siz
  * cbfs_labels_destroy — free the handle. */
 int cbfs_labels_build(cbfs_graph* g, const uint32_t* sources, const uint8_t* sizes, uint32_t n_clusters, uint32_t d,
                       uint32_t dist_bytes, cbfs_labels** out, cbfs_stream stream);
+int cbfs_labels_build_w(cbfs_graph* g, const uint32_t* sources, const uint8_t* sizes, uint32_t n_clusters,
+                        uint32_t d, uint32_t dist_bytes, uint32_t word_bits, cbfs_labels** out, cbfs_stream stream);
+int cbfs_labels_word_bits(const cbfs_labels* l, uint32_t* word_bits);
 int cbfs_labels_info(const cbfs_labels* l, uint32_t* n, uint32_t* n_clusters, uint32_t* d, uint32_t* dist_bytes,
                      uint64_t* image_bytes);
 int cbfs_labels_export(const cbfs_labels* l, void* buf, uint64_t bytes);

@@ -61,6 +61,8 @@ _sig("cbfs_query_distance", [_u32, _u32, _u32, _u32, _vp, _u32, _vp, _vp, _vp, _
 _sig("cbfs_query_stream", [_vp, _vp, _vp, _u32, _u32, _vp, _vp, _u64, _vp, _vp, _vp])
 _sig("cbfs_query_bidir", [_vp, _vp, _vp, _u64, _u32, _vp, _vp])
 _sig("cbfs_labels_build", [_vp, _vp, _vp, _u32, _u32, _u32, ctypes.POINTER(_vp), _vp])
+_sig("cbfs_labels_build_w", [_vp, _vp, _vp, _u32, _u32, _u32, _u32, ctypes.POINTER(_vp), _vp])
+_sig("cbfs_labels_word_bits", [_vp, ctypes.POINTER(_u32)])
 _sig("cbfs_labels_info", [_vp, ctypes.POINTER(_u32), ctypes.POINTER(_u32), ctypes.POINTER(_u32), ctypes.POINTER(_u32),
                           ctypes.POINTER(_u64)])
 _sig("cbfs_labels_export", [_vp, _vp, _u64])
@@ -203,18 +205,24 @@ def cbfs_query_bidir(h, s, t, tau, inout_best, stream=None):
     _check(_lib.cbfs_query_bidir(h, _ptr(s), _ptr(t), len(s), tau, _ptr(inout_best), _stream(stream)))
 
 
-def cbfs_labels_build(g, sources, sizes, n_clusters, d, dist_bytes=2, stream=None):
+def cbfs_labels_build(g, sources, sizes, n_clusters, d, dist_bytes=2, stream=None, word_bits=64):
     h = _vp()
-    _check(_lib.cbfs_labels_build(g, _ptr(sources), _ptr(sizes), n_clusters, d, dist_bytes, ctypes.byref(h),
-                                  _stream(stream)))
+    if word_bits == 64:
+        _check(_lib.cbfs_labels_build(g, _ptr(sources), _ptr(sizes), n_clusters, d, dist_bytes, ctypes.byref(h),
+                                      _stream(stream)))
+    else:
+        _check(_lib.cbfs_labels_build_w(g, _ptr(sources), _ptr(sizes), n_clusters, d, dist_bytes, word_bits,
+                                        ctypes.byref(h), _stream(stream)))
     return h
 
 
 def cbfs_labels_info(lh):
-    n, C, d, db, b = _u32(), _u32(), _u32(), _u32(), _u64()
+    n, C, d, db, b, w = _u32(), _u32(), _u32(), _u32(), _u64(), _u32()
     _check(_lib.cbfs_labels_info(lh, ctypes.byref(n), ctypes.byref(C), ctypes.byref(d), ctypes.byref(db),
                                  ctypes.byref(b)))
-    return dict(n=n.value, clusters=C.value, d=d.value, dist_bytes=db.value, image_bytes=b.value)
+    _check(_lib.cbfs_labels_word_bits(lh, ctypes.byref(w)))
+    return dict(n=n.value, clusters=C.value, d=d.value, dist_bytes=db.value, image_bytes=b.value,
+                word_bits=w.value)
 
 
 def cbfs_labels_export(lh, buf):

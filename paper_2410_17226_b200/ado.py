@@ -9,8 +9,9 @@ psi = query / delta, reported as epsilon = mean(psi) - 1 (P:1031-1034) over
 sampled pairs (100,000 pairs, 10,000 on the largest graphs).
 
 Everything here drives the C-ABI (argument marshalling only): the index is
-`cbfs_select_clusters` + `cbfs_run(planes = d)` (R14 records), the answers
-come from `cbfs_query_distance`, and the exact distances of the sampled pairs
+`cbfs_select_clusters` + `cbfs_labels_build_w` (R14 records in a store of
+word size w), the answers come from `cbfs_labels_query`, and the
+exact distances of the sampled pairs
 from C-BFS itself: a cluster of one source with d = 0 is a plain BFS
 (R3), so each batch of 64 single-source "clusters" yields the true
 distances from 64 sampled sources at once.
@@ -20,41 +21,69 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from . import (CBFS_QUERY_UNREACHED, CBFS_ROOT_DEGREE, cbfs_query_bidir, cbfs_query_distance, cbfs_run,
-               cbfs_select_clusters)
+from . import (CBFS_QUERY_UNREACHED, CBFS_ROOT_DEGREE, cbfs_labels_build, cbfs_labels_destroy, cbfs_labels_info,
+               cbfs_labels_query, cbfs_query_bidir, cbfs_run, cbfs_select_clusters)
 
 UNREACHED16 = 0xFFFF
 
 
-class LandmarkIndex:
-    """Labels of r clusters (k <= 64 sources, diameter bound d) in the
-    cbfs_run layout: dist [n][r] u16, masks [d][n][r] (S_v[0..d-1], R14)."""
+def record_bytes(word_bits: int, d: int, dist_bytes: int = 1) -> int:
+    """Bytes of one (cluster, vertex) record: Delta + d bit-subsets of w bits
+    (P:1446-1447: 17 B at w = 64, d = 2; 3 B at w = 8); d = 0 keeps S_v[0];
+    w = 0 is a plain landmark (Delta alone)."""
+    return dist_bytes + (max(d, 1) * word_bits // 8 if word_bits else 0)
 
-    def __init__(self, graph, r: int, k: int = 64, d: int = 2, root_policy: int = CBFS_ROOT_DEGREE, seed: int = 0):
+
+def clusters_for_budget(t_bytes: int, word_bits: int, d: int, dist_bytes: int = 1) -> int:
+    """Clusters whose records fit t bytes per vertex."""
+    return t_bytes // record_bytes(word_bits, d, dist_bytes)
+
+
+class LandmarkIndex:
+    """Labels of r clusters (k <= w sources, diameter bound d) in a label
+    store of word size w = word_bits (cbfs_labels_build_w): per vertex and
+    cluster Delta (dist_bytes) + S_v[0..d-1] in w-bit words (R14)."""
+
+    def __init__(self, graph, r: int, k: int = 64, d: int = 2, root_policy: int = CBFS_ROOT_DEGREE, seed: int = 0,
+                 word_bits: int = 64, dist_bytes: int = 2):
+        """word_bits = 0: plain landmark labeling (k = 1, d = 0: r single
+        vertices by the same selection rule, 1-2 byte records)."""
+        if not 1 <= k <= max(word_bits, 1) or (word_bits == 0 and d != 0):
+            raise ValueError("cluster size k must be 1..word_bits (plain landmarks: k = 1, d = 0)")
         dev = f"cuda:{graph.device}"
         src = torch.empty((max(r, 1), 64), dtype=torch.int32, device=dev)
         sz = torch.empty((max(r, 1),), dtype=torch.uint8, device=dev)
-        got = cbfs_select_clusters(graph.h, r, k, d, root_policy, seed, src, sz)
-        self.graph, self.d, self.r = graph, d, got
-        self.planes = d if d > 0 else 1
+        got = cbfs_select_clusters(graph.h, r, k, d, root_policy, seed, src, sz) if r else 0
+        self.graph, self.d, self.r, self.word_bits, self.dist_bytes = graph, d, got, word_bits, dist_bytes
         self.sources, self.sizes = src[:got].contiguous(), sz[:got].contiguous()
-        n = graph.n
-        self.dist = torch.empty((n, max(got, 1)), dtype=torch.int16, device=dev)
-        self.masks = torch.empty((self.planes, n, max(got, 1)), dtype=torch.int64, device=dev)
-        if got:
-            cbfs_run(graph.h, self.sources, self.sizes, got, d, 2, self.dist, self.masks, self.planes, None)
+        self.labels = cbfs_labels_build(graph.h, self.sources, self.sizes, got, d, dist_bytes,
+                                        word_bits=word_bits) if got else None
+
+    @property
+    def image_bytes(self) -> int:
+        return cbfs_labels_info(self.labels)["image_bytes"] if self.labels else 0
 
     def query(self, s: torch.Tensor, t: torch.Tensor, tau: int = 0) -> torch.Tensor:
         """int32 answers, CBFS_QUERY_UNREACHED where no cluster reaches both
         ends; tau > 0 adds the Appendix B bi-directional search:
         the answer is the minimum of the index's and the search's."""
         best = torch.full((int(s.shape[0]),), CBFS_QUERY_UNREACHED, dtype=torch.int32, device=s.device)
-        if self.r:
-            cbfs_query_distance(self.graph.n, self.r, self.d, self.planes, self.dist, 2, self.masks, self.sizes,
-                                s, t, best)
+        if self.labels:
+            cbfs_labels_query(self.labels, s, t, best)
         if tau:
             cbfs_query_bidir(self.graph.h, s, t, tau, best)
         return best
+
+    def close(self):
+        if self.labels:
+            cbfs_labels_destroy(self.labels)
+            self.labels = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def exact_distances(graph, s: np.ndarray, t: np.ndarray) -> np.ndarray:

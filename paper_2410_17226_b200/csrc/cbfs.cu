@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(256) k_fold(const uint32_t* __restrict__ F, ui
                                               uint16_t* __restrict__ dist, const uint64_t* __restrict__ off,
                                               const uint32_t* __restrict__ perm, uint32_t n, uint32_t C,
                                               uint32_t cbase, uint32_t planes, void* __restrict__ out_dist,
-                                              uint64_t* __restrict__ out_masks, uint64_t* __restrict__ pre,
+                                              void* __restrict__ out_masks, uint32_t mb, uint64_t* __restrict__ pre,
                                               int write_pre, const uint8_t* __restrict__ sizes,
                                               uint64_t* __restrict__ fullm, unsigned long long* __restrict__ ctr) {
   const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(256) k_fold(const uint32_t* __restrict__ F, ui
         }
       }
       const uint32_t oi = i - dv[q];
-      if (out_masks && oi < planes) out_masks[(uint64_t)oi * n * C + col] = nw[q];
+      if (out_masks && oi < planes) store_mask(out_masks, (uint64_t)oi * n * C + col, nw[q], mb);
     }
     // per-vertex "subset full" bits (read by the dense pull instead of the
     // whole S_seen row): one 64-bit atomic per distinct vertex in the warp
@@ -769,11 +769,11 @@ static int slot_round(Graph* g, Slot* w) {
   if (g_prof.on) CBFS_CUDA(cudaEventRecord(w->pe[0], st));
   if (a.dist_bytes == 1)
     k_fold<1><<<fb, 256, 0, st>>>(w->cur, (uint32_t)nF, i, w->seen, w->pend, w->dist, g->off, a.out_internal ? nullptr : g->perm, n, a.C,
-                                  a.cbase, a.planes, a.out_dist, a.out_masks, w->pre, write_pre, a.sizes, w->fullm,
+                                  a.cbase, a.planes, a.out_dist, a.out_masks, a.mask_bytes, w->pre, write_pre, a.sizes, w->fullm,
                                   w->ctr);
   else
     k_fold<2><<<fb, 256, 0, st>>>(w->cur, (uint32_t)nF, i, w->seen, w->pend, w->dist, g->off, a.out_internal ? nullptr : g->perm, n, a.C,
-                                  a.cbase, a.planes, a.out_dist, a.out_masks, w->pre, write_pre, a.sizes, w->fullm,
+                                  a.cbase, a.planes, a.out_dist, a.out_masks, a.mask_bytes, w->pre, write_pre, a.sizes, w->fullm,
                                   w->ctr);
   CBFS_LAUNCHED();
   if (g_prof.on) CBFS_CUDA(cudaEventRecord(w->pe[1], st));
@@ -983,25 +983,19 @@ int check_run_args(const Graph* g, const void* sources, const void* sizes, uint3
   return CBFS_OK;
 }
 
-}  // namespace cbfs
-
-using namespace cbfs;
-
-extern "C" {
-
-int cbfs_run(cbfs_graph* gh, const uint32_t* sources, const uint8_t* sizes, uint32_t n_clusters, uint32_t d,
-             uint32_t dist_bytes, void* out_dist, uint64_t* out_masks, uint32_t planes, uint64_t* out_stats,
-             uint32_t direction, cbfs_stream stream) {
-  Graph* g = reinterpret_cast<Graph*>(gh);
+int run_arrays(Graph* g, const uint32_t* sources, const uint8_t* sizes, uint32_t n_clusters, uint32_t d,
+               uint32_t dist_bytes, void* out_dist, void* out_masks, uint32_t mask_bytes, uint32_t planes,
+               uint64_t* out_stats, uint32_t direction, cudaStream_t st) {
   int rc = check_run_args(g, sources, sizes, n_clusters, d, dist_bytes, planes, direction);
   if (rc) return rc;
+  if (mask_bytes != 1 && mask_bytes != 2 && mask_bytes != 4 && mask_bytes != 8)
+    return fail(CBFS_EINVAL, "mask word must be 1, 2, 4 or 8 bytes");
   CBFS_CUDA(cudaSetDevice(g->device));
-  cudaStream_t st = (cudaStream_t)stream;
   WorkLease lease(g);
   if (lease.rc) return lease.rc;
   const uint64_t C = n_clusters;
   if (out_dist) CBFS_CUDA(cudaMemsetAsync(out_dist, 0xFF, (uint64_t)g->n * C * dist_bytes, st));
-  if (out_masks) CBFS_CUDA(cudaMemsetAsync(out_masks, 0, (uint64_t)planes * g->n * C * sizeof(uint64_t), st));
+  if (out_masks) CBFS_CUDA(cudaMemsetAsync(out_masks, 0, (uint64_t)planes * g->n * C * mask_bytes, st));
   ArraySource src;
   src.proto = RunArgs{};
   src.proto.d = d;
@@ -1013,6 +1007,7 @@ int cbfs_run(cbfs_graph* gh, const uint32_t* sources, const uint8_t* sizes, uint
   if (src.proto.engine < 0) return CBFS_ECUDA;
   src.proto.out_dist = out_dist;
   src.proto.out_masks = out_masks;
+  src.proto.mask_bytes = mask_bytes;
   src.sources = sources;
   src.sizes = sizes;
   src.n_clusters = n_clusters;
@@ -1021,6 +1016,18 @@ int cbfs_run(cbfs_graph* gh, const uint32_t* sources, const uint8_t* sizes, uint
   if (rc) return rc;
   CBFS_CUDA(cudaStreamSynchronize(st));
   return CBFS_OK;
+}
+}  // namespace cbfs
+
+using namespace cbfs;
+
+extern "C" {
+
+int cbfs_run(cbfs_graph* gh, const uint32_t* sources, const uint8_t* sizes, uint32_t n_clusters, uint32_t d,
+             uint32_t dist_bytes, void* out_dist, uint64_t* out_masks, uint32_t planes, uint64_t* out_stats,
+             uint32_t direction, cbfs_stream stream) {
+  return run_arrays(reinterpret_cast<Graph*>(gh), sources, sizes, n_clusters, d, dist_bytes, out_dist, out_masks, 8,
+                    planes, out_stats, direction, (cudaStream_t)stream);
 }
 
 // A1 overlapped with A2-A8: the selection CTA runs on a side stream and

@@ -86,8 +86,9 @@ struct RunArgs {
   int engine;               // ENGINE_BATCHED / ENGINE_SPARSE (engine.cuh)
   int out_internal;         // output rows are internal ids (library-internal staging), not original ids
   void* out_dist;           // device [n][C] or null
-  uint64_t* out_masks;      // device [planes][n][C] or null
+  void* out_masks;          // device [planes][n][C] words of mask_bytes, or null
   uint64_t* out_stats;      // device [nb][4] or null
+  uint32_t mask_bytes;      // 8 (cbfs_run) or 1/2/4 (packed label stores, w = 8 * mask_bytes; 0 reads as 8)
 };
 // A producer of batches for run_batches (several batches run concurrently,
 // one per workspace slot, each on its own stream).
@@ -116,6 +117,14 @@ int select_launch(const Graph* g, uint32_t r, uint32_t k, uint32_t d, uint32_t r
                   cudaStream_t st);
 int check_select_args(const Graph* g, uint32_t r, uint32_t k, uint32_t d, uint32_t root_policy,
                       const void* out_sources, const void* out_sizes);
+// cbfs_run with the output bit-subset words mask_bytes wide (1/2/4/8)
+int run_arrays(Graph* g, const uint32_t* sources, const uint8_t* sizes, uint32_t n_clusters, uint32_t d,
+               uint32_t dist_bytes, void* out_dist, void* out_masks, uint32_t mask_bytes, uint32_t planes,
+               uint64_t* out_stats, uint32_t direction, cudaStream_t st);
+// cbfs_query_distance over a store whose bit-subset words are mask_bytes wide
+int query_store(uint32_t n, uint32_t C, uint32_t d, uint32_t planes, const void* dist, uint32_t dist_bytes,
+                const void* masks, uint32_t mask_bytes, const uint8_t* sizes, const uint32_t* s, const uint32_t* t,
+                uint64_t q, int32_t* inout_best, cudaStream_t st);
 int check_run_args(const Graph* g, const void* sources, const void* sizes, uint32_t n_clusters, uint32_t d,
                    uint32_t dist_bytes, uint32_t planes, uint32_t direction);
 
@@ -137,6 +146,17 @@ __host__ __device__ inline uint64_t bounded(uint64_t x, uint64_t n) {
 #else
   return (uint64_t)(((unsigned __int128)x * n) >> 64);
 #endif
+}
+
+// one output bit-subset word: a full u64, or the low 8/16/32 bits of a packed
+// w-bit label store (the cluster has <= w sources, so nothing is dropped)
+__device__ __forceinline__ void store_mask(void* p, uint64_t idx, uint64_t v, uint32_t mb) {
+  switch (mb) {
+    case 1: ((uint8_t*)p)[idx] = (uint8_t)v; break;
+    case 2: ((uint16_t*)p)[idx] = (uint16_t)v; break;
+    case 4: ((uint32_t*)p)[idx] = (uint32_t)v; break;
+    default: ((uint64_t*)p)[idx] = v; break;
+  }
 }
 
 __host__ __device__ inline uint64_t full_mask(uint32_t k) { return k >= 64 ? ~0ULL : ((1ULL << k) - 1); }

@@ -51,9 +51,9 @@ struct SpDesc {
   const uint32_t* sources;   // [nb][64]
   const uint8_t* sizes;      // [nb]
   void* out_dist;            // [n][C] or null
-  uint64_t* out_masks;       // [planes][n][C] or null
+  void* out_masks;           // [planes][n][C] words of mask_bytes, or null
   uint64_t C, cbase;
-  uint32_t n, nb, d, planes, dist_bytes, pad;
+  uint32_t n, nb, d, planes, dist_bytes, mask_bytes;
 };
 // Round state of a sparse-engine batch (device-resident).
 struct SpCtl {

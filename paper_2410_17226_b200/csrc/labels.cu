@@ -4,13 +4,21 @@
 // (P:1013-1021), and move it between ranks as one flat byte
 // image (export / import: the unit the NCCL all-gather of A12 moves).
 //
+// The store's word size w (Tables 4/8: w = 64, 32, 16, 8) is the
+// width of one bit-subset: clusters hold at most w sources, and a record
+// (c, v) is Delta (dist_bytes) + d words of w/8 bytes — 17 B at w = 64, d = 2
+// (u8 Delta), 3 B at w = 8.  The traversal itself always runs on 64-bit
+// subsets; its output writes store the low w bits (all that a cluster of
+// <= w sources can set).
+//
 // Image layout (one device allocation, the handle's own storage):
-//   [0, 64)            header {magic "CBFSLBL1", version, n, C, d, planes,
-//                      dist_bytes, total bytes}
+//   [0, 64)            header {magic "CBFSLBL1", version 2, n, C, d, planes,
+//                      dist_bytes, total bytes, word_bits}
 //   sizes  [C]         u8 cluster sizes            (padded to 16 bytes)
 //   dist   [n][C]      Delta, dist_bytes each       (padded to 16 bytes)
-//   masks  [planes][n][C] u64 bit-subsets S_v[0..planes-1]
+//   masks  [planes][n][C] w-bit bit-subsets S_v[0..planes-1]
 #include <cstring>
+#include <vector>
 
 #include "common.cuh"
 
@@ -20,7 +28,8 @@ struct LabelHeader {
   char magic[8];
   uint32_t version, n, C, d, planes, dist_bytes;
   uint64_t bytes;
-  uint8_t pad[64 - 8 - 6 * 4 - 8];
+  uint32_t word_bits;
+  uint8_t pad[64 - 8 - 6 * 4 - 8 - 4];
 };
 static_assert(sizeof(LabelHeader) == 64, "64-byte header");
 
@@ -30,26 +39,29 @@ struct Labels {
   uint8_t* blob = nullptr;  // device image
   uint8_t* sizes() const { return blob + 64; }
   void* dist() const { return blob + 64 + pad16(h.C); }
-  uint64_t* masks() const {
-    return reinterpret_cast<uint64_t*>(blob + 64 + pad16(h.C) + pad16((uint64_t)h.n * h.C * h.dist_bytes));
-  }
+  void* masks() const { return blob + 64 + pad16(h.C) + pad16((uint64_t)h.n * h.C * h.dist_bytes); }
   static uint64_t pad16(uint64_t x) { return (x + 15) & ~15ull; }
 };
 
-static uint64_t image_bytes(uint32_t n, uint32_t C, uint32_t planes, uint32_t dist_bytes) {
-  return 64 + Labels::pad16(C) + Labels::pad16((uint64_t)n * C * dist_bytes) + (uint64_t)planes * n * C * 8;
+static uint64_t image_bytes(uint32_t n, uint32_t C, uint32_t planes, uint32_t dist_bytes, uint32_t word_bits) {
+  return 64 + Labels::pad16(C) + Labels::pad16((uint64_t)n * C * dist_bytes) + (uint64_t)planes * n * C * (word_bits / 8);
 }
 
-static void make_header(LabelHeader& h, uint32_t n, uint32_t C, uint32_t d, uint32_t dist_bytes) {
+// w = 0: plain landmarks (the paper's "Plain" LL): d = 0 and
+// single-source clusters, records are Delta alone (no subset planes)
+static bool word_ok(uint32_t w) { return w == 0 || w == 8 || w == 16 || w == 32 || w == 64; }
+
+static void make_header(LabelHeader& h, uint32_t n, uint32_t C, uint32_t d, uint32_t dist_bytes, uint32_t word_bits) {
   std::memset(&h, 0, sizeof h);
   std::memcpy(h.magic, "CBFSLBL1", 8);
-  h.version = 1;
+  h.version = 2;
+  h.word_bits = word_bits;
   h.n = n;
   h.C = C;
   h.d = d;
-  h.planes = d > 0 ? d : 1;
+  h.planes = word_bits == 0 ? 0 : (d > 0 ? d : 1);
   h.dist_bytes = dist_bytes;
-  h.bytes = image_bytes(n, C, h.planes, dist_bytes);
+  h.bytes = image_bytes(n, C, h.planes, dist_bytes, word_bits);
 }
 
 }  // namespace cbfs
@@ -58,19 +70,29 @@ using namespace cbfs;
 
 extern "C" {
 
-int cbfs_labels_build(cbfs_graph* gh, const uint32_t* sources, const uint8_t* sizes, uint32_t n_clusters, uint32_t d,
-                      uint32_t dist_bytes, cbfs_labels** out, cbfs_stream stream) {
+int cbfs_labels_build_w(cbfs_graph* gh, const uint32_t* sources, const uint8_t* sizes, uint32_t n_clusters,
+                        uint32_t d, uint32_t dist_bytes, uint32_t word_bits, cbfs_labels** out, cbfs_stream stream) {
   Graph* g = reinterpret_cast<Graph*>(gh);
   if (!out) return fail(CBFS_EINVAL, "null out");
   *out = nullptr;
   if (!g) return fail(CBFS_EINVAL, "null graph");
   if (dist_bytes != 1 && dist_bytes != 2) return fail(CBFS_EINVAL, "dist_bytes must be 1 or 2");
   if (d > CBFS_MAX_D) return fail(CBFS_EUNSUPPORTED, "d > CBFS_MAX_D");
+  if (!word_ok(word_bits)) return fail(CBFS_EINVAL, "word_bits must be 0, 8, 16, 32 or 64");
+  if (word_bits == 0 && d != 0) return fail(CBFS_EINVAL, "plain landmarks (word_bits 0) need d = 0");
+  if (n_clusters && !sizes) return fail(CBFS_EINVAL, "null sizes");
   CBFS_CUDA(cudaSetDevice(g->device));
   cudaStream_t st = (cudaStream_t)stream;
+  if (word_bits < 64 && n_clusters) {  // a cluster must fit one w-bit word
+    std::vector<uint8_t> hs(n_clusters);
+    CBFS_CUDA(cudaMemcpyAsync(hs.data(), sizes, n_clusters, cudaMemcpyDefault, st));
+    CBFS_CUDA(cudaStreamSynchronize(st));
+    for (uint8_t x : hs)
+      if (x > (word_bits ? word_bits : 1u)) return fail(CBFS_EINVAL, "a cluster has more sources than the word has bits");
+  }
   Labels* L = new Labels();
   L->device = g->device;
-  make_header(L->h, g->n, n_clusters, d, dist_bytes);
+  make_header(L->h, g->n, n_clusters, d, dist_bytes, word_bits);
   if (cudaMalloc(&L->blob, L->h.bytes) != cudaSuccess) {
     delete L;
     cudaGetLastError();
@@ -81,8 +103,8 @@ int cbfs_labels_build(cbfs_graph* gh, const uint32_t* sources, const uint8_t* si
       (n_clusters && cudaMemcpyAsync(L->sizes(), sizes, n_clusters, cudaMemcpyDefault, st) != cudaSuccess))
     rc = cuda_fail(cudaGetLastError(), "label header");
   if (rc == CBFS_OK && n_clusters)
-    rc = cbfs_run(gh, sources, sizes, n_clusters, d, dist_bytes, L->dist(), L->masks(), L->h.planes, nullptr,
-                  CBFS_DIR_AUTO, stream);
+    rc = run_arrays(g, sources, sizes, n_clusters, d, dist_bytes, L->dist(), word_bits ? L->masks() : nullptr,
+                    word_bits ? word_bits / 8 : 8, word_bits ? L->h.planes : 1, nullptr, CBFS_DIR_AUTO, st);
   if (rc == CBFS_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = cuda_fail(cudaGetLastError(), "label build");
   if (rc != CBFS_OK) {
     cudaFree(L->blob);
@@ -90,6 +112,18 @@ int cbfs_labels_build(cbfs_graph* gh, const uint32_t* sources, const uint8_t* si
     return rc;
   }
   *out = reinterpret_cast<cbfs_labels*>(L);
+  return CBFS_OK;
+}
+
+int cbfs_labels_build(cbfs_graph* gh, const uint32_t* sources, const uint8_t* sizes, uint32_t n_clusters, uint32_t d,
+                      uint32_t dist_bytes, cbfs_labels** out, cbfs_stream stream) {
+  return cbfs_labels_build_w(gh, sources, sizes, n_clusters, d, dist_bytes, 64, out, stream);
+}
+
+int cbfs_labels_word_bits(const cbfs_labels* lh, uint32_t* word_bits) {
+  const Labels* L = reinterpret_cast<const Labels*>(lh);
+  if (!L || !word_bits) return fail(CBFS_EINVAL, "null argument");
+  *word_bits = L->h.word_bits;
   return CBFS_OK;
 }
 
@@ -123,10 +157,12 @@ int cbfs_labels_import(cbfs_graph* gh, const void* buf, uint64_t bytes, cbfs_lab
   CBFS_CUDA(cudaSetDevice(g->device));
   LabelHeader h;
   CBFS_CUDA(cudaMemcpy(&h, buf, sizeof h, cudaMemcpyDefault));
-  if (std::memcmp(h.magic, "CBFSLBL1", 8) != 0 || h.version != 1) return fail(CBFS_EINVAL, "not a label image");
+  if (std::memcmp(h.magic, "CBFSLBL1", 8) != 0 || h.version != 2) return fail(CBFS_EINVAL, "not a label image");
   if (h.n != g->n) return fail(CBFS_EINVAL, "label image is for another graph size");
-  if ((h.dist_bytes != 1 && h.dist_bytes != 2) || h.d > CBFS_MAX_D || h.planes != (h.d > 0 ? h.d : 1) ||
-      h.bytes != image_bytes(h.n, h.C, h.planes, h.dist_bytes) || bytes < h.bytes)
+  if ((h.dist_bytes != 1 && h.dist_bytes != 2) || h.d > CBFS_MAX_D || h.planes != (h.word_bits == 0 ? 0 : (h.d > 0 ? h.d : 1)) ||
+      (h.word_bits == 0 && h.d != 0) ||
+      !word_ok(h.word_bits) || h.bytes != image_bytes(h.n, h.C, h.planes, h.dist_bytes, h.word_bits) ||
+      bytes < h.bytes)
     return fail(CBFS_EINVAL, "corrupt label image header");
   Labels* L = new Labels();
   L->device = g->device;
@@ -152,8 +188,9 @@ int cbfs_labels_query(const cbfs_labels* lh, const uint32_t* s, const uint32_t* 
   if (!L) return fail(CBFS_EINVAL, "null labels");
   if (L->h.C == 0) return q && (!s || !t || !inout_best) ? fail(CBFS_EINVAL, "null query arrays") : CBFS_OK;
   CBFS_CUDA(cudaSetDevice(L->device));
-  return cbfs_query_distance(L->h.n, L->h.C, L->h.d, L->h.planes, L->dist(), L->h.dist_bytes, L->masks(), L->sizes(),
-                             s, t, q, inout_best, stream);
+  const uint32_t mb = L->h.word_bits ? L->h.word_bits / 8 : 8;
+  return query_store(L->h.n, L->h.C, L->h.d, L->h.planes, L->dist(), L->h.dist_bytes, L->masks(), mb, L->sizes(), s, t,
+                     q, inout_best, (cudaStream_t)stream);
 }
 
 int cbfs_labels_destroy(cbfs_labels* lh) {

@@ -24,6 +24,15 @@ __device__ __forceinline__ uint32_t load_dist(const void* p, uint64_t idx) {
   }
 }
 
+// one bit-subset word of a store with MB-byte words (w = 8 * MB)
+template <int MB>
+__device__ __forceinline__ uint64_t load_mask(const void* p, uint64_t idx) {
+  if (MB == 1) return ((const uint8_t*)p)[idx];
+  if (MB == 2) return ((const uint16_t*)p)[idx];
+  if (MB == 4) return ((const uint32_t*)p)[idx];
+  return ((const uint64_t*)p)[idx];
+}
+
 // ------------------------------------------------------------------ decode
 template <int DB>
 __global__ void k_decode(uint32_t n, uint32_t C, uint32_t d, uint32_t planes, const void* __restrict__ dist,
@@ -49,10 +58,11 @@ __global__ void k_decode(uint32_t n, uint32_t C, uint32_t d, uint32_t planes, co
 // One warp per query pair, lane over clusters.  Per cluster: skip when
 // either Delta is unreachable (R16); else the smallest i+j with
 // S_s[i] & S_t[j] != 0, scanning i+j = 0..2d; S_x[d] is
-// rebuilt from the other subsets when the store keeps only d (R14).
-template <int DB>
+// rebuilt from the other subsets when the store keeps only d (R14).  MB is
+// the store's word: 8 bytes, or 1/2/4 for the packed w = 8/16/32 stores.
+template <int DB, int MB>
 __global__ void __launch_bounds__(256) k_query(uint32_t n, uint32_t C, uint32_t d, uint32_t planes,
-                                               const void* __restrict__ dist, const uint64_t* __restrict__ masks,
+                                               const void* __restrict__ dist, const void* __restrict__ masks,
                                                const uint8_t* __restrict__ sizes, const uint32_t* __restrict__ s,
                                                const uint32_t* __restrict__ t, uint64_t q,
                                                int32_t* __restrict__ best, int* __restrict__ bad,
@@ -83,8 +93,8 @@ __global__ void __launch_bounds__(256) k_query(uint32_t n, uint32_t C, uint32_t 
       uint64_t Sa[CBFS_MAX_D + 1], Sb[CBFS_MAX_D + 1];
       uint64_t ua = 0, ub = 0;
       for (uint32_t i = 0; i < planes; ++i) {
-        Sa[i] = masks[((uint64_t)i * n + a) * C + c];
-        Sb[i] = masks[((uint64_t)i * n + b) * C + c];
+        Sa[i] = load_mask<MB>(masks, ((uint64_t)i * n + a) * C + c);
+        Sb[i] = load_mask<MB>(masks, ((uint64_t)i * n + b) * C + c);
         ua |= Sa[i];
         ub |= Sb[i];
       }
@@ -111,15 +121,29 @@ __global__ void __launch_bounds__(256) k_query(uint32_t n, uint32_t C, uint32_t 
   }
 }
 
+template <int DB>
+static void launch_query_db(unsigned blocks, uint32_t n, uint32_t C, uint32_t d, uint32_t planes, const void* dist,
+                            const void* masks, uint32_t mask_bytes, const uint8_t* sizes, const uint32_t* s,
+                            const uint32_t* t, uint64_t q, int32_t* best, int* bad, cudaStream_t st,
+                            const uint32_t* inv) {
+  switch (mask_bytes) {
+    case 1: k_query<DB, 1><<<blocks, 256, 0, st>>>(n, C, d, planes, dist, masks, sizes, s, t, q, best, bad, inv); break;
+    case 2: k_query<DB, 2><<<blocks, 256, 0, st>>>(n, C, d, planes, dist, masks, sizes, s, t, q, best, bad, inv); break;
+    case 4: k_query<DB, 4><<<blocks, 256, 0, st>>>(n, C, d, planes, dist, masks, sizes, s, t, q, best, bad, inv); break;
+    default: k_query<DB, 8><<<blocks, 256, 0, st>>>(n, C, d, planes, dist, masks, sizes, s, t, q, best, bad, inv);
+  }
+}
+
 static int launch_query(uint32_t n, uint32_t C, uint32_t d, uint32_t planes, const void* dist, uint32_t dist_bytes,
-                        const uint64_t* masks, const uint8_t* sizes, const uint32_t* s, const uint32_t* t, uint64_t q,
-                        int32_t* best, int* bad, cudaStream_t st, const uint32_t* inv = nullptr) {
+                        const void* masks, const uint8_t* sizes, const uint32_t* s, const uint32_t* t, uint64_t q,
+                        int32_t* best, int* bad, cudaStream_t st, const uint32_t* inv = nullptr,
+                        uint32_t mask_bytes = 8) {
   if (q == 0 || C == 0) return CBFS_OK;
   const unsigned blocks = grid_for(q * 32, 256, 148u * 8u * 8u);
   if (dist_bytes == 1)
-    k_query<1><<<blocks, 256, 0, st>>>(n, C, d, planes, dist, masks, sizes, s, t, q, best, bad, inv);
+    launch_query_db<1>(blocks, n, C, d, planes, dist, masks, mask_bytes, sizes, s, t, q, best, bad, st, inv);
   else
-    k_query<2><<<blocks, 256, 0, st>>>(n, C, d, planes, dist, masks, sizes, s, t, q, best, bad, inv);
+    launch_query_db<2>(blocks, n, C, d, planes, dist, masks, mask_bytes, sizes, s, t, q, best, bad, st, inv);
   CBFS_LAUNCHED();
   return CBFS_OK;
 }
@@ -281,18 +305,26 @@ int cbfs_query_bidir(cbfs_graph* gh, const uint32_t* s, const uint32_t* t, uint6
   return CBFS_OK;
 }
 
-int cbfs_query_distance(uint32_t n, uint32_t C, uint32_t d, uint32_t planes, const void* dist, uint32_t dist_bytes,
-                        const uint64_t* masks, const uint8_t* sizes, const uint32_t* s, const uint32_t* t, uint64_t q,
-                        int32_t* inout_best, cbfs_stream stream) {
+}  // extern "C"
+
+namespace cbfs {
+// cbfs_query_distance over a store whose bit-subset words are mask_bytes wide
+int query_store(uint32_t n, uint32_t C, uint32_t d, uint32_t planes, const void* dist, uint32_t dist_bytes,
+                const void* masks, uint32_t mask_bytes, const uint8_t* sizes, const uint32_t* s, const uint32_t* t,
+                uint64_t q, int32_t* inout_best, cudaStream_t st) {
   if (q && (!s || !t || !inout_best)) return fail(CBFS_EINVAL, "null query arrays");
-  if (C && (!dist || !masks || !sizes)) return fail(CBFS_EINVAL, "null label arrays");
-  if (d > CBFS_MAX_D || (planes != d + 1 && !(planes == d && d > 0))) return fail(CBFS_EINVAL, "bad d/planes");
+  // planes = d = 0: plain landmarks (single-source clusters, Delta only; S_v[0]
+  // = FULL is rebuilt like any S_v[d], R14)
+  if (C && (!dist || (!masks && planes) || !sizes)) return fail(CBFS_EINVAL, "null label arrays");
+  if (d > CBFS_MAX_D || (planes != d + 1 && planes != d)) return fail(CBFS_EINVAL, "bad d/planes");
   if (dist_bytes != 1 && dist_bytes != 2) return fail(CBFS_EINVAL, "dist_bytes must be 1 or 2");
-  cudaStream_t st = (cudaStream_t)stream;
+  if (mask_bytes != 1 && mask_bytes != 2 && mask_bytes != 4 && mask_bytes != 8)
+    return fail(CBFS_EINVAL, "mask word must be 1, 2, 4 or 8 bytes");
   int* bad = nullptr;
   CBFS_CUDA(cudaMallocAsync(&bad, sizeof(int), st));
   CBFS_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
-  int rc = launch_query(n, C, d, planes, dist, dist_bytes, masks, sizes, s, t, q, inout_best, bad, st);
+  int rc = launch_query(n, C, d, planes, dist, dist_bytes, masks, sizes, s, t, q, inout_best, bad, st, nullptr,
+                        mask_bytes);
   if (rc) return rc;
   int hbad = 0;
   CBFS_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -300,6 +332,15 @@ int cbfs_query_distance(uint32_t n, uint32_t C, uint32_t d, uint32_t planes, con
   CBFS_CUDA(cudaStreamSynchronize(st));
   if (hbad) return fail(CBFS_EINVAL, "query vertex id >= n");
   return CBFS_OK;
+}
+}  // namespace cbfs
+
+extern "C" {
+
+int cbfs_query_distance(uint32_t n, uint32_t C, uint32_t d, uint32_t planes, const void* dist, uint32_t dist_bytes,
+                        const uint64_t* masks, const uint8_t* sizes, const uint32_t* s, const uint32_t* t, uint64_t q,
+                        int32_t* inout_best, cbfs_stream stream) {
+  return query_store(n, C, d, planes, dist, dist_bytes, masks, 8, sizes, s, t, q, inout_best, (cudaStream_t)stream);
 }
 
 // per-slot label staging; the query runs on the slot's stream when its batch ends

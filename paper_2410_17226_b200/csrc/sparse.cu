@@ -116,7 +116,8 @@ __global__ void __launch_bounds__(SP_THREADS) k_sp_fold(const SpDesc* __restrict
   const uint64_t* __restrict__ off = D->off;
   const uint32_t* __restrict__ perm = D->perm;
   void* __restrict__ out_dist = D->out_dist;
-  uint64_t* __restrict__ out_masks = D->out_masks;
+  void* __restrict__ out_masks = D->out_masks;
+  const uint32_t mb = D->mask_bytes;
   const uint32_t lane = lane_id();
   bool overflow = false;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
@@ -169,7 +170,7 @@ __global__ void __launch_bounds__(SP_THREADS) k_sp_fold(const SpDesc* __restrict
             }
           }
           const uint32_t oi = i - dv;
-          if (out_masks && oi < planes) out_masks[(uint64_t)oi * n * C + col] = nw;
+          if (out_masks && oi < planes) store_mask(out_masks, (uint64_t)oi * n * C + col, nw, mb);
         }
       }
       // per-cluster statistics, one shared atomic per distinct cluster in the warp
@@ -357,7 +358,8 @@ __global__ void __launch_bounds__(SP_THREADS, CBFS_SP_MINB) k_sp_push(const SpDe
               }
             }
             const uint32_t oi = i - dv;
-            if (D->out_masks && oi < D->planes) D->out_masks[(uint64_t)oi * n * D->C + col] = nw[q];
+            if (D->out_masks && oi < D->planes)
+              store_mask(D->out_masks, (uint64_t)oi * n * D->C + col, nw[q], D->mask_bytes);
           }
           if (p) cell->p[cur] = 0;
         }
@@ -563,7 +565,7 @@ int sparse_start(const Graph* g, Slot* w, const RunArgs& a) {
   h->d = a.d;
   h->planes = a.planes;
   h->dist_bytes = a.dist_bytes;
-  h->pad = 0;
+  h->mask_bytes = a.mask_bytes ? a.mask_bytes : 8;
   CBFS_CUDA(cudaMemcpyAsync(w->sp_desc, h, sizeof(SpDesc), cudaMemcpyHostToDevice, st));
   const uint64_t ncell = (uint64_t)n * LANES;
   k_sp_init<<<grid_for(ncell, 256, 148u * 16u), 256, 0, st>>>(reinterpret_cast<SpCell*>(w->blk), ncell);

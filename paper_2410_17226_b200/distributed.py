@@ -120,11 +120,12 @@ def query_gathered(stores, d: int, s: torch.Tensor, t: torch.Tensor, dist_bytes:
     return best
 
 
-def build_local_labels(graph, sources: torch.Tensor, sizes: torch.Tensor, d: int, dist_bytes: int = 2, group=None):
-    """This rank's label store as a cbfs_labels handle (cbfs_labels_build over
-    its round-robin clusters)."""
+def build_local_labels(graph, sources: torch.Tensor, sizes: torch.Tensor, d: int, dist_bytes: int = 2, group=None,
+                       word_bits: int = 64):
+    """This rank's label store as a cbfs_labels handle (cbfs_labels_build_w
+    over its round-robin clusters, store word size word_bits)."""
     src_r, sz_r = local_clusters(sources, sizes, group)
-    return cbfs_labels_build(graph.h, src_r, sz_r, int(sz_r.shape[0]), d, dist_bytes)
+    return cbfs_labels_build(graph.h, src_r, sz_r, int(sz_r.shape[0]), d, dist_bytes, word_bits=word_bits)
 
 
 def gather_label_images(graph, labels, group=None):

@@ -75,3 +75,66 @@ def test_bidir_refine_parity(kind, relabel):
     with pytest.raises(cb.CbfsError):
         cb.cbfs_query_bidir(g.h, sd, td, cb.CBFS_BIDIR_MAX_TAU + 1, best)
     g.close()
+
+
+# ------------------------------------------------------------------ word size w (Tables 4/8)
+@pytest.mark.parametrize("kind,d", [("rmat", 2), ("grid", 4)])
+@pytest.mark.parametrize("w", [0, 8, 16, 32, 64])
+def test_word_size_store_matches_oracle(kind, d, w):
+    """A store of word size w under a t = 256 bytes-per-vertex budget: the
+    cluster count and record size follow the paper's arithmetic (the oracle's
+    pinned record_bytes), the image has exactly that many record bytes, and
+    its answers equal the oracle's streaming query over the same k <= w
+    clusters; an exported packed image answers identically after import.
+    w = 0 is plain landmark labeling (k = 1, d = 0, 1-byte records)."""
+    import paper_2410_17226_b200 as cb
+    if w == 0:
+        d = 0
+    el = ci.rmat(12, 8, 0.57, 0.19, 0.19, seed=51) if kind == "rmat" else ci.grid(60, 0.05, 0.01, 51)
+    ref = orc.csr_from_edgelist(el)
+    g = gpu_graph(el, relabel=(kind == "rmat"))
+    assert ado.record_bytes(w, d) == orc.record_bytes(w, d)
+    r = ado.clusters_for_budget(256, w, d)
+    assert r == orc.budget_to_clusters(256, w, d)
+    k = max(w, 1)
+    idx = ado.LandmarkIndex(g, r, k, d, word_bits=w, dist_bytes=1)
+    osrc, osz = orc.select_clusters(ref, r, k, d)
+    assert idx.r == len(osz) and int(osz.max()) <= k
+    info = cb.cbfs_labels_info(idx.labels)
+    assert info["word_bits"] == w
+    pad16 = lambda x: (x + 15) // 16 * 16  # noqa: E731
+    assert info["image_bytes"] - 64 - pad16(idx.r) == pad16(g.n * idx.r) + g.n * idx.r * d * w // 8
+    assert g.n * idx.r * ado.record_bytes(w, d) <= g.n * 256
+    s, t = ci.query_pairs(el.n, 20000, seed=13, stream=7)
+    sd, td = torch.from_numpy(s.view(np.int32)).cuda(), torch.from_numpy(t.view(np.int32)).cuda()
+    expect = orc.query_stream(ref, osrc, osz, d, s, t)
+    assert np.array_equal(idx.query(sd, td).cpu().numpy(), expect)
+    img = torch.empty(info["image_bytes"], dtype=torch.uint8, device="cuda")
+    cb.cbfs_labels_export(idx.labels, img)
+    h2 = cb.cbfs_labels_import(g.h, img)
+    best = torch.full((len(s),), cb.CBFS_QUERY_UNREACHED, dtype=torch.int32, device="cuda")
+    cb.cbfs_labels_query(h2, sd, td, best)
+    assert np.array_equal(best.cpu().numpy(), expect)
+    cb.cbfs_labels_destroy(h2)
+    idx.close()
+    g.close()
+
+
+def test_word_size_rejects_wide_clusters():
+    import paper_2410_17226_b200 as cb
+    el = ci.rmat(10, 8, 0.57, 0.19, 0.19, seed=52)
+    g = gpu_graph(el, relabel=True)
+    src = torch.empty((4, 64), dtype=torch.int32, device="cuda")
+    sz = torch.empty((4,), dtype=torch.uint8, device="cuda")
+    got = cb.cbfs_select_clusters(g.h, 4, 64, 2, cb.CBFS_ROOT_DEGREE, 0, src, sz)
+    assert int(sz[:got].max()) > 16
+    with pytest.raises(cb.CbfsError):
+        cb.cbfs_labels_build(g.h, src, sz, got, 2, 2, word_bits=16)
+    with pytest.raises(cb.CbfsError):
+        cb.cbfs_labels_build(g.h, src, sz, got, 2, 2, word_bits=12)
+    with pytest.raises(cb.CbfsError):  # plain landmarks need d = 0 and single sources
+        cb.cbfs_labels_build(g.h, src, sz, got, 0, 2, word_bits=0)
+    h = cb.cbfs_labels_build(g.h, src, sz, got, 2, 2, word_bits=64)
+    assert cb.cbfs_labels_info(h)["word_bits"] == 64
+    cb.cbfs_labels_destroy(h)
+    g.close()
