@@ -59,6 +59,7 @@ enum cbfs_status {
 };
 
 #define CBFS_MAX_K 64u
+#define CBFS_WIDE_MAX_W 8u  /* cbfs_run_wide: up to 8 words = 512 sources per cluster */
 #define CBFS_MAX_D 31u
 #define CBFS_MAX_N (1u << 26)          /* (vertex, cluster-in-batch) pairs pack into 32 bits */
 #define CBFS_PAD 0xFFFFFFFFu           /* source-list padding                */
@@ -156,6 +157,31 @@ int cbfs_run(cbfs_graph* g, const uint32_t* sources, const uint8_t* sizes, uint3
              uint32_t dist_bytes, void* out_dist, uint64_t* out_masks, uint32_t planes, uint64_t* out_stats,
              uint32_t direction, cbfs_stream stream);
 
+/* cbfs_run_wide — C-BFS from clusters of more than 64 sources (k > w, the
+ * paper's general k: P:448): each
+ * bit-subset is `words` 64-bit words (bit j of the cluster = bit j % 64 of
+ * word j / 64, R11).  Reading R28: the cluster's 64-source words are
+ * traversed as sub-clusters in lanes of one batch, in lockstep rounds, and
+ * the fold places each word's subsets relative to the cluster's Delta_v
+ * (the least first-visit round over its words).  For a cluster of diameter
+ * <= d this is the cluster distance vector, exactly; for d <
+ * diameter the output is not specified (unlike cbfs_run's R9).
+ *   sources   : device [n_clusters][64 * words] uint32 original ids, row c
+ *               holds sizes[c] distinct ids then padding
+ *   sizes     : device [n_clusters] uint16, 1..64 * words
+ *   words     : 1, 2, 4 or 8 (CBFS_WIDE_MAX_W)
+ *   out_dist  : device [n][n_clusters], Delta_v, or NULL
+ *   out_masks : device [planes][n][n_clusters * words] uint64; word w of
+ *               cluster c in column c * words + w; or NULL
+ *   out_stats : device [n_clusters * words][4], the statistics of each
+ *               64-source word (as cbfs_run's per cluster), or NULL
+ *   other arguments as cbfs_run.  Always the batched engine.
+ * Errors: EINVAL (size 0 or > 64 * words, duplicate or out-of-range source),
+ * EUNSUPPORTED (words not 1/2/4/8, d > MAX_D), EOVERFLOW, ENOMEM, ECUDA. */
+int cbfs_run_wide(cbfs_graph* g, const uint32_t* sources, const uint16_t* sizes, uint32_t n_clusters, uint32_t words,
+                  uint32_t d, uint32_t dist_bytes, void* out_dist, uint64_t* out_masks, uint32_t planes,
+                  uint64_t* out_stats, uint32_t direction, cbfs_stream stream);
+
 /* cbfs_select_and_run — cbfs_select_clusters followed by cbfs_run over the
  * selected clusters, overlapped: the (sequential) selection runs on a side
  * stream and publishes each cluster as it is fixed, and each batch of 64
@@ -202,6 +228,17 @@ int cbfs_run_host(cbfs_graph* g, const uint32_t* sources, const uint8_t* sizes, 
  * Errors: EINVAL. */
 int cbfs_decode(uint32_t n, uint32_t C, uint32_t d, uint32_t planes, const void* dist, uint32_t dist_bytes,
                 const uint64_t* masks, uint32_t c, uint32_t k, uint16_t* out, cbfs_stream stream);
+
+/* cbfs_decode_wide / cbfs_query_distance_wide — cbfs_decode and
+ * cbfs_query_distance over the cbfs_run_wide layout (dist [n][C], masks
+ * [planes][n][C * words], sizes device [C] uint16; k <= 64 * words).
+ * Same semantics, arguments and errors otherwise. */
+int cbfs_decode_wide(uint32_t n, uint32_t C, uint32_t words, uint32_t d, uint32_t planes, const void* dist,
+                     uint32_t dist_bytes, const uint64_t* masks, uint32_t c, uint32_t k, uint16_t* out,
+                     cbfs_stream stream);
+int cbfs_query_distance_wide(uint32_t n, uint32_t C, uint32_t words, uint32_t d, uint32_t planes, const void* dist,
+                             uint32_t dist_bytes, const uint64_t* masks, const uint16_t* sizes, const uint32_t* s,
+                             const uint32_t* t, uint64_t q, int32_t* inout_best, cbfs_stream stream);
 
 /* --------------------------------------------------------------- queries
  * cbfs_query_distance — landmark query with clustered landmarks

@@ -9,7 +9,10 @@ Layers (each cites PAPER.md lines; readings R1..R26 are in DESIGN.md §2):
   * csr_from_edges  — graph normalisation (R17): symmetrise, drop
     self loops, sort + dedup, CSR.  numpy ``unique`` is the sort/dedup step.
   * plain_bfs / brute_cluster — single-source BFS and the
-    definition of the cluster distance vector, in C.
+    definition of the cluster distance vector (P:630-639), in C;
+    brute_cluster_wide / query_brute — the same definition and the landmark
+    query for clusters of any size k (multi-word subsets, NEXT-1), numpy
+    over plain_bfs.
   * cluster_bfs / cluster_bfs_many — Alg. 1, sequential C.
   * select_clusters — P:1061-1069 with R12, sequential C.
   * query / query_stream — P:1013-1021, P:1074-1086 with R14-R16, C.
@@ -188,6 +191,50 @@ def brute_cluster(g: CSR, S, d: int):
     if rc < 0:
         raise ValueError("invalid cluster")
     return dist, sub, bool(rc)
+
+
+def brute_cluster_wide(g: CSR, S, d: int):
+    """The definition P:630-639 for a cluster of any size k (the paper's
+    general k), written out: Delta_v =
+    min_j delta(s_j, v) and S_v[i] = {j : delta(s_j, v) = Delta_v + i},
+    i = 0..d, each subset W = ceil(k / 64) words with bit j of the cluster in
+    bit j % 64 of word j // 64 (R11).  delta from k queue BFS runs.
+    Returns (dist uint16 [n] (INF16 = unreachable), sub uint64 [d+1][n][W],
+    over) where over means some source lies more than d beyond Delta_v."""
+    S = _sources(S)
+    k = len(S)
+    W = (k + 63) // 64
+    D = np.stack([plain_bfs(g, int(x)) for x in S]).astype(np.int64)
+    reach = D != INF32
+    Delta = np.where(reach, D, INF32).min(axis=0)
+    sub = np.zeros((d + 1, g.n, W), np.uint64)
+    over = False
+    for j in range(k):
+        off = D[j] - Delta
+        over |= bool((reach[j] & (off > d)).any())
+        for i in range(d + 1):
+            sel = reach[j] & (off == i)
+            sub[i, sel, j // 64] |= np.uint64(1 << (j % 64))
+    dist = np.where(Delta == INF32, INF16, Delta).astype(np.uint16)
+    return dist, sub, over
+
+
+def query_brute(g: CSR, clusters, s, t) -> np.ndarray:
+    """Landmark query with each cluster's sources as its landmarks
+    (R16): min over clusters and sources s_j of delta(u, s_j) +
+    delta(s_j, v), INT32_MAX when no source reaches both ends; clusters of
+    any size.  For clusters of diameter <= d this is the value of the
+    (d+1)^2 subset scan (R15)."""
+    s = np.asarray(s, dtype=np.int64)
+    t = np.asarray(t, dtype=np.int64)
+    big = np.int64(1) << 40
+    best = np.full(len(s), big, np.int64)
+    for S in clusters:
+        for x in _sources(S):
+            D = plain_bfs(g, int(x)).astype(np.int64)
+            D[D == INF32] = big
+            best = np.minimum(best, D[s] + D[t])
+    return np.where(best >= big, INT32_MAX, best).astype(np.int32)
 
 
 def cluster_bfs(g: CSR, S, d: int, max_rounds: int = 1 << 16) -> ClusterResult:

@@ -56,6 +56,9 @@ _sig("cbfs_select_and_run", [_vp, _u32, _u32, _u32, _u32, _u64, _vp, _vp, ctypes
 _sig("cbfs_select_and_run_shard", [_vp, _u32, _u32, _u32, _u32, _u64, _u32, _u32, _vp, _vp, ctypes.POINTER(_u32), _u32,
                                     _vp, _vp, _u32, _vp, _u32, _vp])
 _sig("cbfs_run_host", [_vp, _vp, _vp, _u32, _u32, _u32, _vp, _vp, _u32, _vp, _u32, _vp])
+_sig("cbfs_run_wide", [_vp, _vp, _vp, _u32, _u32, _u32, _u32, _vp, _vp, _u32, _vp, _u32, _vp])
+_sig("cbfs_decode_wide", [_u32, _u32, _u32, _u32, _u32, _vp, _u32, _vp, _u32, _u32, _vp, _vp])
+_sig("cbfs_query_distance_wide", [_u32, _u32, _u32, _u32, _u32, _vp, _u32, _vp, _vp, _vp, _vp, _u64, _vp, _vp])
 _sig("cbfs_decode", [_u32, _u32, _u32, _u32, _vp, _u32, _vp, _u32, _u32, _vp, _vp])
 _sig("cbfs_query_distance", [_u32, _u32, _u32, _u32, _vp, _u32, _vp, _vp, _vp, _vp, _u64, _vp, _vp])
 _sig("cbfs_query_stream", [_vp, _vp, _vp, _u32, _u32, _vp, _vp, _u64, _vp, _vp, _vp])
@@ -185,6 +188,24 @@ def cbfs_run_host(h, sources, sizes, n_clusters, d, dist_bytes, out_dist, out_ma
                   direction=CBFS_DIR_AUTO, stream=None):
     _check(_lib.cbfs_run_host(h, _ptr(sources), _ptr(sizes), n_clusters, d, dist_bytes, _ptr(out_dist),
                               _ptr(out_masks), planes, _ptr(out_stats), direction, _stream(stream)))
+
+
+def cbfs_run_wide(h, sources, sizes, n_clusters, words, d, dist_bytes, out_dist, out_masks, planes, out_stats=None,
+                  direction=CBFS_DIR_AUTO, stream=None):
+    """sources [C][64 * words] int32, sizes [C] int16/uint16 (k <= 64 * words);
+    out_masks [planes][n][C * words] (word w of cluster c at column c * words + w)."""
+    _check(_lib.cbfs_run_wide(h, _ptr(sources), _ptr(sizes), n_clusters, words, d, dist_bytes, _ptr(out_dist),
+                              _ptr(out_masks), planes, _ptr(out_stats), direction, _stream(stream)))
+
+
+def cbfs_decode_wide(n, C, words, d, planes, dist, dist_bytes, masks, c, k, out, stream=None):
+    _check(_lib.cbfs_decode_wide(n, C, words, d, planes, _ptr(dist), dist_bytes, _ptr(masks), c, k, _ptr(out),
+                                 _stream(stream)))
+
+
+def cbfs_query_distance_wide(n, C, words, d, planes, dist, dist_bytes, masks, sizes, s, t, inout_best, stream=None):
+    _check(_lib.cbfs_query_distance_wide(n, C, words, d, planes, _ptr(dist), dist_bytes, _ptr(masks), _ptr(sizes),
+                                         _ptr(s), _ptr(t), len(s), _ptr(inout_best), _stream(stream)))
 
 
 def cbfs_decode(n, C, d, planes, dist, dist_bytes, masks, c, k, out, stream=None):

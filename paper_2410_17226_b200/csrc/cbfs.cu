@@ -186,7 +186,7 @@ __device__ __forceinline__ void stats_flush(uint64_t* __restrict__ bstats, uint3
 __global__ void k_seed(const uint32_t* __restrict__ sources, const uint8_t* __restrict__ sizes, uint32_t nb,
                        uint32_t n, const uint32_t* __restrict__ inv, const uint64_t* __restrict__ off,
                        uint64_t* __restrict__ pend, uint32_t* __restrict__ list, uint32_t* __restrict__ ubits0,
-                       uint64_t* __restrict__ bstats, unsigned long long* __restrict__ ctr) {
+                       uint64_t* __restrict__ bstats, unsigned long long* __restrict__ ctr, int allow_empty) {
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;  // 64 threads per cluster
   const uint32_t c = t >> 6, j = t & 63;
   bool claim = false;
@@ -194,7 +194,7 @@ __global__ void k_seed(const uint32_t* __restrict__ sources, const uint8_t* __re
   unsigned long long deg = 0;
   if (c < nb) {
     const uint32_t k = sizes[c];
-    if (k == 0 || k > 64) {
+    if ((k == 0 && !allow_empty) || k > 64) {
       if (j == 0) atomicOr(&ctr[2], ERR_BAD_SIZE);
     } else if (j < k) {
       const uint32_t s = sources[(uint64_t)c * 64 + j];
@@ -240,7 +240,8 @@ __global__ void __launch_bounds__(256) k_fold(const uint32_t* __restrict__ F, ui
                                               uint32_t cbase, uint32_t planes, void* __restrict__ out_dist,
                                               void* __restrict__ out_masks, uint32_t mb, uint64_t* __restrict__ pre,
                                               int write_pre, const uint8_t* __restrict__ sizes,
-                                              uint64_t* __restrict__ fullm, unsigned long long* __restrict__ ctr) {
+                                              uint64_t* __restrict__ fullm, unsigned long long* __restrict__ ctr,
+                                              uint32_t W) {
   const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
   const uint32_t lane = lane_id();
@@ -276,15 +277,27 @@ __global__ void __launch_bounds__(256) k_fold(const uint32_t* __restrict__ F, ui
       if (write_pre) pre[t0 + q * nth] = off[v + 1] - off[v];
       const uint32_t orig = perm ? perm[v] : v;
       const uint64_t col = (uint64_t)orig * C + cbase + c;
-      if (first && out_dist) {
+      // wide clusters (k > 64, cbfs_run_wide): the W lanes of a cluster are
+      // its 64-source words, each traversed as its own sub-cluster; the
+      // cluster's Delta_v is the least over its lanes (all in lockstep
+      // rounds, so a lane reaching v later has a larger Delta) and every
+      // lane's subsets are placed relative to it
+      uint32_t dc = dv[q];
+      uint64_t dcol = col;
+      if (W > 1) {
+        const uint32_t b0 = e[q] & ~(W - 1);
+        for (uint32_t x = 0; x < W; ++x) dc = min(dc, (uint32_t)dist[b0 + x]);
+        dcol = (uint64_t)orig * (C / W) + (cbase + c) / W;
+      }
+      if (first && out_dist && dc == i) {
         if (DB == 1) {
           overflow |= i > 254;
-          ((uint8_t*)out_dist)[col] = (uint8_t)(i > 254 ? 254 : i);
+          ((uint8_t*)out_dist)[dcol] = (uint8_t)(i > 254 ? 254 : i);
         } else {
-          ((uint16_t*)out_dist)[col] = (uint16_t)i;
+          ((uint16_t*)out_dist)[dcol] = (uint16_t)i;
         }
       }
-      const uint32_t oi = i - dv[q];
+      const uint32_t oi = i - dc;
       if (out_masks && oi < planes) store_mask(out_masks, (uint64_t)oi * n * C + col, nw[q], mb);
     }
     // per-vertex "subset full" bits (read by the dense pull instead of the
@@ -747,7 +760,7 @@ static int slot_start(Graph* g, Slot* w, const RunArgs& a) {
   CBFS_CUDA(cudaMemsetAsync(w->fullm, 0, (uint64_t)(n + 1) * sizeof(uint64_t), st));
   CBFS_CUDA(cudaMemsetAsync(w->ctr, 0, 4 * sizeof(unsigned long long), st));
   k_seed<<<(a.nb * 64 + 255) / 256, 256, 0, st>>>(a.sources, a.sizes, a.nb, n, g->inv, g->off, w->pend, w->listA,
-                                                   w->ubits, w->bstats, w->ctr);
+                                                   w->ubits, w->bstats, w->ctr, a.wide > 1);
   CBFS_LAUNCHED();
   return queue_counters(w);
 }
@@ -770,11 +783,11 @@ static int slot_round(Graph* g, Slot* w) {
   if (a.dist_bytes == 1)
     k_fold<1><<<fb, 256, 0, st>>>(w->cur, (uint32_t)nF, i, w->seen, w->pend, w->dist, g->off, a.out_internal ? nullptr : g->perm, n, a.C,
                                   a.cbase, a.planes, a.out_dist, a.out_masks, a.mask_bytes, w->pre, write_pre, a.sizes, w->fullm,
-                                  w->ctr);
+                                  w->ctr, a.wide > 1 ? a.wide : 1);
   else
     k_fold<2><<<fb, 256, 0, st>>>(w->cur, (uint32_t)nF, i, w->seen, w->pend, w->dist, g->off, a.out_internal ? nullptr : g->perm, n, a.C,
                                   a.cbase, a.planes, a.out_dist, a.out_masks, a.mask_bytes, w->pre, write_pre, a.sizes, w->fullm,
-                                  w->ctr);
+                                  w->ctr, a.wide > 1 ? a.wide : 1);
   CBFS_LAUNCHED();
   if (g_prof.on) CBFS_CUDA(cudaEventRecord(w->pe[1], st));
   CBFS_CUDA(cudaMemsetAsync(w->ctr, 0, 2 * sizeof(unsigned long long), st));
@@ -983,6 +996,29 @@ int check_run_args(const Graph* g, const void* sources, const void* sizes, uint3
   return CBFS_OK;
 }
 
+// cbfs_run_wide: split each cluster of k <= 64 W sources into W lane sizes
+// (lane w holds sources 64w .. 64w+63) and check the cluster (R2: no
+// duplicate across its words; 1 <= k <= 64 W; ids < n).  One block per
+// cluster, one thread per source slot.
+__global__ void k_wide_prep(const uint32_t* __restrict__ sources, const uint16_t* __restrict__ sizes, uint32_t C,
+                            uint32_t W, uint32_t n, uint8_t* __restrict__ lane_sizes, int* __restrict__ bad) {
+  __shared__ uint32_t s_src[64 * CBFS_WIDE_MAX_W];
+  const uint32_t c = blockIdx.x, j = threadIdx.x, K = 64 * W;
+  const uint32_t k = sizes[c];
+  const uint32_t s = sources[(uint64_t)c * K + j];
+  s_src[j] = s;
+  __syncthreads();
+  if (k == 0 || k > K) {
+    if (j == 0) atomicOr(bad, 1);
+    return;
+  }
+  if (j < W) lane_sizes[(uint64_t)c * W + j] = (uint8_t)(k > 64 * j ? min(64u, k - 64 * j) : 0u);
+  if (j >= k) return;
+  if (s >= n) atomicOr(bad, 2);
+  for (uint32_t x = 0; x < j; ++x)
+    if (s_src[x] == s) atomicOr(bad, 4);
+}
+
 int run_arrays(Graph* g, const uint32_t* sources, const uint8_t* sizes, uint32_t n_clusters, uint32_t d,
                uint32_t dist_bytes, void* out_dist, void* out_masks, uint32_t mask_bytes, uint32_t planes,
                uint64_t* out_stats, uint32_t direction, cudaStream_t st) {
@@ -1163,6 +1199,66 @@ int cbfs_select_and_run_shard(cbfs_graph* gh, uint32_t r, uint32_t k, uint32_t d
   if (!prog[1]) return fail(CBFS_ECUDA, "cluster selection ended without publishing");
   CBFS_CUDA(cudaStreamSynchronize(st));
   *out_r = prog[0];
+  return CBFS_OK;
+}
+
+int cbfs_run_wide(cbfs_graph* gh, const uint32_t* sources, const uint16_t* sizes, uint32_t n_clusters,
+                  uint32_t words, uint32_t d, uint32_t dist_bytes, void* out_dist, uint64_t* out_masks,
+                  uint32_t planes, uint64_t* out_stats, uint32_t direction, cbfs_stream stream) {
+  Graph* g = reinterpret_cast<Graph*>(gh);
+  if (words != 1 && words != 2 && words != 4 && words != 8) return fail(CBFS_EUNSUPPORTED, "words must be 1, 2, 4 or 8");
+  int rc = check_run_args(g, sources, sizes, n_clusters, d, dist_bytes, planes, direction);
+  if (rc) return rc;
+  if ((uint64_t)n_clusters * words > 0xFFFFFFFFull) return fail(CBFS_EINVAL, "too many clusters");
+  CBFS_CUDA(cudaSetDevice(g->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  WorkLease lease(g);
+  if (lease.rc) return lease.rc;
+  const uint64_t C = n_clusters, L = C * words;
+  if (out_dist) CBFS_CUDA(cudaMemsetAsync(out_dist, 0xFF, (uint64_t)g->n * C * dist_bytes, st));
+  if (out_masks) CBFS_CUDA(cudaMemsetAsync(out_masks, 0, (uint64_t)planes * g->n * L * sizeof(uint64_t), st));
+  if (C == 0) {
+    CBFS_CUDA(cudaStreamSynchronize(st));
+    return CBFS_OK;
+  }
+  uint8_t* lane_sizes = nullptr;
+  int* bad = nullptr;
+  CBFS_CUDA(cudaMallocAsync(&lane_sizes, L, st));
+  CBFS_CUDA(cudaMallocAsync(&bad, sizeof(int), st));
+  CBFS_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+  k_wide_prep<<<(unsigned)C, 64 * words, 0, st>>>(sources, sizes, n_clusters, words, g->n, lane_sizes, bad);
+  CBFS_LAUNCHED();
+  int hbad = 0;
+  CBFS_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CBFS_CUDA(cudaStreamSynchronize(st));
+  if (hbad) {
+    cudaFreeAsync(lane_sizes, st);
+    cudaFreeAsync(bad, st);
+    cudaStreamSynchronize(st);
+    return fail(CBFS_EINVAL, (hbad & 1) ? "cluster size must be 1..64*words"
+                             : (hbad & 2) ? "source id >= n" : "duplicate source in a cluster");
+  }
+  ArraySource src;
+  src.proto = RunArgs{};
+  src.proto.d = d;
+  src.proto.planes = planes;
+  src.proto.dist_bytes = dist_bytes;
+  src.proto.C = (uint32_t)L;
+  src.proto.direction = direction;
+  src.proto.engine = ENGINE_BATCHED;  // lanes of a cluster advance in lockstep rounds (the Delta merge relies on it)
+  src.proto.out_dist = out_dist;
+  src.proto.out_masks = out_masks;
+  src.proto.mask_bytes = 8;
+  src.proto.wide = words;
+  src.sources = sources;  // [C][64 W] is [C W][64]: lane c W + w = word w of cluster c
+  src.sizes = lane_sizes;
+  src.n_clusters = (uint32_t)L;
+  src.out_stats = out_stats;
+  rc = run_batches(g, src, st);
+  cudaFreeAsync(lane_sizes, st);
+  cudaFreeAsync(bad, st);
+  if (rc) return rc;
+  CBFS_CUDA(cudaStreamSynchronize(st));
   return CBFS_OK;
 }
 

@@ -134,6 +134,114 @@ static void launch_query_db(unsigned blocks, uint32_t n, uint32_t C, uint32_t d,
   }
 }
 
+// ------------------------------------------------------------------ wide clusters (k > 64)
+// The cbfs_run_wide layout: dist [n][C], masks [planes][n][C W] (word w of
+// cluster c in column c W + w), sizes [C] uint16.  Bit j of the cluster is
+// bit j % 64 of word j / 64 (R11).
+__device__ __forceinline__ uint64_t wide_full(uint32_t k, uint32_t w) {
+  return k > 64 * w ? full_mask(k - 64 * w) : 0ULL;
+}
+
+template <int DB>
+__global__ void k_decode_wide(uint32_t n, uint32_t C, uint32_t W, uint32_t d, uint32_t planes,
+                              const void* __restrict__ dist, const uint64_t* __restrict__ masks, uint32_t c,
+                              uint32_t k, uint16_t* __restrict__ out) {
+  const uint64_t CW = (uint64_t)C * W;
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t dv = load_dist<DB>(dist, v * C + c);
+    for (uint32_t j = 0; j < k; ++j) {
+      const uint32_t w = j >> 6;
+      const uint64_t* col = masks + v * CW + (uint64_t)c * W + w;  // plane i at col[i * n * CW]
+      uint32_t r = 0xFFFFu;
+      if (dv != 0xFFFFFFFFu) {
+        uint64_t uni = 0;
+        for (uint32_t i = 0; i <= d; ++i) {
+          const uint64_t S = i < planes ? col[(uint64_t)i * n * CW] : (wide_full(k, w) & ~uni);  // R14
+          uni |= S;
+          if ((S >> (j & 63)) & 1ULL) { r = dv + i; break; }
+        }
+      }
+      out[(uint64_t)j * n + v] = (uint16_t)(r > 0xFFFFu ? 0xFFFFu : r);
+    }
+  }
+}
+
+// One warp per query pair, lane over clusters, as k_query; the subsets are
+// W words, S_x[d] rebuilt word by word when the store keeps d planes.
+template <int DB, int W>
+__global__ void __launch_bounds__(256) k_query_wide(uint32_t n, uint32_t C, uint32_t d, uint32_t planes,
+                                                    const void* __restrict__ dist,
+                                                    const uint64_t* __restrict__ masks,
+                                                    const uint16_t* __restrict__ sizes,
+                                                    const uint32_t* __restrict__ s, const uint32_t* __restrict__ t,
+                                                    uint64_t q, int32_t* __restrict__ best, int* __restrict__ bad) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+  const uint64_t CW = (uint64_t)C * W, plane = (uint64_t)n * CW;
+  for (uint64_t qi = warp; qi < q; qi += nwarps) {
+    const uint32_t a = s[qi], b = t[qi];
+    if (a >= n || b >= n) {
+      if (lane == 0) *bad = 1;
+      continue;
+    }
+    const int32_t prev = best[qi];
+    int32_t mine = prev;
+    for (uint32_t c = lane; c < C; c += 32) {
+      const uint32_t da = load_dist<DB>(dist, (uint64_t)a * C + c);
+      const uint32_t db = load_dist<DB>(dist, (uint64_t)b * C + c);
+      if (da == 0xFFFFFFFFu || db == 0xFFFFFFFFu) continue;
+      if ((int32_t)(da + db) >= mine) continue;
+      const uint64_t* ca = masks + (uint64_t)a * CW + (uint64_t)c * W;
+      const uint64_t* cb = masks + (uint64_t)b * CW + (uint64_t)c * W;
+      uint64_t ra[W], rb[W];  // S_x[d] per word (only read when planes == d)
+      if (planes == d) {
+        const uint32_t k = sizes[c];
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          uint64_t ua = 0, ub = 0;
+          for (uint32_t i = 0; i < planes; ++i) { ua |= ca[i * plane + w]; ub |= cb[i * plane + w]; }
+          ra[w] = wide_full(k, w) & ~ua;
+          rb[w] = wide_full(k, w) & ~ub;
+        }
+      }
+      for (uint32_t tt = 0; tt <= 2 * d; ++tt) {
+        bool hit = false;
+        const uint32_t i0 = tt > d ? tt - d : 0, i1 = tt < d ? tt : d;
+        for (uint32_t i = i0; i <= i1 && !hit; ++i) {
+          const uint32_t j = tt - i;
+#pragma unroll
+          for (int w = 0; w < W; ++w) {
+            const uint64_t x = i < planes ? ca[i * plane + w] : ra[w];
+            const uint64_t y = j < planes ? cb[j * plane + w] : rb[w];
+            hit |= (x & y) != 0;
+          }
+        }
+        if (hit) {
+          const int32_t val = (int32_t)(da + db + tt);
+          if (val < mine) mine = val;
+          break;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mine = min(mine, __shfl_xor_sync(0xFFFFFFFFu, mine, o));
+    if (lane == 0 && mine < prev) atomicMin(&best[qi], mine);
+  }
+}
+
+template <int DB>
+static void launch_query_wide_db(unsigned blocks, uint32_t n, uint32_t C, uint32_t W, uint32_t d, uint32_t planes,
+                                 const void* dist, const uint64_t* masks, const uint16_t* sizes, const uint32_t* s,
+                                 const uint32_t* t, uint64_t q, int32_t* best, int* bad, cudaStream_t st) {
+  switch (W) {
+    case 1: k_query_wide<DB, 1><<<blocks, 256, 0, st>>>(n, C, d, planes, dist, masks, sizes, s, t, q, best, bad); break;
+    case 2: k_query_wide<DB, 2><<<blocks, 256, 0, st>>>(n, C, d, planes, dist, masks, sizes, s, t, q, best, bad); break;
+    case 4: k_query_wide<DB, 4><<<blocks, 256, 0, st>>>(n, C, d, planes, dist, masks, sizes, s, t, q, best, bad); break;
+    default: k_query_wide<DB, 8><<<blocks, 256, 0, st>>>(n, C, d, planes, dist, masks, sizes, s, t, q, best, bad);
+  }
+}
+
 static int launch_query(uint32_t n, uint32_t C, uint32_t d, uint32_t planes, const void* dist, uint32_t dist_bytes,
                         const void* masks, const uint8_t* sizes, const uint32_t* s, const uint32_t* t, uint64_t q,
                         int32_t* best, int* bad, cudaStream_t st, const uint32_t* inv = nullptr,
@@ -274,6 +382,51 @@ int cbfs_decode(uint32_t n, uint32_t C, uint32_t d, uint32_t planes, const void*
   else
     k_decode<2><<<grid_for(n, 256), 256, 0, st>>>(n, C, d, planes, dist, masks, c, k, out);
   CBFS_LAUNCHED();
+  return CBFS_OK;
+}
+
+int cbfs_decode_wide(uint32_t n, uint32_t C, uint32_t words, uint32_t d, uint32_t planes, const void* dist,
+                     uint32_t dist_bytes, const uint64_t* masks, uint32_t c, uint32_t k, uint16_t* out,
+                     cbfs_stream stream) {
+  if (!dist || !masks || !out) return fail(CBFS_EINVAL, "null argument");
+  if (words != 1 && words != 2 && words != 4 && words != 8) return fail(CBFS_EUNSUPPORTED, "words must be 1, 2, 4 or 8");
+  if (c >= C || k == 0 || k > 64 * words) return fail(CBFS_EINVAL, "bad cluster index or k");
+  if (d > CBFS_MAX_D || (planes != d + 1 && !(planes == d && d > 0))) return fail(CBFS_EINVAL, "bad d/planes");
+  if (dist_bytes != 1 && dist_bytes != 2) return fail(CBFS_EINVAL, "dist_bytes must be 1 or 2");
+  if (n == 0) return CBFS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dist_bytes == 1)
+    k_decode_wide<1><<<grid_for(n, 256), 256, 0, st>>>(n, C, words, d, planes, dist, masks, c, k, out);
+  else
+    k_decode_wide<2><<<grid_for(n, 256), 256, 0, st>>>(n, C, words, d, planes, dist, masks, c, k, out);
+  CBFS_LAUNCHED();
+  return CBFS_OK;
+}
+
+int cbfs_query_distance_wide(uint32_t n, uint32_t C, uint32_t words, uint32_t d, uint32_t planes, const void* dist,
+                             uint32_t dist_bytes, const uint64_t* masks, const uint16_t* sizes, const uint32_t* s,
+                             const uint32_t* t, uint64_t q, int32_t* inout_best, cbfs_stream stream) {
+  if (q && (!s || !t || !inout_best)) return fail(CBFS_EINVAL, "null query arrays");
+  if (C && (!dist || !masks || !sizes)) return fail(CBFS_EINVAL, "null label arrays");
+  if (words != 1 && words != 2 && words != 4 && words != 8) return fail(CBFS_EUNSUPPORTED, "words must be 1, 2, 4 or 8");
+  if (d > CBFS_MAX_D || (planes != d + 1 && !(planes == d && d > 0))) return fail(CBFS_EINVAL, "bad d/planes");
+  if (dist_bytes != 1 && dist_bytes != 2) return fail(CBFS_EINVAL, "dist_bytes must be 1 or 2");
+  if (q == 0 || C == 0) return CBFS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  int* bad = nullptr;
+  CBFS_CUDA(cudaMallocAsync(&bad, sizeof(int), st));
+  CBFS_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+  const unsigned blocks = grid_for(q * 32, 256, 148u * 8u * 8u);
+  if (dist_bytes == 1)
+    launch_query_wide_db<1>(blocks, n, C, words, d, planes, dist, masks, sizes, s, t, q, inout_best, bad, st);
+  else
+    launch_query_wide_db<2>(blocks, n, C, words, d, planes, dist, masks, sizes, s, t, q, inout_best, bad, st);
+  CBFS_LAUNCHED();
+  int hbad = 0;
+  CBFS_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CBFS_CUDA(cudaFreeAsync(bad, st));
+  CBFS_CUDA(cudaStreamSynchronize(st));
+  if (hbad) return fail(CBFS_EINVAL, "query vertex id >= n");
   return CBFS_OK;
 }
 

@@ -482,3 +482,94 @@ def test_bidir_refine_pins():
     a = np.array([0], np.uint32); b = np.array([9], np.uint32)
     assert orc.bidir_refine(p, a, b, 5)[0] == orc.INT32_MAX  # {0..4} and {5..9} are disjoint
     assert orc.bidir_refine(p, a, b, 6)[0] == 9               # they meet at 4 and 5
+
+
+# ------------------------------------------------------------------ clusters of k > 64 (NEXT-1)
+def _wide_from_definition(D: np.ndarray, d: int):
+    """The definition P:630-636 from a scipy [k][n] matrix, one word per 64 sources."""
+    k, n = D.shape
+    W = (k + 63) // 64
+    dist = np.full(n, orc.INF16, np.uint16)
+    sub = np.zeros((d + 1, n, W), np.uint64)
+    for v in range(n):
+        col = D[:, v]
+        if not (col >= 0).any():
+            continue
+        mn = int(col[col >= 0].min())
+        dist[v] = mn
+        for j in np.flatnonzero(col >= 0):
+            sub[int(col[j]) - mn, v, j // 64] |= np.uint64(1 << (int(j) % 64))
+    return dist, sub
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_wide_definition_matches_scipy_and_alg1(seed):
+    """brute_cluster_wide == the definition over scipy distances for k up to
+    300, and == Alg. 1 (the C oracle, pinned above) word for word when
+    k <= 64."""
+    rng = np.random.default_rng(900 + seed)
+    n = int(rng.integers(400, 700))
+    g = random_graph(rng, n, "er" if seed % 2 else "pa")
+    root = int(np.argmax(g.degrees()))
+    for h in range(2, 8):  # the smallest ball radius that holds more than 64 sources
+        S = ball_cluster(g, root, h, 300, rng)
+        if len(S) > 64:
+            break
+    assert len(S) > 64
+    d = 2 * h
+    dist, sub, over = orc.brute_cluster_wide(g, S, d)
+    assert not over
+    rd, rs = _wide_from_definition(scipy_dist(g, S), d)
+    assert np.array_equal(dist, rd) and np.array_equal(sub, rs)
+    small = S[:40]
+    dist, sub, _ = orc.brute_cluster_wide(g, small, d)
+    res = orc.cluster_bfs(g, small, d)
+    assert sub.shape[2] == 1
+    assert np.array_equal(dist, res.dist) and np.array_equal(sub[:, :, 0], res.sub)
+
+
+def test_wide_star_closed_form():
+    """K_{1,L} with S = centre + 199 leaves (4 words): centre Delta 0,
+    S[0] = {c}, S[1] = the member leaves; a member leaf: S[0] = itself,
+    S[1] = {c}, S[2] = the other members; any other leaf: Delta 1,
+    S[0] = {c}, S[1] = the members (SURVEY §8(c) closed forms at k > 64)."""
+    L, k = 260, 200
+    g = graph_from_pairs(L + 1, [x for i in range(1, L + 1) for x in (0, i)])
+    S = list(range(k))
+    dist, sub, over = orc.brute_cluster_wide(g, S, 2)
+    assert not over and sub.shape == (3, L + 1, 4)
+
+    def words(bits):
+        w = [0, 0, 0, 0]
+        for j in bits:
+            w[j // 64] |= 1 << (j % 64)
+        return [np.uint64(x) for x in w]
+    members = range(1, k)
+    assert dist[0] == 0 and list(sub[0, 0]) == words([0]) and list(sub[1, 0]) == words(members)
+    for j in (1, 63, 64, 130, 199):
+        assert dist[j] == 0 and list(sub[0, j]) == words([j]) and list(sub[1, j]) == words([0])
+        assert list(sub[2, j]) == words([x for x in members if x != j])
+    for v in (200, 260):
+        assert dist[v] == 1 and list(sub[0, v]) == words([0]) and list(sub[1, v]) == words(members)
+        assert not sub[2, v].any()
+
+
+def test_wide_query_brute_pins():
+    """query_brute == the C R15 scan (orc.query over Alg. 1 labels, pinned in
+    test_query_pins) on k <= 64 clusters of diameter <= d, and on a path it
+    is min_j |u - s_j| + |s_j - v| (closed form) for a cluster of 150."""
+    rng = np.random.default_rng(77)
+    g = random_graph(rng, 300, "pa")
+    d = 4
+    src, sz = orc.select_clusters(g, 5, 30, d)
+    many = orc.cluster_bfs_many(g, src, sz, d, threads=2)
+    s = rng.integers(0, g.n, 400).astype(np.uint32); t = rng.integers(0, g.n, 400).astype(np.uint32)
+    clusters = [src[c, :sz[c]] for c in range(len(sz))]
+    assert np.array_equal(orc.query_brute(g, clusters, s, t), orc.query(many["dist"], many["sub"], s, t))
+    n = 500
+    g = graph_from_pairs(n, [x for i in range(n - 1) for x in (i, i + 1)])
+    S = np.arange(200, 350)
+    s = rng.integers(0, n, 300); t = rng.integers(0, n, 300)
+    got = orc.query_brute(g, [S], s, t)
+    expect = [min(abs(int(u) - int(x)) + abs(int(x) - int(v)) for x in S) for u, v in zip(s, t)]
+    assert np.array_equal(got, np.array(expect, np.int32))
