@@ -129,6 +129,17 @@ int cbfs_select_clusters(const cbfs_graph* g, uint32_t r, uint32_t k, uint32_t d
                          uint64_t seed, uint32_t* out_sources, uint8_t* out_sizes, uint32_t* out_r,
                          cbfs_stream stream);
 
+/* cbfs_select_clusters_wide — the same rule for clusters of up to
+ * k <= 64 * words sources (general k; input of cbfs_run_wide):
+ *   out_sources : device [r][64 * words] uint32 (padding 0xFFFFFFFF)
+ *   out_sizes   : device [r] uint16
+ *   words       : 1, 2, 4 or 8
+ * Errors: EINVAL (k == 0 or k > 64 * words, null outputs), EUNSUPPORTED
+ * (words, d > MAX_D).  Synchronises. */
+int cbfs_select_clusters_wide(const cbfs_graph* g, uint32_t r, uint32_t k, uint32_t d, uint32_t root_policy,
+                              uint64_t seed, uint32_t words, uint32_t* out_sources, uint16_t* out_sizes,
+                              uint32_t* out_r, cbfs_stream stream);
+
 /* --------------------------------------------------------------- C-BFS
  * cbfs_run — Cluster-BFS (Alg. 1, with R1 seeding, R3 cap, R4
  * claim, R5 output) from each of `n_clusters` clusters, d = the cluster

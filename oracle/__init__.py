@@ -74,6 +74,10 @@ def lib():
         L.or_select_clusters.restype = ctypes.c_int64
         L.or_select_clusters.argtypes = [ctypes.c_uint32, u64p, u32p, ctypes.c_uint32, ctypes.c_uint32,
                                          ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64, _RANDFN, u32p, u8p]
+        L.or_select_clusters_wide.restype = ctypes.c_int64
+        L.or_select_clusters_wide.argtypes = [ctypes.c_uint32, u64p, u32p, ctypes.c_uint32, ctypes.c_uint32,
+                                              ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64, _RANDFN,
+                                              ctypes.c_uint32, u32p, u16p]
         L.or_query.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, u16p, u64p, ctypes.c_uint64, u32p,
                                u32p, i32p]
         L.or_query_stream.argtypes = [ctypes.c_uint32, u64p, u32p, u32p, u8p, ctypes.c_uint32, ctypes.c_uint32,
@@ -298,6 +302,20 @@ def select_clusters(g: CSR, r: int, k: int, d: int, policy: int = ROOT_DEGREE, s
     sizes = np.zeros(max(r, 1), np.uint8)
     got = lib().or_select_clusters(g.n, _p(g.off, ctypes.c_uint64), _p(g.cols, ctypes.c_uint32), r, k, d, policy,
                                    seed, _rand_cb, _p(out, ctypes.c_uint32), _p(sizes, ctypes.c_uint8))
+    if got < 0:
+        raise ValueError("bad selection arguments")
+    return out[:got].copy(), sizes[:got].copy()
+
+
+def select_clusters_wide(g: CSR, r: int, k: int, d: int, words: int, policy: int = ROOT_DEGREE, seed: int = 0):
+    """The same rule (R12) for clusters of up to k <= 64 * words
+    sources (the paper's general k).  Returns (sources [r'][64 words]
+    uint32 padded with 0xFFFFFFFF, sizes [r'] uint16)."""
+    out = np.full((max(r, 1), 64 * words), PAD, np.uint32)
+    sizes = np.zeros(max(r, 1), np.uint16)
+    got = lib().or_select_clusters_wide(g.n, _p(g.off, ctypes.c_uint64), _p(g.cols, ctypes.c_uint32), r, k, d,
+                                        policy, seed, _rand_cb, words, _p(out, ctypes.c_uint32),
+                                        _p(sizes, ctypes.c_uint16))
     if got < 0:
         raise ValueError("bad selection arguments")
     return out[:got].copy(), sizes[:got].copy()

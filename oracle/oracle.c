@@ -253,10 +253,13 @@ static int by_deg_desc_id_asc(const void* a, const void* b) {
   return x < y ? -1 : (x > y ? 1 : 0);
 }
 
-int64_t or_select_clusters(uint32_t n, const uint64_t* off, const uint32_t* cols, uint32_t r, uint32_t k,
-                           uint32_t d, uint32_t policy, uint64_t seed, or_rand_fn rand_fn,
-                           uint32_t* out_sources, uint8_t* out_sizes) {
-  if (k == 0 || k > 64 || (policy == 1 && !rand_fn)) return -1;
+/* clusters of up to k <= stride sources (stride = 64 words of 64 sources
+ * each for k > 64, the paper's general k); sizes as uint8 (k <= 64)
+ * or uint16 */
+static int64_t select_clusters_any(uint32_t n, const uint64_t* off, const uint32_t* cols, uint32_t r, uint32_t k,
+                                   uint32_t d, uint32_t policy, uint64_t seed, or_rand_fn rand_fn, uint32_t stride,
+                                   uint32_t* out_sources, uint8_t* out_sizes8, uint16_t* out_sizes16) {
+  if (k == 0 || k > stride || (policy == 1 && !rand_fn)) return -1;
   uint32_t* deg = (uint32_t*)malloc(sizeof(uint32_t) * (n ? n : 1));
   for (uint32_t v = 0; v < n; ++v) deg[v] = (uint32_t)(off[v + 1] - off[v]);
   uint8_t* marked = (uint8_t*)calloc(n ? n : 1, 1);
@@ -302,16 +305,32 @@ int64_t or_select_clusters(uint32_t n, const uint64_t* off, const uint32_t* cols
     for (uint64_t t = 0; t < nb; ++t) hop[ball[t]] = OR_INF32;
     qsort(cand, nc, sizeof(uint32_t), by_deg_desc_id_asc);
     uint32_t sz = 0;
-    uint32_t* outS = out_sources + (size_t)c * 64;
-    for (int j = 0; j < 64; ++j) outS[j] = OR_INF32;
+    uint32_t* outS = out_sources + (size_t)c * stride;
+    for (uint32_t j = 0; j < stride; ++j) outS[j] = OR_INF32;
     outS[sz++] = root;
     for (uint64_t t = 0; t < nc && sz < k; ++t) outS[sz++] = cand[t];
     for (uint32_t j = 0; j < sz; ++j) { marked[outS[j]] = 1; avail -= deg[outS[j]] > 0; }
-    out_sizes[c] = (uint8_t)sz;
+    if (out_sizes8) out_sizes8[c] = (uint8_t)sz;
+    if (out_sizes16) out_sizes16[c] = (uint16_t)sz;
     produced++;
   }
   free(deg); free(marked); free(hop); free(ball); free(cand); free(order);
   return produced;
+}
+
+int64_t or_select_clusters(uint32_t n, const uint64_t* off, const uint32_t* cols, uint32_t r, uint32_t k,
+                           uint32_t d, uint32_t policy, uint64_t seed, or_rand_fn rand_fn,
+                           uint32_t* out_sources, uint8_t* out_sizes) {
+  if (k > 64) return -1;
+  return select_clusters_any(n, off, cols, r, k, d, policy, seed, rand_fn, 64, out_sources, out_sizes, NULL);
+}
+
+/* the same rule for k up to 64 * words sources: out_sources [r][64 words], sizes uint16 */
+int64_t or_select_clusters_wide(uint32_t n, const uint64_t* off, const uint32_t* cols, uint32_t r, uint32_t k,
+                                uint32_t d, uint32_t policy, uint64_t seed, or_rand_fn rand_fn, uint32_t words,
+                                uint32_t* out_sources, uint16_t* out_sizes) {
+  if (words == 0 || words > 64) return -1;
+  return select_clusters_any(n, off, cols, r, k, d, policy, seed, rand_fn, 64 * words, out_sources, NULL, out_sizes);
 }
 
 /* ---------------------------------------------------------------------

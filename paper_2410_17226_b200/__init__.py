@@ -50,6 +50,7 @@ _sig("cbfs_graph_info", [_vp, ctypes.POINTER(_u32), ctypes.POINTER(_u64), ctypes
 _sig("cbfs_graph_export_csr", [_vp, _vp, _vp])
 _sig("cbfs_graph_destroy", [_vp])
 _sig("cbfs_select_clusters", [_vp, _u32, _u32, _u32, _u32, _u64, _vp, _vp, ctypes.POINTER(_u32), _vp])
+_sig("cbfs_select_clusters_wide", [_vp, _u32, _u32, _u32, _u32, _u64, _u32, _vp, _vp, ctypes.POINTER(_u32), _vp])
 _sig("cbfs_run", [_vp, _vp, _vp, _u32, _u32, _u32, _vp, _vp, _u32, _vp, _u32, _vp])
 _sig("cbfs_select_and_run", [_vp, _u32, _u32, _u32, _u32, _u64, _vp, _vp, ctypes.POINTER(_u32), _u32, _vp, _vp,
                               _u32, _vp, _u32, _vp])
@@ -157,6 +158,14 @@ def cbfs_select_clusters(h, r, k, d, root_policy, seed, out_sources, out_sizes, 
     got = _u32()
     _check(_lib.cbfs_select_clusters(h, r, k, d, root_policy, seed, _ptr(out_sources), _ptr(out_sizes),
                                      ctypes.byref(got), _stream(stream)))
+    return got.value
+
+
+def cbfs_select_clusters_wide(h, r, k, d, root_policy, seed, words, out_sources, out_sizes, stream=None) -> int:
+    """out_sources [r][64 * words] int32, out_sizes [r] int16 (uint16 values)."""
+    got = _u32()
+    _check(_lib.cbfs_select_clusters_wide(h, r, k, d, root_policy, seed, words, _ptr(out_sources), _ptr(out_sizes),
+                                          ctypes.byref(got), _stream(stream)))
     return got.value
 
 

@@ -116,7 +116,7 @@ int run_batches(Graph* g, BatchSource& src, cudaStream_t st);
 int num_slots(const Graph* g);  // concurrent batches of the leased workspace
 int select_launch(const Graph* g, uint32_t r, uint32_t k, uint32_t d, uint32_t root_policy, uint64_t seed,
                   uint32_t* out_sources, uint8_t* out_sizes, uint32_t* d_count, volatile uint32_t* progress,
-                  cudaStream_t st);
+                  cudaStream_t st, uint32_t words = 1, uint16_t* out_sizes16 = nullptr);
 int check_select_args(const Graph* g, uint32_t r, uint32_t k, uint32_t d, uint32_t root_policy,
                       const void* out_sources, const void* out_sizes);
 // cbfs_run with the output bit-subset words mask_bytes wide (1/2/4/8)

@@ -32,12 +32,12 @@ k_select(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cols, co
          const uint32_t* __restrict__ order, const uint32_t* __restrict__ perm, const uint32_t* __restrict__ inv,
          uint32_t n, uint32_t r, uint32_t k, uint32_t d, uint32_t policy, uint64_t seed, SelScratch S,
          uint32_t* __restrict__ out_sources, uint8_t* __restrict__ out_sizes, uint32_t* __restrict__ out_count,
-         volatile uint32_t* progress) {
+         volatile uint32_t* progress, uint32_t stride, uint16_t* __restrict__ out_sizes16) {
   __shared__ unsigned s_na, s_nb, s_nc, s_nsel, s_root;
   __shared__ unsigned long long s_avail;
   __shared__ unsigned hist[256];
   __shared__ unsigned s_need, s_prefix, s_pmask;
-  __shared__ unsigned sel[64];
+  __shared__ unsigned sel[64 * CBFS_WIDE_MAX_W];
   __shared__ unsigned s_cand[SEL_THREADS];  // the first SEL_THREADS candidate ranks (the common case)
   const unsigned tid = threadIdx.x, lane = tid & 31;
   const uint32_t h = d / 2;
@@ -128,7 +128,7 @@ k_select(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cols, co
     // ---- the best k-1 candidates by rank (degree desc, id asc), in rank order
     const unsigned nc = s_nc;
     const unsigned ns = min(nc, want);
-    uint32_t* outS = out_sources + (uint64_t)c * 64;
+    uint32_t* outS = out_sources + (uint64_t)c * stride;
     unsigned long long dec = 0;
     if (nc <= SEL_THREADS) {
       // rank by counting (ranks are unique): candidate t is selected iff fewer
@@ -205,7 +205,8 @@ k_select(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cols, co
       outS[0] = perm ? perm[root] : root;
       S.marked[root] = 1;
       dec += 1;  // root is non-isolated
-      out_sizes[c] = (uint8_t)(1 + ns);
+      if (out_sizes16) out_sizes16[c] = (uint16_t)(1 + ns);
+      else out_sizes[c] = (uint8_t)(1 + ns);
     }
     if (dec) atomicAdd(&s_avail, (unsigned long long)0 - dec);  // subtract
     ++produced;
@@ -240,7 +241,7 @@ namespace cbfs {
 // every cluster.
 int select_launch(const Graph* g, uint32_t r, uint32_t k, uint32_t d, uint32_t root_policy, uint64_t seed,
                   uint32_t* out_sources, uint8_t* out_sizes, uint32_t* d_count, volatile uint32_t* progress,
-                  cudaStream_t st) {
+                  cudaStream_t st, uint32_t words, uint16_t* out_sizes16) {
   const uint32_t n = g->n;
   SelScratch S;
   CBFS_CUDA(cudaMallocAsync(&S.marked, n, st));
@@ -250,10 +251,11 @@ int select_launch(const Graph* g, uint32_t r, uint32_t k, uint32_t d, uint32_t r
   CBFS_CUDA(cudaMallocAsync(&S.cand, sizeof(uint32_t) * n, st));
   CBFS_CUDA(cudaMemsetAsync(S.marked, 0, n, st));
   CBFS_CUDA(cudaMemsetAsync(S.stamp, 0, sizeof(uint32_t) * n, st));
-  CBFS_CUDA(cudaMemsetAsync(out_sources, 0xFF, sizeof(uint32_t) * 64ULL * r, st));
-  CBFS_CUDA(cudaMemsetAsync(out_sizes, 0, r, st));
+  CBFS_CUDA(cudaMemsetAsync(out_sources, 0xFF, sizeof(uint32_t) * 64ULL * words * r, st));
+  if (out_sizes16) CBFS_CUDA(cudaMemsetAsync(out_sizes16, 0, sizeof(uint16_t) * (uint64_t)r, st));
+  else CBFS_CUDA(cudaMemsetAsync(out_sizes, 0, r, st));
   k_select<<<1, SEL_THREADS, 0, st>>>(g->off, g->cols, g->rank, g->order, g->perm, g->inv, n, r, k, d, root_policy,
-                                      seed, S, out_sources, out_sizes, d_count, progress);
+                                      seed, S, out_sources, out_sizes, d_count, progress, 64 * words, out_sizes16);
   CBFS_LAUNCHED();
   CBFS_CUDA(cudaFreeAsync(S.marked, st));
   CBFS_CUDA(cudaFreeAsync(S.stamp, st));
@@ -274,6 +276,30 @@ int check_select_args(const Graph* g, uint32_t r, uint32_t k, uint32_t d, uint32
 }
 }  // namespace cbfs
 
+extern "C" int cbfs_select_clusters_wide(const cbfs_graph* gh, uint32_t r, uint32_t k, uint32_t d,
+                                         uint32_t root_policy, uint64_t seed, uint32_t words, uint32_t* out_sources,
+                                         uint16_t* out_sizes, uint32_t* out_r, cbfs_stream stream) {
+  const Graph* g = reinterpret_cast<const Graph*>(gh);
+  if (words != 1 && words != 2 && words != 4 && words != 8) return fail(CBFS_EUNSUPPORTED, "words must be 1, 2, 4 or 8");
+  if (k > 64 * words) return fail(CBFS_EINVAL, "k > 64 * words");
+  int rc = check_select_args(g, r, k <= CBFS_MAX_K ? k : 1, d, root_policy, out_sources, out_sizes);
+  if (rc) return rc;
+  if (k == 0) return fail(CBFS_EINVAL, "k must be >= 1");
+  if (!out_r) return fail(CBFS_EINVAL, "null out_r");
+  *out_r = 0;
+  if (r == 0 || g->n == 0) return CBFS_OK;
+  CBFS_CUDA(cudaSetDevice(g->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  uint32_t* d_count = nullptr;
+  CBFS_CUDA(cudaMallocAsync(&d_count, sizeof(uint32_t), st));
+  rc = select_launch(g, r, k, d, root_policy, seed, out_sources, nullptr, d_count, nullptr, st, words, out_sizes);
+  if (rc) return rc;
+  CBFS_CUDA(cudaMemcpyAsync(out_r, d_count, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  CBFS_CUDA(cudaFreeAsync(d_count, st));
+  CBFS_CUDA(cudaStreamSynchronize(st));
+  return CBFS_OK;
+}
+
 extern "C" int cbfs_select_clusters(const cbfs_graph* gh, uint32_t r, uint32_t k, uint32_t d, uint32_t root_policy,
                                     uint64_t seed, uint32_t* out_sources, uint8_t* out_sizes, uint32_t* out_r,
                                     cbfs_stream stream) {
@@ -287,7 +313,7 @@ extern "C" int cbfs_select_clusters(const cbfs_graph* gh, uint32_t r, uint32_t k
   cudaStream_t st = (cudaStream_t)stream;
   uint32_t* d_count = nullptr;
   CBFS_CUDA(cudaMallocAsync(&d_count, sizeof(uint32_t), st));
-  rc = select_launch(g, r, k, d, root_policy, seed, out_sources, out_sizes, d_count, nullptr, st);
+  rc = select_launch(g, r, k, d, root_policy, seed, out_sources, out_sizes, d_count, nullptr, st, 1, nullptr);
   if (rc) return rc;
   CBFS_CUDA(cudaMemcpyAsync(out_r, d_count, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   CBFS_CUDA(cudaFreeAsync(d_count, st));

@@ -184,3 +184,27 @@ def test_wide_c2_full_size_sampled():
         assert np.array_equal(dh[:, c], od)
         assert np.array_equal(mh[:, :, c * 4:c * 4 + osub.shape[2]], osub)
     g.close()
+
+
+@pytest.mark.parametrize("kind,d,W,k,relabel,policy", [("rmat", 2, 4, 256, True, 0), ("rmat", 2, 2, 100, False, 0),
+                                                       ("er", 4, 8, 512, True, 0), ("grid", 4, 2, 70, False, 1),
+                                                       ("rmat", 2, 8, 300, True, 1)])
+def test_select_wide_matches_oracle_and_runs(kind, d, W, k, relabel, policy):
+    """cbfs_select_clusters_wide == the oracle's selection (R12, general k),
+    and the selected clusters through cbfs_run_wide == the definition."""
+    el = GRAPHS[kind]()
+    ref = orc.csr_from_edgelist(el)
+    g = gpu_graph(el, relabel=relabel)
+    r = 40
+    src = torch.empty((r, 64 * W), dtype=torch.int32, device=DEV)
+    sz = torch.empty((r,), dtype=torch.int16, device=DEV)
+    got = cb.cbfs_select_clusters_wide(g.h, r, k, d, policy, 5, W, src, sz)
+    osrc, osz = orc.select_clusters_wide(ref, r, k, d, W, policy, seed=5)
+    assert got == len(osz)
+    assert np.array_equal(src[:got].cpu().numpy().view(np.uint32), osrc)
+    assert np.array_equal(sz[:got].cpu().numpy().view(np.uint16), osz)
+    assert int(osz.max()) > 64 or W == 2 or policy == 1
+    lists = [osrc[c, :osz[c]] for c in range(got)]
+    dist, masks, _ = run_wide(g, osrc, osz, W, d)
+    check_against_oracle(ref, lists[:12], dist, masks, W, d, d + 1)
+    g.close()

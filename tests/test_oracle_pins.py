@@ -573,3 +573,33 @@ def test_wide_query_brute_pins():
     got = orc.query_brute(g, [S], s, t)
     expect = [min(abs(int(u) - int(x)) + abs(int(x) - int(v)) for x in S) for u, v in zip(s, t)]
     assert np.array_equal(got, np.array(expect, np.int32))
+
+
+def test_select_wide_pins():
+    """Selection with k > 64 (R12, general k): equals the k <= 64
+    rule (pinned above) when k <= 64; on K_{1,300} with k = 200 the first
+    cluster is the centre + the 199 lowest-id leaves (all leaves tie on
+    degree), the next roots are the remaining leaves in id order; clusters
+    are disjoint and within floor(d/2) hops of their root."""
+    rng = np.random.default_rng(31)
+    g = random_graph(rng, 400, "pa")
+    a_src, a_sz = orc.select_clusters(g, 9, 40, 2)
+    b_src, b_sz = orc.select_clusters_wide(g, 9, 40, 2, 2)
+    assert np.array_equal(a_sz, b_sz) and np.array_equal(a_src, b_src[:, :64]) and (b_src[:, 64:] == orc.PAD).all()
+    L = 300
+    star = graph_from_pairs(L + 1, [x for i in range(1, L + 1) for x in (0, i)])
+    src, sz = orc.select_clusters_wide(star, 3, 200, 2, 4)
+    assert list(sz) == [200, 1, 1]
+    assert list(src[0, :200]) == list(range(200)) and (src[0, 200:] == orc.PAD).all()
+    assert src[1, 0] == 200 and src[2, 0] == 201
+    src, sz = orc.select_clusters_wide(g, 6, 150, 4, 4)
+    seen = set()
+    for c in range(len(sz)):
+        S = src[c, :sz[c]].tolist()
+        assert not (set(S) & seen)
+        seen |= set(S)
+        D = scipy_dist(g, [S[0]])[0]
+        assert all(0 <= D[x] <= 2 for x in S)
+        degs = g.degrees()[S[1:]].astype(np.int64)
+        assert all((degs[i] > degs[i + 1]) or (degs[i] == degs[i + 1] and S[1 + i] < S[2 + i])
+                   for i in range(len(degs) - 1))
