@@ -78,6 +78,11 @@ def lib():
         L.or_select_clusters_wide.argtypes = [ctypes.c_uint32, u64p, u32p, ctypes.c_uint32, ctypes.c_uint32,
                                               ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64, _RANDFN,
                                               ctypes.c_uint32, u32p, u16p]
+        L.or_pll_build.restype = ctypes.c_int64
+        L.or_pll_build.argtypes = [ctypes.c_uint32, u64p, u32p, u32p, u8p, ctypes.c_uint32, ctypes.c_uint32, u16p,
+                                   u64p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, u32p, u32p]
+        L.or_pll_query.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, u16p, u64p, ctypes.c_uint32,
+                                   u32p, u32p, ctypes.c_uint64, u32p, u32p, i32p]
         L.or_query.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, u16p, u64p, ctypes.c_uint64, u32p,
                                u32p, i32p]
         L.or_query_stream.argtypes = [ctypes.c_uint32, u64p, u32p, u32p, u8p, ctypes.c_uint32, ctypes.c_uint32,
@@ -373,3 +378,53 @@ def record_bytes(w: int, d: int) -> int:
 
 def budget_to_clusters(t: int, w: int, d: int) -> int:
     return int(lib().or_budget_to_clusters(t, w, d))
+
+
+# ---------------------------------------------------------------- exact 2-hop oracle (PLL, NEXT-4)
+def pll_build(g: CSR, sources, sizes, d: int, first: int = 200, bmax: int = 1000, cap: int = 256,
+              threads: int | None = None) -> dict:
+    """PLL with a C-BFS first phase, reading R29: the given
+    clusters' labels (Alg. 1) for every vertex, then pruned BFSs from the
+    uncovered vertices in (degree desc, id asc) order, batches first,
+    floor(3/2 b), ... up to bmax, each batch pruned against the index as of
+    its start.  Returns dict(counts [n], entries [n][cap] (pos << 8 | dist,
+    ascending), cdist [C][n], csub [C][d+1][n], total, d, cap)."""
+    sources = np.ascontiguousarray(sources, dtype=np.uint32).reshape(-1, 64)
+    sizes = np.ascontiguousarray(sizes, dtype=np.uint8)
+    C = len(sizes)
+    if C:
+        many = cluster_bfs_many(g, sources, sizes, d, threads=threads)
+        cdist, csub = many["dist"], many["sub"]
+    else:
+        cdist = np.zeros((0, g.n), np.uint16)
+        csub = np.zeros((0, d + 1, g.n), np.uint64)
+    counts = np.zeros(max(g.n, 1), np.uint32)
+    entries = np.zeros((max(g.n, 1), cap), np.uint32)
+    total = lib().or_pll_build(g.n, _p(g.off, ctypes.c_uint64), _p(g.cols, ctypes.c_uint32),
+                               _p(sources, ctypes.c_uint32), _p(sizes, ctypes.c_uint8), C, d,
+                               _p(np.ascontiguousarray(cdist), ctypes.c_uint16),
+                               _p(np.ascontiguousarray(csub), ctypes.c_uint64), first, bmax, cap,
+                               _p(counts, ctypes.c_uint32), _p(entries, ctypes.c_uint32))
+    if total == -2:
+        raise OverflowError("a label list exceeds cap")
+    if total < 0:
+        raise ValueError(f"pll_build failed ({total})")
+    return dict(counts=counts[:g.n], entries=entries[:g.n], cdist=cdist, csub=csub, total=int(total), d=d, cap=cap,
+                n=g.n)
+
+
+def pll_query(idx: dict, s, t) -> np.ndarray:
+    """Exact distance by the 2-hop cover: min of the cluster
+    labels' value (R15 scan) and min over common hubs; INT32_MAX unreachable."""
+    s = np.ascontiguousarray(s, dtype=np.uint32)
+    t = np.ascontiguousarray(t, dtype=np.uint32)
+    out = np.empty(len(s), np.int32)
+    C = idx["cdist"].shape[0]
+    rc = lib().or_pll_query(idx["n"], C, idx["d"], _p(np.ascontiguousarray(idx["cdist"]), ctypes.c_uint16),
+                            _p(np.ascontiguousarray(idx["csub"]), ctypes.c_uint64), idx["cap"],
+                            _p(np.ascontiguousarray(idx["counts"]), ctypes.c_uint32),
+                            _p(np.ascontiguousarray(idx["entries"]), ctypes.c_uint32), len(s),
+                            _p(s, ctypes.c_uint32), _p(t, ctypes.c_uint32), _p(out, ctypes.c_int32))
+    if rc:
+        raise ValueError("query vertex out of range")
+    return out

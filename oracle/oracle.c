@@ -557,3 +557,126 @@ int or_bidir_refine(uint32_t n, const uint64_t* off, const uint32_t* cols, uint6
   free(mark_s); free(dist_s); free(ord_s); free(mark_t); free(dist_t); free(ord_t);
   return 0;
 }
+
+/* ---------------------------------------------------------------------
+ * Exact 2-hop distance oracle: PLL with a C-BFS first phase,
+ * reading R29.
+ *   vertex order: degree desc, id asc (pos[v] = position);
+ *   phase 1: the C given clusters (diameter <= d); their labels are the
+ *     cluster distance vectors of every vertex (dist16 [C][n], sub
+ *     [C][d+1][n], from Alg. 1); every source of a cluster is "covered";
+ *   phase 2: the uncovered vertices in order, in batches b_0 = first,
+ *     b_{i+1} = min(bmax, floor(3 b_i / 2)) (200 x 1.5^i up to
+ *     1000); each root r of a batch runs a BFS pruned against the index as it
+ *     was when the batch started (R29): at a visited u at distance delta, if
+ *     query(r, u) <= delta then u is pruned (no label, not expanded),
+ *     otherwise (pos[r], delta) is appended to L(u) and u is expanded
+ *     (P:1883-1887).
+ *   query(s, t) = min(min over clusters of the R15 scan value, min over hubs
+ *     h in L(s) and L(t) of d_s(h) + d_t(h)).
+ * Labels: counts [n], entries [n][cap] = pos << 8 | dist, each list ascending
+ * (roots run in increasing pos, one entry per root per vertex).
+ * Returns the number of phase-2 labels, -1 bad arguments, -2 a list would
+ * exceed cap, -3 a label distance > 254.
+ * ------------------------------------------------------------------- */
+static int32_t pll_cluster_part(uint32_t n, uint32_t C, uint32_t d, const uint16_t* dist, const uint64_t* sub,
+                                uint32_t u, uint32_t v) {
+  int32_t best = INT32_MAX;
+  for (uint32_t c = 0; c < C; ++c) {
+    int32_t x = query_one_cluster(n, d, dist + (size_t)c * n, sub + (size_t)c * (d + 1) * n, u, v);
+    if (x < best) best = x;
+  }
+  return best;
+}
+
+static int pll_cmp_pos(const void* a, const void* b) {
+  uint32_t x = *(const uint32_t*)a, y = *(const uint32_t*)b;
+  const uint32_t* deg = g_sel_deg;
+  if (deg[x] != deg[y]) return deg[x] > deg[y] ? -1 : 1;
+  return x < y ? -1 : (x > y);
+}
+
+int64_t or_pll_build(uint32_t n, const uint64_t* off, const uint32_t* cols, const uint32_t* sources,
+                     const uint8_t* sizes, uint32_t C, uint32_t d, const uint16_t* cdist, const uint64_t* csub,
+                     uint32_t first, uint32_t bmax, uint32_t cap, uint32_t* counts, uint32_t* entries) {
+  if (first == 0 || bmax == 0 || cap == 0) return -1;
+  const size_t N = n ? n : 1;
+  uint32_t* deg = (uint32_t*)malloc(sizeof(uint32_t) * N);
+  uint32_t* order = (uint32_t*)malloc(sizeof(uint32_t) * N);
+  uint32_t* pos = (uint32_t*)malloc(sizeof(uint32_t) * N);
+  uint8_t* covered = (uint8_t*)calloc(N, 1);
+  uint32_t* snap = (uint32_t*)malloc(sizeof(uint32_t) * N);
+  int32_t* tmp = (int32_t*)malloc(sizeof(int32_t) * N);   /* hub pos -> d(r, hub) of the root's snapshot label */
+  uint32_t* mark = (uint32_t*)calloc(N, sizeof(uint32_t));
+  uint32_t* qv = (uint32_t*)malloc(sizeof(uint32_t) * N);
+  uint32_t* qd = (uint32_t*)malloc(sizeof(uint32_t) * N);
+  uint32_t* roots = (uint32_t*)malloc(sizeof(uint32_t) * N);
+  for (uint32_t v = 0; v < n; ++v) { deg[v] = (uint32_t)(off[v + 1] - off[v]); order[v] = v; counts[v] = 0; tmp[v] = -1; }
+  g_sel_deg = deg;
+  qsort(order, n, sizeof(uint32_t), pll_cmp_pos);
+  for (uint32_t p = 0; p < n; ++p) pos[order[p]] = p;
+  for (uint32_t c = 0; c < C; ++c)
+    for (uint32_t j = 0; j < sizes[c]; ++j) covered[sources[(size_t)c * 64 + j]] = 1;
+  uint32_t nroots = 0;
+  for (uint32_t p = 0; p < n; ++p) if (!covered[order[p]]) roots[nroots++] = order[p];
+  int64_t total = 0, rc = 0;
+  uint32_t b = first, stamp = 0;
+  for (uint32_t r0 = 0; r0 < nroots && rc == 0; r0 += b, b = (b * 3 / 2 < bmax ? b * 3 / 2 : bmax)) {
+    if (b > bmax) b = bmax;
+    const uint32_t r1 = r0 + b < nroots ? r0 + b : nroots;
+    memcpy(snap, counts, sizeof(uint32_t) * n);  /* the index as of the batch start */
+    for (uint32_t ri = r0; ri < r1 && rc == 0; ++ri) {
+      const uint32_t r = roots[ri];
+      for (uint32_t a = 0; a < snap[r]; ++a) tmp[entries[(size_t)r * cap + a] >> 8] = (int32_t)(entries[(size_t)r * cap + a] & 255u);
+      ++stamp;
+      uint64_t head = 0, tail = 0;
+      qv[tail] = r; qd[tail++] = 0; mark[r] = stamp;
+      while (head < tail) {
+        const uint32_t u = qv[head], du = qd[head]; ++head;
+        int64_t q = pll_cluster_part(n, C, d, cdist, csub, r, u);
+        for (uint32_t a = 0; a < snap[u]; ++a) {
+          const uint32_t e = entries[(size_t)u * cap + a];
+          if (tmp[e >> 8] >= 0 && (int64_t)tmp[e >> 8] + (e & 255u) < q) q = (int64_t)tmp[e >> 8] + (e & 255u);
+        }
+        if (q <= (int64_t)du) continue;  /* pruned */
+        if (counts[u] >= cap) { rc = -2; break; }
+        if (du > 254) { rc = -3; break; }
+        entries[(size_t)u * cap + counts[u]++] = (pos[r] << 8) | du;
+        ++total;
+        for (uint64_t e = off[u]; e < off[u + 1]; ++e) {
+          const uint32_t x = cols[e];
+          if (mark[x] != stamp) { mark[x] = stamp; qv[tail] = x; qd[tail++] = du + 1; }
+        }
+      }
+      for (uint32_t a = 0; a < snap[r]; ++a) tmp[entries[(size_t)r * cap + a] >> 8] = -1;
+    }
+  }
+  free(deg); free(order); free(pos); free(covered); free(snap); free(tmp); free(mark); free(qv); free(qd); free(roots);
+  return rc ? rc : total;
+}
+
+int or_pll_query(uint32_t n, uint32_t C, uint32_t d, const uint16_t* cdist, const uint64_t* csub, uint32_t cap,
+                 const uint32_t* counts, const uint32_t* entries, uint64_t q, const uint32_t* s, const uint32_t* t,
+                 int32_t* out) {
+  for (uint64_t j = 0; j < q; ++j) {
+    if (s[j] >= n || t[j] >= n) return -1;
+    int64_t best = pll_cluster_part(n, C, d, cdist, csub, s[j], t[j]);
+    const uint32_t* A = entries + (size_t)s[j] * cap;
+    const uint32_t* B = entries + (size_t)t[j] * cap;
+    uint32_t a = 0, bb = 0;
+    while (a < counts[s[j]] && bb < counts[t[j]]) {  /* merge of two ascending hub lists */
+      const uint32_t ha = A[a] >> 8, hb = B[bb] >> 8;
+      if (ha == hb) {
+        const int64_t x = (int64_t)(A[a] & 255u) + (B[bb] & 255u);
+        if (x < best) best = x;
+        ++a; ++bb;
+      } else if (ha < hb) {
+        ++a;
+      } else {
+        ++bb;
+      }
+    }
+    out[j] = (int32_t)best;
+  }
+  return 0;
+}

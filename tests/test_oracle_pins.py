@@ -603,3 +603,69 @@ def test_select_wide_pins():
         degs = g.degrees()[S[1:]].astype(np.int64)
         assert all((degs[i] > degs[i + 1]) or (degs[i] == degs[i + 1] and S[1 + i] < S[2 + i])
                    for i in range(len(degs) - 1))
+
+
+# ------------------------------------------------------------------ exact 2-hop oracle (PLL, NEXT-4)
+def _pll_order(g):
+    deg = g.degrees().astype(np.int64)
+    return np.lexsort((np.arange(g.n), -deg))  # degree desc, id asc
+
+
+def _batches(nroots, first, bmax):
+    out, r0, b = [], 0, min(first, bmax)
+    while r0 < nroots:
+        out.append((r0, min(r0 + b, nroots)))
+        r0 += b
+        b = min(bmax, b * 3 // 2)
+    return out
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_pll_exact_and_label_characterisation(seed):
+    """PLL (R29): every pair's answer is the BFS distance, and the label set
+    is exactly {(h, delta(h, v)) : h a phase-2 root reaching v, no vertex
+    visible to h's batch (cluster sources and roots of earlier batches) on a
+    shortest h-v path} — computed by brute force from all-pairs distances.
+    With no clusters and batches of one this is sequential PLL's canonical
+    labeling (P:1876-1887)."""
+    rng = np.random.default_rng(1300 + seed)
+    n = int(rng.integers(60, 130))
+    g = random_graph(rng, n, "er" if seed % 2 else "pa")
+    C = [0, 3, 2, 0, 5, 1][seed]
+    first, bmax = [(1, 1), (4, 16), (3, 7), (5, 30), (2, 9), (200, 1000)][seed]
+    src, sz = orc.select_clusters(g, C, 16, 2) if C else (np.zeros((0, 64), np.uint32), np.zeros(0, np.uint8))
+    idx = orc.pll_build(g, src, sz, 2, first=first, bmax=bmax, cap=n)
+    D = scipy_dist(g, np.arange(n))  # -1 = unreachable
+    s = np.repeat(np.arange(n), n).astype(np.uint32); t = np.tile(np.arange(n), n).astype(np.uint32)
+    truth = np.where(D < 0, orc.INT32_MAX, D).reshape(-1)
+    assert np.array_equal(orc.pll_query(idx, s, t), truth)
+    order = _pll_order(g)
+    pos = np.empty(n, np.int64); pos[order] = np.arange(n)
+    covered = set(src[c, j] for c in range(len(sz)) for j in range(sz[c]))
+    roots = [int(v) for v in order if v not in covered]
+    visible = np.zeros(n, bool); visible[list(covered)] = True
+    expect = {v: [] for v in range(n)}
+    for r0, r1 in _batches(len(roots), first, bmax):
+        vis_idx = np.flatnonzero(visible)
+        for h in roots[r0:r1]:
+            for v in range(n):
+                if D[h, v] < 0:
+                    continue
+                on_path = [(D[h, w] >= 0 and D[w, v] >= 0 and D[h, w] + D[w, v] == D[h, v]) for w in vis_idx]
+                if not any(on_path):
+                    expect[v].append((int(pos[h]) << 8) | int(D[h, v]))
+        visible[roots[r0:r1]] = True
+    for v in range(n):
+        assert list(idx["entries"][v, :idx["counts"][v]]) == sorted(expect[v]), v
+
+
+def test_pll_cap_overflow_and_isolated():
+    g = graph_from_pairs(6, [0, 1, 1, 2])  # vertices 3..5 isolated
+    idx = orc.pll_build(g, np.zeros((0, 64), np.uint32), np.zeros(0, np.uint8), 2, first=1, bmax=1, cap=4)
+    for v in (3, 4, 5):  # an isolated vertex's only label is itself
+        assert idx["counts"][v] == 1 and idx["entries"][v, 0] & 255 == 0
+    a = orc.pll_query(idx, np.array([0, 3, 3], np.uint32), np.array([2, 3, 4], np.uint32))
+    assert list(a) == [2, 0, orc.INT32_MAX]
+    path = graph_from_pairs(40, [x for i in range(39) for x in (i, i + 1)])
+    with pytest.raises(OverflowError):
+        orc.pll_build(path, np.zeros((0, 64), np.uint32), np.zeros(0, np.uint8), 2, first=40, bmax=40, cap=3)

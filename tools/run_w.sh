@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_wide.py -q -x > gpurun_out/wide.log 2>&1; echo "wide rc $?"; tail -3 gpurun_out/wide.log
-timeout 600 python tools/wide_probe.py c2_rmat20 1,2,4,8 > gpurun_out/wide_probe.log 2>&1; echo "probe rc $?"; cat gpurun_out/wide_probe.log | tail -5
-timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "select" > gpurun_out/w_sel.log 2>&1; echo "sel rc $?"; tail -1 gpurun_out/w_sel.log
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_wide.py tests/test_gpu_ado.py tests/test_gpu_distributed.py -q -x > gpurun_out/init.log 2>&1; echo "tests rc $?"; tail -3 gpurun_out/init.log
+for i in 1 2; do timeout 600 python bench.py --steps 5 --warmup 3 > gpurun_out/b_init$i.log 2>&1; echo "bench rc $?"; tail -1 gpurun_out/b_init$i.log | python -c "import json,sys; r=json.loads(sys.stdin.read()); print(r['value'], r['ms_per_step'], r['roofline']['frac'], r['e2e']['value'], r.get('phases_ms'))"; done
