@@ -316,6 +316,44 @@ int cbfs_labels_query(const cbfs_labels* l, const uint32_t* s, const uint32_t* t
                       cbfs_stream stream);
 int cbfs_labels_destroy(cbfs_labels* l);
 
+/* --------------------------------------------------------------- exact 2-hop oracle (PLL)
+ * cbfs_pll_build — Pruned Landmark Labeling with a C-BFS first phase
+ * (SURVEY §8(f) NEXT-4), reading R29:
+ *   phase 1: the n_clusters (<= 64) given clusters (diameter <= d, as
+ *     cbfs_run) are traversed by C-BFS; every vertex keeps its cluster
+ *     distance vector (all d+1 subsets) as its cluster label;
+ *   phase 2: every vertex not in a cluster, in (degree desc, original id
+ *     asc) order, runs a BFS pruned by the index: at a vertex u at distance
+ *     delta, if query(root, u) <= delta then u gets no label and is not
+ *     expanded, else (root, delta) joins L(u).  Roots run in batches of
+ *     first, floor(3/2 first), ... up to bmax (200 x 1.5^i up to
+ *     1000); the roots of a batch run in parallel, each pruned against the
+ *     index as it was when its batch started.
+ *   sources, sizes : device [n_clusters][64] / [n_clusters] (cbfs_run layout)
+ *   cap            : label entries per vertex (EOVERFLOW beyond; distances
+ *                    above 254 are EOVERFLOW too)
+ * The graph must outlive the index.  Errors: EINVAL, EUNSUPPORTED
+ * (n_clusters > 64, n >= 2^24), EOVERFLOW, ENOMEM, ECUDA.  Synchronises.
+ * cbfs_pll_info — phase-2 label count, largest list, roots, batches, and
+ *   the device time of phase 1 (C-BFS) and phase 2 (pruned BFSs) in ms.
+ * cbfs_pll_export — the phase-2 labels by original vertex id: counts
+ *   device [n] uint32, entries device [n][cap] uint32 = hub position << 8 |
+ *   distance (hub position in the degree order above), ascending, zero
+ *   padded.  Either pointer may be NULL.
+ * cbfs_pll_query — exact distances: out[i] = delta(s[i],
+ *   t[i]) (int32 device [q], INT32_MAX = unreachable); s, t device [q]
+ *   uint32 original ids; EINVAL on an id >= n.
+ * cbfs_pll_destroy — free the index. */
+typedef struct cbfs_pll cbfs_pll;
+int cbfs_pll_build(cbfs_graph* g, const uint32_t* sources, const uint8_t* sizes, uint32_t n_clusters, uint32_t d,
+                   uint32_t first, uint32_t bmax, uint32_t cap, cbfs_pll** out, cbfs_stream stream);
+int cbfs_pll_info(const cbfs_pll* p, uint64_t* total_labels, uint32_t* max_labels, uint32_t* roots,
+                  uint32_t* batches, float* ms_cbfs, float* ms_pbfs);
+int cbfs_pll_export(const cbfs_pll* p, uint32_t* counts, uint32_t* entries, cbfs_stream stream);
+int cbfs_pll_query(const cbfs_pll* p, const uint32_t* s, const uint32_t* t, uint64_t q, int32_t* out,
+                   cbfs_stream stream);
+int cbfs_pll_destroy(cbfs_pll* p);
+
 /* cbfs_query_bidir — the fixed-size bi-directional search of Appendix B
  * (P:1790-1800), reading R27: from each endpoint a BFS over the sorted
  * original-id CSR visits vertices in discovery order (the endpoint first)

@@ -64,6 +64,12 @@ _sig("cbfs_decode", [_u32, _u32, _u32, _u32, _vp, _u32, _vp, _u32, _u32, _vp, _v
 _sig("cbfs_query_distance", [_u32, _u32, _u32, _u32, _vp, _u32, _vp, _vp, _vp, _vp, _u64, _vp, _vp])
 _sig("cbfs_query_stream", [_vp, _vp, _vp, _u32, _u32, _vp, _vp, _u64, _vp, _vp, _vp])
 _sig("cbfs_query_bidir", [_vp, _vp, _vp, _u64, _u32, _vp, _vp])
+_sig("cbfs_pll_build", [_vp, _vp, _vp, _u32, _u32, _u32, _u32, _u32, ctypes.POINTER(_vp), _vp])
+_sig("cbfs_pll_info", [_vp, ctypes.POINTER(_u64), ctypes.POINTER(_u32), ctypes.POINTER(_u32), ctypes.POINTER(_u32),
+                       ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)])
+_sig("cbfs_pll_export", [_vp, _vp, _vp, _vp])
+_sig("cbfs_pll_query", [_vp, _vp, _vp, _u64, _vp, _vp])
+_sig("cbfs_pll_destroy", [_vp])
 _sig("cbfs_labels_build", [_vp, _vp, _vp, _u32, _u32, _u32, ctypes.POINTER(_vp), _vp])
 _sig("cbfs_labels_build_w", [_vp, _vp, _vp, _u32, _u32, _u32, _u32, ctypes.POINTER(_vp), _vp])
 _sig("cbfs_labels_word_bits", [_vp, ctypes.POINTER(_u32)])
@@ -233,6 +239,34 @@ def cbfs_query_stream(h, sources, sizes, n_clusters, d, s, t, inout_best, out_st
 
 def cbfs_query_bidir(h, s, t, tau, inout_best, stream=None):
     _check(_lib.cbfs_query_bidir(h, _ptr(s), _ptr(t), len(s), tau, _ptr(inout_best), _stream(stream)))
+
+
+def cbfs_pll_build(g, sources, sizes, n_clusters, d, first=200, bmax=1000, cap=256, stream=None):
+    h = _vp()
+    _check(_lib.cbfs_pll_build(g, _ptr(sources), _ptr(sizes), n_clusters, d, first, bmax, cap, ctypes.byref(h),
+                               _stream(stream)))
+    return h
+
+
+def cbfs_pll_info(ph):
+    tot, mx, roots, nb = _u64(), _u32(), _u32(), _u32()
+    m1, m2 = ctypes.c_float(), ctypes.c_float()
+    _check(_lib.cbfs_pll_info(ph, ctypes.byref(tot), ctypes.byref(mx), ctypes.byref(roots), ctypes.byref(nb),
+                              ctypes.byref(m1), ctypes.byref(m2)))
+    return dict(total_labels=tot.value, max_labels=mx.value, roots=roots.value, batches=nb.value,
+                ms_cbfs=m1.value, ms_pbfs=m2.value)
+
+
+def cbfs_pll_export(ph, counts, entries, stream=None):
+    _check(_lib.cbfs_pll_export(ph, _ptr(counts), _ptr(entries), _stream(stream)))
+
+
+def cbfs_pll_query(ph, s, t, out, stream=None):
+    _check(_lib.cbfs_pll_query(ph, _ptr(s), _ptr(t), len(s), _ptr(out), _stream(stream)))
+
+
+def cbfs_pll_destroy(ph):
+    _check(_lib.cbfs_pll_destroy(ph))
 
 
 def cbfs_labels_build(g, sources, sizes, n_clusters, d, dist_bytes=2, stream=None, word_bits=64):
