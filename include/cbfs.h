@@ -319,7 +319,7 @@ int cbfs_labels_destroy(cbfs_labels* l);
 /* --------------------------------------------------------------- exact 2-hop oracle (PLL)
  * cbfs_pll_build — Pruned Landmark Labeling with a C-BFS first phase
  * (SURVEY §8(f) NEXT-4), reading R29:
- *   phase 1: the n_clusters (<= 64) given clusters (diameter <= d, as
+ *   phase 1: the n_clusters given clusters (diameter <= d, as
  *     cbfs_run) are traversed by C-BFS; every vertex keeps its cluster
  *     distance vector (all d+1 subsets) as its cluster label;
  *   phase 2: every vertex not in a cluster, in (degree desc, original id
@@ -333,7 +333,8 @@ int cbfs_labels_destroy(cbfs_labels* l);
  *   cap            : label entries per vertex (EOVERFLOW beyond; distances
  *                    above 254 are EOVERFLOW too)
  * The graph must outlive the index.  Errors: EINVAL, EUNSUPPORTED
- * (n_clusters > 64, n >= 2^24), EOVERFLOW, ENOMEM, ECUDA.  Synchronises.
+ * (n_clusters * (8 (d+1) + 4) > 200 KB: a root's cluster labels live in
+ * shared memory; n >= 2^24), EOVERFLOW, ENOMEM, ECUDA.  Synchronises.
  * cbfs_pll_info — phase-2 label count, largest list, roots, batches, and
  *   the device time of phase 1 (C-BFS) and phase 2 (pruned BFSs) in ms.
  * cbfs_pll_export — the phase-2 labels by original vertex id: counts

@@ -2,9 +2,9 @@
 // Landmark Labeling with a C-BFS first phase, reading R29
 // (DESIGN.md §2).
 //
-//   phase 1  the caller's clusters (<= 64, diameter <= d) run as one C-BFS
-//            batch (cbfs_run's engines): their labels are every vertex's
-//            cluster distance vector, kept with rows by internal id;
+//   phase 1  the caller's r clusters (diameter <= d) run as C-BFS batches
+//            (cbfs_run's engines): their labels are every vertex's cluster
+//            distance vector, kept with rows by internal id;
 //   phase 2  the uncovered vertices in (degree desc, id asc) order, in
 //            batches b_0 = first, b_{i+1} = min(bmax, floor(3 b_i / 2))
 //            (200 x 1.5^i up to 1000).  Every root of a batch
@@ -33,7 +33,7 @@ namespace cbfs {
 
 constexpr int PLL_THREADS = 256;
 constexpr int PLL_WARPS = PLL_THREADS / 32;
-constexpr uint32_t PLL_MAX_C = 64;
+constexpr uint32_t PLL_SMEM_MAX = 200u << 10;  // the root's cluster labels staged in shared memory
 enum : unsigned { PLL_ERR_CAP = 1, PLL_ERR_PAIRS = 2, PLL_ERR_DIST = 4 };
 
 struct Pll {
@@ -57,7 +57,7 @@ __device__ __forceinline__ bool cluster_within(const uint64_t* __restrict__ sa, 
   for (int tt = 0; tt <= tmax; ++tt) {
     const int i0 = tt > (int)d ? tt - (int)d : 0, i1 = tt < (int)d ? tt : (int)d;
     for (int i = i0; i <= i1; ++i)
-      if (sa[i * PLL_MAX_C + c] & cmask[((uint64_t)(tt - i) * n + b) * C + c]) return true;
+      if (sa[i * C + c] & cmask[((uint64_t)(tt - i) * n + b) * C + c]) return true;
   }
   return false;
 }
@@ -69,8 +69,9 @@ __global__ void __launch_bounds__(PLL_THREADS) k_pll_bfs(
     const uint32_t* __restrict__ snap, const uint32_t* __restrict__ entries, uint32_t cap,
     unsigned long long* __restrict__ pairs, unsigned long long pair_cap, unsigned long long* __restrict__ ctl,
     uint32_t* __restrict__ visited_all, uint8_t* __restrict__ tmp_all, uint32_t* __restrict__ q_all) {
-  __shared__ uint32_t s_da[PLL_MAX_C];
-  __shared__ uint64_t s_mask[(CBFS_MAX_D + 1) * PLL_MAX_C];
+  extern __shared__ uint64_t s_dyn[];  // the root's cluster labels: subsets [d+1][C], then Delta [C]
+  uint64_t* s_mask = s_dyn;
+  uint32_t* s_da = reinterpret_cast<uint32_t*>(s_dyn + (uint64_t)(d + 1) * C);
   __shared__ uint32_t s_ri, s_nf;
   const uint32_t tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
   uint32_t* visited = visited_all + (uint64_t)blockIdx.x * n;
@@ -87,7 +88,7 @@ __global__ void __launch_bounds__(PLL_THREADS) k_pll_bfs(
     const uint32_t pos_r = rank[r];
     for (uint32_t c = tid; c < C; c += PLL_THREADS) {
       s_da[c] = cdist[(uint64_t)r * C + c];
-      for (uint32_t i = 0; i <= d; ++i) s_mask[i * PLL_MAX_C + c] = cmask[((uint64_t)i * n + r) * C + c];
+      for (uint32_t i = 0; i <= d; ++i) s_mask[i * C + c] = cmask[((uint64_t)i * n + r) * C + c];
     }
     const uint32_t sr = snap[r];
     for (uint32_t a = tid; a < sr; a += PLL_THREADS) {
@@ -340,7 +341,7 @@ static int pll_build(Graph* g, const uint32_t* sources, const uint8_t* sizes, ui
   CBFS_CUDA(cudaMemsetAsync(covered, 0, N, st));
   // ---- phase 1: the clusters' C-BFS (one batch of <= 64 lanes), rows by internal id
   if (C) {
-    k_pll_flags<<<(C * 64 + 255) / 256, 256, 0, st>>>(sources, sizes, C, g->inv, n, covered, bad);
+    k_pll_flags<<<(unsigned)(((uint64_t)C * 64 + 255) / 256), 256, 0, st>>>(sources, sizes, C, g->inv, n, covered, bad);
     CBFS_LAUNCHED();
     int hbad = 0;
     CBFS_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -409,6 +410,8 @@ static int pll_build(Graph* g, const uint32_t* sources, const uint8_t* sizes, ui
   }
   uint8_t* sort_tmp = nullptr;
   if ((rc = S.alloc(&sort_tmp, sort_tb))) return rc;
+  const size_t smem = (size_t)C * (8 * (P->d + 1) + 4);
+  CBFS_CUDA(cudaFuncSetAttribute(k_pll_bfs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLL_SMEM_MAX));
   unsigned long long hctl[4];
   uint32_t b = std::min(P->first, P->bmax);
   uint32_t batches = 0;
@@ -417,7 +420,7 @@ static int pll_build(Graph* g, const uint32_t* sources, const uint8_t* sizes, ui
     ++batches;
     CBFS_CUDA(cudaMemcpyAsync(snap, P->counts, sizeof(uint32_t) * N, cudaMemcpyDeviceToDevice, st));
     CBFS_CUDA(cudaMemsetAsync(ctl, 0, 4 * sizeof(unsigned long long), st));
-    k_pll_bfs<<<std::min(ctas, nb), PLL_THREADS, 0, st>>>(g->off, g->cols, g->rank, n, roots + r0, nb, r0, C, P->d,
+    k_pll_bfs<<<std::min(ctas, nb), PLL_THREADS, smem, st>>>(g->off, g->cols, g->rank, n, roots + r0, nb, r0, C, P->d,
                                                          P->cdist, P->cmask, P->counts, snap, P->entries, P->cap,
                                                          pairs, pair_cap, ctl, visited, tmpmap, queues);
     CBFS_LAUNCHED();
@@ -462,9 +465,10 @@ int cbfs_pll_build(cbfs_graph* gh, const uint32_t* sources, const uint8_t* sizes
   if (!out) return fail(CBFS_EINVAL, "null out");
   *out = nullptr;
   if (!g) return fail(CBFS_EINVAL, "null graph");
-  if (n_clusters > PLL_MAX_C) return fail(CBFS_EUNSUPPORTED, "PLL takes at most 64 first-phase clusters");
-  if (n_clusters && (!sources || !sizes)) return fail(CBFS_EINVAL, "null sources/sizes");
   if (d > CBFS_MAX_D) return fail(CBFS_EUNSUPPORTED, "d > CBFS_MAX_D");
+  if ((uint64_t)n_clusters * (8ull * (d + 1) + 4) > PLL_SMEM_MAX)
+    return fail(CBFS_EUNSUPPORTED, "too many first-phase clusters for d (n_clusters * (8 (d+1) + 4) > 200 KB)");
+  if (n_clusters && (!sources || !sizes)) return fail(CBFS_EINVAL, "null sources/sizes");
   if (first == 0 || bmax == 0 || cap == 0) return fail(CBFS_EINVAL, "first, bmax and cap must be >= 1");
   if (g->n >= (1u << 24)) return fail(CBFS_EUNSUPPORTED, "PLL hub positions are 24-bit (n < 2^24)");
   CBFS_CUDA(cudaSetDevice(g->device));

@@ -39,7 +39,7 @@ def build_both(el, C, k, first, bmax, cap, relabel):
 @pytest.mark.parametrize("kind,C,k,first,bmax,relabel", [
     ("er", 0, 1, 1, 1, False), ("er", 4, 16, 4, 16, True), ("rmat", 16, 64, 200, 1000, True),
     ("rmat", 64, 64, 7, 50, False), ("grid", 8, 13, 5, 40, False), ("er_sparse", 3, 8, 16, 64, True),
-    ("rmat", 0, 1, 200, 1000, False)])
+    ("rmat", 0, 1, 200, 1000, False), ("rmat", 200, 64, 50, 400, True), ("er", 100, 8, 30, 90, False)])
 def test_pll_labels_and_queries_match_oracle(kind, C, k, first, bmax, relabel):
     el = GRAPHS[kind]()
     cap = 512
@@ -95,8 +95,8 @@ def test_pll_errors():
     with pytest.raises(cb.CbfsError):  # a grid's labels do not fit 3 entries
         cb.cbfs_pll_build(g.h, None, None, 0, 2, 200, 1000, 3)
     src, sz = orc.select_clusters(ref, 65, 13, 2)
-    with pytest.raises(cb.CbfsError):  # at most 64 first-phase clusters
-        cb.cbfs_pll_build(g.h, to_dev_u32(src), to_dev_u8(sz), 65, 2, 200, 1000, 256)
+    with pytest.raises(cb.CbfsError):  # a root's cluster labels must fit shared memory (checked before any read)
+        cb.cbfs_pll_build(g.h, to_dev_u32(src), to_dev_u8(sz), 800, 31, 200, 1000, 256)
     h = cb.cbfs_pll_build(g.h, to_dev_u32(src[:4]), to_dev_u8(sz[:4]), 4, 2, 200, 1000, g.n)
     bad = torch.tensor([g.n], dtype=torch.int32, device=DEV)
     out = torch.empty((1,), dtype=torch.int32, device=DEV)
