@@ -230,10 +230,18 @@ __global__ void k_seed(const uint32_t* __restrict__ sources, const uint8_t* __re
 // Delta_u on first visit, S_u[i - Delta_u] = S_new, S_seen[u] |= S_new; plus
 // the output writes and the degrees for the push scan.  Independent per
 // entry; FOLD_ILP entries per thread are loaded before any is used.
-constexpr int FOLD_ILP = 4;
+#ifndef CBFS_FOLD_ILP
+#define CBFS_FOLD_ILP 4
+#endif
+constexpr int FOLD_ILP = CBFS_FOLD_ILP;
+#ifdef CBFS_FOLD_MINB  // experiments; an explicit minimum of 1 block lets ptxas double the registers
+#define CBFS_FOLD_BOUNDS __launch_bounds__(256, CBFS_FOLD_MINB)
+#else
+#define CBFS_FOLD_BOUNDS __launch_bounds__(256)
+#endif
 
-template <int DB>
-__global__ void __launch_bounds__(256) k_fold(const uint32_t* __restrict__ F, uint32_t nF, uint32_t i,
+template <int DB, bool WIDE>
+__global__ void CBFS_FOLD_BOUNDS k_fold(const uint32_t* __restrict__ F, uint32_t nF, uint32_t i,
                                               uint64_t* __restrict__ seen, uint64_t* __restrict__ pend,
                                               uint16_t* __restrict__ dist, const uint64_t* __restrict__ off,
                                               const uint32_t* __restrict__ perm, uint32_t n, uint32_t C,
@@ -284,12 +292,12 @@ __global__ void __launch_bounds__(256) k_fold(const uint32_t* __restrict__ F, ui
       // lane's subsets are placed relative to it
       uint32_t dc = dv[q];
       uint64_t dcol = col;
-      if (W > 1) {
+      if (WIDE) {
         const uint32_t b0 = e[q] & ~(W - 1);
         for (uint32_t x = 0; x < W; ++x) dc = min(dc, (uint32_t)dist[b0 + x]);
         dcol = (uint64_t)orig * (C / W) + (cbase + c) / W;
       }
-      if (first && out_dist && dc == i) {
+      if (first && out_dist && (!WIDE || dc == i)) {
         if (DB == 1) {
           overflow |= i > 254;
           ((uint8_t*)out_dist)[dcol] = (uint8_t)(i > 254 ? 254 : i);
@@ -298,7 +306,10 @@ __global__ void __launch_bounds__(256) k_fold(const uint32_t* __restrict__ F, ui
         }
       }
       const uint32_t oi = i - dc;
-      if (out_masks && oi < planes) store_mask(out_masks, (uint64_t)oi * n * C + col, nw[q], mb);
+      if (out_masks && oi < planes) {
+        if (WIDE || mb != 8) store_mask(out_masks, (uint64_t)oi * n * C + col, nw[q], mb);
+        else ((uint64_t*)out_masks)[(uint64_t)oi * n * C + col] = nw[q];
+      }
     }
     // per-vertex "subset full" bits (read by the dense pull instead of the
     // whole S_seen row): one 64-bit atomic per distinct vertex in the warp
@@ -780,14 +791,20 @@ static int slot_round(Graph* g, Slot* w) {
   const int write_pre = pull ? 0 : 1;
   const unsigned fb = grid_for((nF + FOLD_ILP - 1) / FOLD_ILP, 256);
   if (g_prof.on) CBFS_CUDA(cudaEventRecord(w->pe[0], st));
-  if (a.dist_bytes == 1)
-    k_fold<1><<<fb, 256, 0, st>>>(w->cur, (uint32_t)nF, i, w->seen, w->pend, w->dist, g->off, a.out_internal ? nullptr : g->perm, n, a.C,
-                                  a.cbase, a.planes, a.out_dist, a.out_masks, a.mask_bytes, w->pre, write_pre, a.sizes, w->fullm,
-                                  w->ctr, a.wide > 1 ? a.wide : 1);
-  else
-    k_fold<2><<<fb, 256, 0, st>>>(w->cur, (uint32_t)nF, i, w->seen, w->pend, w->dist, g->off, a.out_internal ? nullptr : g->perm, n, a.C,
-                                  a.cbase, a.planes, a.out_dist, a.out_masks, a.mask_bytes, w->pre, write_pre, a.sizes, w->fullm,
-                                  w->ctr, a.wide > 1 ? a.wide : 1);
+  const uint32_t W = a.wide > 1 ? a.wide : 1;
+  const uint32_t mb = a.mask_bytes ? a.mask_bytes : 8;
+  const uint32_t* fperm = a.out_internal ? nullptr : g->perm;
+#define CBFS_FOLD_ARGS                                                                                              \
+  w->cur, (uint32_t)nF, i, w->seen, w->pend, w->dist, g->off, fperm, n, a.C, a.cbase, a.planes, a.out_dist,          \
+      a.out_masks, mb, w->pre, write_pre, a.sizes, w->fullm, w->ctr, W
+  if (a.dist_bytes == 1) {
+    if (W > 1) k_fold<1, true><<<fb, 256, 0, st>>>(CBFS_FOLD_ARGS);
+    else k_fold<1, false><<<fb, 256, 0, st>>>(CBFS_FOLD_ARGS);
+  } else {
+    if (W > 1) k_fold<2, true><<<fb, 256, 0, st>>>(CBFS_FOLD_ARGS);
+    else k_fold<2, false><<<fb, 256, 0, st>>>(CBFS_FOLD_ARGS);
+  }
+#undef CBFS_FOLD_ARGS
   CBFS_LAUNCHED();
   if (g_prof.on) CBFS_CUDA(cudaEventRecord(w->pe[1], st));
   CBFS_CUDA(cudaMemsetAsync(w->ctr, 0, 2 * sizeof(unsigned long long), st));

@@ -1,5 +1,4 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_pll.py -q -x > gpurun_out/pll.log 2>&1; echo "pll rc $?"; tail -3 gpurun_out/pll.log
-timeout 300 python tools/pll_probe.py c1_er 16 1024 > gpurun_out/pll_probe.log 2>&1; echo "c1 rc $?"
-timeout 900 python tools/pll_probe.py c2_rmat20 64 2048 >> gpurun_out/pll_probe.log 2>&1; echo "c2 rc $?"
-cat gpurun_out/pll_probe.log | tail -6
+summ() { tail -1 $1 | python -c "import json,sys; r=json.loads(sys.stdin.read()); print(round(r['ms_per_step'],2), r['config']['phase_ms_rank0'], round(r['roofline']['frac'],3), {k:v['event_ms_per_step'] for k,v in r['roofline']['per_kernel'].items()})"; }
+for i in 1 2; do timeout 600 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu > gpurun_out/b_base$i.log 2>&1; echo -n "base: "; summ gpurun_out/b_base$i.log; done
+for v in f2m8 f8m4 f4m5 f8; do CBFS_LIB_PATH=build_var/$v/libcbfs.so timeout 600 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu > gpurun_out/b_$v.log 2>&1; echo -n "$v: "; summ gpurun_out/b_$v.log; done
