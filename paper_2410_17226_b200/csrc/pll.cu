@@ -19,22 +19,30 @@
 // one map probe per label entry of u; the cluster part skips every cluster
 // with Delta_r + Delta_u > delta before touching a subset word.
 //
-// A batch's new labels are staged as (vertex, pos << 8 | dist) keys, radix
-// sorted and scattered after the batch, so each label list stays sorted by
-// hub position (deterministic layout; the query merges two sorted lists).
+// A root appends (pos << 8 | dist) to L(u) beyond u's batch-start length
+// (invisible to the batch's own queries); batches follow each other on the
+// stream with no host round trip, and one bitonic sort per list at the end
+// makes every list ascending by hub position (a deterministic layout; the
+// query binary-searches one list for the hubs of the other).
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "engine.cuh"
 
 namespace cbfs {
 
-constexpr int PLL_THREADS = 256;
+#ifndef CBFS_PLL_THREADS
+#define CBFS_PLL_THREADS 256
+#endif
+constexpr int PLL_THREADS = CBFS_PLL_THREADS;
 constexpr int PLL_WARPS = PLL_THREADS / 32;
 constexpr uint32_t PLL_SMEM_MAX = 200u << 10;  // the root's cluster labels staged in shared memory
-enum : unsigned { PLL_ERR_CAP = 1, PLL_ERR_PAIRS = 2, PLL_ERR_DIST = 4 };
+enum : unsigned { PLL_ERR_CAP = 1, PLL_ERR_DIST = 4 };
+constexpr uint32_t PLL_MAX_CAP = 8192;  // a list is sorted in shared memory at the end
 
 struct Pll {
   int device = 0;
@@ -66,8 +74,9 @@ __global__ void __launch_bounds__(PLL_THREADS) k_pll_bfs(
     const uint64_t* __restrict__ off, const uint32_t* __restrict__ cols, const uint32_t* __restrict__ rank,
     uint32_t n, const uint32_t* __restrict__ roots, uint32_t nb, uint32_t tag_base, uint32_t C, uint32_t d,
     const uint16_t* __restrict__ cdist, const uint64_t* __restrict__ cmask, uint32_t* __restrict__ counts,
-    const uint32_t* __restrict__ snap, const uint32_t* __restrict__ entries, uint32_t cap,
-    unsigned long long* __restrict__ pairs, unsigned long long pair_cap, unsigned long long* __restrict__ ctl,
+    const uint32_t* __restrict__ snap, const uint32_t* entries, uint32_t cap,
+    uint32_t* entries_w /* == entries: appends land beyond the batch-start lengths this batch reads */,
+    unsigned long long* __restrict__ ctl,
     uint32_t* __restrict__ visited_all, uint8_t* __restrict__ tmp_all, uint32_t* __restrict__ q_all) {
   extern __shared__ uint64_t s_dyn[];  // the root's cluster labels: subsets [d+1][C], then Delta [C]
   uint64_t* s_mask = s_dyn;
@@ -137,12 +146,8 @@ __global__ void __launch_bounds__(PLL_THREADS) k_pll_bfs(
             atomicOr(&ctl[2], (unsigned long long)PLL_ERR_CAP);
           } else if (delta > 254) {
             atomicOr(&ctl[2], (unsigned long long)PLL_ERR_DIST);
-          } else {
-            const unsigned long long p = atomicAdd(&ctl[1], 1ULL);
-            if (p < pair_cap)
-              pairs[p] = ((unsigned long long)u << 32) | ((unsigned long long)pos_r << 8) | delta;
-            else
-              atomicOr(&ctl[2], (unsigned long long)PLL_ERR_PAIRS);
+          } else {  // beyond u's batch-start length: invisible to this batch's queries
+            entries_w[(uint64_t)u * cap + slot] = (pos_r << 8) | delta;
           }
         }
         const uint64_t e0 = off[u], e1 = off[u + 1];
@@ -170,19 +175,33 @@ __global__ void __launch_bounds__(PLL_THREADS) k_pll_bfs(
   }
 }
 
-// sorted (vertex, entry) keys -> appended to each vertex's list after its
-// batch-start length, in key order
-__global__ void k_pll_scatter(const unsigned long long* __restrict__ keys, uint64_t cnt,
-                              const uint32_t* __restrict__ snap, uint32_t* __restrict__ entries, uint32_t cap) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * blockDim.x) {
-    const unsigned long long k = keys[i];
-    const uint32_t v = (uint32_t)(k >> 32);
-    uint64_t lo = 0, hi = i;  // first index of v's run
-    while (lo < hi) {
-      const uint64_t mid = (lo + hi) >> 1;
-      if ((uint32_t)(keys[mid] >> 32) < v) lo = mid + 1; else hi = mid;
-    }
-    entries[(uint64_t)v * cap + snap[v] + (i - lo)] = (uint32_t)k;
+// Each list holds its batches' segments in batch order, each segment in
+// arrival order; one bitonic sort per list (block per vertex, shared memory
+// of the next power of two >= the list) makes it ascending by hub position.
+__global__ void __launch_bounds__(256) k_pll_sort(uint32_t* __restrict__ entries, const uint32_t* __restrict__ counts,
+                                                  uint32_t n, uint32_t cap) {
+  extern __shared__ uint32_t s_key[];
+  for (uint32_t v = blockIdx.x; v < n; v += gridDim.x) {
+    const uint32_t L = min(counts[v], cap);
+    if (L < 2) continue;
+    uint32_t P = 1;
+    while (P < L) P <<= 1;
+    uint32_t* row = entries + (uint64_t)v * cap;
+    for (uint32_t x = threadIdx.x; x < P; x += blockDim.x) s_key[x] = x < L ? row[x] : 0xFFFFFFFFu;
+    __syncthreads();
+    for (uint32_t k = 2; k <= P; k <<= 1)
+      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+        for (uint32_t x = threadIdx.x; x < P; x += blockDim.x) {
+          const uint32_t y = x ^ j;
+          if (y > x) {
+            const uint32_t a = s_key[x], b = s_key[y];
+            if (((x & k) == 0) == (a > b)) { s_key[x] = b; s_key[y] = a; }
+          }
+        }
+        __syncthreads();
+      }
+    for (uint32_t x = threadIdx.x; x < L; x += blockDim.x) row[x] = s_key[x];
+    __syncthreads();
   }
 }
 
@@ -390,53 +409,47 @@ static int pll_build(Graph* g, const uint32_t* sources, const uint8_t* sizes, ui
   size_t fr = 0, tot = 0;
   CBFS_CUDA(cudaMemGetInfo(&fr, &tot));
   const uint64_t per_cta = 13ull * N;
-  uint32_t ctas = std::min<uint64_t>(148ull * 2, std::max<uint64_t>(1, (fr / 4) / per_cta));
+  uint64_t want_ctas = 148ull * 8;
+  if (const char* e = getenv("CBFS_PLL_CTAS")) want_ctas = std::max(1, atoi(e));  // experiments
+  uint32_t ctas = std::min<uint64_t>(want_ctas, std::max<uint64_t>(1, (fr / 4) / per_cta));
   ctas = std::min<uint32_t>(ctas, std::max<uint32_t>(1, std::min(P->bmax, nroots)));
-  uint64_t pair_cap = std::min<uint64_t>((uint64_t)N * std::min(P->bmax, std::max(nroots, 1u)),
-                                         std::max<uint64_t>(1 << 20, (fr / 4) / 16));
   uint32_t *visited = nullptr, *queues = nullptr, *snap = nullptr;
   uint8_t* tmpmap = nullptr;
-  unsigned long long *pairs = nullptr, *alt = nullptr, *ctl = nullptr, *stats = nullptr;
+  unsigned long long *ctl = nullptr, *stats = nullptr;
   if ((rc = S.alloc(&visited, (uint64_t)ctas * N)) || (rc = S.alloc(&tmpmap, (uint64_t)ctas * N)) ||
-      (rc = S.alloc(&queues, 2ull * ctas * N)) || (rc = S.alloc(&snap, N)) || (rc = S.alloc(&pairs, pair_cap)) ||
-      (rc = S.alloc(&alt, pair_cap)) || (rc = S.alloc(&ctl, 4)) || (rc = S.alloc(&stats, 2)))
+      (rc = S.alloc(&queues, 2ull * ctas * N)) || (rc = S.alloc(&snap, N)) || (rc = S.alloc(&ctl, 4)) ||
+      (rc = S.alloc(&stats, 2)))
     return rc;
   CBFS_CUDA(cudaMemsetAsync(visited, 0, sizeof(uint32_t) * ctas * N, st));
   CBFS_CUDA(cudaMemsetAsync(tmpmap, 0xFF, (uint64_t)ctas * N, st));
-  size_t sort_tb = 0;
-  {
-    cub::DoubleBuffer<unsigned long long> db(pairs, alt);
-    CBFS_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, sort_tb, db, (int64_t)pair_cap, 0, 64, st));
-  }
-  uint8_t* sort_tmp = nullptr;
-  if ((rc = S.alloc(&sort_tmp, sort_tb))) return rc;
+  CBFS_CUDA(cudaMemsetAsync(ctl, 0, 4 * sizeof(unsigned long long), st));
   const size_t smem = (size_t)C * (8 * (P->d + 1) + 4);
   CBFS_CUDA(cudaFuncSetAttribute(k_pll_bfs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLL_SMEM_MAX));
-  unsigned long long hctl[4];
+  // batches run back to back on the stream (no host round trip): each takes
+  // a snapshot of the list lengths, then its roots' pruned BFSs; errors
+  // accumulate in ctl[2] and are checked once at the end
   uint32_t b = std::min(P->first, P->bmax);
   uint32_t batches = 0;
   for (uint32_t r0 = 0; r0 < nroots; r0 += b, b = std::min<uint32_t>(P->bmax, b * 3 / 2)) {
     const uint32_t nb = std::min(b, nroots - r0);
     ++batches;
     CBFS_CUDA(cudaMemcpyAsync(snap, P->counts, sizeof(uint32_t) * N, cudaMemcpyDeviceToDevice, st));
-    CBFS_CUDA(cudaMemsetAsync(ctl, 0, 4 * sizeof(unsigned long long), st));
+    CBFS_CUDA(cudaMemsetAsync(ctl, 0, sizeof(unsigned long long), st));  // the batch's root counter
     k_pll_bfs<<<std::min(ctas, nb), PLL_THREADS, smem, st>>>(g->off, g->cols, g->rank, n, roots + r0, nb, r0, C, P->d,
-                                                         P->cdist, P->cmask, P->counts, snap, P->entries, P->cap,
-                                                         pairs, pair_cap, ctl, visited, tmpmap, queues);
-    CBFS_LAUNCHED();
-    CBFS_CUDA(cudaMemcpyAsync(hctl, ctl, sizeof(hctl), cudaMemcpyDeviceToHost, st));
-    CBFS_CUDA(cudaStreamSynchronize(st));
-    if (hctl[2] & PLL_ERR_CAP) return fail(CBFS_EOVERFLOW, "a PLL label list exceeds cap");
-    if (hctl[2] & PLL_ERR_DIST) return fail(CBFS_EOVERFLOW, "a PLL label distance exceeds 254");
-    if (hctl[2] & PLL_ERR_PAIRS) return fail(CBFS_ENOMEM, "PLL batch label staging buffer too small");
-    const uint64_t np = hctl[1];
-    if (np == 0) continue;
-    cub::DoubleBuffer<unsigned long long> db(pairs, alt);
-    size_t tb2 = sort_tb;
-    CBFS_CUDA(cub::DeviceRadixSort::SortKeys(sort_tmp, tb2, db, (int64_t)np, 0, 64, st));
-    k_pll_scatter<<<grid_for(np, 256), 256, 0, st>>>(db.Current(), np, snap, P->entries, P->cap);
+                                                             P->cdist, P->cmask, P->counts, snap, P->entries, P->cap,
+                                                             P->entries, ctl, visited, tmpmap, queues);
     CBFS_LAUNCHED();
   }
+  unsigned long long hctl[4];
+  CBFS_CUDA(cudaMemcpyAsync(hctl, ctl, sizeof(hctl), cudaMemcpyDeviceToHost, st));
+  CBFS_CUDA(cudaStreamSynchronize(st));
+  if (hctl[2] & PLL_ERR_CAP) return fail(CBFS_EOVERFLOW, "a PLL label list exceeds cap");
+  if (hctl[2] & PLL_ERR_DIST) return fail(CBFS_EOVERFLOW, "a PLL label distance exceeds 254");
+  uint32_t P2 = 1;
+  while (P2 < P->cap) P2 <<= 1;
+  CBFS_CUDA(cudaFuncSetAttribute(k_pll_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(P2 * 4)));
+  k_pll_sort<<<148 * 8, 256, P2 * 4, st>>>(P->entries, P->counts, n, P->cap);
+  CBFS_LAUNCHED();
   P->batches = batches;
   CBFS_CUDA(cudaEventRecord(ev[2], st));
   CBFS_CUDA(cudaMemsetAsync(stats, 0, 2 * sizeof(unsigned long long), st));
@@ -470,6 +483,7 @@ int cbfs_pll_build(cbfs_graph* gh, const uint32_t* sources, const uint8_t* sizes
     return fail(CBFS_EUNSUPPORTED, "too many first-phase clusters for d (n_clusters * (8 (d+1) + 4) > 200 KB)");
   if (n_clusters && (!sources || !sizes)) return fail(CBFS_EINVAL, "null sources/sizes");
   if (first == 0 || bmax == 0 || cap == 0) return fail(CBFS_EINVAL, "first, bmax and cap must be >= 1");
+  if (cap > PLL_MAX_CAP) return fail(CBFS_EUNSUPPORTED, "cap > 8192 label entries per vertex");
   if (g->n >= (1u << 24)) return fail(CBFS_EUNSUPPORTED, "PLL hub positions are 24-bit (n < 2^24)");
   CBFS_CUDA(cudaSetDevice(g->device));
   Pll* P = new Pll();

@@ -1,4 +1,4 @@
 mkdir -p gpurun_out
-summ() { tail -1 $1 | python -c "import json,sys; r=json.loads(sys.stdin.read()); print(round(r['ms_per_step'],2), r['config']['phase_ms_rank0'], round(r['roofline']['frac'],3), {k:v['event_ms_per_step'] for k,v in r['roofline']['per_kernel'].items()})"; }
-for i in 1 2; do timeout 600 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu > gpurun_out/b_base$i.log 2>&1; echo -n "base: "; summ gpurun_out/b_base$i.log; done
-for v in f2m8 f8m4 f4m5 f8; do CBFS_LIB_PATH=build_var/$v/libcbfs.so timeout 600 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu > gpurun_out/b_$v.log 2>&1; echo -n "$v: "; summ gpurun_out/b_$v.log; done
+timeout 600 python -m pytest tests/test_gpu_pll.py -q -x > gpurun_out/pll.log 2>&1; echo "pll rc $?"; tail -2 gpurun_out/pll.log
+for i in 1 2; do timeout 300 python tools/pll_probe.py c2_rmat20 64 2048 > gpurun_out/pll_p$i.log 2>&1; tail -1 gpurun_out/pll_p$i.log | cut -c 150-400; done
+timeout 300 python tools/pll_probe.py c1_er 16 1024 > gpurun_out/pll_c1.log 2>&1; tail -1 gpurun_out/pll_c1.log | cut -c 150-400
