@@ -36,7 +36,7 @@
 namespace cbfs {
 
 #ifndef CBFS_PLL_THREADS
-#define CBFS_PLL_THREADS 256
+#define CBFS_PLL_THREADS 1024
 #endif
 constexpr int PLL_THREADS = CBFS_PLL_THREADS;
 constexpr int PLL_WARPS = PLL_THREADS / 32;
@@ -409,7 +409,7 @@ static int pll_build(Graph* g, const uint32_t* sources, const uint8_t* sizes, ui
   size_t fr = 0, tot = 0;
   CBFS_CUDA(cudaMemGetInfo(&fr, &tot));
   const uint64_t per_cta = 13ull * N;
-  uint64_t want_ctas = 148ull * 8;
+  uint64_t want_ctas = 148ull * (2048 / PLL_THREADS);  // persistent CTAs: one resident set
   if (const char* e = getenv("CBFS_PLL_CTAS")) want_ctas = std::max(1, atoi(e));  // experiments
   uint32_t ctas = std::min<uint64_t>(want_ctas, std::max<uint64_t>(1, (fr / 4) / per_cta));
   ctas = std::min<uint32_t>(ctas, std::max<uint32_t>(1, std::min(P->bmax, nroots)));
