@@ -65,20 +65,21 @@ def test_query_stream_sharded(nccl_group):
     g.close()
 
 
-@pytest.mark.parametrize("d,dist_bytes", [(2, 1), (0, 2), (6, 2)])
-def test_label_images_gather_and_query(nccl_group, d, dist_bytes):
-    """cbfs_labels_build -> export -> NCCL all_gather -> import -> query ==
-    the oracle; host-buffer export/import round trip; bad images rejected."""
+@pytest.mark.parametrize("d,dist_bytes,w", [(2, 1, 64), (0, 2, 64), (6, 2, 64), (2, 1, 8), (4, 2, 16), (0, 1, 0)])
+def test_label_images_gather_and_query(nccl_group, d, dist_bytes, w):
+    """cbfs_labels_build_w -> export -> NCCL all_gather -> import -> query ==
+    the oracle, for stores of word size w (0 = plain landmarks); host-buffer
+    export/import round trip; bad images rejected."""
     import paper_2410_17226_b200 as cb
     el = ci.rmat(12, 8, 0.57, 0.19, 0.19, seed=44) if d <= 2 else ci.grid(50, 0.05, 0.01, 44)
     ref = orc.csr_from_edgelist(el)
-    src, sz = orc.select_clusters(ref, 70, 64, max(d, 1) if d else 2)
+    src, sz = orc.select_clusters(ref, 70, max(w, 1) if w < 64 else 64, max(d, 1) if d else 2)
     if d == 0:  # d = 0 labels: single-source clusters (plain BFS landmarks)
         src = src.copy(); src[:, 1:] = orc.PAD; sz = np.ones_like(sz)
     g = gpu_graph(el, relabel=(d == 2))
-    h = pd.build_local_labels(g, to_dev_u32(src), to_dev_u8(sz), d, dist_bytes)
+    h = pd.build_local_labels(g, to_dev_u32(src), to_dev_u8(sz), d, dist_bytes, word_bits=w)
     info = cb.cbfs_labels_info(h)
-    assert info["clusters"] == len(sz) and info["d"] == d and info["n"] == g.n
+    assert info["clusters"] == len(sz) and info["d"] == d and info["n"] == g.n and info["word_bits"] == w
     handles = pd.gather_label_images(g, h)
     s, t = ci.query_pairs(g.n, 20000, seed=12)
     best = pd.query_label_handles(handles, to_dev_u32(s), to_dev_u32(t))
