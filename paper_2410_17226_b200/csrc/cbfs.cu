@@ -820,7 +820,7 @@ static int slot_round(Graph* g, Slot* w) {
   if (pull) {
     w->kind = PK_PULL;
     if (g_prof.on) CBFS_CUDA(cudaEventRecord(w->pe[2], st));
-    const unsigned pb = grid_for(g->n_chunks * 32, PULL_WARPS * 32, 148u * 8u);
+    const unsigned pb = grid_for(g->n_chunks * 32, PULL_WARPS * 32, 148u * CBFS_PULL_MINB);
     k_pull<<<pb, PULL_WARPS * 32, 0, st>>>(g->off, g->cols, g->chunk_v, g->n_chunks, g->m, n, w->seen, w->dist,
                                            w->pend, ub_cur, ub_nxt, a.sizes, a.nb, w->nxt, w->bstats, w->ctr, w->fullm,
                                            i, a.d);

@@ -339,8 +339,15 @@ static void pll_free(Pll* P) {
 static int pll_build(Graph* g, const uint32_t* sources, const uint8_t* sizes, uint32_t C, Pll* P, cudaStream_t st) {
   const uint32_t n = g->n;
   const uint64_t N = n ? n : 1;
-  cudaEvent_t ev[3];
-  for (auto& e : ev) CBFS_CUDA(cudaEventCreate(&e));
+  struct Events {  // destroyed on every return path
+    cudaEvent_t e[3] = {nullptr, nullptr, nullptr};
+    ~Events() {
+      for (cudaEvent_t x : e)
+        if (x) cudaEventDestroy(x);
+    }
+  } E;
+  cudaEvent_t* ev = E.e;
+  for (int k = 0; k < 3; ++k) CBFS_CUDA(cudaEventCreate(&ev[k]));
   CBFS_CUDA(cudaEventRecord(ev[0], st));
   if (cudaMalloc(&P->cdist, sizeof(uint16_t) * N * (C ? C : 1)) != cudaSuccess ||
       cudaMalloc(&P->cmask, sizeof(uint64_t) * P->planes * N * (C ? C : 1)) != cudaSuccess ||
@@ -462,7 +469,6 @@ static int pll_build(Graph* g, const uint32_t* sources, const uint8_t* sizes, ui
   P->max_count = (uint32_t)hs[1];
   CBFS_CUDA(cudaEventElapsedTime(&P->ms_cbfs, ev[0], ev[1]));
   CBFS_CUDA(cudaEventElapsedTime(&P->ms_pbfs, ev[1], ev[2]));
-  for (auto& e : ev) cudaEventDestroy(e);
   return CBFS_OK;
 }
 

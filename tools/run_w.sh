@@ -1,5 +1,4 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_distributed.py -q -x > gpurun_out/dist.log 2>&1; echo "dist rc $?"; tail -1 gpurun_out/dist.log
-timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/c2_launches.csv python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --no-clocks > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc $?"
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_pll_bfs|k_pll_query|k_pll_sort" --launch-skip 600 --launch-count 3 -o gpurun_out/pll_full -f python tools/pll_probe.py c2_rmat20 64 2048 > gpurun_out/ncu_pll.log 2>&1; echo "ncu pll rc $?"
-ls -la gpurun_out/ | tail -5
+summ() { tail -1 $1 | python -c "import json,sys; r=json.loads(sys.stdin.read()); print(round(r['ms_per_step'],2), r['config']['phase_ms_rank0'], round(r['roofline']['frac'],3), {k:v['event_ms_per_step'] for k,v in r['roofline']['per_kernel'].items()})"; }
+timeout 600 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu > gpurun_out/b_base.log 2>&1; echo -n "base: "; summ gpurun_out/b_base.log
+for v in m16 mb12 mb10 m12mb10 m4mb12; do CBFS_LIB_PATH=build_var/$v/libcbfs.so timeout 600 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu > gpurun_out/b_$v.log 2>&1; echo -n "$v: "; summ gpurun_out/b_$v.log; done
