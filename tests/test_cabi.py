@@ -46,6 +46,23 @@ def test_host_side_argument_errors():
                                    None, None, 0, None, None) == cb.CBFS_EINVAL  # planes must be d or d+1
     assert lib.cbfs_set_direction_alpha(ctypes.c_double(0.0)) == cb.CBFS_EINVAL
     assert b"alpha" in lib.cbfs_last_error()
+    h = ctypes.c_void_p()
+    fake = ctypes.c_void_p(8)
+    # the NEXT-row entry points: host-side argument checks before any device work
+    assert lib.cbfs_labels_build_w(None, None, None, 0, 2, 2, 64, ctypes.byref(h), None) == cb.CBFS_EINVAL
+    assert lib.cbfs_run_wide(None, None, None, 1, 3, 2, 2, None, None, 3, None, 0, None) == cb.CBFS_EUNSUPPORTED
+    assert b"words" in lib.cbfs_last_error()
+    assert lib.cbfs_run_wide(None, None, None, 1, 2, 2, 2, None, None, 3, None, 0, None) == cb.CBFS_EINVAL
+    assert lib.cbfs_select_clusters_wide(None, 1, 100, 2, 0, 0, 3, fake, fake, ctypes.byref(ctypes.c_uint32()),
+                                         None) == cb.CBFS_EUNSUPPORTED
+    assert lib.cbfs_select_clusters_wide(None, 1, 200, 2, 0, 0, 2, fake, fake, ctypes.byref(ctypes.c_uint32()),
+                                         None) == cb.CBFS_EINVAL  # k > 64 * words
+    assert lib.cbfs_decode_wide(10, 1, 2, 2, 3, fake, 2, fake, 0, 129, fake, None) == cb.CBFS_EINVAL  # k > 128
+    assert lib.cbfs_query_distance_wide(10, 1, 3, 2, 3, fake, 2, fake, fake, fake, fake, 1, fake,
+                                        None) == cb.CBFS_EUNSUPPORTED
+    assert lib.cbfs_pll_build(None, None, None, 0, 2, 200, 1000, 256, ctypes.byref(h), None) == cb.CBFS_EINVAL
+    assert lib.cbfs_pll_query(None, fake, fake, 1, fake, None) == cb.CBFS_EINVAL
+    assert lib.cbfs_pll_destroy(None) == cb.CBFS_OK
     assert cb.cbfs_version().startswith("cbfs-b200")
 
 
