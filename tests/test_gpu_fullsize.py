@@ -94,3 +94,44 @@ def test_c5_prefix_sampled_and_queries():
     assert np.array_equal(got, expect)
     assert (expect < orc.INT32_MAX).sum() > 0
     g.close()
+
+
+@pytest.mark.timeout(900)
+def test_intact_grid_manhattan_full_size():
+    """SURVEY §8(c) closed form at config 4's size: on the intact 4096² grid
+    (no deletions, no diagonals; id = y·4096 + x, R21) the distance from a
+    source is the Manhattan distance, so every Delta and every subset of
+    every radius-2-ball cluster is known without an oracle.  64 clusters
+    (random roots, d = 4) in one cbfs_run — ~8,000 rounds — checked element by
+    element on the device, and their round counts = 1 + max distance."""
+    side = 4096
+    el = ci.grid(side, 0.0, 0.0, 4)
+    g = cb.Graph(cb.cbfs_graph_create(el.n, torch.from_numpy(el.src.view(np.int32)).to(DEV),
+                                      torch.from_numpy(el.dst.view(np.int32)).to(DEV), 0, 0), 0)
+    assert g.m == 4 * side * (side - 1)
+    d, C = 4, 64
+    src = torch.empty((C, 64), dtype=torch.int32, device=DEV)
+    sz = torch.empty((C,), dtype=torch.uint8, device=DEV)
+    assert cb.cbfs_select_clusters(g.h, C, 64, d, cb.CBFS_ROOT_RANDOM, 4, src, sz) == C
+    dist = torch.empty((g.n, C), dtype=torch.int16, device=DEV)
+    masks = torch.empty((d + 1, g.n, C), dtype=torch.int64, device=DEV)
+    stats = torch.zeros((C, 4), dtype=torch.int64, device=DEV)
+    cb.cbfs_run(g.h, src, sz, C, d, 2, dist, masks, d + 1, stats)
+    torch.cuda.synchronize()
+    v = torch.arange(g.n, device=DEV, dtype=torch.int64)
+    x, y = v % side, v // side
+    st = stats.cpu().numpy()
+    for c in range(C):
+        k = int(sz[c])
+        S = src[c, :k].to(torch.int64)
+        D = (x[None, :] - (S % side)[:, None]).abs() + (y[None, :] - (S // side)[:, None]).abs()  # [k][n]
+        delta = D.min(dim=0).values
+        assert torch.equal(dist[:, c].to(torch.int64) & 0xFFFF, delta), c
+        off = D - delta[None, :]
+        assert int(off.max()) <= d  # a radius-2 ball has diameter <= 4
+        bits = (torch.ones(k, dtype=torch.int64, device=DEV) << torch.arange(k, device=DEV))[:, None]
+        for i in range(d + 1):
+            expect = ((off == i).to(torch.int64) * bits).sum(dim=0)
+            assert torch.equal(masks[i, :, c], expect), (c, i)
+        assert int(st[c, 0]) == 1 + int(D.max()), c  # rounds executed = 1 + max distance (SURVEY §8(c))
+    g.close()
