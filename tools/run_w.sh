@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
-for m in query stats; do timeout 900 python bench.py --config c5_knn --clusters 512 --mode $m --steps 1 --warmup 1 --no-e2e --no-cpu --no-clocks > gpurun_out/c5_$m.log 2>&1; echo "$m rc $?"; tail -1 gpurun_out/c5_$m.log | python -c "import json,sys; r=json.loads(sys.stdin.read()); print(r['ms_per_step'], r['config'].get('phase_ms_rank0'))"; done
+for cfg in c1_er:16 c2_rmat20:64; do name=${cfg%%:*}; r=${cfg##*:}
+ for sched in "200 1000" "1 1"; do timeout 900 python tools/pll_probe.py $name $r 4096 $sched 100000 > gpurun_out/pll_seq.log 2>&1; echo -n "$name r=$r sched=$sched: "; tail -1 gpurun_out/pll_seq.log | python -c "import json,sys; r=json.loads(sys.stdin.read()); print(r['labels_per_vertex'], r['max_labels'], r['batches'], r['ms_pbfs'])"; done; done
