@@ -104,3 +104,29 @@ def test_pll_errors():
         cb.cbfs_pll_query(h, bad, bad, out)
     cb.cbfs_pll_destroy(h)
     g.close()
+
+
+def test_pll_edgeless_and_tiny():
+    """Degenerate inputs (R26): an edgeless graph labels every vertex with
+    itself only (answers 0 on the diagonal, INT32_MAX elsewhere); a single
+    edge; both equal the oracle."""
+    for n, pairs in ((100, []), (2, [(0, 1)]), (5, [(1, 2), (2, 3)])):
+        src = np.array([p[0] for p in pairs], np.uint32)
+        dst = np.array([p[1] for p in pairs], np.uint32)
+        ref = orc.csr_from_edges(n, src, dst)
+        oidx = orc.pll_build(ref, np.zeros((0, 64), np.uint32), np.zeros(0, np.uint8), 2, first=2, bmax=4, cap=8)
+        g = cb.Graph.from_edges(n, src, dst)
+        h = cb.cbfs_pll_build(g.h, None, None, 0, 2, 2, 4, 8)
+        counts = torch.empty((n,), dtype=torch.int32, device=DEV)
+        entries = torch.empty((n, 8), dtype=torch.int32, device=DEV)
+        cb.cbfs_pll_export(h, counts, entries)
+        assert np.array_equal(np_u32(counts), oidx["counts"])
+        s = np.repeat(np.arange(n), n).astype(np.uint32); t = np.tile(np.arange(n), n).astype(np.uint32)
+        out = torch.empty((n * n,), dtype=torch.int32, device=DEV)
+        cb.cbfs_pll_query(h, to_dev_u32(s), to_dev_u32(t), out)
+        assert np.array_equal(out.cpu().numpy(), orc.pll_query(oidx, s, t))
+        if not pairs:
+            assert (np_u32(counts) == 1).all()
+            assert (out.cpu().numpy().reshape(n, n) == np.where(np.eye(n, dtype=bool), 0, orc.INT32_MAX)).all()
+        cb.cbfs_pll_destroy(h)
+        g.close()
