@@ -153,6 +153,33 @@ def query_label_handles(handles, s: torch.Tensor, t: torch.Tensor) -> torch.Tens
     return best
 
 
+def query_block(q: int, world: int, rank: int):
+    """[lo, hi) of the contiguous block of q queries rank `rank` answers, and
+    the common block length (equal shapes for all_gather)."""
+    per = (q + world - 1) // world if world else q
+    lo = min(rank * per, q)
+    return lo, min(lo + per, q), per
+
+
+def query_index_sharded(answer_fn, s: torch.Tensor, t: torch.Tensor, group=None) -> torch.Tensor:
+    """once every rank holds every label store (the
+    all-gather above), the queries are sharded by index — rank r answers its
+    contiguous block with answer_fn(s_block, t_block) (e.g. a
+    query_label_handles closure) — and the int32 blocks are all-gathered, so
+    every rank ends with all q answers."""
+    world, rank = _world(group)
+    q = int(s.shape[0])
+    lo, hi, per = query_block(q, world, rank)
+    mine = torch.full((per,), CBFS_QUERY_UNREACHED, dtype=torch.int32, device=s.device)
+    if hi > lo:
+        mine[:hi - lo] = answer_fn(s[lo:hi], t[lo:hi])
+    if world == 1:
+        return mine[:q]
+    parts = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(parts, mine, group=group)
+    return torch.cat(parts)[:q]
+
+
 def min_reduce_answers(best: torch.Tensor, group=None) -> torch.Tensor:
     """MIN all-reduce of per-rank partial answers (int32, CBFS_QUERY_UNREACHED =
     no cluster reached both ends), in place."""
@@ -173,4 +200,4 @@ def query_stream_sharded(graph, sources: torch.Tensor, sizes: torch.Tensor, d: i
 
 __all__ = ["cluster_shard", "shard_width", "local_clusters", "build_label_shard", "all_gather_shards",
            "gather_labels", "query_gathered", "build_local_labels", "gather_label_images", "query_label_handles",
-           "min_reduce_answers", "query_stream_sharded", "CBFS_UNREACHED_U16"]
+           "min_reduce_answers", "query_stream_sharded", "query_block", "query_index_sharded", "CBFS_UNREACHED_U16"]

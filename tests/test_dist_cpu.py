@@ -104,8 +104,21 @@ def _a12_worker(rank, world, port, out):
     for dp, mp_ in zip(*parts):
         merged = np.minimum(merged, orc.query(dp.numpy().view(np.uint16), mp_.numpy().view(np.uint64), s, t))
     full = orc.query_stream(g, src, sz, d, s, t, threads=1)
+
+    def answer(sb, tb):  # every gathered shard, min-merged, for one block of queries
+        a = np.full(len(sb), orc.INT32_MAX, np.int32)
+        for dp, mp_ in zip(*parts):
+            a = np.minimum(a, orc.query(dp.numpy().view(np.uint16), mp_.numpy().view(np.uint64), sb.numpy(),
+                                        tb.numpy()))
+        return torch.from_numpy(a)
+    # queries sharded by index after the gather, answers all-gathered (501 = ragged over 2 ranks)
+    s2, t2 = ci.query_pairs(g.n, 501, seed=6)
+    by_index = pd.query_index_sharded(answer, torch.from_numpy(s2.astype(np.int64)),
+                                      torch.from_numpy(t2.astype(np.int64)))
+    ok_index = bool(np.array_equal(by_index.numpy(), orc.query_stream(g, src, sz, d, s2, t2, threads=1)))
+    lo, hi, per = pd.query_block(501, world, rank)
     out.put((rank, idx.tolist(), bool(np.array_equal(best.numpy(), full)), bool(np.array_equal(merged, full)),
-             int((full < orc.INT32_MAX).sum())))
+             int((full < orc.INT32_MAX).sum()), ok_index, (lo, hi, per)))
     dist.destroy_process_group()
 
 
@@ -122,8 +135,9 @@ def test_a12_shard_min_reduce_and_label_gather_gloo():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert res[0][1] == [0, 2, 4, 6, 8, 10] and res[1][1] == [1, 3, 5, 7, 9]
-    for _, _, ok_min, ok_gather, reached in res:
-        assert ok_min and ok_gather and reached > 0
+    assert res[0][6] == (0, 251, 251) and res[1][6] == (251, 501, 251)
+    for _, _, ok_min, ok_gather, reached, ok_index, _ in res:
+        assert ok_min and ok_gather and reached > 0 and ok_index
 
 
 def test_cluster_shard_partition():

@@ -85,6 +85,8 @@ def test_label_images_gather_and_query(nccl_group, d, dist_bytes, w):
     best = pd.query_label_handles(handles, to_dev_u32(s), to_dev_u32(t))
     expect = orc.query_stream(ref, src, sz, d, s, t)
     assert np.array_equal(best.cpu().numpy(), expect)
+    by_index = pd.query_index_sharded(lambda a, b: pd.query_label_handles(handles, a, b), to_dev_u32(s), to_dev_u32(t))
+    assert np.array_equal(by_index.cpu().numpy(), expect)
     img = np.zeros(info["image_bytes"], np.uint8)  # host round trip
     cb.cbfs_labels_export(h, img)
     h2 = cb.cbfs_labels_import(g.h, img)
