@@ -85,17 +85,22 @@ __global__ void k_csr_keys(const uint64_t* __restrict__ off, const uint32_t* __r
   }
 }
 
-__global__ void k_split_keys(const uint64_t* __restrict__ keys, uint64_t m, uint32_t n, uint32_t* __restrict__ cols,
-                             uint64_t* __restrict__ off) {
-  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e <= m; e += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t r = e < m ? (uint32_t)(keys[e] >> 32) : n;
-    uint32_t rp = e > 0 ? (uint32_t)(keys[e - 1] >> 32) : 0;
-    if (e < m) cols[e] = (uint32_t)keys[e];
-    if (e == 0) {
-      for (uint32_t x = 0; x <= r; ++x) off[x] = 0;
-    } else {
-      for (uint32_t x = rp + 1; x <= r; ++x) off[x] = e;
+// sorted (row << 32 | col) keys -> cols; the row offsets come from
+// k_row_offsets (a binary search per row: runs of empty rows — the isolated
+// vertices, all at the end after the degree relabel — cost nothing extra)
+__global__ void k_split_keys(const uint64_t* __restrict__ keys, uint64_t m, uint32_t* __restrict__ cols) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m; e += (uint64_t)gridDim.x * blockDim.x)
+    cols[e] = (uint32_t)keys[e];
+}
+// off[x] = first e with row(keys[e]) >= x, x = 0..n
+__global__ void k_row_offsets(const uint64_t* __restrict__ keys, uint64_t m, uint32_t n, uint64_t* __restrict__ off) {
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x <= n; x += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t lo = 0, hi = m;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if ((keys[mid] >> 32) < x) lo = mid + 1; else hi = mid;
     }
+    off[x] = lo;
   }
 }
 
@@ -252,7 +257,9 @@ static int keys_to_csr(const uint64_t* keys, uint64_t m, uint32_t n, cudaStream_
     CBFS_CUDA(cudaMemsetAsync(*off, 0, sizeof(uint64_t) * (n + 1ULL), st));
     return CBFS_OK;
   }
-  k_split_keys<<<grid_for(m + 1, 256), 256, 0, st>>>(keys, m, n, *cols, *off);
+  k_split_keys<<<grid_for(m, 256), 256, 0, st>>>(keys, m, *cols);
+  CBFS_LAUNCHED();
+  k_row_offsets<<<grid_for(n + 1ull, 256), 256, 0, st>>>(keys, m, n, *off);
   CBFS_LAUNCHED();
   return CBFS_OK;
 }

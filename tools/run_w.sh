@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_distributed.py -q -x > gpurun_out/dist.log 2>&1; echo "dist rc $?"; tail -1 gpurun_out/dist.log
-timeout 900 python tools/query_probe.py > gpurun_out/qprobe.log 2>&1; echo "qprobe rc $?"; tail -8 gpurun_out/qprobe.log
+echo new; timeout 600 python tools/build_probe.py c3_rmat24 2 2>&1 | head -4
+echo old; CBFS_LIB_PATH=build_var/old/libcbfs.so timeout 600 python tools/build_probe.py c3_rmat24 2 2>&1 | head -4
