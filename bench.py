@@ -223,7 +223,7 @@ def run_reference(args, world, rank):
               f"selection ({r['select_s']:.1f}s) excluded")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * float(np.mean(secs)) if secs else None,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": args.config, "graph": el.name, "n": el.n, "clusters": cfg["clusters"],
                        "k": cfg["k"], "d": cfg["d"]},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
