@@ -186,7 +186,8 @@ int cbfs_run(cbfs_graph* g, const uint32_t* sources, const uint8_t* sizes, uint3
  *               cluster c in column c * words + w; or NULL
  *   out_stats : device [n_clusters * words][4], the statistics of each
  *               64-source word (as cbfs_run's per cluster), or NULL
- *   other arguments as cbfs_run.  Always the batched engine.
+ *   other arguments as cbfs_run (either engine: both advance the lanes of a
+ *   batch in lockstep rounds, which the Delta merge relies on).
  * Errors: EINVAL (size 0 or > 64 * words, duplicate or out-of-range source),
  * EUNSUPPORTED (words not 1/2/4/8, d > MAX_D), EOVERFLOW, ENOMEM, ECUDA. */
 int cbfs_run_wide(cbfs_graph* g, const uint32_t* sources, const uint16_t* sizes, uint32_t n_clusters, uint32_t words,

@@ -1350,7 +1350,8 @@ int cbfs_run_wide(cbfs_graph* gh, const uint32_t* sources, const uint16_t* sizes
   src.proto.dist_bytes = dist_bytes;
   src.proto.C = (uint32_t)L;
   src.proto.direction = direction;
-  src.proto.engine = ENGINE_BATCHED;  // lanes of a cluster advance in lockstep rounds (the Delta merge relies on it)
+  src.proto.engine = choose_engine(g, direction);  // both engines advance a batch's lanes in lockstep rounds
+  if (src.proto.engine < 0) return CBFS_ECUDA;
   src.proto.out_dist = out_dist;
   src.proto.out_masks = out_masks;
   src.proto.mask_bytes = 8;

@@ -54,6 +54,7 @@ struct SpDesc {
   void* out_masks;           // [planes][n][C] words of mask_bytes, or null
   uint64_t C, cbase;
   uint32_t n, nb, d, planes, dist_bytes, mask_bytes;
+  uint32_t wide, pad2;       // W > 1: lanes are the 64-source words of clusters of W lanes (cbfs_run_wide)
 };
 // Round state of a sparse-engine batch (device-resident).
 struct SpCtl {

@@ -62,14 +62,14 @@ __global__ void k_sp_init(SpCell* __restrict__ cells, uint64_t count) {
 // R1 (S_next[s_j] = {j}, F_0 = S): P_0 of cell (c, s_j) = bit j.
 __global__ void k_sp_seed(const uint32_t* __restrict__ sources, const uint8_t* __restrict__ sizes, uint32_t nb,
                           uint32_t n, const uint32_t* __restrict__ inv, SpCell* __restrict__ cells,
-                          uint32_t* __restrict__ list0, SpCtl* __restrict__ ctl) {
+                          uint32_t* __restrict__ list0, SpCtl* __restrict__ ctl, int allow_empty) {
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;  // 64 threads per cluster
   const uint32_t c = t >> 6, j = t & 63;
   bool claim = false;
   uint32_t e = 0;
   if (c < nb) {
     const uint32_t k = sizes[c];
-    if (k == 0 || k > 64) {
+    if ((k == 0 && !allow_empty) || k > 64) {
       if (j == 0) atomicOr(&ctl->err, ERR_BAD_SIZE);
     } else if (j < k) {
       const uint32_t s = sources[(uint64_t)c * 64 + j];
@@ -98,6 +98,38 @@ __global__ void k_sp_seed(const uint32_t* __restrict__ sources, const uint8_t* _
 // P_i \ S_seen; Delta on first visit; S_v[i - Delta] = S_new; S_seen |=
 // S_new; the output writes; per-cluster statistics.  P_i keeps S_new for the
 // push of the same round.
+
+// Output of one folded entry (cluster lane c, vertex v, first visit in round
+// dv): Delta on the first visit, S_new into plane i - Delta.  With wide
+// clusters (W > 1, cbfs_run_wide, R28) the cluster's Delta is the least first
+// visit over its W lanes (their cells at the same vertex; lanes advance in
+// lockstep rounds) and out_dist has one column per cluster.
+template <int DB>
+__device__ __forceinline__ void sp_output(const SpDesc* __restrict__ D, const SpCell* __restrict__ cells, uint32_t n,
+                                          uint32_t c, uint32_t v, uint32_t i, uint32_t dv, bool first, uint64_t nw,
+                                          bool& overflow) {
+  const uint32_t orig = D->perm ? D->perm[v] : v;
+  const uint64_t col = (uint64_t)orig * D->C + D->cbase + c;
+  uint32_t dc = dv;
+  uint64_t dcol = col;
+  const uint32_t W = D->wide;
+  if (W > 1) {
+    const uint32_t c0 = c & ~(W - 1);
+    for (uint32_t x = 0; x < W; ++x) dc = min(dc, (uint32_t)cells[(uint64_t)(c0 + x) * n + v].dist);
+    dcol = (uint64_t)orig * (D->C / W) + (D->cbase + c) / W;
+  }
+  if (first && D->out_dist && dc == i) {
+    if (DB == 1) {
+      overflow |= i > 254;
+      ((uint8_t*)D->out_dist)[dcol] = (uint8_t)(i > 254 ? 254 : i);
+    } else {
+      ((uint16_t*)D->out_dist)[dcol] = (uint16_t)i;
+    }
+  }
+  const uint32_t oi = i - dc;
+  if (D->out_masks && oi < D->planes) store_mask(D->out_masks, (uint64_t)oi * n * D->C + col, nw, D->mask_bytes);
+}
+
 template <int DB>
 __global__ void __launch_bounds__(SP_THREADS) k_sp_fold(const SpDesc* __restrict__ D, SpCtl* __restrict__ ctl,
                                                         SpCell* __restrict__ cells,
@@ -159,18 +191,7 @@ __global__ void __launch_bounds__(SP_THREADS) k_sp_fold(const SpDesc* __restrict
           if (first) dv = i;
           *reinterpret_cast<ulonglong2*>(cell) = make_ulonglong2(sd[q].x | nw, (unsigned long long)dv);
           deg = (uint32_t)(o1[q] - o0[q]);
-          const uint32_t orig = perm ? perm[v] : v;
-          const uint64_t col = (uint64_t)orig * C + cbase + c;
-          if (first && out_dist) {
-            if (DB == 1) {
-              overflow |= i > 254;
-              ((uint8_t*)out_dist)[col] = (uint8_t)(i > 254 ? 254 : i);
-            } else {
-              ((uint16_t*)out_dist)[col] = (uint16_t)i;
-            }
-          }
-          const uint32_t oi = i - dv;
-          if (out_masks && oi < planes) store_mask(out_masks, (uint64_t)oi * n * C + col, nw, mb);
+          if (out_dist || out_masks) sp_output<DB>(D, cells, n, c, v, i, dv, first, nw, overflow);
         }
       }
       // per-cluster statistics, one shared atomic per distinct cluster in the warp
@@ -347,19 +368,7 @@ __global__ void __launch_bounds__(SP_THREADS, CBFS_SP_MINB) k_sp_push(const SpDe
             if (first) dv = i;
             *reinterpret_cast<ulonglong2*>(cell) = make_ulonglong2(sd0[q].x | nw[q], (unsigned long long)dv);
             deg = (uint32_t)(o1[q] - o0[q]);
-            const uint32_t orig = D->perm ? D->perm[v] : v;
-            const uint64_t col = (uint64_t)orig * D->C + D->cbase + c;
-            if (first && D->out_dist) {
-              if (DB == 1) {
-                overflow |= i > 254;
-                ((uint8_t*)D->out_dist)[col] = (uint8_t)(i > 254 ? 254 : i);
-              } else {
-                ((uint16_t*)D->out_dist)[col] = (uint16_t)i;
-              }
-            }
-            const uint32_t oi = i - dv;
-            if (D->out_masks && oi < D->planes)
-              store_mask(D->out_masks, (uint64_t)oi * n * D->C + col, nw[q], D->mask_bytes);
+            if (D->out_dist || D->out_masks) sp_output<DB>(D, cells, n, c, v, i, dv, first, nw[q], overflow);
           }
           if (p) cell->p[cur] = 0;
         }
@@ -566,6 +575,7 @@ int sparse_start(const Graph* g, Slot* w, const RunArgs& a) {
   h->planes = a.planes;
   h->dist_bytes = a.dist_bytes;
   h->mask_bytes = a.mask_bytes ? a.mask_bytes : 8;
+  h->wide = a.wide > 1 ? a.wide : 1;
   CBFS_CUDA(cudaMemcpyAsync(w->sp_desc, h, sizeof(SpDesc), cudaMemcpyHostToDevice, st));
   const uint64_t ncell = (uint64_t)n * LANES;
   k_sp_init<<<grid_for(ncell, 256, 148u * 16u), 256, 0, st>>>(reinterpret_cast<SpCell*>(w->blk), ncell);
@@ -573,7 +583,8 @@ int sparse_start(const Graph* g, Slot* w, const RunArgs& a) {
   CBFS_CUDA(cudaMemsetAsync(w->bstats, 0, LANES * 4 * sizeof(uint64_t), st));
   CBFS_CUDA(cudaMemsetAsync(w->sp_ctl, 0, sizeof(SpCtl), st));
   k_sp_seed<<<(a.nb * 64 + 255) / 256, 256, 0, st>>>(a.sources, a.sizes, a.nb, n, g->inv,
-                                                     reinterpret_cast<SpCell*>(w->blk), w->listA, w->sp_ctl);
+                                                     reinterpret_cast<SpCell*>(w->blk), w->listA, w->sp_ctl,
+                                                     a.wide > 1);
   CBFS_LAUNCHED();
   CBFS_CUDA(cudaMemcpyAsync(w->sp_ctl_h, w->sp_ctl, sizeof(SpCtl), cudaMemcpyDeviceToHost, st));
   CBFS_CUDA(cudaEventRecord(w->ready, st));

@@ -140,6 +140,26 @@ def test_wide_labels_decode_and_query(kind, d, W):
     g.close()
 
 
+@pytest.mark.parametrize("engine", ["batched", "sparse"])
+def test_run_wide_each_engine(engine):
+    """Both engines (forced) give the definition's output for wide clusters,
+    on a low- and a high-diameter graph."""
+    eng = cb.CBFS_ENGINE_BATCHED if engine == "batched" else cb.CBFS_ENGINE_SPARSE
+    cb.cbfs_set_engine(eng)
+    try:
+        for kind, d, W in (("rmat", 2, 4), ("grid", 4, 2), ("er", 4, 8)):
+            el = GRAPHS[kind]()
+            ref = orc.csr_from_edgelist(el)
+            src, sz, lists = wide_clusters(ref, 20, W, d, np.random.default_rng(77 + W))
+            g = gpu_graph(el, relabel=(kind == "rmat"))
+            for dist_bytes in (1, 2):
+                dist, masks, _ = run_wide(g, src, sz, W, d, dist_bytes=dist_bytes)
+                check_against_oracle(ref, lists, dist, masks, W, d, d + 1)
+            g.close()
+    finally:
+        cb.cbfs_set_engine(cb.CBFS_ENGINE_AUTO)
+
+
 def test_wide_errors_and_empty():
     el = GRAPHS["rmat"]()
     ref = orc.csr_from_edgelist(el)

@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-for q in 1 10000000; do timeout 900 python bench.py --config c5_knn --clusters 512 --mode query --queries $q --steps 1 --warmup 1 --no-e2e --no-cpu --no-clocks > gpurun_out/c5_q$q.log 2>&1; echo -n "queries $q: "; tail -1 gpurun_out/c5_q$q.log | python -c "import json,sys; r=json.loads(sys.stdin.read()); print(r['ms_per_step'], r['config'].get('phase_ms_rank0'))"; done
-timeout 900 python bench.py --config c5_knn --clusters 512 --mode stats --steps 1 --warmup 1 --no-e2e --no-cpu --no-clocks > gpurun_out/c5_st.log 2>&1; echo -n "stats: "; tail -1 gpurun_out/c5_st.log | python -c "import json,sys; r=json.loads(sys.stdin.read()); print(r['ms_per_step'], r['config'].get('phase_ms_rank0'))"
+CBFS_LIB_PATH=build_var/dbg/libcbfs.so timeout 600 python tools/pull_stats.py > gpurun_out/pstats.log 2>&1; tail -3 gpurun_out/pstats.log | cut -c1-400
