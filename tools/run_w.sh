@@ -1,2 +1,2 @@
 mkdir -p gpurun_out
-CBFS_LIB_PATH=build_var/dbg/libcbfs.so timeout 600 python tools/pull_stats.py > gpurun_out/pstats.log 2>&1; tail -3 gpurun_out/pstats.log | cut -c1-400
+LANES_TOTAL=256 timeout 1200 python tools/wide_probe.py c5_knn 1,2,4 > gpurun_out/wp_c5.log 2>&1; tail -3 gpurun_out/wp_c5.log

@@ -33,7 +33,8 @@ for W in Ws:
     sz = torch.empty((r,), dtype=torch.int16, device=dev)
     got = cb.cbfs_select_clusters_wide(g.h, r, 64 * W, d, cb.CBFS_ROOT_DEGREE, 0, W, src, sz)
     src, sz = src[:got].contiguous(), sz[:got].contiguous()
-    dist = torch.empty((n, got), dtype=torch.uint8, device=dev)
+    db = 1 if cfg["kind"] in ("rmat", "er") else 2  # u8 Delta only where every distance fits (R10)
+    dist = torch.empty((n, got), dtype=torch.uint8 if db == 1 else torch.int16, device=dev)
     masks = torch.empty((d + 1, n, got * W), dtype=torch.int64, device=dev)
     stats = torch.zeros((got * W, 4), dtype=torch.int64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -43,7 +44,7 @@ for W in Ws:
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        cb.cbfs_run_wide(g.h, src, sz, got, W, d, 1, dist, masks, d + 1, stats)
+        cb.cbfs_run_wide(g.h, src, sz, got, W, d, db, dist, masks, d + 1, stats)
         e1.record()
         torch.cuda.synchronize()
         if it:
