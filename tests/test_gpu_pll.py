@@ -130,3 +130,34 @@ def test_pll_edgeless_and_tiny():
             assert (out.cpu().numpy().reshape(n, n) == np.where(np.eye(n, dtype=bool), 0, orc.INT32_MAX)).all()
         cb.cbfs_pll_destroy(h)
         g.close()
+
+
+@pytest.mark.timeout(600)
+def test_pll_c2_full_size_exact_sampled():
+    """Config 2's graph at full size (RMAT-20, r = 64 clusters, the paper's
+    batch schedule): the index is an exact distance oracle — 40 sampled
+    sources × 5,000 targets each against textbook BFS (the oracle PLL is too
+    slow at this size; its labels are pinned on smaller graphs above)."""
+    el = ci.make_graph("c2_rmat20")
+    ref = orc.csr_from_edgelist(el)
+    g = gpu_graph(el, relabel=True)
+    src = torch.empty((64, 64), dtype=torch.int32, device=DEV)
+    sz = torch.empty((64,), dtype=torch.uint8, device=DEV)
+    got = cb.cbfs_select_clusters(g.h, 64, 64, 2, cb.CBFS_ROOT_DEGREE, 0, src, sz)
+    h = cb.cbfs_pll_build(g.h, src[:got].contiguous(), sz[:got].contiguous(), got, 2, 200, 1000, 2048)
+    info = cb.cbfs_pll_info(h)
+    assert info["roots"] == g.n - int(sz[:got].sum()) and info["total_labels"] > 0
+    rng = np.random.default_rng(5)
+    deg = ref.degrees()
+    cand = np.flatnonzero(deg > 0)
+    sources = np.concatenate([rng.choice(cand, 36, replace=False), np.argsort(-deg.astype(np.int64))[:4]])
+    for x in sources:
+        bfs = orc.plain_bfs(ref, int(x))
+        tt = rng.integers(0, g.n, 5000).astype(np.uint32)
+        ss = np.full(len(tt), x, np.uint32)
+        out = torch.empty((len(tt),), dtype=torch.int32, device=DEV)
+        cb.cbfs_pll_query(h, to_dev_u32(ss), to_dev_u32(tt), out)
+        expect = np.where(bfs[tt] == orc.INF32, orc.INT32_MAX, bfs[tt]).astype(np.int64)
+        assert np.array_equal(out.cpu().numpy().astype(np.int64), expect), int(x)
+    cb.cbfs_pll_destroy(h)
+    g.close()
