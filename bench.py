@@ -546,7 +546,7 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=32)
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--separate-select", action="store_true", help="select, then run (no A1/A2-A8 overlap)")
-    ap.add_argument("--clock-ms", type=int, default=500)
+    ap.add_argument("--clock-ms", type=int, default=100)
     ap.add_argument("--concurrency", type=int, default=0, help="concurrent batches per GPU (0 = library default)")
     ap.add_argument("--engine", type=int, default=0, help="0 auto, 1 batched, 2 sparse (cbfs_set_engine)")
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
