@@ -424,6 +424,10 @@ def run_ours(args, world, rank, local):
     per_kernel = {kk: {"event_ms_per_step": round(v["ms"], 3), "launches_per_step": v["launches"],
                        "share_of_event_time": round(v["ms"] / ksum, 4)}
                   for kk, v in perstep.items() if v["launches"]}
+    for kk, pk in per_kernel.items():  # the kernel's own algorithmic bytes over its summed launch time; with
+        if kk in parts and pk["event_ms_per_step"] > 0:  # batches in flight on 4 streams each launch shares the GPU
+            pk["alg_bytes_per_step"] = float(parts[kk])
+            pk["alg_gbs_over_own_event_time"] = round(parts[kk] / (pk["event_ms_per_step"] / 1000.0) / 1e9, 1)
     dom = max(per_kernel, key=lambda kk: per_kernel[kk]["event_ms_per_step"]) if per_kernel else None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic,
