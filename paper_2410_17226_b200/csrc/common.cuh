@@ -89,6 +89,7 @@ struct RunArgs {
   void* out_masks;          // device [planes][n][C] words of mask_bytes, or null
   uint64_t* out_stats;      // device [nb][4] or null
   uint32_t mask_bytes;      // 8 (cbfs_run) or 1/2/4 (packed label stores, w = 8 * mask_bytes; 0 reads as 8)
+  uint32_t out_cmajor;      // outputs cluster-major (Delta at col * n + row; library-internal staging, sparse engine)
   uint32_t wide;            // W > 1: lanes are the 64-source words of clusters of W lanes (cbfs_run_wide); out_dist
                             // has C / W columns
 };

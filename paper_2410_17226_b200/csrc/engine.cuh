@@ -54,7 +54,8 @@ struct SpDesc {
   void* out_masks;           // [planes][n][C] words of mask_bytes, or null
   uint64_t C, cbase;
   uint32_t n, nb, d, planes, dist_bytes, mask_bytes;
-  uint32_t wide, pad2;       // W > 1: lanes are the 64-source words of clusters of W lanes (cbfs_run_wide)
+  uint32_t wide;             // W > 1: lanes are the 64-source words of clusters of W lanes (cbfs_run_wide)
+  uint32_t out_cmajor;       // outputs cluster-major (RunArgs::out_cmajor)
 };
 // Round state of a sparse-engine batch (device-resident).
 struct SpCtl {

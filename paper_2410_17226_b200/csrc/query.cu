@@ -60,7 +60,11 @@ __global__ void k_decode(uint32_t n, uint32_t C, uint32_t d, uint32_t planes, co
 // S_s[i] & S_t[j] != 0, scanning i+j = 0..2d; S_x[d] is
 // rebuilt from the other subsets when the store keeps only d (R14).  MB is
 // the store's word: 8 bytes, or 1/2/4 for the packed w = 8/16/32 stores.
-template <int DB, int MB>
+// CM: the subsets are cluster-major (subset i of cluster c at (i * C + c) *
+// n + v) — the streaming query's staging when the sparse engine (cluster-
+// major frontier) writes them; Delta is vertex-major (transposed after the
+// batch, k_transpose_dist), so the per-query Delta rows stay coalesced.
+template <int DB, int MB, bool CM = false>
 __global__ void __launch_bounds__(256) k_query(uint32_t n, uint32_t C, uint32_t d, uint32_t planes,
                                                const void* __restrict__ dist, const void* __restrict__ masks,
                                                const uint8_t* __restrict__ sizes, const uint32_t* __restrict__ s,
@@ -93,8 +97,8 @@ __global__ void __launch_bounds__(256) k_query(uint32_t n, uint32_t C, uint32_t 
       uint64_t Sa[CBFS_MAX_D + 1], Sb[CBFS_MAX_D + 1];
       uint64_t ua = 0, ub = 0;
       for (uint32_t i = 0; i < planes; ++i) {
-        Sa[i] = load_mask<MB>(masks, ((uint64_t)i * n + a) * C + c);
-        Sb[i] = load_mask<MB>(masks, ((uint64_t)i * n + b) * C + c);
+        Sa[i] = load_mask<MB>(masks, CM ? ((uint64_t)i * C + c) * n + a : ((uint64_t)i * n + a) * C + c);
+        Sb[i] = load_mask<MB>(masks, CM ? ((uint64_t)i * C + c) * n + b : ((uint64_t)i * n + b) * C + c);
         ua |= Sa[i];
         ub |= Sb[i];
       }
@@ -242,12 +246,36 @@ static void launch_query_wide_db(unsigned blocks, uint32_t n, uint32_t C, uint32
   }
 }
 
+// [LANES][n] u16 -> [n][LANES]: 32 vertices x 64 clusters per block through
+// shared memory, both sides coalesced
+__global__ void __launch_bounds__(256) k_transpose_dist(const uint16_t* __restrict__ in, uint32_t n,
+                                                        uint16_t* __restrict__ out) {
+  __shared__ uint16_t tile[LANES][33];
+  for (uint64_t v0 = (uint64_t)blockIdx.x * 32; v0 < n; v0 += (uint64_t)gridDim.x * 32) {
+    for (uint32_t x = threadIdx.x; x < LANES * 32; x += blockDim.x) {
+      const uint32_t c = x >> 5, j = x & 31;
+      tile[c][j] = v0 + j < n ? in[(uint64_t)c * n + v0 + j] : 0xFFFFu;
+    }
+    __syncthreads();
+    for (uint32_t x = threadIdx.x; x < LANES * 32; x += blockDim.x) {
+      const uint32_t j = x >> 6, c = x & 63;
+      if (v0 + j < n) out[(v0 + j) * LANES + c] = tile[c][j];
+    }
+    __syncthreads();
+  }
+}
+
 static int launch_query(uint32_t n, uint32_t C, uint32_t d, uint32_t planes, const void* dist, uint32_t dist_bytes,
                         const void* masks, const uint8_t* sizes, const uint32_t* s, const uint32_t* t, uint64_t q,
                         int32_t* best, int* bad, cudaStream_t st, const uint32_t* inv = nullptr,
-                        uint32_t mask_bytes = 8) {
+                        uint32_t mask_bytes = 8, bool cmajor = false) {
   if (q == 0 || C == 0) return CBFS_OK;
   const unsigned blocks = grid_for(q * 32, 256, 148u * 8u * 8u);
+  if (cmajor) {  // the streaming query's cluster-major staging (u16 Delta, u64 subsets)
+    k_query<2, 8, true><<<blocks, 256, 0, st>>>(n, C, d, planes, dist, masks, sizes, s, t, q, best, bad, inv);
+    CBFS_LAUNCHED();
+    return CBFS_OK;
+  }
   if (dist_bytes == 1)
     launch_query_db<1>(blocks, n, C, d, planes, dist, masks, mask_bytes, sizes, s, t, q, best, bad, st, inv);
   else
@@ -499,7 +527,7 @@ int cbfs_query_distance(uint32_t n, uint32_t C, uint32_t d, uint32_t planes, con
 // per-slot label staging; the query runs on the slot's stream when its batch ends
 struct QuerySource : ArraySource {
   uint32_t n = 0, d = 0, planes = 0;
-  std::vector<uint16_t*> sd;
+  std::vector<uint16_t*> sd, sdt;  // Delta staging (cluster-major when the sparse engine writes it) + transposed
   std::vector<uint64_t*> sm;
   const uint32_t *s = nullptr, *t = nullptr;
   uint64_t q = 0;
@@ -512,13 +540,23 @@ struct QuerySource : ArraySource {
     a.C = LANES;
     a.cbase = 0;
     a.out_internal = 1;  // rows by internal id: the fold's writes follow the traversal's locality
+    // the sparse engine's frontier is cluster-major: its label writes coalesce
+    // in a cluster-major staging (the batched engine's are vertex-grouped)
+    a.out_cmajor = a.engine == ENGINE_SPARSE && !getenv("CBFS_QUERY_VMAJOR");
     CBFS_CUDA(cudaMemsetAsync(sd[slot], 0xFF, sizeof(uint16_t) * (uint64_t)n * LANES, st));
     CBFS_CUDA(cudaMemsetAsync(sm[slot], 0, sizeof(uint64_t) * (uint64_t)planes * n * LANES, st));
     return CBFS_OK;
   }
   int finished(const RunArgs& a, int slot, cudaStream_t st) override {
     // lanes >= nb stay unreachable (dist 0xFFFF), so the query skips them
-    return launch_query(n, LANES, d, planes, sd[slot], 2, sm[slot], a.sizes, s, t, q, best, bad, st, inv);
+    const uint16_t* dq = sd[slot];
+    if (a.out_cmajor && q) {
+      k_transpose_dist<<<grid_for((n + 31ull) / 32, 1, 148u * 16u), 256, 0, st>>>(sd[slot], n, sdt[slot]);
+      CBFS_LAUNCHED();
+      dq = sdt[slot];
+    }
+    return launch_query(n, LANES, d, planes, dq, 2, sm[slot], a.sizes, s, t, q, best, bad, st, inv, 8,
+                        a.out_cmajor != 0);
   }
 };
 
@@ -552,9 +590,11 @@ int cbfs_query_stream(cbfs_graph* gh, const uint32_t* sources, const uint8_t* si
   src.n = n; src.d = d; src.planes = planes; src.s = s; src.t = t; src.q = q; src.best = inout_best;
   src.inv = g->inv;
   src.sd.assign(P, nullptr);
+  src.sdt.assign(P, nullptr);
   src.sm.assign(P, nullptr);
   for (int k = 0; k < P; ++k) {
     CBFS_CUDA(cudaMallocAsync(&src.sd[k], sizeof(uint16_t) * (uint64_t)n * LANES + 16, st));
+    CBFS_CUDA(cudaMallocAsync(&src.sdt[k], sizeof(uint16_t) * (uint64_t)n * LANES + 16, st));
     CBFS_CUDA(cudaMallocAsync(&src.sm[k], sizeof(uint64_t) * (uint64_t)planes * n * LANES + 16, st));
   }
   CBFS_CUDA(cudaMallocAsync(&src.bad, sizeof(int), st));
@@ -564,6 +604,7 @@ int cbfs_query_stream(cbfs_graph* gh, const uint32_t* sources, const uint8_t* si
   CBFS_CUDA(cudaMemcpyAsync(&hbad, src.bad, sizeof(int), cudaMemcpyDeviceToHost, st));
   for (int k = 0; k < P; ++k) {
     CBFS_CUDA(cudaFreeAsync(src.sd[k], st));
+    CBFS_CUDA(cudaFreeAsync(src.sdt[k], st));
     CBFS_CUDA(cudaFreeAsync(src.sm[k], st));
   }
   CBFS_CUDA(cudaFreeAsync(src.bad, st));

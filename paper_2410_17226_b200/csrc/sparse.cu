@@ -118,6 +118,14 @@ __device__ __forceinline__ void sp_output(const SpDesc* __restrict__ D, const Sp
     for (uint32_t x = 0; x < W; ++x) dc = min(dc, (uint32_t)cells[(uint64_t)(c0 + x) * n + v].dist);
     dcol = (uint64_t)orig * (D->C / W) + (D->cbase + c) / W;
   }
+  if (D->out_cmajor) {  // library staging: Delta at c * n + row, subset i at (i * C + c) * n + row
+    dcol = (D->cbase + c) * (uint64_t)n + orig;
+    if (first && D->out_dist && dc == i) ((uint16_t*)D->out_dist)[dcol] = (uint16_t)i;
+    const uint32_t oi = i - dc;
+    if (D->out_masks && oi < D->planes)
+      store_mask(D->out_masks, ((uint64_t)oi * D->C + D->cbase + c) * n + orig, nw, D->mask_bytes);
+    return;
+  }
   if (first && D->out_dist && dc == i) {
     if (DB == 1) {
       overflow |= i > 254;
@@ -576,6 +584,7 @@ int sparse_start(const Graph* g, Slot* w, const RunArgs& a) {
   h->dist_bytes = a.dist_bytes;
   h->mask_bytes = a.mask_bytes ? a.mask_bytes : 8;
   h->wide = a.wide > 1 ? a.wide : 1;
+  h->out_cmajor = a.out_cmajor;
   CBFS_CUDA(cudaMemcpyAsync(w->sp_desc, h, sizeof(SpDesc), cudaMemcpyHostToDevice, st));
   const uint64_t ncell = (uint64_t)n * LANES;
   k_sp_init<<<grid_for(ncell, 256, 148u * 16u), 256, 0, st>>>(reinterpret_cast<SpCell*>(w->blk), ncell);
