@@ -6,7 +6,7 @@ NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -std=c++17 $(ARCH) -O3 -lineinfo -Xcompiler -fPIC -Xptxas -v
 CSRC := paper_2410_17226_b200/csrc
-SRCS := $(CSRC)/graph.cu $(CSRC)/cbfs.cu $(CSRC)/sparse.cu $(CSRC)/select.cu $(CSRC)/query.cu $(CSRC)/labels.cu $(CSRC)/pll.cu
+SRCS := $(CSRC)/graph.cu $(CSRC)/cbfs.cu $(CSRC)/sparse.cu $(CSRC)/select.cu $(CSRC)/query.cu $(CSRC)/labels.cu $(CSRC)/pll.cu $(CSRC)/digest.cu
 OBJS := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
 
 all: paper_2410_17226_b200/libcbfs.so oracle/liboracle.so cbfs_inputs/libcbfsgen.so

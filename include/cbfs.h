@@ -168,6 +168,59 @@ int cbfs_run(cbfs_graph* g, const uint32_t* sources, const uint8_t* sizes, uint3
              uint32_t dist_bytes, void* out_dist, uint64_t* out_masks, uint32_t planes, uint64_t* out_stats,
              uint32_t direction, cbfs_stream stream);
 
+/* cbfs_run_digest — cbfs_run whose full outputs are consumed inside the
+ * call: every batch of 64 clusters writes its cluster distance vectors
+ * <Delta_v, S_v[0..planes-1]> (the same fold and the same layout
+ * as cbfs_run's out_dist / out_masks, 64 columns) into a library-owned
+ * staging store in HBM, and when the batch's last round has been queued a
+ * kernel on the batch's stream reads the store back, reduces each cluster
+ * to cbfs_digest_store's digest and resets the store for the next batch.
+ * For configurations whose whole output does not fit HBM (n * C * (dist_bytes
+ * + 8 planes) bytes) this is the full-output run; the digests are compared
+ * with the oracle's (tests/golden).  As many batches run concurrently as
+ * there are workspace slots with room for a staging store next to them
+ * (n * 64 * (dist_bytes + 8 planes) bytes each).
+ *   out_digest: device [n_clusters] uint64 (overwritten)
+ *   out_stats : as cbfs_run, or NULL
+ *   other arguments as cbfs_run.
+ * Errors: as cbfs_run; ENOMEM when not even one staging store fits. */
+int cbfs_run_digest(cbfs_graph* g, const uint32_t* sources, const uint8_t* sizes, uint32_t n_clusters, uint32_t d,
+                    uint32_t dist_bytes, uint32_t planes, uint64_t* out_digest, uint64_t* out_stats,
+                    uint32_t direction, cbfs_stream stream);
+
+/* cbfs_digest_store — 64-bit digest of every column c of a vertex-major
+ * store (cbfs_run's output layout) dist [n][C] (dist_bytes 1 or 2, 0xFF /
+ * 0xFFFF = unreached), masks [planes][n][C] uint64 (NULL if planes == 0),
+ * all device:
+ *   fin(z)  = SplitMix64 finaliser: z ^= z>>30; z *= 0xBF58476D1CE4E5B9;
+ *             z ^= z>>27; z *= 0x94D049BB133111EB; z ^= z>>31
+ *   x_v     = fin((v * 0x9E3779B97F4A7C15 + 0xD1B54A32D192ED03) ^ (D_v << 48)),
+ *             D_v = Delta_v as a 16-bit value (0xFFFF unreached, also for
+ *             dist_bytes == 1); then x_v = fin(x_v ^ S_v[i]) for i = 0 ..
+ *             planes-1
+ *   digest  = sum over v = 0 .. n-1 of x_v, mod 2^64
+ * (an order-independent sum, so it is formed in parallel).  Used to compare
+ * whole outputs with the oracle (which implements the same definition
+ * independently, oracle.c or_digest_cluster); not part of the method.
+ *   out_digest: device [C] uint64 (overwritten).  Synchronises.
+ * Errors: EINVAL (dist_bytes, planes > CBFS_MAX_D + 1, null pointers). */
+int cbfs_digest_store(uint32_t n, uint32_t C, uint32_t planes, const void* dist, uint32_t dist_bytes,
+                      const uint64_t* masks, uint64_t* out_digest, cbfs_stream stream);
+
+/* cbfs_run_rounds — cbfs_run recording the frontier of every round: for
+ * cluster c and round i < max_rounds, out_rounds[c][i] = {|F_i|, E_i} (the
+ * frontier size and its degree sum; the per-round invariants of
+ * a vertex appears in at most d+1 frontiers, and
+ * the rounds executed are 1 + the largest source distance).  Rounds
+ * past the cluster's last are 0.  No distance outputs.
+ *   out_rounds: device [n_clusters][max_rounds][2] uint64 (overwritten)
+ *   max_rounds: >= 1; rounds beyond it are counted in out_stats only
+ *   out_stats, direction, stream: as cbfs_run.
+ * Errors: as cbfs_run; EINVAL for a null out_rounds or max_rounds == 0. */
+int cbfs_run_rounds(cbfs_graph* g, const uint32_t* sources, const uint8_t* sizes, uint32_t n_clusters, uint32_t d,
+                    uint64_t* out_rounds, uint32_t max_rounds, uint64_t* out_stats, uint32_t direction,
+                    cbfs_stream stream);
+
 /* cbfs_run_wide — C-BFS from clusters of more than 64 sources (k > w, the
  * paper's general k: P:448): each
  * bit-subset is `words` 64-bit words (bit j of the cluster = bit j % 64 of
@@ -392,9 +445,11 @@ int cbfs_set_engine(int engine);
 /* Kernel-level timing of the C-BFS engine (process-wide, not thread-safe):
  * when enabled, CUDA events are recorded on the launching stream around every
  * fold / push / pull launch and read after the round's synchronisation.
- * cbfs_profile_read fills arrays of 4 entries indexed {0 fold, 1 push,
+ * cbfs_profile_read fills arrays of 5 entries indexed {0 fold, 1 push,
  * 2 pull, 3 sparse-engine round loop (one graph launch per batch; its
- * "launches" count the kernels the loop ran)}: total device ms, launches, frontier (cluster, arc) pairs,
+ * "launches" count the kernels the loop ran), 4 output consumer of
+ * cbfs_run_digest (per batch; the call synchronises the batch's stream
+ * after it while profiling)}: total device ms, launches, frontier (cluster, arc) pairs,
  * frontier (vertex, cluster) entries, distinct frontier vertices |U_i| and
  * distinct vertices claimed for the next frontier |U_{i+1}| summed over the
  * launches (host pointers, any may be NULL). */

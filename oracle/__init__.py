@@ -69,6 +69,13 @@ def lib():
                                      u64p, u32p, u64p, ctypes.c_uint32]
         L.or_cluster_bfs_many.argtypes = [ctypes.c_uint32, u64p, u32p, u32p, u8p, ctypes.c_uint32, ctypes.c_uint32,
                                           ctypes.c_int, u16p, u64p, u64p, u64p]
+        L.or_cluster_bfs_many_ex.argtypes = [ctypes.c_uint32, u64p, u32p, u32p, u8p, ctypes.c_uint32,
+                                             ctypes.c_uint32, ctypes.c_int, u16p, u64p, u64p, u64p, u64p, u32p, u64p,
+                                             ctypes.c_uint32]
+        L.or_digest_cluster.restype = ctypes.c_uint64
+        L.or_digest_cluster.argtypes = [ctypes.c_uint32, ctypes.c_uint32, u16p, u64p]
+        L.or_query_stream_ex.argtypes = [ctypes.c_uint32, u64p, u32p, u32p, u8p, ctypes.c_uint32, ctypes.c_uint32,
+                                         ctypes.c_uint64, u32p, u32p, ctypes.c_int, i32p, u64p, u64p]
         L.or_hash_cluster.restype = ctypes.c_uint64
         L.or_hash_cluster.argtypes = [ctypes.c_uint32, ctypes.c_uint32, u16p, u64p]
         L.or_select_clusters.restype = ctypes.c_int64
@@ -265,27 +272,50 @@ def cluster_bfs(g: CSR, S, d: int, max_rounds: int = 1 << 16) -> ClusterResult:
 
 
 def cluster_bfs_many(g: CSR, sources: np.ndarray, sizes: np.ndarray, d: int, threads: int | None = None,
-                     want_outputs: bool = True):
+                     want_outputs: bool = True, want_digest: bool = False, max_rounds: int = 0):
     """Alg. 1 per cluster, clusters over host threads.  sources [C][64] uint32,
     sizes [C] uint8.  Returns dict(dist [C][n], sub [C][d+1][n], stats [C][4],
-    hash [C])."""
+    hash [C]); with want_digest also digest [C] (digest_cluster of each
+    output), with max_rounds > 0 also round_F [C][max_rounds] (|F_i|) and
+    round_E [C][max_rounds] (E_i), zero past the cluster's last round."""
     sources = np.ascontiguousarray(sources, dtype=np.uint32)
     sizes = np.ascontiguousarray(sizes, dtype=np.uint8)
     C = sources.shape[0]
     assert sources.shape == (C, 64) and sizes.shape == (C,)
     stats = np.zeros((C, 4), np.uint64)
     h = np.zeros(C, np.uint64)
+    dg = np.zeros(C, np.uint64) if want_digest else None
+    rF = np.zeros((C, max_rounds), np.uint32) if max_rounds else None
+    rE = np.zeros((C, max_rounds), np.uint64) if max_rounds else None
     dist = np.empty((C, g.n), np.uint16) if want_outputs else None
     sub = np.empty((C, d + 1, g.n), np.uint64) if want_outputs else None
-    rc = lib().or_cluster_bfs_many(g.n, _p(g.off, ctypes.c_uint64), _p(g.cols, ctypes.c_uint32),
-                                   _p(sources, ctypes.c_uint32), _p(sizes, ctypes.c_uint8), C, d,
-                                   threads or default_threads(),
-                                   _p(dist, ctypes.c_uint16) if want_outputs else None,
-                                   _p(sub, ctypes.c_uint64) if want_outputs else None,
-                                   _p(stats, ctypes.c_uint64), _p(h, ctypes.c_uint64))
+    rc = lib().or_cluster_bfs_many_ex(g.n, _p(g.off, ctypes.c_uint64), _p(g.cols, ctypes.c_uint32),
+                                      _p(sources, ctypes.c_uint32), _p(sizes, ctypes.c_uint8), C, d,
+                                      threads or default_threads(),
+                                      _p(dist, ctypes.c_uint16) if want_outputs else None,
+                                      _p(sub, ctypes.c_uint64) if want_outputs else None,
+                                      _p(stats, ctypes.c_uint64), _p(h, ctypes.c_uint64),
+                                      _p(dg, ctypes.c_uint64) if want_digest else None,
+                                      _p(rF, ctypes.c_uint32) if max_rounds else None,
+                                      _p(rE, ctypes.c_uint64) if max_rounds else None, max_rounds)
     if rc:
         raise ValueError("invalid cluster in batch")
-    return dict(dist=dist, sub=sub, stats=stats, hash=h)
+    out = dict(dist=dist, sub=sub, stats=stats, hash=h)
+    if want_digest:
+        out["digest"] = dg
+    if max_rounds:
+        out["round_F"], out["round_E"] = rF, rE
+    return out
+
+
+def digest_cluster(dist: np.ndarray, sub: np.ndarray) -> int:
+    """Order-independent digest of one cluster's output (oracle.c
+    or_digest_cluster): sum over v of a SplitMix64 chain over (v and Delta_v,
+    then S_v[0..planes-1]), mod 2^64.  dist uint16 [n], sub uint64 [planes][n]."""
+    dist = np.ascontiguousarray(dist, dtype=np.uint16)
+    sub = np.ascontiguousarray(sub, dtype=np.uint64)
+    return int(lib().or_digest_cluster(dist.shape[0], sub.shape[0], _p(dist, ctypes.c_uint16),
+                                       _p(sub, ctypes.c_uint64)))
 
 
 def hash_cluster(dist: np.ndarray, sub: np.ndarray) -> int:
@@ -343,19 +373,26 @@ def query(dist: np.ndarray, sub: np.ndarray, s: np.ndarray, t: np.ndarray) -> np
     return out
 
 
-def query_stream(g: CSR, sources, sizes, d: int, s, t, threads: int | None = None) -> np.ndarray:
+def query_stream(g: CSR, sources, sizes, d: int, s, t, threads: int | None = None, with_stats: bool = False):
+    """Streaming index build + query (Alg. 2 with C-BFS, then
+    P:1013-1021).  Returns the answers int32 [q]; with_stats also returns
+    (answers, stats [C][4], digest [C]) of every cluster's Alg. 1 run."""
     sources = np.ascontiguousarray(sources, dtype=np.uint32)
     sizes = np.ascontiguousarray(sizes, dtype=np.uint8)
     s = np.ascontiguousarray(s, dtype=np.uint32)
     t = np.ascontiguousarray(t, dtype=np.uint32)
     out = np.empty(len(s), np.int32)
-    rc = lib().or_query_stream(g.n, _p(g.off, ctypes.c_uint64), _p(g.cols, ctypes.c_uint32),
-                               _p(sources, ctypes.c_uint32), _p(sizes, ctypes.c_uint8), sources.shape[0], d, len(s),
-                               _p(s, ctypes.c_uint32), _p(t, ctypes.c_uint32), threads or default_threads(),
-                               _p(out, ctypes.c_int32))
+    C = sources.shape[0]
+    stats = np.zeros((C, 4), np.uint64) if with_stats else None
+    dg = np.zeros(C, np.uint64) if with_stats else None
+    rc = lib().or_query_stream_ex(g.n, _p(g.off, ctypes.c_uint64), _p(g.cols, ctypes.c_uint32),
+                                  _p(sources, ctypes.c_uint32), _p(sizes, ctypes.c_uint8), C, d, len(s),
+                                  _p(s, ctypes.c_uint32), _p(t, ctypes.c_uint32), threads or default_threads(),
+                                  _p(out, ctypes.c_int32), _p(stats, ctypes.c_uint64) if with_stats else None,
+                                  _p(dg, ctypes.c_uint64) if with_stats else None)
     if rc:
         raise ValueError("bad stream query")
-    return out
+    return (out, stats, dg) if with_stats else out
 
 
 def bidir_refine(g: CSR, s, t, tau: int) -> np.ndarray:

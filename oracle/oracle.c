@@ -165,11 +165,13 @@ int or_cluster_bfs(uint32_t n, const uint64_t* off, const uint32_t* cols, const 
  * stats [C][4].  out_hash [C] (may be NULL) = or_hash_cluster of each output.
  * ------------------------------------------------------------------- */
 uint64_t or_hash_cluster(uint32_t n, uint32_t d, const uint16_t* dist, const uint64_t* sub);
+uint64_t or_digest_cluster(uint32_t n, uint32_t planes, const uint16_t* dist, const uint64_t* sub);
 
 typedef struct {
   uint32_t n; const uint64_t* off; const uint32_t* cols; const uint32_t* sources; const uint8_t* sizes;
   uint32_t C, d; uint16_t* out_dist; uint64_t* out_sub; uint64_t* stats; uint64_t* hash;
   int* status; uint32_t next_c; pthread_mutex_t* mu;
+  uint64_t* digest; uint32_t* round_F; uint64_t* round_E; uint32_t max_rounds;
 } many_job;
 
 static void* many_worker(void* p) {
@@ -183,25 +185,30 @@ static void* many_worker(void* p) {
     if (c >= J->C) break;
     uint64_t st[4];
     int rc = or_cluster_bfs(J->n, J->off, J->cols, J->sources + (size_t)c * 64, J->sizes[c], J->d, dist, sub, st,
-                            NULL, NULL, 0);
+                            J->round_F ? J->round_F + (size_t)c * J->max_rounds : NULL,
+                            J->round_E ? J->round_E + (size_t)c * J->max_rounds : NULL,
+                            J->round_F ? J->max_rounds : 0);
     J->status[c] = rc;
     if (rc) continue;
     if (J->stats) memcpy(J->stats + 4 * (size_t)c, st, sizeof st);
     if (J->out_dist) memcpy(J->out_dist + (size_t)c * J->n, dist, sizeof(uint16_t) * J->n);
     if (J->out_sub) memcpy(J->out_sub + (size_t)c * (J->d + 1) * J->n, sub, sizeof(uint64_t) * (size_t)(J->d + 1) * J->n);
     if (J->hash) J->hash[c] = or_hash_cluster(J->n, J->d, dist, sub);
+    if (J->digest) J->digest[c] = or_digest_cluster(J->n, J->d + 1, dist, sub);
   }
   free(dist); free(sub);
   return NULL;
 }
 
-int or_cluster_bfs_many(uint32_t n, const uint64_t* off, const uint32_t* cols, const uint32_t* sources,
-                        const uint8_t* sizes, uint32_t C, uint32_t d, int threads, uint16_t* out_dist,
-                        uint64_t* out_sub, uint64_t* stats, uint64_t* hash) {
+int or_cluster_bfs_many_ex(uint32_t n, const uint64_t* off, const uint32_t* cols, const uint32_t* sources,
+                           const uint8_t* sizes, uint32_t C, uint32_t d, int threads, uint16_t* out_dist,
+                           uint64_t* out_sub, uint64_t* stats, uint64_t* hash, uint64_t* digest, uint32_t* round_F,
+                           uint64_t* round_E, uint32_t max_rounds) {
   if (threads < 1) threads = 1;
   int* status = (int*)calloc(C ? C : 1, sizeof(int));
   pthread_mutex_t mu = PTHREAD_MUTEX_INITIALIZER;
-  many_job J = {n, off, cols, sources, sizes, C, d, out_dist, out_sub, stats, hash, status, 0, &mu};
+  many_job J = {n, off, cols, sources, sizes, C, d, out_dist, out_sub, stats, hash, status, 0, &mu,
+                digest, round_F, round_E, max_rounds};
   pthread_t* th = (pthread_t*)calloc((size_t)threads, sizeof(pthread_t));
   for (int t = 0; t < threads; ++t) pthread_create(&th[t], NULL, many_worker, &J);
   for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
@@ -209,6 +216,38 @@ int or_cluster_bfs_many(uint32_t n, const uint64_t* off, const uint32_t* cols, c
   for (uint32_t c = 0; c < C; ++c) if (status[c]) rc = -1;
   free(th); free(status);
   return rc;
+}
+
+int or_cluster_bfs_many(uint32_t n, const uint64_t* off, const uint32_t* cols, const uint32_t* sources,
+                        const uint8_t* sizes, uint32_t C, uint32_t d, int threads, uint16_t* out_dist,
+                        uint64_t* out_sub, uint64_t* stats, uint64_t* hash) {
+  return or_cluster_bfs_many_ex(n, off, cols, sources, sizes, C, d, threads, out_dist, out_sub, stats, hash, NULL,
+                                NULL, NULL, 0);
+}
+
+/* Order-independent 64-bit digest of one cluster's output vector, used to
+ * compare whole outputs at full size (not part of the method).  Written out:
+ *   fin(z)  = the SplitMix64 finaliser (z ^= z>>30; z *= 0xBF58476D1CE4E5B9;
+ *             z ^= z>>27; z *= 0x94D049BB133111EB; z ^= z>>31);
+ *   x       = fin((v * 0x9E3779B97F4A7C15 + 0xD1B54A32D192ED03) ^ (Delta_v << 48))
+ *             (Delta_v as u16, 0xFFFF unreached; arithmetic mod 2^64);
+ *   x       = fin(x ^ S_v[i]) for i = 0 .. planes-1 in order;
+ *   digest  = sum over v = 0 .. n-1 of x, mod 2^64.
+ * The product computes the same definition independently (include/cbfs.h,
+ * cbfs_digest_store); a sum is used so that it can be formed in any order. */
+static uint64_t dg_fin(uint64_t z) {
+  z ^= z >> 30; z *= 0xBF58476D1CE4E5B9ULL;
+  z ^= z >> 27; z *= 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+uint64_t or_digest_cluster(uint32_t n, uint32_t planes, const uint16_t* dist, const uint64_t* sub) {
+  uint64_t sum = 0;
+  for (uint32_t v = 0; v < n; ++v) {
+    uint64_t x = dg_fin(((uint64_t)v * 0x9E3779B97F4A7C15ULL + 0xD1B54A32D192ED03ULL) ^ ((uint64_t)dist[v] << 48));
+    for (uint32_t i = 0; i < planes; ++i) x = dg_fin(x ^ sub[(size_t)i * n + v]);
+    sum += x;
+  }
+  return sum;
 }
 
 /* Order-dependent 64-bit digest of one cluster's output (dist[v], then the
@@ -375,6 +414,7 @@ typedef struct {
   uint32_t n; const uint64_t* off; const uint32_t* cols; const uint32_t* sources; const uint8_t* sizes;
   uint32_t C, d; uint64_t q; const uint32_t* s; const uint32_t* t; int32_t* best;
   uint32_t* next_c; pthread_mutex_t* mu; int status;
+  uint64_t* stats; uint64_t* digest;
 } stream_job;
 
 static void* stream_worker(void* p) {
@@ -387,8 +427,11 @@ static void* stream_worker(void* p) {
     uint32_t c = (*J->next_c)++;
     pthread_mutex_unlock(J->mu);
     if (c >= J->C) break;
-    if (or_cluster_bfs(J->n, J->off, J->cols, J->sources + (size_t)c * 64, J->sizes[c], J->d, dist, sub, NULL, NULL,
+    uint64_t st[4];
+    if (or_cluster_bfs(J->n, J->off, J->cols, J->sources + (size_t)c * 64, J->sizes[c], J->d, dist, sub, st, NULL,
                        NULL, 0)) { J->status = -1; continue; }
+    if (J->stats) memcpy(J->stats + 4 * (size_t)c, st, sizeof st);
+    if (J->digest) J->digest[c] = or_digest_cluster(J->n, J->d + 1, dist, sub);
     for (uint64_t j = 0; j < J->q; ++j) {
       int32_t x = query_one_cluster(J->n, J->d, dist, sub, J->s[j], J->t[j]);
       if (x < J->best[j]) J->best[j] = x;
@@ -398,9 +441,9 @@ static void* stream_worker(void* p) {
   return NULL;
 }
 
-int or_query_stream(uint32_t n, const uint64_t* off, const uint32_t* cols, const uint32_t* sources,
-                    const uint8_t* sizes, uint32_t C, uint32_t d, uint64_t q, const uint32_t* s, const uint32_t* t,
-                    int threads, int32_t* out) {
+int or_query_stream_ex(uint32_t n, const uint64_t* off, const uint32_t* cols, const uint32_t* sources,
+                       const uint8_t* sizes, uint32_t C, uint32_t d, uint64_t q, const uint32_t* s, const uint32_t* t,
+                       int threads, int32_t* out, uint64_t* stats, uint64_t* digest) {
   for (uint64_t j = 0; j < q; ++j) if (s[j] >= n || t[j] >= n) return -1;
   if (threads < 1) threads = 1;
   pthread_mutex_t mu = PTHREAD_MUTEX_INITIALIZER;
@@ -408,7 +451,7 @@ int or_query_stream(uint32_t n, const uint64_t* off, const uint32_t* cols, const
   stream_job* jobs = (stream_job*)calloc((size_t)threads, sizeof(stream_job));
   pthread_t* th = (pthread_t*)calloc((size_t)threads, sizeof(pthread_t));
   for (int i = 0; i < threads; ++i) {
-    jobs[i] = (stream_job){n, off, cols, sources, sizes, C, d, q, s, t, NULL, &next_c, &mu, 0};
+    jobs[i] = (stream_job){n, off, cols, sources, sizes, C, d, q, s, t, NULL, &next_c, &mu, 0, stats, digest};
     jobs[i].best = (int32_t*)malloc(sizeof(int32_t) * (q ? q : 1));
     pthread_create(&th[i], NULL, stream_worker, &jobs[i]);
   }
@@ -422,6 +465,12 @@ int or_query_stream(uint32_t n, const uint64_t* off, const uint32_t* cols, const
   }
   free(jobs); free(th);
   return rc;
+}
+
+int or_query_stream(uint32_t n, const uint64_t* off, const uint32_t* cols, const uint32_t* sources,
+                    const uint8_t* sizes, uint32_t C, uint32_t d, uint64_t q, const uint32_t* s, const uint32_t* t,
+                    int threads, int32_t* out) {
+  return or_query_stream_ex(n, off, cols, sources, sizes, C, d, q, s, t, threads, out, NULL, NULL);
 }
 
 /* ---------------------------------------------------------------------

@@ -56,6 +56,9 @@ _sig("cbfs_select_and_run", [_vp, _u32, _u32, _u32, _u32, _u64, _vp, _vp, ctypes
                               _u32, _vp, _u32, _vp])
 _sig("cbfs_select_and_run_shard", [_vp, _u32, _u32, _u32, _u32, _u64, _u32, _u32, _vp, _vp, ctypes.POINTER(_u32), _u32,
                                     _vp, _vp, _u32, _vp, _u32, _vp])
+_sig("cbfs_run_digest", [_vp, _vp, _vp, _u32, _u32, _u32, _u32, _vp, _vp, _u32, _vp])
+_sig("cbfs_run_rounds", [_vp, _vp, _vp, _u32, _u32, _vp, _u32, _vp, _u32, _vp])
+_sig("cbfs_digest_store", [_u32, _u32, _u32, _vp, _u32, _vp, _vp, _vp])
 _sig("cbfs_run_host", [_vp, _vp, _vp, _u32, _u32, _u32, _vp, _vp, _u32, _vp, _u32, _vp])
 _sig("cbfs_run_wide", [_vp, _vp, _vp, _u32, _u32, _u32, _u32, _vp, _vp, _u32, _vp, _u32, _vp])
 _sig("cbfs_decode_wide", [_u32, _u32, _u32, _u32, _u32, _vp, _u32, _vp, _u32, _u32, _vp, _vp])
@@ -199,6 +202,27 @@ def cbfs_select_and_run_shard(h, r, k, d, root_policy, seed, world, rank, out_so
     return got.value
 
 
+def cbfs_run_digest(h, sources, sizes, n_clusters, d, dist_bytes, planes, out_digest, out_stats=None,
+                    direction=CBFS_DIR_AUTO, stream=None):
+    """Full output vectors of every cluster written batch by batch to HBM staging and reduced to one 64-bit
+    digest per cluster (out_digest [C] int64/uint64 device)."""
+    _check(_lib.cbfs_run_digest(h, _ptr(sources), _ptr(sizes), n_clusters, d, dist_bytes, planes, _ptr(out_digest),
+                                _ptr(out_stats), direction, _stream(stream)))
+
+
+def cbfs_run_rounds(h, sources, sizes, n_clusters, d, out_rounds, max_rounds, out_stats=None,
+                    direction=CBFS_DIR_AUTO, stream=None):
+    """Per-round frontier statistics: out_rounds [C][max_rounds][2] {|F_i|, E_i} (device)."""
+    _check(_lib.cbfs_run_rounds(h, _ptr(sources), _ptr(sizes), n_clusters, d, _ptr(out_rounds), max_rounds,
+                                _ptr(out_stats), direction, _stream(stream)))
+
+
+def cbfs_digest_store(n, C, planes, dist, dist_bytes, masks, out_digest, stream=None):
+    """Digest of every column of a vertex-major store dist [n][C], masks [planes][n][C] (cbfs_run's layout)."""
+    _check(_lib.cbfs_digest_store(n, C, planes, _ptr(dist), dist_bytes, _ptr(masks), _ptr(out_digest),
+                                  _stream(stream)))
+
+
 def cbfs_run_host(h, sources, sizes, n_clusters, d, dist_bytes, out_dist, out_masks, planes, out_stats=None,
                   direction=CBFS_DIR_AUTO, stream=None):
     _check(_lib.cbfs_run_host(h, _ptr(sources), _ptr(sizes), n_clusters, d, dist_bytes, _ptr(out_dist),
@@ -326,12 +350,12 @@ def cbfs_profile_enable(on: bool = True):
 
 
 def cbfs_profile_read(reset: bool = False) -> dict:
-    ms = np.zeros(4, np.float64)
-    la, arcs, ent, ui, uo = (np.zeros(4, np.uint64) for _ in range(5))
+    ms = np.zeros(5, np.float64)
+    la, arcs, ent, ui, uo = (np.zeros(5, np.uint64) for _ in range(5))
     _check(_lib.cbfs_profile_read(_ptr(ms), _ptr(la), _ptr(arcs), _ptr(ent), _ptr(ui), _ptr(uo), int(reset)))
     return {name: dict(ms=float(ms[i]), launches=int(la[i]), arcs=int(arcs[i]), entries=int(ent[i]),
                        u_in=int(ui[i]), u_out=int(uo[i]))
-            for i, name in enumerate(("fold", "push", "pull", "sparse"))}
+            for i, name in enumerate(("fold", "push", "pull", "sparse", "consume"))}
 
 
 def cbfs_graph_nonisolated(h) -> int:

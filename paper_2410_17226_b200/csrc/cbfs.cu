@@ -39,17 +39,22 @@ static int g_max_slots = 4;
 // the launching stream around each fold / push / pull launch; read after the
 // round's counters arrive, so no extra sync is added.  With concurrent
 // batches a launch's time includes the time it shares the GPU.
-enum { PK_FOLD = 0, PK_PUSH = 1, PK_PULL = 2, PK_SPARSE = 3, PK_N = 4 };
 struct Prof {
   bool on = false;
-  double ms[PK_N] = {0, 0, 0, 0};
-  uint64_t launches[PK_N] = {0, 0, 0, 0};
-  uint64_t arcs[PK_N] = {0, 0, 0, 0};     // frontier (cluster, arc) pairs processed
-  uint64_t entries[PK_N] = {0, 0, 0, 0};  // frontier entries processed
-  uint64_t u_in[PK_N] = {0, 0, 0, 0};     // distinct frontier vertices |U_i|
-  uint64_t u_out[PK_N] = {0, 0, 0, 0};    // distinct claimed vertices |U_{i+1}|
+  double ms[PK_N] = {};
+  uint64_t launches[PK_N] = {};
+  uint64_t arcs[PK_N] = {};     // frontier (cluster, arc) pairs processed
+  uint64_t entries[PK_N] = {};  // frontier entries processed
+  uint64_t u_in[PK_N] = {};     // distinct frontier vertices |U_i|
+  uint64_t u_out[PK_N] = {};    // distinct claimed vertices |U_{i+1}|
 };
 static Prof g_prof;
+bool prof_on() { return g_prof.on; }
+void prof_add(int kind, double ms, uint64_t launches, uint64_t entries) {
+  g_prof.ms[kind] += ms;
+  g_prof.launches[kind] += launches;
+  g_prof.entries[kind] += entries;
+}
 
 // The slots are cached per device and reused by every graph handle
 // (allocating and mapping a few GB per cbfs_run would cost tens of ms).  A
@@ -172,13 +177,21 @@ __device__ __forceinline__ uint32_t warp_set_bit(bool flag, uint32_t v, uint32_t
 // Per-cluster statistics are counted where an entry is CLAIMED for the next
 // frontier (so the fold stays a pure streaming kernel): bstats[c] =
 // {rounds, sum_i |F_i|, sum_i E_i, sum of degrees of first visits}.
+// With `rstats` (cbfs_run_rounds) the counts also go to the per-round record
+// rstats[c][rounds - 1] = {|F_i|, E_i} of the round the claims belong to.
 __device__ __forceinline__ void stats_flush(uint64_t* __restrict__ bstats, uint32_t c, unsigned long long aF,
-                                            unsigned long long aE, unsigned long long aM, uint32_t rounds) {
+                                            unsigned long long aE, unsigned long long aM, uint32_t rounds,
+                                            uint64_t* __restrict__ rstats = nullptr, uint32_t R = 0) {
   if (!aF) return;
   atomicAdd((unsigned long long*)&bstats[c * 4 + 1], aF);
   atomicAdd((unsigned long long*)&bstats[c * 4 + 2], aE);
   if (aM) atomicAdd((unsigned long long*)&bstats[c * 4 + 3], aM);
   atomicMax((unsigned long long*)&bstats[c * 4 + 0], (unsigned long long)rounds);
+  if (rstats && rounds - 1 < R) {
+    uint64_t* r = rstats + ((uint64_t)c * R + rounds - 1) * 2;
+    atomicAdd((unsigned long long*)&r[0], aF);
+    atomicAdd((unsigned long long*)&r[1], aE);
+  }
 }
 
 // ------------------------------------------------------------------ init
@@ -186,7 +199,8 @@ __device__ __forceinline__ void stats_flush(uint64_t* __restrict__ bstats, uint3
 __global__ void k_seed(const uint32_t* __restrict__ sources, const uint8_t* __restrict__ sizes, uint32_t nb,
                        uint32_t n, const uint32_t* __restrict__ inv, const uint64_t* __restrict__ off,
                        uint64_t* __restrict__ pend, uint32_t* __restrict__ list, uint32_t* __restrict__ ubits0,
-                       uint64_t* __restrict__ bstats, unsigned long long* __restrict__ ctr, int allow_empty) {
+                       uint64_t* __restrict__ bstats, unsigned long long* __restrict__ ctr, int allow_empty,
+                       uint64_t* __restrict__ rstats, uint32_t R) {
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;  // 64 threads per cluster
   const uint32_t c = t >> 6, j = t & 63;
   bool claim = false;
@@ -213,6 +227,10 @@ __global__ void k_seed(const uint32_t* __restrict__ sources, const uint8_t* __re
           atomicAdd((unsigned long long*)&bstats[c * 4 + 2], deg);
           atomicAdd((unsigned long long*)&bstats[c * 4 + 3], deg);
           atomicMax((unsigned long long*)&bstats[c * 4 + 0], 1ULL);
+          if (rstats && R) {
+            atomicAdd((unsigned long long*)&rstats[(uint64_t)c * R * 2], 1ULL);
+            atomicAdd((unsigned long long*)&rstats[(uint64_t)c * R * 2 + 1], deg);
+          }
         }
       }
     }
@@ -364,7 +382,7 @@ __global__ void __launch_bounds__(256) k_push(const uint64_t* __restrict__ off, 
                                               const uint16_t* __restrict__ dist, uint64_t* __restrict__ pend,
                                               uint32_t* __restrict__ out_list, uint32_t* __restrict__ ubits_next,
                                               uint64_t* __restrict__ bstats, unsigned long long* __restrict__ ctr,
-                                              uint32_t i, uint32_t d) {
+                                              uint32_t i, uint32_t d, uint64_t* __restrict__ rstats, uint32_t R) {
   __shared__ unsigned long long sF[LANES], sE[LANES], sM[LANES];
   __shared__ uint32_t s_out[8][PUSH_CHUNK];  // per-warp claims of the current chunk
   for (uint32_t c = threadIdx.x; c < LANES; c += blockDim.x) sF[c] = sE[c] = sM[c] = 0;
@@ -437,7 +455,8 @@ __global__ void __launch_bounds__(256) k_push(const uint64_t* __restrict__ off, 
   if (lane == 0 && degsum) atomicAdd(&ctr[1], degsum);
   if (lane == 0 && nu) atomicAdd(&ctr[3], nu);
   __syncthreads();
-  for (uint32_t c = threadIdx.x; c < LANES; c += blockDim.x) stats_flush(bstats, c, sF[c], sE[c], sM[c], i + 2);
+  for (uint32_t c = threadIdx.x; c < LANES; c += blockDim.x)
+    stats_flush(bstats, c, sF[c], sE[c], sM[c], i + 2, rstats, R);
 }
 
 // ------------------------------------------------------------------ pull
@@ -555,7 +574,8 @@ __global__ void __launch_bounds__(PULL_WARPS * 32, CBFS_PULL_MINB) k_pull(
     uint64_t n_chunks, uint64_t m, uint32_t n, const uint64_t* __restrict__ seen, const uint16_t* __restrict__ dist,
     uint64_t* __restrict__ pend, const uint32_t* __restrict__ ubits, uint32_t* __restrict__ ubits_next,
     const uint8_t* __restrict__ sizes, uint32_t nb, uint32_t* __restrict__ out_list, uint64_t* __restrict__ bstats,
-    unsigned long long* __restrict__ ctr, const uint64_t* __restrict__ fullm, uint32_t i, uint32_t d) {
+    unsigned long long* __restrict__ ctr, const uint64_t* __restrict__ fullm, uint32_t i, uint32_t d,
+    uint64_t* __restrict__ rstats, uint32_t R) {
   __shared__ uint32_t s_list[PULL_WARPS][PULL_CHUNK + 32];
   __shared__ uint32_t s_cnt[PULL_WARPS][32];
   __shared__ unsigned long long s_stat[PULL_WARPS][3][LANES];  // per-warp F / E / M per cluster
@@ -819,8 +839,8 @@ __global__ void __launch_bounds__(PULL_WARPS * 32, CBFS_PULL_MINB) k_pull(
   nu = warp_sum(nu);
   if (lane == 0 && degsum) atomicAdd(&ctr[1], degsum);
   if (lane == 0 && nu) atomicAdd(&ctr[3], nu);
-  stats_flush(bstats, c0, stat[0][c0], stat[1][c0], stat[2][c0], i + 2);
-  stats_flush(bstats, c1, stat[0][c1], stat[1][c1], stat[2][c1], i + 2);
+  stats_flush(bstats, c0, stat[0][c0], stat[1][c0], stat[2][c0], i + 2, rstats, R);
+  stats_flush(bstats, c1, stat[0][c1], stat[1][c1], stat[2][c1], i + 2, rstats, R);
 }
 
 __global__ void k_set_u64(uint64_t* p, uint64_t v) { *p = v; }
@@ -859,7 +879,8 @@ static int slot_start(Graph* g, Slot* w, const RunArgs& a) {
   CBFS_CUDA(cudaMemsetAsync(w->fullm, 0, (uint64_t)(n + 1) * sizeof(uint64_t), st));
   CBFS_CUDA(cudaMemsetAsync(w->ctr, 0, 4 * sizeof(unsigned long long), st));
   k_seed<<<(a.nb * 64 + 255) / 256, 256, 0, st>>>(a.sources, a.sizes, a.nb, n, g->inv, g->off, w->pend, w->listA,
-                                                   w->ubits, w->bstats, w->ctr, a.wide > 1);
+                                                   w->ubits, w->bstats, w->ctr, a.wide > 1, a.out_rounds,
+                                                   a.out_rounds ? a.max_rounds : 0);
   CBFS_LAUNCHED();
   return queue_counters(w);
 }
@@ -904,7 +925,7 @@ static int slot_round(Graph* g, Slot* w) {
     const unsigned pb = grid_for(g->n_chunks * 32, PULL_WARPS * 32, 148u * CBFS_PULL_MINB);
     k_pull<<<pb, PULL_WARPS * 32, 0, st>>>(g->off, g->cols, g->chunk_v, g->n_chunks, g->m, n, w->seen, w->dist,
                                            w->pend, ub_cur, ub_nxt, a.sizes, a.nb, w->nxt, w->bstats, w->ctr, w->fullm,
-                                           i, a.d);
+                                           i, a.d, a.out_rounds, a.out_rounds ? a.max_rounds : 0);
     CBFS_LAUNCHED();
     if (g_prof.on) CBFS_CUDA(cudaEventRecord(w->pe[3], st));
   } else if (E > 0) {
@@ -917,7 +938,7 @@ static int slot_round(Graph* g, Slot* w) {
     const unsigned pb = grid_for(warps * 32, 256, 148u * 8u * 4u);
     if (g_prof.on) CBFS_CUDA(cudaEventRecord(w->pe[2], st));
     k_push<<<pb, 256, 0, st>>>(g->off, g->cols, w->cur, w->pre, (uint32_t)nF, E, w->seen, w->dist, w->pend, w->nxt,
-                               ub_nxt, w->bstats, w->ctr, i, a.d);
+                               ub_nxt, w->bstats, w->ctr, i, a.d, a.out_rounds, a.out_rounds ? a.max_rounds : 0);
     CBFS_LAUNCHED();
     if (g_prof.on) CBFS_CUDA(cudaEventRecord(w->pe[3], st));
   }
@@ -1017,13 +1038,13 @@ static int slot_step(Graph* g, Slot* w, BatchSource& src, int slot, int* err) {
 // Drive all batches of `src` through the device's slots; every slot stream
 // first waits for the caller's prior work on `st`, and `st` waits for all of
 // them at the end.
-int run_batches(Graph* g, BatchSource& src, cudaStream_t st) {
+int run_batches(Graph* g, BatchSource& src, cudaStream_t st, int max_slots) {
   DevSlots& D = *reinterpret_cast<DevSlots*>(g->work);
-  const int P = (int)D.slots.size();
+  const int P = max_slots > 0 ? std::min<int>(max_slots, (int)D.slots.size()) : (int)D.slots.size();
   cudaEvent_t start;
   CBFS_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
   CBFS_CUDA(cudaEventRecord(start, st));
-  for (Slot* w : D.slots) CBFS_CUDA(cudaStreamWaitEvent(w->s, start, 0));
+  for (int k = 0; k < P; ++k) CBFS_CUDA(cudaStreamWaitEvent(D.slots[k]->s, start, 0));
   CBFS_CUDA(cudaEventDestroy(start));
   int err = CBFS_OK;
   bool exhausted = false;
@@ -1059,8 +1080,8 @@ int run_batches(Graph* g, BatchSource& src, cudaStream_t st) {
   }
   cudaEvent_t done;
   CBFS_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
-  for (Slot* w : D.slots) {
-    CBFS_CUDA(cudaEventRecord(done, w->s));
+  for (int k = 0; k < P; ++k) {
+    CBFS_CUDA(cudaEventRecord(done, D.slots[k]->s));
     CBFS_CUDA(cudaStreamWaitEvent(st, done, 0));
   }
   CBFS_CUDA(cudaEventDestroy(done));
@@ -1084,6 +1105,8 @@ int ArraySource::next(RunArgs& a) {
   a.nb = std::min<uint32_t>(LANES, n_clusters - next_c);
   a.cbase = proto.cbase + next_c;
   a.out_stats = out_stats ? out_stats + (uint64_t)next_c * 4 : nullptr;
+  a.out_rounds = out_rounds ? out_rounds + (uint64_t)next_c * max_rounds * 2 : nullptr;
+  a.max_rounds = max_rounds;
   next_c += a.nb;
   return 1;
 }
@@ -1206,6 +1229,8 @@ struct SelectSource : ArraySource {
     a.sizes = sizes + g0;
     a.cbase = proto.cbase + next_c;
     a.out_stats = out_stats ? out_stats + (uint64_t)next_c * 4 : nullptr;
+    a.out_rounds = out_rounds ? out_rounds + (uint64_t)next_c * max_rounds * 2 : nullptr;
+    a.max_rounds = max_rounds;
     next_c += a.nb;
     return 1;
   }

@@ -92,6 +92,8 @@ struct RunArgs {
   uint32_t out_cmajor;      // outputs cluster-major (Delta at col * n + row; library-internal staging, sparse engine)
   uint32_t wide;            // W > 1: lanes are the 64-source words of clusters of W lanes (cbfs_run_wide); out_dist
                             // has C / W columns
+  uint64_t* out_rounds;     // device [nb][max_rounds][2] {|F_i|, E_i} per round, or null (added to: zeroed by the caller)
+  uint32_t max_rounds;      // rounds recorded per cluster in out_rounds
 };
 // A producer of batches for run_batches (several batches run concurrently,
 // one per workspace slot, each on its own stream).
@@ -111,9 +113,13 @@ struct ArraySource : BatchSource {
   const uint8_t* sizes = nullptr;
   uint32_t n_clusters = 0, next_c = 0;
   uint64_t* out_stats = nullptr;
+  uint64_t* out_rounds = nullptr;  // [n_clusters][max_rounds][2] or null
+  uint32_t max_rounds = 0;
   int next(RunArgs& a) override;
 };
-int run_batches(Graph* g, BatchSource& src, cudaStream_t st);
+// Drive all batches of `src` through the device's slots (at most max_slots of
+// them when > 0: callers that stage outputs per slot bound their memory).
+int run_batches(Graph* g, BatchSource& src, cudaStream_t st, int max_slots = 0);
 int num_slots(const Graph* g);  // concurrent batches of the leased workspace
 int select_launch(const Graph* g, uint32_t r, uint32_t k, uint32_t d, uint32_t root_policy, uint64_t seed,
                   uint32_t* out_sources, uint8_t* out_sizes, uint32_t* d_count, volatile uint32_t* progress,

@@ -1,0 +1,248 @@
+// digest.cu — full-size output consumers of the C-BFS engines:
+//  * cbfs_run_digest: every batch of 64 clusters writes its full output
+//    vectors <Delta_v, S_v[0..planes-1]> into a per-slot staging
+//    store in HBM (the fold's ordinary output path); when the batch's last
+//    round is queued, k_digest reads the store back on the slot's stream,
+//    reduces every cluster to its 64-bit digest and resets the store for the
+//    slot's next batch.  This is how configurations whose whole output does
+//    not fit HBM (config 3: 1.7 TB) are run with every output written and
+//    consumed inside the call, and compared with the oracle at full size;
+//  * cbfs_digest_store: the same digest over a caller's [n][C] store;
+//  * cbfs_run_rounds: per-round frontier statistics {|F_i|, E_i}.
+// The digest definition is in include/cbfs.h (cbfs_digest_store); the oracle
+// computes it independently (oracle.c or_digest_cluster).
+#include <algorithm>
+#include <vector>
+
+#include "engine.cuh"
+
+namespace cbfs {
+
+__device__ __forceinline__ uint64_t dg_fin(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ULL;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+// One 64-column strip [c0, c0 + 64) of a vertex-major store (row stride L
+// columns): a warp per row, lane l owns columns c0 + 2l and c0 + 2l + 1, so
+// every Delta / subset load of the warp is one contiguous row segment.  Each
+// lane accumulates its two clusters' sums over its rows in registers and adds
+// them to out[] once.  With `clear`, the strip is reset to the unreached state
+// (Delta = sentinel, subsets 0) after it is read (staging reuse).
+template <int DB>
+__global__ void __launch_bounds__(256) k_digest(void* __restrict__ dist, uint64_t* __restrict__ masks, uint32_t n,
+                                                uint64_t L, uint32_t c0, uint32_t nc, uint32_t planes,
+                                                uint64_t* __restrict__ out, int clear) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t cb = c0 + 64 * blockIdx.y;  // this block's strip
+  const uint32_t ca = cb + 2 * lane, cc = ca + 1;
+  const bool ha = ca < nc, hb = cc < nc;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t plane_stride = (uint64_t)n * L;
+  uint64_t sa = 0, sb = 0;
+  if (ha || hb) {
+    for (uint64_t v = warp; v < n; v += nwarps) {
+      const uint64_t row = v * L;
+      uint64_t da = 0xFFFF, db = 0xFFFF;
+      if (DB == 1) {
+        const uint8_t* p = (const uint8_t*)dist + row;
+        if (ha) { const uint8_t x = p[ca]; da = x == 0xFF ? 0xFFFFu : x; }
+        if (hb) { const uint8_t x = p[cc]; db = x == 0xFF ? 0xFFFFu : x; }
+      } else {
+        const uint16_t* p = (const uint16_t*)dist + row;
+        if (ha) da = p[ca];
+        if (hb) db = p[cc];
+      }
+      const uint64_t key = v * 0x9E3779B97F4A7C15ULL + 0xD1B54A32D192ED03ULL;
+      uint64_t xa = dg_fin(key ^ (da << 48)), xb = dg_fin(key ^ (db << 48));
+      for (uint32_t i = 0; i < planes; ++i) {
+        uint64_t* mp = masks + i * plane_stride + row;
+        const uint64_t ma = ha ? mp[ca] : 0, mb = hb ? mp[cc] : 0;
+        xa = dg_fin(xa ^ ma);
+        xb = dg_fin(xb ^ mb);
+        if (clear) {
+          if (ha && ma) mp[ca] = 0;
+          if (hb && mb) mp[cc] = 0;
+        }
+      }
+      if (clear) {
+        if (DB == 1) {
+          uint8_t* p = (uint8_t*)dist + row;
+          if (ha && da != 0xFFFF) p[ca] = 0xFF;
+          if (hb && db != 0xFFFF) p[cc] = 0xFF;
+        } else {
+          uint16_t* p = (uint16_t*)dist + row;
+          if (ha && da != 0xFFFF) p[ca] = 0xFFFF;
+          if (hb && db != 0xFFFF) p[cc] = 0xFFFF;
+        }
+      }
+      sa += xa;
+      sb += xb;
+    }
+  }
+  if (ha) atomicAdd((unsigned long long*)&out[ca], (unsigned long long)sa);
+  if (hb) atomicAdd((unsigned long long*)&out[cc], (unsigned long long)sb);
+}
+
+static int launch_digest(const void* dist, uint32_t dist_bytes, const uint64_t* masks, uint32_t n, uint64_t L,
+                         uint32_t nc, uint32_t planes, uint64_t* out, int clear, cudaStream_t st) {
+  if (nc == 0 || n == 0) return CBFS_OK;
+  const uint32_t strips = (nc + 63) / 64;
+  const unsigned bx = std::max(1u, grid_for((uint64_t)n * 32, 256, 148u * 8u) / std::max(1u, std::min(strips, 8u)));
+  const dim3 grid(bx, strips);
+  if (dist_bytes == 1)
+    k_digest<1><<<grid, 256, 0, st>>>(const_cast<void*>(dist), const_cast<uint64_t*>(masks), n, L, 0, nc, planes, out,
+                                      clear);
+  else
+    k_digest<2><<<grid, 256, 0, st>>>(const_cast<void*>(dist), const_cast<uint64_t*>(masks), n, L, 0, nc, planes, out,
+                                      clear);
+  CBFS_LAUNCHED();
+  return CBFS_OK;
+}
+
+// per-slot staging store: the batch writes its outputs there; the digest
+// reads (and resets) it on the slot's stream when the batch ends
+struct DigestSource : ArraySource {
+  uint32_t n = 0, planes = 0, dist_bytes = 0;
+  uint64_t* digest = nullptr;  // [n_clusters]
+  std::vector<void*> sd;
+  std::vector<uint64_t*> sm;
+  int bind(RunArgs& a, int slot, cudaStream_t) override {
+    a.out_dist = sd[slot];
+    a.out_masks = sm[slot];
+    a.C = LANES;
+    a.cbase = 0;
+    return CBFS_OK;
+  }
+  int finished(const RunArgs& a, int slot, cudaStream_t st) override {
+    const uint64_t c0 = (uint64_t)(a.sizes - sizes);  // first cluster of the batch
+    if (!prof_on()) return launch_digest(sd[slot], dist_bytes, sm[slot], n, LANES, a.nb, planes, digest + c0, 1, st);
+    if (!ev[0]) {
+      CBFS_CUDA(cudaEventCreate(&ev[0]));
+      CBFS_CUDA(cudaEventCreate(&ev[1]));
+    }
+    CBFS_CUDA(cudaEventRecord(ev[0], st));
+    int rc = launch_digest(sd[slot], dist_bytes, sm[slot], n, LANES, a.nb, planes, digest + c0, 1, st);
+    if (rc) return rc;
+    CBFS_CUDA(cudaEventRecord(ev[1], st));
+    CBFS_CUDA(cudaEventSynchronize(ev[1]));
+    float ms = 0;
+    CBFS_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+    prof_add(PK_CONSUME, ms, 1, (uint64_t)n * a.nb);
+    return CBFS_OK;
+  }
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  ~DigestSource() override {
+    if (ev[0]) cudaEventDestroy(ev[0]);
+    if (ev[1]) cudaEventDestroy(ev[1]);
+  }
+};
+
+}  // namespace cbfs
+
+using namespace cbfs;
+
+extern "C" {
+
+int cbfs_digest_store(uint32_t n, uint32_t C, uint32_t planes, const void* dist, uint32_t dist_bytes,
+                      const uint64_t* masks, uint64_t* out_digest, cbfs_stream stream) {
+  if (dist_bytes != 1 && dist_bytes != 2) return fail(CBFS_EINVAL, "dist_bytes must be 1 or 2");
+  if (planes > CBFS_MAX_D + 1) return fail(CBFS_EINVAL, "planes must be <= CBFS_MAX_D + 1");
+  if (C && (!out_digest || (n && (!dist || (planes && !masks))))) return fail(CBFS_EINVAL, "null store / digest");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (C == 0) return CBFS_OK;
+  CBFS_CUDA(cudaMemsetAsync(out_digest, 0, sizeof(uint64_t) * C, st));
+  int rc = launch_digest(dist, dist_bytes, masks, n, C, C, planes, out_digest, 0, st);
+  if (rc) return rc;
+  CBFS_CUDA(cudaStreamSynchronize(st));
+  return CBFS_OK;
+}
+
+// one staging store per slot used: as many slots as fit next to the stores
+static int run_consumed(Graph* g, const uint32_t* sources, const uint8_t* sizes, uint32_t n_clusters, uint32_t d,
+                        uint32_t dist_bytes, uint32_t planes, uint64_t* out_digest, uint64_t* out_stats,
+                        uint64_t* out_rounds, uint32_t max_rounds, uint32_t direction, cudaStream_t st) {
+  WorkLease lease(g);
+  if (lease.rc) return lease.rc;
+  const uint32_t n = g->n;
+  const uint64_t C = n_clusters;
+  if (out_digest && C) CBFS_CUDA(cudaMemsetAsync(out_digest, 0, sizeof(uint64_t) * C, st));
+  if (out_rounds && C) CBFS_CUDA(cudaMemsetAsync(out_rounds, 0, sizeof(uint64_t) * 2 * max_rounds * C, st));
+  DigestSource src;
+  src.proto = RunArgs{};
+  src.proto.d = d;
+  src.proto.planes = planes;
+  src.proto.dist_bytes = dist_bytes;
+  src.proto.C = n_clusters;
+  src.proto.direction = direction;
+  src.proto.engine = choose_engine(g, direction);
+  if (src.proto.engine < 0) return CBFS_ECUDA;
+  src.sources = sources;
+  src.sizes = sizes;
+  src.n_clusters = n_clusters;
+  src.out_stats = out_stats;
+  src.out_rounds = out_rounds;
+  src.max_rounds = max_rounds;
+  src.n = n;
+  src.planes = planes;
+  src.dist_bytes = dist_bytes;
+  src.digest = out_digest;
+  int P = num_slots(g);
+  if (out_digest) {
+    const uint64_t per = (uint64_t)n * LANES * (dist_bytes + 8ull * planes) + 64;
+    size_t fr = 0, tot = 0;
+    CBFS_CUDA(cudaMemGetInfo(&fr, &tot));
+    const uint64_t margin = 1ull << 30;
+    const uint64_t fit = fr > margin ? (fr - margin) / per : 0;
+    if (fit == 0) return fail(CBFS_ENOMEM, "no room for one output staging store");
+    P = (int)std::min<uint64_t>((uint64_t)P, fit);
+    src.sd.assign(P, nullptr);
+    src.sm.assign(P, nullptr);
+    for (int k = 0; k < P; ++k) {
+      CBFS_CUDA(cudaMallocAsync(&src.sd[k], (uint64_t)n * LANES * dist_bytes + 16, st));
+      CBFS_CUDA(cudaMemsetAsync(src.sd[k], 0xFF, (uint64_t)n * LANES * dist_bytes, st));
+      if (planes) {
+        CBFS_CUDA(cudaMallocAsync(&src.sm[k], sizeof(uint64_t) * planes * (uint64_t)n * LANES + 16, st));
+        CBFS_CUDA(cudaMemsetAsync(src.sm[k], 0, sizeof(uint64_t) * planes * (uint64_t)n * LANES, st));
+      }
+    }
+  }
+  int rc = run_batches(g, src, st, P);
+  for (int k = 0; k < (int)src.sd.size(); ++k) {
+    cudaFreeAsync(src.sd[k], st);
+    if (src.sm[k]) cudaFreeAsync(src.sm[k], st);
+  }
+  if (rc) return rc;
+  CBFS_CUDA(cudaStreamSynchronize(st));
+  return CBFS_OK;
+}
+
+int cbfs_run_digest(cbfs_graph* gh, const uint32_t* sources, const uint8_t* sizes, uint32_t n_clusters, uint32_t d,
+                    uint32_t dist_bytes, uint32_t planes, uint64_t* out_digest, uint64_t* out_stats,
+                    uint32_t direction, cbfs_stream stream) {
+  Graph* g = reinterpret_cast<Graph*>(gh);
+  int rc = check_run_args(g, sources, sizes, n_clusters, d, dist_bytes, planes, direction);
+  if (rc) return rc;
+  if (n_clusters && !out_digest) return fail(CBFS_EINVAL, "null out_digest");
+  CBFS_CUDA(cudaSetDevice(g->device));
+  return run_consumed(g, sources, sizes, n_clusters, d, dist_bytes, planes, out_digest, out_stats, nullptr, 0,
+                      direction, (cudaStream_t)stream);
+}
+
+int cbfs_run_rounds(cbfs_graph* gh, const uint32_t* sources, const uint8_t* sizes, uint32_t n_clusters, uint32_t d,
+                    uint64_t* out_rounds, uint32_t max_rounds, uint64_t* out_stats, uint32_t direction,
+                    cbfs_stream stream) {
+  Graph* g = reinterpret_cast<Graph*>(gh);
+  int rc = check_run_args(g, sources, sizes, n_clusters, d, 2, d + 1, direction);
+  if (rc) return rc;
+  if (n_clusters && (!out_rounds || max_rounds == 0)) return fail(CBFS_EINVAL, "null out_rounds / max_rounds == 0");
+  CBFS_CUDA(cudaSetDevice(g->device));
+  return run_consumed(g, sources, sizes, n_clusters, d, 2, d + 1, nullptr, out_stats, out_rounds, max_rounds,
+                      direction, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -16,6 +16,10 @@ namespace cbfs {
 enum : unsigned long long { ERR_BAD_SOURCE = 1, ERR_DUP_SOURCE = 2, ERR_BAD_SIZE = 4, ERR_OVERFLOW = 8,
                             ERR_ROUNDS = 16 };
 enum { ENGINE_BATCHED = 0, ENGINE_SPARSE = 1 };
+// kernel-level profiling (cbfs_profile_*): kinds of cbfs_profile_read
+enum { PK_FOLD = 0, PK_PUSH = 1, PK_PULL = 2, PK_SPARSE = 3, PK_CONSUME = 4, PK_N = 5 };
+bool prof_on();
+void prof_add(int kind, double ms, uint64_t launches, uint64_t entries);
 
 constexpr unsigned FULLW = 0xFFFFFFFFu;
 
@@ -56,6 +60,8 @@ struct SpDesc {
   uint32_t n, nb, d, planes, dist_bytes, mask_bytes;
   uint32_t wide;             // W > 1: lanes are the 64-source words of clusters of W lanes (cbfs_run_wide)
   uint32_t out_cmajor;       // outputs cluster-major (RunArgs::out_cmajor)
+  uint64_t* rounds;          // [nb][max_rounds][2] per-round {|F_i|, E_i}, or null
+  uint32_t max_rounds;
 };
 // Round state of a sparse-engine batch (device-resident).
 struct SpCtl {

@@ -138,6 +138,15 @@ __device__ __forceinline__ void sp_output(const SpDesc* __restrict__ D, const Sp
   if (D->out_masks && oi < D->planes) store_mask(D->out_masks, (uint64_t)oi * n * D->C + col, nw, D->mask_bytes);
 }
 
+// per-round record {|F_i|, E_i} of cluster lane c (cbfs_run_rounds)
+__device__ __forceinline__ void sp_round_record(const SpDesc* __restrict__ D, uint32_t c, uint32_t i,
+                                                unsigned long long f, unsigned long long e) {
+  if (!D->rounds || i >= D->max_rounds) return;
+  uint64_t* r = D->rounds + ((uint64_t)c * D->max_rounds + i) * 2;
+  atomicAdd((unsigned long long*)&r[0], f);
+  atomicAdd((unsigned long long*)&r[1], e);
+}
+
 template <int DB>
 __global__ void __launch_bounds__(SP_THREADS) k_sp_fold(const SpDesc* __restrict__ D, SpCtl* __restrict__ ctl,
                                                         SpCell* __restrict__ cells,
@@ -222,6 +231,7 @@ __global__ void __launch_bounds__(SP_THREADS) k_sp_fold(const SpDesc* __restrict
     atomicAdd((unsigned long long*)&bstats[c * 4 + 2], sE[c]);
     if (sM[c]) atomicAdd((unsigned long long*)&bstats[c * 4 + 3], sM[c]);
     atomicMax((unsigned long long*)&bstats[c * 4 + 0], (unsigned long long)(i + 1));
+    sp_round_record(D, c, i, sF[c], sE[c]);
   }
 }
 
@@ -467,6 +477,7 @@ __global__ void __launch_bounds__(SP_THREADS, CBFS_SP_MINB) k_sp_push(const SpDe
       atomicAdd((unsigned long long*)&bstats[c * 4 + 2], sE[c]);
       if (sM[c]) atomicAdd((unsigned long long*)&bstats[c * 4 + 3], sM[c]);
       atomicMax((unsigned long long*)&bstats[c * 4 + 0], (unsigned long long)(i + 1));
+      sp_round_record(D, c, i, sF[c], sE[c]);
     }
   }
   sp_round_end(ctl, hcond);
@@ -585,6 +596,8 @@ int sparse_start(const Graph* g, Slot* w, const RunArgs& a) {
   h->mask_bytes = a.mask_bytes ? a.mask_bytes : 8;
   h->wide = a.wide > 1 ? a.wide : 1;
   h->out_cmajor = a.out_cmajor;
+  h->rounds = a.out_rounds;
+  h->max_rounds = a.out_rounds ? a.max_rounds : 0;
   CBFS_CUDA(cudaMemcpyAsync(w->sp_desc, h, sizeof(SpDesc), cudaMemcpyHostToDevice, st));
   const uint64_t ncell = (uint64_t)n * LANES;
   k_sp_init<<<grid_for(ncell, 256, 148u * 16u), 256, 0, st>>>(reinterpret_cast<SpCell*>(w->blk), ncell);

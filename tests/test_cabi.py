@@ -63,6 +63,12 @@ def test_host_side_argument_errors():
     assert lib.cbfs_pll_build(None, None, None, 0, 2, 200, 1000, 256, ctypes.byref(h), None) == cb.CBFS_EINVAL
     assert lib.cbfs_pll_query(None, fake, fake, 1, fake, None) == cb.CBFS_EINVAL
     assert lib.cbfs_pll_destroy(None) == cb.CBFS_OK
+    # output consumers / per-round statistics (host-side checks)
+    assert lib.cbfs_run_digest(None, None, None, 0, 2, 2, 3, None, None, 0, None) == cb.CBFS_EINVAL
+    assert lib.cbfs_run_rounds(None, None, None, 0, 2, None, 8, None, 0, None) == cb.CBFS_EINVAL
+    assert lib.cbfs_digest_store(10, 1, 3, fake, 3, fake, fake, None) == cb.CBFS_EINVAL  # dist_bytes
+    assert lib.cbfs_digest_store(10, 1, 3, fake, 2, None, fake, None) == cb.CBFS_EINVAL  # null masks
+    assert lib.cbfs_digest_store(10, 0, 3, None, 2, None, None, None) == cb.CBFS_OK  # nothing to do
     assert cb.cbfs_version().startswith("cbfs-b200")
 
 

@@ -27,7 +27,7 @@ def _run(*args, timeout=600):
     return json.loads(lines[0])
 
 
-@pytest.mark.parametrize("mode", ["full", "stats", "query"])
+@pytest.mark.parametrize("mode", ["full", "digest", "query"])
 def test_bench_line_c1(mode):
     extra = ["--queries", "20000"] if mode == "query" else []
     j = _run("--config", "c1_er", "--mode", mode, "--steps", "3", "--warmup", "3", "--ref-sample", "4", *extra)
@@ -40,6 +40,8 @@ def test_bench_line_c1(mode):
     e = j["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert "sm_mhz" in j["clocks"]
+    if mode == "digest":
+        assert j["parity"] is None or j["parity"]["match"]
 
 
 def test_bench_reference_arm():
