@@ -61,7 +61,8 @@ enum cbfs_status {
 #define CBFS_MAX_K 64u
 #define CBFS_WIDE_MAX_W 8u  /* cbfs_run_wide: up to 8 words = 512 sources per cluster */
 #define CBFS_MAX_D 31u
-#define CBFS_MAX_N (1u << 26)          /* (vertex, cluster-in-batch) pairs pack into 32 bits */
+#define CBFS_MAX_N ((1u << 26) - 1)    /* (vertex, cluster-in-batch) pairs pack into 32 bits below the
+                                          all-ones empty-slot sentinel */
 #define CBFS_PAD 0xFFFFFFFFu           /* source-list padding                */
 #define CBFS_UNREACHED_U16 0xFFFFu     /* Delta sentinel, dist_bytes == 2    */
 #define CBFS_UNREACHED_U8 0xFFu        /* Delta sentinel, dist_bytes == 1    */
@@ -442,6 +443,21 @@ int cbfs_set_direction_alpha(double alpha);
  * direction == CBFS_DIR_PULL always uses BATCHED.  Outputs are identical.
  * Errors: EINVAL (unknown engine). */
 int cbfs_set_engine(int engine);
+/* Free the device's cached traversal workspace (the batch slots; the next
+ * traversal re-allocates them).  Errors: EINVAL (device out of range). */
+int cbfs_release_workspace(int device);
+
+/* Index budget arithmetic: bytes of one (cluster,
+ * vertex) label record — Delta (dist_bytes: 1 as the paper counts, or 2) plus
+ * d bit-subsets of word_bits bits (S_v[0..d-1], R14; d = 0 keeps S_v[0];
+ * word_bits = 0: a plain landmark, Delta alone) — and the number
+ * of clusters whose records fit t_bytes per vertex (t = 1,024, w = 64,
+ * d = 2 -> 17 B, 60 clusters).  Host outputs.
+ * Errors: EINVAL (word_bits not 0/8/16/32/64, dist_bytes, null out),
+ * EUNSUPPORTED (d > CBFS_MAX_D). */
+int cbfs_record_bytes(uint32_t word_bits, uint32_t d, uint32_t dist_bytes, uint64_t* out_bytes);
+int cbfs_budget_clusters(uint64_t t_bytes, uint32_t word_bits, uint32_t d, uint32_t dist_bytes, uint64_t* out_r);
+
 /* Kernel-level timing of the C-BFS engine (process-wide, not thread-safe):
  * when enabled, CUDA events are recorded on the launching stream around every
  * fold / push / pull launch and read after the round's synchronisation.

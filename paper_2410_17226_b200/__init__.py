@@ -24,7 +24,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 # ------------------------------------------------------------------ constants (include/cbfs.h)
 CBFS_OK, CBFS_EINVAL, CBFS_ENOMEM, CBFS_ECUDA, CBFS_EOVERFLOW, CBFS_EUNSUPPORTED = 0, -1, -2, -3, -4, -5
-CBFS_MAX_K, CBFS_MAX_D, CBFS_MAX_N = 64, 31, 1 << 26
+CBFS_MAX_K, CBFS_MAX_D, CBFS_MAX_N = 64, 31, (1 << 26) - 1
 CBFS_PAD = 0xFFFFFFFF
 CBFS_UNREACHED_U16, CBFS_UNREACHED_U8 = 0xFFFF, 0xFF
 CBFS_QUERY_UNREACHED = 0x7FFFFFFF
@@ -82,8 +82,11 @@ _sig("cbfs_labels_export", [_vp, _vp, _u64])
 _sig("cbfs_labels_import", [_vp, _vp, _u64, ctypes.POINTER(_vp)])
 _sig("cbfs_labels_query", [_vp, _vp, _vp, _u64, _vp, _vp])
 _sig("cbfs_labels_destroy", [_vp])
+_sig("cbfs_record_bytes", [_u32, _u32, _u32, ctypes.POINTER(_u64)])
+_sig("cbfs_budget_clusters", [_u64, _u32, _u32, _u32, ctypes.POINTER(_u64)])
 _sig("cbfs_set_direction_alpha", [ctypes.c_double])
 _sig("cbfs_set_concurrency", [_i32])
+_sig("cbfs_release_workspace", [_i32])
 _sig("cbfs_set_engine", [_i32])
 _sig("cbfs_profile_enable", [_i32])
 _sig("cbfs_profile_read", [_vp, _vp, _vp, _vp, _vp, _vp, _i32])
@@ -333,8 +336,24 @@ def cbfs_labels_destroy(lh):
     _check(_lib.cbfs_labels_destroy(lh))
 
 
+def cbfs_record_bytes(word_bits: int, d: int, dist_bytes: int = 1) -> int:
+    out = _u64()
+    _check(_lib.cbfs_record_bytes(word_bits, d, dist_bytes, ctypes.byref(out)))
+    return out.value
+
+
+def cbfs_budget_clusters(t_bytes: int, word_bits: int, d: int, dist_bytes: int = 1) -> int:
+    out = _u64()
+    _check(_lib.cbfs_budget_clusters(t_bytes, word_bits, d, dist_bytes, ctypes.byref(out)))
+    return out.value
+
+
 def cbfs_set_direction_alpha(alpha: float):
     _check(_lib.cbfs_set_direction_alpha(alpha))
+
+
+def cbfs_release_workspace(device: int = 0):
+    _check(_lib.cbfs_release_workspace(device))
 
 
 def cbfs_set_concurrency(batches: int):

@@ -21,22 +21,21 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from . import (CBFS_QUERY_UNREACHED, CBFS_ROOT_DEGREE, cbfs_labels_build, cbfs_labels_destroy, cbfs_labels_info,
-               cbfs_labels_query, cbfs_query_bidir, cbfs_run, cbfs_select_clusters)
+from . import (CBFS_QUERY_UNREACHED, CBFS_ROOT_DEGREE, cbfs_budget_clusters, cbfs_labels_build, cbfs_labels_destroy,
+               cbfs_labels_info, cbfs_labels_query, cbfs_query_bidir, cbfs_record_bytes, cbfs_run,
+               cbfs_select_clusters)
 
 UNREACHED16 = 0xFFFF
 
 
 def record_bytes(word_bits: int, d: int, dist_bytes: int = 1) -> int:
-    """Bytes of one (cluster, vertex) record: Delta + d bit-subsets of w bits
-    (P:1446-1447: 17 B at w = 64, d = 2; 3 B at w = 8); d = 0 keeps S_v[0];
-    w = 0 is a plain landmark (Delta alone)."""
-    return dist_bytes + (max(d, 1) * word_bits // 8 if word_bits else 0)
+    """Bytes of one (cluster, vertex) record (cbfs_record_bytes)."""
+    return cbfs_record_bytes(word_bits, d, dist_bytes)
 
 
 def clusters_for_budget(t_bytes: int, word_bits: int, d: int, dist_bytes: int = 1) -> int:
-    """Clusters whose records fit t bytes per vertex."""
-    return t_bytes // record_bytes(word_bits, d, dist_bytes)
+    """Clusters whose records fit t bytes per vertex (cbfs_budget_clusters)."""
+    return cbfs_budget_clusters(t_bytes, word_bits, d, dist_bytes)
 
 
 class LandmarkIndex:

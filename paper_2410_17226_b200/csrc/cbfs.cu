@@ -23,6 +23,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <thread>
@@ -33,6 +34,13 @@
 namespace cbfs {
 
 static double g_alpha = 100.0;
+// rows of S_seen the pull keeps in L2 with an evict_last hint (64 MiB of
+// 512-byte rows; CBFS_PULL_HUB_MB overrides, for measurements)
+static const uint32_t g_hub_rows = [] {
+  const char* e = getenv("CBFS_PULL_HUB_MB");
+  const uint64_t mb = e ? (uint64_t)atoll(e) : 64;
+  return (uint32_t)std::min<uint64_t>(0xFFFFFFFFull, (mb << 20) / (LANES * 8));
+}();
 static int g_max_slots = 4;
 
 // ---- optional per-kernel timing (cbfs_profile_*): CUDA events recorded on
@@ -81,17 +89,21 @@ void work_free(Graph* g) { g->work = nullptr; }  // the cache outlives graphs
 // One block per slot holds the per-cell state of either engine: the batched
 // engine's seen [cap + 64] | pend [cap] | pre [cap + 1] (u64) | dist [cap]
 // (u16), or the sparse engine's 32-byte cells (sparse.cu).
-static uint64_t blk_bytes(uint64_t cap) {
+// The block is sized for the engine the call uses (-1: either).
+static uint64_t blk_bytes(uint64_t cap, int engine) {
   const uint64_t batched = (cap + LANES) * 8 + cap * 8 + (cap + LANES) * 8 + cap * 2;
+  if (engine == ENGINE_BATCHED) return batched;
   return std::max<uint64_t>(batched, cap * SPARSE_CELL_BYTES);
 }
 
-static uint64_t slot_bytes(uint64_t cap) { return blk_bytes(cap) + cap * 4 * 2 + cap / 4 + cap / 8; }
+static uint64_t slot_bytes(uint64_t cap, int engine) {
+  return blk_bytes(cap, engine) + cap * 4 * 2 + cap / 4 + cap / 8;
+}
 
-static int slot_alloc(Slot* w, uint64_t cap) {
+static int slot_alloc(Slot* w, uint64_t cap, uint64_t blk) {
   w->cap = cap;
   const uint64_t ubw = 2 * ((cap / LANES >> 5) + 1);
-  CBFS_CUDA(cudaMalloc(&w->blk, blk_bytes(cap)));
+  CBFS_CUDA(cudaMalloc(&w->blk, blk));
   w->seen = reinterpret_cast<uint64_t*>(w->blk);  // [cap + LANES]: + all-zero row n
   w->pend = w->seen + cap + LANES;
   w->pre = w->pend + cap;
@@ -114,31 +126,44 @@ static int slot_alloc(Slot* w, uint64_t cap) {
   return sparse_alloc(w);
 }
 
-static int work_grow(DevSlots& D, uint32_t n) {
-  const uint64_t cap = (uint64_t)(n ? n : 1) * LANES;
-  if (D.cap >= cap && !D.slots.empty()) return CBFS_OK;
+static void work_release(DevSlots& D) {
   for (Slot* w : D.slots) slot_free(w);
   D.slots.clear();
-  D.cap = cap;
+  D.cap = 0;
+  D.blk = 0;
+}
+
+// Slots for graphs of n vertices and the given engine (-1: either).  As many
+// concurrent batches as half the free memory allows (>= 1, <= the
+// concurrency setting); a caller that stages `extra` bytes per slot next to
+// it (output consumers) bounds the count by 90% of the free memory.
+static int work_grow(DevSlots& D, uint32_t n, int engine, uint64_t extra) {
+  const uint64_t cap = (uint64_t)(n ? n : 1) * LANES;
+  const uint64_t blk = blk_bytes(cap, engine);
+  if (D.cap >= cap && D.blk >= blk && !D.slots.empty()) return CBFS_OK;
+  work_release(D);
   size_t fr = 0, tot = 0;
   CBFS_CUDA(cudaMemGetInfo(&fr, &tot));
-  // as many concurrent batches as half the free memory allows (>= 1)
-  int P = (int)std::min<uint64_t>((uint64_t)g_max_slots, std::max<uint64_t>(1, (fr / 2) / slot_bytes(cap)));
-  for (int k = 0; k < P; ++k) {
+  const uint64_t sb = slot_bytes(cap, engine);
+  uint64_t P = std::min<uint64_t>((uint64_t)g_max_slots, std::max<uint64_t>(1, (fr / 2) / sb));
+  if (extra) P = std::min<uint64_t>(P, std::max<uint64_t>(1, (uint64_t)(0.9 * fr) / (sb + extra)));
+  D.cap = cap;
+  D.blk = blk;
+  for (uint64_t k = 0; k < P; ++k) {
     Slot* w = new Slot();
     D.slots.push_back(w);
-    int rc = slot_alloc(w, cap);
+    int rc = slot_alloc(w, cap, blk);
     if (rc) return rc;
   }
   CBFS_CUDA(cudaDeviceSynchronize());
   return CBFS_OK;
 }
 
-WorkLease::WorkLease(Graph* g) : g_(g) {
+WorkLease::WorkLease(Graph* g, int engine, uint64_t extra_per_slot) : g_(g) {
   if (g->device < 0 || g->device >= MAX_DEV) { rc = fail(CBFS_EUNSUPPORTED, "device ordinal >= 64"); return; }
   g_work_mu[g->device].lock();
   locked_ = true;
-  rc = work_grow(g_dev[g->device], g->n);
+  rc = work_grow(g_dev[g->device], g->n, engine, extra_per_slot);
   if (rc == CBFS_OK) g->work = reinterpret_cast<struct Work*>(&g_dev[g->device]);
 }
 
@@ -471,16 +496,15 @@ __global__ void __launch_bounds__(256) k_push(const uint64_t* __restrict__ off, 
 // A warp owns a PULL_CHUNK-arc slice of the CSR; its vertices are handled in
 // groups of up to 32:
 //   (1) one coalesced load gives the group's 32 offsets;
-//   (2) the group's per-vertex state rows are loaded back to back; cap and
-//       first-visit bits are kept in registers;
+//   (2) the group's per-vertex state (Delta row, "subset full" word) is
+//       loaded back to back; cap and first-visit bits are kept in registers;
 //   (3) pass A streams the group's arcs 32 at a time (coalesced columns +
 //       union-frontier bits), finds each arc's vertex by a shuffle binary
 //       search and compacts the useful neighbours into a shared-memory list
 //       that is sorted by vertex, with per-vertex counts;
 //   (4) pass B walks each active vertex's segment of the list, gathering
-//       PULL_MLP neighbour rows at a time into a register accumulator
-//       (no per-arc vertex bookkeeping), with the R7 full-subset early exit,
-//       and decides the vertex's claims;
+//       PULL_MLP neighbour rows at a time into a register accumulator, with
+//       the R7 full-subset exit checked after every batch;
 //   (5) the group's claims are appended with one atomic.
 #ifndef CBFS_PULL_MLP
 #define CBFS_PULL_MLP 8
@@ -493,12 +517,15 @@ constexpr int PULL_MLP = CBFS_PULL_MLP;  // neighbour rows in flight per warp
 #define CBFS_PULL_WARPS 4
 #endif
 constexpr int PULL_WARPS = CBFS_PULL_WARPS;  // warps per block
+#ifndef CBFS_PULL_SKIP
+#define CBFS_PULL_SKIP 0
+#endif
 
 #ifdef CBFS_PULL_STATS
-__device__ unsigned long long g_dbg[8];
+__device__ unsigned long long g_dbg[32];
 extern "C" int cbfs_debug_read(unsigned long long* out) {
   cudaMemcpyFromSymbol(out, g_dbg, sizeof(g_dbg));
-  unsigned long long z[8] = {0};
+  unsigned long long z[32] = {0};
   cudaMemcpyToSymbol(g_dbg, z, sizeof(z));
   return 0;
 }
@@ -508,62 +535,35 @@ struct U2 {
   uint64_t a, b;
 };
 
-// ---- TMA (cp.async.bulk) row staging for the dense pull's gathers (build
-// with -DCBFS_PULL_TMA=1).  Measured on config 2: the step takes 75 ms with
-// 8 rows staged per bulk batch and 82 ms with 16, against 68.8 ms for the
-// default 16-byte-per-lane register gathers (8 rows in flight per warp): one
-// lane issuing 512-byte bulk copies and the mbarrier round trip add latency
-// to a loop that is latency-bound already.  Off by default; parity-tested.
-#ifndef CBFS_PULL_TMA
-#define CBFS_PULL_TMA 0
+// L2 eviction-priority hints for the pull (CBFS_PULL_HINT, default on):
+// the hub rows (lowest internal ids, gathered by most vertices) are loaded
+// with an evict_last policy, the other gathered rows and the streamed CSR
+// columns with evict_first, so the one-touch traffic does not push the hub
+// rows out of L2.
+#ifndef CBFS_PULL_HINT
+#define CBFS_PULL_HINT 1
 #endif
-// cp.async (LDGSTS) row staging for the pull's gathers (-DCBFS_PULL_ASYNC=1):
-// each lane copies its 16 bytes of PULL_AMLP rows into a per-warp shared
-// stage, two stages deep, so the next rows are in flight while the current
-// ones are ORed, without holding them in registers.  Measured on config 2
-// (parity-tested): 76.5 ms (4 rows per stage), 77.7 (6), 78.7 (8) against
-// 68.8-69.2 ms for the register gathers; off by default.
-#ifndef CBFS_PULL_ASYNC
-#define CBFS_PULL_ASYNC 0
-#endif
-#ifndef CBFS_PULL_AMLP
-#define CBFS_PULL_AMLP 4
-#endif
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(gmem)
-               : "memory");
+__device__ __forceinline__ uint64_t l2_policy_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ uint64_t l2_policy_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ ulonglong2 ld_row_hint(const ulonglong2* p, uint64_t pol) {
+  ulonglong2 r;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;" : "=l"(r.x), "=l"(r.y) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ uint32_t ld_u32_hint(const uint32_t* p, uint64_t pol) {
+  uint32_t r;
+  asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+  return r;
+}
 
-#ifndef CBFS_PULL_SKIP
-#define CBFS_PULL_SKIP 0  // 1: skip row loads of capped-out or full lanes (measured slower: 72.6 vs 68.6 ms on config 2)
-#endif
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(phase)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
 __device__ __forceinline__ U2 ld2(const uint64_t* p) {
   const ulonglong2 x = __ldg(reinterpret_cast<const ulonglong2*>(p));
   return {x.x, x.y};
@@ -575,21 +575,13 @@ __global__ void __launch_bounds__(PULL_WARPS * 32, CBFS_PULL_MINB) k_pull(
     uint64_t* __restrict__ pend, const uint32_t* __restrict__ ubits, uint32_t* __restrict__ ubits_next,
     const uint8_t* __restrict__ sizes, uint32_t nb, uint32_t* __restrict__ out_list, uint64_t* __restrict__ bstats,
     unsigned long long* __restrict__ ctr, const uint64_t* __restrict__ fullm, uint32_t i, uint32_t d,
-    uint64_t* __restrict__ rstats, uint32_t R) {
+    uint64_t* __restrict__ rstats, uint32_t R, uint32_t hub_rows) {
   __shared__ uint32_t s_list[PULL_WARPS][PULL_CHUNK + 32];
+#if CBFS_PULL_HINT
+  const uint64_t pol_last = l2_policy_last(), pol_first = l2_policy_first();
+#endif
   __shared__ uint32_t s_cnt[PULL_WARPS][32];
   __shared__ unsigned long long s_stat[PULL_WARPS][3][LANES];  // per-warp F / E / M per cluster
-#if CBFS_PULL_ASYNC
-  __shared__ __align__(16) ulonglong2 s_ast[PULL_WARPS][2][CBFS_PULL_AMLP][LANES / 2];  // two stages of rows
-#endif
-#if CBFS_PULL_TMA
-  __shared__ __align__(128) ulonglong2 s_rows[PULL_WARPS][PULL_MLP][LANES / 2];  // staged neighbour rows
-  __shared__ __align__(8) uint64_t s_bar[PULL_WARPS];
-  uint32_t tma_phase = 0;
-  if (lane_id() == 0) mbar_init(&s_bar[threadIdx.x >> 5], 1);
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  __syncwarp();
-#endif
   const uint32_t lane = lane_id();
   const uint32_t wib = threadIdx.x >> 5;
   uint32_t* list = s_list[wib];
@@ -660,7 +652,11 @@ __global__ void __launch_bounds__(PULL_WARPS * 32, CBFS_PULL_MINB) k_pull(
         for (uint64_t wb = e; wb < ge; wb += 32) {
           const uint64_t a = wb + lane;
           const bool inr = a < ge;
+#if CBFS_PULL_HINT
+          const uint32_t u = inr ? ld_u32_hint(cols + a, pol_first) : 0u;
+#else
           const uint32_t u = inr ? cols[a] : 0u;
+#endif
           uint32_t jv = 0;  // largest j < nv with ob_j <= a
 #pragma unroll
           for (int step = 16; step > 0; step >>= 1) {
@@ -676,10 +672,6 @@ __global__ void __launch_bounds__(PULL_WARPS * 32, CBFS_PULL_MINB) k_pull(
           nl += __popc(fm);
           __syncwarp();
         }
-#ifdef CBFS_PULL_STATS
-        if (lane == 0) { atomicAdd(&g_dbg[0], 1ULL); atomicAdd(&g_dbg[1], (unsigned long long)__popc(actv));
-                         atomicAdd(&g_dbg[2], (unsigned long long)nl); atomicAdd(&g_dbg[3], (unsigned long long)(ge - e)); }
-#endif
         const uint32_t myc = cnt[lane];
         uint32_t incl = myc;  // per-vertex segment ends (inclusive scan, lane = vertex)
 #pragma unroll
@@ -688,9 +680,9 @@ __global__ void __launch_bounds__(PULL_WARPS * 32, CBFS_PULL_MINB) k_pull(
           if (lane >= (uint32_t)o) incl += y;
         }
         __syncwarp();
-        // ---- (4) pass B: per active vertex, gather its segment PULL_MLP rows
-        // at a time into a register accumulator, checking the R7 full-subset
-        // exit every batch, then decide the vertex's claims
+        // ---- (4) pass B: per active vertex, OR its neighbours' contributions
+        // into a register accumulator, checking the R7 full-subset exit after
+        // every batch, then decide the vertex's claims
         unsigned myb0 = 0, myb1 = 0;  // lane j: claim ballots of vertex j
         unsigned rem = actv;
         while (rem) {
@@ -702,83 +694,52 @@ __global__ void __launch_bounds__(PULL_WARPS * 32, CBFS_PULL_MINB) k_pull(
           const U2 sv = ld2(seen2 + row);
           const bool k0 = (cap0 >> j) & 1u, k1 = (cap1 >> j) & 1u;
           uint64_t acc0 = 0, acc1 = 0;
-#if CBFS_PULL_ASYNC
           {
-            constexpr uint32_t AM = CBFS_PULL_AMLP;
-            ulonglong2(*stg)[AM][LANES / 2] = s_ast[wib];
-            // every lane copies and later reads only its own 16 bytes of each
-            // row: the wait_group of the lane itself orders them
-            auto issue = [&](uint32_t qq, int sbuf) {
-              const uint32_t nr = min(AM, s1 - qq);
-              for (uint32_t r = 0; r < nr; ++r)
-                cp_async16(&stg[sbuf][r][lane], rows2 + (uint64_t)list[qq + r] * (LANES / 2));
-              cp_async_commit();
-            };
-            int sb = 0;
-            issue(s0, 0);
-            for (uint32_t q = s0; q < s1; q += AM) {
-              const uint32_t qn = q + AM;
-              if (qn < s1) issue(qn, sb ^ 1);
-              else cp_async_commit();  // an empty group keeps "all but the newest" meaning the current stage
-              cp_async_wait<1>();
-              const uint32_t nr = min(AM, s1 - q);
-              for (uint32_t r = 0; r < nr; ++r) {
-                const ulonglong2 y = stg[sb][r][lane];
-                acc0 |= y.x;
-                acc1 |= y.y;
-              }
-              sb ^= 1;
-              if (qn < s1 && !__ballot_sync(FULLW, (k0 && ((acc0 | sv.a) & full0) != full0) ||
-                                                       (k1 && ((acc1 | sv.b) & full1) != full1)))
-                break;  // R7
-            }
-            cp_async_wait<0>();  // the stage still in flight after an early exit
-          }
-          if (false)
-#endif
-          for (uint32_t q = s0; q < s1; q += PULL_MLP) {
-#if CBFS_PULL_TMA
-            // one lane stages up to PULL_MLP neighbour rows (512 B each) into
-            // shared memory with bulk copies; the warp ORs them from there
-            const uint32_t nr = min((uint32_t)PULL_MLP, s1 - q);
-            ulonglong2(*rows_s)[LANES / 2] = s_rows[wib];
-            if (lane == 0) {
-              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of the buffer
-              mbar_expect_tx(&s_bar[wib], nr * LANES * 8);
-              for (uint32_t r = 0; r < nr; ++r)
-                bulk_g2s(rows_s[r], seen + (uint64_t)list[q + r] * LANES, LANES * 8, &s_bar[wib]);
-            }
-            mbar_wait(&s_bar[wib], tma_phase);
-            tma_phase ^= 1;
-            for (uint32_t r = 0; r < nr; ++r) {
-              const ulonglong2 y = rows_s[r][lane];
-              acc0 |= y.x;
-              acc1 |= y.y;
-            }
-            __syncwarp();
+            for (uint32_t q = s0; q < s1; q += PULL_MLP) {
+              // CBFS_PULL_SKIP: a lane loads its 16 bytes of the rows only while
+              // one of its clusters is capped and not yet full (config 3: 52% of
+              // the sectors are needed in the first dense round, 1% in the
+              // second; measured slower on configs 2 and 3, off by default)
+              const bool need = CBFS_PULL_SKIP == 0 || (k0 && ((acc0 | sv.a) & full0) != full0) ||
+                                (k1 && ((acc1 | sv.b) & full1) != full1);
+              U2 g[PULL_MLP];
+#pragma unroll
+              for (int r = 0; r < PULL_MLP; ++r) {
+                const uint32_t x = q + r < s1 ? list[q + r] : n;  // past the segment: the zero row
+                ulonglong2 y = make_ulonglong2(0ULL, 0ULL);
+#if CBFS_PULL_HINT
+                if (need) y = ld_row_hint(rows2 + x * (LANES / 2), x < hub_rows ? pol_last : pol_first);
 #else
-            U2 g[PULL_MLP];
-            // a lane whose two clusters are capped out or already hold their
-            // full subset loads nothing: its 16 bytes of the row stay unread
-            const bool need = (k0 && ((acc0 | sv.a) & full0) != full0) || (k1 && ((acc1 | sv.b) & full1) != full1);
-#pragma unroll
-            for (int r = 0; r < PULL_MLP; ++r) {
-              const uint32_t x = q + r < s1 ? list[q + r] : n;  // past the segment: the zero row
-              ulonglong2 y = make_ulonglong2(0ULL, 0ULL);
-              if (CBFS_PULL_SKIP == 0 || need) y = __ldg(rows2 + x * (LANES / 2));  // 32-bit index: x * 32 < 2^31
-              g[r] = {y.x, y.y};
-            }
-#pragma unroll
-            for (int r = 0; r < PULL_MLP; ++r) { acc0 |= g[r].a; acc1 |= g[r].b; }
+                if (need) y = __ldg(rows2 + x * (LANES / 2));  // 32-bit index: x * 32 < 2^31
 #endif
-            // R7: stop once every capped lane holds its full subset
-            if (q + PULL_MLP < s1 &&
-                !__ballot_sync(FULLW, (k0 && ((acc0 | sv.a) & full0) != full0) ||
-                                          (k1 && ((acc1 | sv.b) & full1) != full1))) {
+                g[r] = {y.x, y.y};
+              }
+#pragma unroll
+              for (int r = 0; r < PULL_MLP; ++r) { acc0 |= g[r].a; acc1 |= g[r].b; }
 #ifdef CBFS_PULL_STATS
-              if (lane == 0) { atomicAdd(&g_dbg[4], 1ULL); atomicAdd(&g_dbg[5], (unsigned long long)(s1 - q - PULL_MLP)); }
+              {  // gathered rows, their non-zero 32-byte sectors, and those a capped non-full lane needs
+                const bool need = (k0 && ((acc0 | sv.a) & full0) != full0) || (k1 && ((acc1 | sv.b) & full1) != full1);
+                unsigned long long rows = 0, nzs = 0, nds = 0;
+                for (int r = 0; r < PULL_MLP; ++r) {
+                  if (q + r >= s1) break;
+                  const unsigned nzl = __ballot_sync(FULLW, (g[r].a | g[r].b) != 0);
+                  const unsigned ndl = __ballot_sync(FULLW, (g[r].a | g[r].b) != 0 && need);
+                  rows += 1;
+                  nzs += __popc((nzl | (nzl >> 1)) & 0x55555555u);
+                  nds += __popc((ndl | (ndl >> 1)) & 0x55555555u);
+                }
+                if (lane == 0 && i < 8) {
+                  atomicAdd(&g_dbg[i * 4 + 0], rows);
+                  atomicAdd(&g_dbg[i * 4 + 1], nzs);
+                  atomicAdd(&g_dbg[i * 4 + 2], nds);
+                }
+              }
 #endif
-              break;
+              // R7: stop once every capped lane holds its full subset
+              if (q + PULL_MLP < s1 &&
+                  !__ballot_sync(FULLW, (k0 && ((acc0 | sv.a) & full0) != full0) ||
+                                            (k1 && ((acc1 | sv.b) & full1) != full1)))
+                break;
             }
           }
           const uint64_t nw0 = k0 ? (acc0 & ~sv.a) : 0, nw1 = k1 ? (acc1 & ~sv.b) : 0;
@@ -925,7 +886,8 @@ static int slot_round(Graph* g, Slot* w) {
     const unsigned pb = grid_for(g->n_chunks * 32, PULL_WARPS * 32, 148u * CBFS_PULL_MINB);
     k_pull<<<pb, PULL_WARPS * 32, 0, st>>>(g->off, g->cols, g->chunk_v, g->n_chunks, g->m, n, w->seen, w->dist,
                                            w->pend, ub_cur, ub_nxt, a.sizes, a.nb, w->nxt, w->bstats, w->ctr, w->fullm,
-                                           i, a.d, a.out_rounds, a.out_rounds ? a.max_rounds : 0);
+                                           i, a.d, a.out_rounds, a.out_rounds ? a.max_rounds : 0,
+                                           std::min<uint32_t>(n, g_hub_rows));
     CBFS_LAUNCHED();
     if (g_prof.on) CBFS_CUDA(cudaEventRecord(w->pe[3], st));
   } else if (E > 0) {
@@ -1155,7 +1117,9 @@ int run_arrays(Graph* g, const uint32_t* sources, const uint8_t* sizes, uint32_t
   if (mask_bytes != 1 && mask_bytes != 2 && mask_bytes != 4 && mask_bytes != 8)
     return fail(CBFS_EINVAL, "mask word must be 1, 2, 4 or 8 bytes");
   CBFS_CUDA(cudaSetDevice(g->device));
-  WorkLease lease(g);
+  const int engine = choose_engine(g, direction);
+  if (engine < 0) return CBFS_ECUDA;
+  WorkLease lease(g, engine);
   if (lease.rc) return lease.rc;
   const uint64_t C = n_clusters;
   if (out_dist) CBFS_CUDA(cudaMemsetAsync(out_dist, 0xFF, (uint64_t)g->n * C * dist_bytes, st));
@@ -1167,8 +1131,7 @@ int run_arrays(Graph* g, const uint32_t* sources, const uint8_t* sizes, uint32_t
   src.proto.dist_bytes = dist_bytes;
   src.proto.C = n_clusters;
   src.proto.direction = direction;
-  src.proto.engine = choose_engine(g, direction);
-  if (src.proto.engine < 0) return CBFS_ECUDA;
+  src.proto.engine = engine;
   src.proto.out_dist = out_dist;
   src.proto.out_masks = out_masks;
   src.proto.mask_bytes = mask_bytes;
@@ -1261,7 +1224,9 @@ int cbfs_select_and_run_shard(cbfs_graph* gh, uint32_t r, uint32_t k, uint32_t d
   if (r == 0 || g->n == 0) return CBFS_OK;
   CBFS_CUDA(cudaSetDevice(g->device));
   cudaStream_t st = (cudaStream_t)stream;
-  WorkLease lease(g);
+  const int engine = choose_engine(g, direction);
+  if (engine < 0) return CBFS_ECUDA;
+  WorkLease lease(g, engine);
   if (lease.rc) return lease.rc;
   static cudaStream_t side[MAX_DEV];
   static volatile uint32_t* prog_h[MAX_DEV];
@@ -1298,8 +1263,7 @@ int cbfs_select_and_run_shard(cbfs_graph* gh, uint32_t r, uint32_t k, uint32_t d
   src.proto.dist_bytes = dist_bytes;
   src.proto.C = (uint32_t)C;
   src.proto.direction = direction;
-  src.proto.engine = choose_engine(g, direction);
-  if (src.proto.engine < 0) return CBFS_ECUDA;
+  src.proto.engine = engine;
   src.proto.out_dist = out_dist;
   src.proto.out_masks = out_masks;
   src.sources = out_sources;
@@ -1406,15 +1370,23 @@ int cbfs_profile_enable(int on) {
   return CBFS_OK;
 }
 
+int cbfs_release_workspace(int device) {
+  if (device < 0 || device >= MAX_DEV) return fail(CBFS_EINVAL, "bad device");
+  std::lock_guard<std::mutex> lk(g_work_mu[device]);
+  if (g_dev[device].slots.empty()) return CBFS_OK;
+  CBFS_CUDA(cudaSetDevice(device));
+  CBFS_CUDA(cudaDeviceSynchronize());
+  work_release(g_dev[device]);
+  return CBFS_OK;
+}
+
 int cbfs_set_concurrency(int batches) {
   if (batches < 1 || batches > 16) return fail(CBFS_EINVAL, "concurrency must be 1..16");
   for (int dv = 0; dv < MAX_DEV; ++dv) {  // re-size the slot sets lazily
     std::lock_guard<std::mutex> lk(g_work_mu[dv]);
     if ((int)g_dev[dv].slots.size() != batches && !g_dev[dv].slots.empty()) {
       cudaSetDevice(dv);
-      for (Slot* w : g_dev[dv].slots) slot_free(w);
-      g_dev[dv].slots.clear();
-      g_dev[dv].cap = 0;
+      work_release(g_dev[dv]);
     }
   }
   g_max_slots = batches;

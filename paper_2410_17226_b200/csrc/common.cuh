@@ -69,7 +69,9 @@ int graph_free(Graph* g);
 
 // RAII lease of the device's cached traversal workspace (sets g->work)
 struct WorkLease {
-  explicit WorkLease(Graph* g);
+  // engine: ENGINE_* the call runs (-1: either; sizes the state block);
+  // extra_per_slot: bytes the caller will allocate per slot (staging)
+  explicit WorkLease(Graph* g, int engine = -1, uint64_t extra_per_slot = 0);
   ~WorkLease();
   int rc = CBFS_OK;
  private:

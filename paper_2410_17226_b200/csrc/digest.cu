@@ -112,6 +112,7 @@ struct DigestSource : ArraySource {
   std::vector<void*> sd;
   std::vector<uint64_t*> sm;
   int bind(RunArgs& a, int slot, cudaStream_t) override {
+    if (sd.empty()) return CBFS_OK;  // statistics only (cbfs_run_rounds)
     a.out_dist = sd[slot];
     a.out_masks = sm[slot];
     a.C = LANES;
@@ -119,6 +120,7 @@ struct DigestSource : ArraySource {
     return CBFS_OK;
   }
   int finished(const RunArgs& a, int slot, cudaStream_t st) override {
+    if (sd.empty()) return CBFS_OK;
     const uint64_t c0 = (uint64_t)(a.sizes - sizes);  // first cluster of the batch
     if (!prof_on()) return launch_digest(sd[slot], dist_bytes, sm[slot], n, LANES, a.nb, planes, digest + c0, 1, st);
     if (!ev[0]) {
@@ -166,7 +168,10 @@ int cbfs_digest_store(uint32_t n, uint32_t C, uint32_t planes, const void* dist,
 static int run_consumed(Graph* g, const uint32_t* sources, const uint8_t* sizes, uint32_t n_clusters, uint32_t d,
                         uint32_t dist_bytes, uint32_t planes, uint64_t* out_digest, uint64_t* out_stats,
                         uint64_t* out_rounds, uint32_t max_rounds, uint32_t direction, cudaStream_t st) {
-  WorkLease lease(g);
+  const int engine = choose_engine(g, direction);
+  if (engine < 0) return CBFS_ECUDA;
+  const uint64_t stage = out_digest ? (uint64_t)g->n * LANES * (dist_bytes + 8ull * planes) + 64 : 0;
+  WorkLease lease(g, engine, stage);
   if (lease.rc) return lease.rc;
   const uint32_t n = g->n;
   const uint64_t C = n_clusters;
@@ -179,8 +184,7 @@ static int run_consumed(Graph* g, const uint32_t* sources, const uint8_t* sizes,
   src.proto.dist_bytes = dist_bytes;
   src.proto.C = n_clusters;
   src.proto.direction = direction;
-  src.proto.engine = choose_engine(g, direction);
-  if (src.proto.engine < 0) return CBFS_ECUDA;
+  src.proto.engine = engine;
   src.sources = sources;
   src.sizes = sizes;
   src.n_clusters = n_clusters;
@@ -193,7 +197,7 @@ static int run_consumed(Graph* g, const uint32_t* sources, const uint8_t* sizes,
   src.digest = out_digest;
   int P = num_slots(g);
   if (out_digest) {
-    const uint64_t per = (uint64_t)n * LANES * (dist_bytes + 8ull * planes) + 64;
+    const uint64_t per = stage;
     size_t fr = 0, tot = 0;
     CBFS_CUDA(cudaMemGetInfo(&fr, &tot));
     const uint64_t margin = 1ull << 30;

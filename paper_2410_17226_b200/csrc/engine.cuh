@@ -123,7 +123,8 @@ struct Slot {
 
 struct DevSlots {
   std::vector<Slot*> slots;
-  uint64_t cap = 0;
+  uint64_t cap = 0;  // cells per slot (n * LANES)
+  uint64_t blk = 0;  // bytes of each slot's state block (engine-dependent)
 };
 
 // sparse.cu

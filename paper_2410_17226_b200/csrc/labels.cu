@@ -202,4 +202,26 @@ int cbfs_labels_destroy(cbfs_labels* lh) {
   return CBFS_OK;
 }
 
+// Index budget: a (cluster, vertex) record is
+// Delta (dist_bytes) plus d bit-subsets of w bits (S_v[0..d-1], R14; d = 0
+// keeps S_v[0]); w = 0 is a plain landmark, Delta alone.
+int cbfs_record_bytes(uint32_t word_bits, uint32_t d, uint32_t dist_bytes, uint64_t* out_bytes) {
+  if (!out_bytes) return fail(CBFS_EINVAL, "null out_bytes");
+  if (word_bits != 0 && word_bits != 8 && word_bits != 16 && word_bits != 32 && word_bits != 64)
+    return fail(CBFS_EINVAL, "word_bits must be 0, 8, 16, 32 or 64");
+  if (dist_bytes != 1 && dist_bytes != 2) return fail(CBFS_EINVAL, "dist_bytes must be 1 or 2");
+  if (d > CBFS_MAX_D) return fail(CBFS_EUNSUPPORTED, "d > CBFS_MAX_D");
+  *out_bytes = dist_bytes + (word_bits ? (uint64_t)(d > 0 ? d : 1) * (word_bits / 8) : 0);
+  return CBFS_OK;
+}
+
+int cbfs_budget_clusters(uint64_t t_bytes, uint32_t word_bits, uint32_t d, uint32_t dist_bytes, uint64_t* out_r) {
+  if (!out_r) return fail(CBFS_EINVAL, "null out_r");
+  uint64_t rb = 0;
+  int rc = cbfs_record_bytes(word_bits, d, dist_bytes, &rb);
+  if (rc) return rc;
+  *out_r = t_bytes / rb;
+  return CBFS_OK;
+}
+
 }  // extern "C"

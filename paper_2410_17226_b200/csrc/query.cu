@@ -569,7 +569,10 @@ int cbfs_query_stream(cbfs_graph* gh, const uint32_t* sources, const uint8_t* si
   if (q && (!s || !t || !inout_best)) return fail(CBFS_EINVAL, "null query arrays");
   CBFS_CUDA(cudaSetDevice(g->device));
   cudaStream_t st = (cudaStream_t)stream;
-  WorkLease lease(g);
+  const int engine = choose_engine(g, CBFS_DIR_AUTO);
+  if (engine < 0) return CBFS_ECUDA;
+  const uint64_t stage = (uint64_t)g->n * LANES * (2 * sizeof(uint16_t) + sizeof(uint64_t) * (d > 0 ? d : 1)) + 64;
+  WorkLease lease(g, engine, stage);
   if (lease.rc) return lease.rc;
   const uint32_t n = g->n;
   // label records keep S_v[0..d-1] only (R14): S_v[d] is rebuilt
@@ -581,8 +584,7 @@ int cbfs_query_stream(cbfs_graph* gh, const uint32_t* sources, const uint8_t* si
   src.proto.planes = planes;
   src.proto.dist_bytes = 2;
   src.proto.direction = CBFS_DIR_AUTO;
-  src.proto.engine = choose_engine(g, CBFS_DIR_AUTO);
-  if (src.proto.engine < 0) return CBFS_ECUDA;
+  src.proto.engine = engine;
   src.sources = sources;
   src.sizes = sizes;
   src.n_clusters = n_clusters;
@@ -653,7 +655,9 @@ int cbfs_run_host(cbfs_graph* gh, const uint32_t* sources, const uint8_t* sizes,
   if (rc) return rc;
   CBFS_CUDA(cudaSetDevice(g->device));
   cudaStream_t st = (cudaStream_t)stream;
-  WorkLease lease(g);
+  const int engine = choose_engine(g, direction);
+  if (engine < 0) return CBFS_ECUDA;
+  WorkLease lease(g, engine);
   if (lease.rc) return lease.rc;
   const uint32_t n = g->n;
   const uint64_t C = n_clusters;
@@ -668,8 +672,6 @@ int cbfs_run_host(cbfs_graph* gh, const uint32_t* sources, const uint8_t* sizes,
     CBFS_CUDA(cudaMemcpyAsync(dsrc, sources, sizeof(uint32_t) * 64 * C, cudaMemcpyHostToDevice, st));
     CBFS_CUDA(cudaMemcpyAsync(dsz, sizes, C, cudaMemcpyHostToDevice, st));
   }
-  const int engine = choose_engine(g, direction);
-  if (engine < 0) return CBFS_ECUDA;
   // When the whole output fits next to the workspace, traverse into a
   // device-resident [n][C] store and copy it out with one contiguous DMA per
   // array (the per-batch path below copies 64-column strips: 64..512-byte

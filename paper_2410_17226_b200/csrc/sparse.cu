@@ -31,7 +31,7 @@ namespace cbfs {
 
 int g_engine_policy = CBFS_ENGINE_AUTO;
 
-constexpr uint32_t VBITS = 26;  // list entry = c << 26 | v  (n <= CBFS_MAX_N = 2^26)
+constexpr uint32_t VBITS = 26;  // list entry = c << 26 | v  (n <= CBFS_MAX_N = 2^26 - 1: never all-ones)
 constexpr uint32_t VMASK = (1u << VBITS) - 1;
 constexpr int SP_THREADS = 256;
 constexpr int SP_WARPS = SP_THREADS / 32;
@@ -136,6 +136,18 @@ __device__ __forceinline__ void sp_output(const SpDesc* __restrict__ D, const Sp
   }
   const uint32_t oi = i - dc;
   if (D->out_masks && oi < D->planes) store_mask(D->out_masks, (uint64_t)oi * n * D->C + col, nw, D->mask_bytes);
+}
+
+// {S_seen, Delta} of a neighbour's cell in the push.  In the FUSED kernel the
+// cell may be folded by another thread of the same launch, so the read is a
+// relaxed (coherent, non-.nc) load: each 64-bit half is the value before or
+// after that fold, and either is harmless (see the FUSED note at k_sp_push).
+// Without fusion no cell is written during the push: read-only path.
+__device__ __forceinline__ ulonglong2 ld_cell(const SpCell* p, bool fused) {
+  if (!fused) return __ldg(reinterpret_cast<const ulonglong2*>(p));
+  ulonglong2 r;
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(r.x), "=l"(r.y) : "l"(p) : "memory");
+  return r;
 }
 
 // per-round record {|F_i|, E_i} of cluster lane c (cbfs_run_rounds)
@@ -444,7 +456,7 @@ __global__ void __launch_bounds__(SP_THREADS, CBFS_SP_MINB) k_sp_push(const SpDe
       }
 #pragma unroll
       for (int r = 0; r < SP_ILP; ++r)
-        if (u[r] != 0xFFFFFFFFu) sd[r] = __ldg(reinterpret_cast<const ulonglong2*>(cells + (uint64_t)cq[r] * n + u[r]));
+        if (u[r] != 0xFFFFFFFFu) sd[r] = ld_cell(cells + (uint64_t)cq[r] * n + u[r], FUSED);
 #pragma unroll
       for (int r = 0; r < SP_ILP; ++r) {
         claim[r] = false;

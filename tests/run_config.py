@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--reps", type=int, default=1)
     ap.add_argument("--profile", action="store_true")
     ap.add_argument("--conc", type=int, default=0)
+    ap.add_argument("--alpha", type=float, default=0.0)
     args = ap.parse_args()
     cfg = ci.CONFIGS[args.config]
     dev = torch.device("cuda:0")
@@ -48,6 +49,8 @@ def main():
     st = torch.cuda.current_stream()
     if args.conc:
         cb.cbfs_set_concurrency(args.conc)
+    if args.alpha:
+        cb.cbfs_set_direction_alpha(args.alpha)
     if args.profile:
         cb.cbfs_profile_enable(True)
     res = {"config": args.config, "n": n, "pairs": len(el.src), "gen_s": t_gen, "clusters": C, "d": d}

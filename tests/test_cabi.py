@@ -69,7 +69,27 @@ def test_host_side_argument_errors():
     assert lib.cbfs_digest_store(10, 1, 3, fake, 3, fake, fake, None) == cb.CBFS_EINVAL  # dist_bytes
     assert lib.cbfs_digest_store(10, 1, 3, fake, 2, None, fake, None) == cb.CBFS_EINVAL  # null masks
     assert lib.cbfs_digest_store(10, 0, 3, None, 2, None, None, None) == cb.CBFS_OK  # nothing to do
+    # n must stay below 2^26 (packed (vertex, lane) entries never equal the all-ones sentinel)
+    assert lib.cbfs_graph_create(1 << 26, fake, fake, 1, 0, 0, None, ctypes.byref(h)) == cb.CBFS_EUNSUPPORTED
+    assert cb.CBFS_MAX_N == (1 << 26) - 1
     assert cb.cbfs_version().startswith("cbfs-b200")
+
+
+def test_budget_arithmetic_in_the_library():
+    """K12 budget arithmetic through the C-ABI against the
+    paper-printed values of tests/golden/budget.txt (record bytes and cluster
+    counts at t = 1,024 B/vertex)."""
+    import paper_2410_17226_b200 as cb
+    rows = [ln.split() for ln in open(os.path.join(ROOT, "tests", "golden", "budget.txt"))
+            if ln.strip() and not ln.startswith("#")]
+    assert rows
+    for t, w, d, rb, r, *_ in rows:
+        assert cb.cbfs_record_bytes(int(w), int(d), 1) == int(rb)
+        assert cb.cbfs_budget_clusters(int(t), int(w), int(d), 1) == int(r)
+    assert cb.cbfs_record_bytes(0, 2, 1) == 1  # plain landmark: Delta alone (P:1464-1467)
+    assert cb.cbfs_record_bytes(64, 2, 2) == 18
+    with pytest.raises(cb.CbfsError):
+        cb.cbfs_record_bytes(12, 2, 1)
 
 
 def _sources(dirpath, exts):

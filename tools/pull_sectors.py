@@ -1,0 +1,42 @@
+"""Pull-round statistics of a -DCBFS_PULL_STATS build (tools/build_variant.sh
+stats "-DCBFS_PULL_STATS"; CBFS_LIB_PATH=build_var/stats/libcbfs.so): per
+round i, the S_seen rows the dense pull gathered, their non-zero 32-byte
+sectors, and the non-zero sectors of lanes that still needed bits.
+
+    python tools/pull_sectors.py CONFIG [CLUSTERS]
+"""
+import ctypes
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import cbfs_inputs as ci  # noqa: E402
+import paper_2410_17226_b200 as cb  # noqa: E402
+
+name = sys.argv[1]
+C = int(sys.argv[2]) if len(sys.argv) > 2 else 64
+cfg = ci.CONFIGS[name]
+el = ci.make_graph(name)
+src_d = torch.from_numpy(el.src.view(np.int32)).cuda()
+dst_d = torch.from_numpy(el.dst.view(np.int32)).cuda()
+g = cb.Graph(cb.cbfs_graph_create(el.n, src_d, dst_d, cb.Graph.relabel_flags(cfg.get("relabel", "none")), 0), 0)
+del src_d, dst_d
+src, sz = g.select_clusters(C, cfg["k"], cfg["d"])
+cb._lib.cbfs_debug_read.argtypes = [ctypes.c_void_p]
+buf = np.zeros(32, np.uint64)
+cb._lib.cbfs_debug_read(buf.ctypes.data)
+stats = torch.zeros((len(sz), 4), dtype=torch.int64, device="cuda")
+cb.cbfs_run(g.h, src, sz, len(sz), cfg["d"], 2, None, None, cfg["d"] + 1, stats)
+torch.cuda.synchronize()
+cb._lib.cbfs_debug_read(buf.ctypes.data)
+out = {}
+for i in range(8):
+    rows, nzs, nds = (int(x) for x in buf[4 * i:4 * i + 3])
+    if rows:
+        out[i] = {"rows": rows, "nonzero_sectors_per_row": nzs / rows, "needed_sectors_per_row": nds / rows,
+                  "sector_fraction_needed": nds / rows / 16}
+print(json.dumps({"config": name, "clusters": len(sz), "rounds": out}))
