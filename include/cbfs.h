@@ -443,6 +443,12 @@ int cbfs_set_direction_alpha(double alpha);
  * direction == CBFS_DIR_PULL always uses BATCHED.  Outputs are identical.
  * Errors: EINVAL (unknown engine). */
 int cbfs_set_engine(int engine);
+/* Dense-pull tuning (batched engine; outputs never change): the S_seen rows
+ * of the `rows` lowest internal ids (the hubs under CBFS_RELABEL_DEGREE) are
+ * gathered with an L2 evict_last hint, every other row and the CSR columns
+ * with evict_first.  Default 131,072 rows (64 MiB of 512-byte rows). */
+int cbfs_set_pull_hub_rows(uint32_t rows);
+
 /* Free the device's cached traversal workspace (the batch slots; the next
  * traversal re-allocates them).  Errors: EINVAL (device out of range). */
 int cbfs_release_workspace(int device);

@@ -36,7 +36,7 @@ namespace cbfs {
 static double g_alpha = 100.0;
 // rows of S_seen the pull keeps in L2 with an evict_last hint (64 MiB of
 // 512-byte rows; CBFS_PULL_HUB_MB overrides, for measurements)
-static const uint32_t g_hub_rows = [] {
+static uint32_t g_hub_rows = [] {
   const char* e = getenv("CBFS_PULL_HUB_MB");
   const uint64_t mb = e ? (uint64_t)atoll(e) : 64;
   return (uint32_t)std::min<uint64_t>(0xFFFFFFFFull, (mb << 20) / (LANES * 8));
@@ -326,6 +326,7 @@ __global__ void CBFS_FOLD_BOUNDS k_fold(const uint32_t* __restrict__ F, uint32_t
       fvx[q] = 0xFFFFFFFFu;
       if (e[q] == 0xFFFFFFFFu) continue;
       const uint32_t v = e[q] >> LSHIFT, c = e[q] & (LANES - 1);
+      CBFS_DCHECK(v < n && (W > 1 || (sizes[c] >= 1 && sizes[c] <= 64)));
       pend[e[q]] = 0;
       seen[e[q]] = sv[q] | nw[q];
       if ((sv[q] | nw[q]) == full_mask(sizes[c])) fvx[q] = v;
@@ -355,6 +356,7 @@ __global__ void CBFS_FOLD_BOUNDS k_fold(const uint32_t* __restrict__ F, uint32_t
         }
       }
       const uint32_t oi = i - dc;
+      CBFS_DCHECK(!out_masks || (orig < n && cbase + c < C));
       if (out_masks && oi < planes) {
         if (WIDE || mb != 8) store_mask(out_masks, (uint64_t)oi * n * C + col, nw[q], mb);
         else ((uint64_t*)out_masks)[(uint64_t)oi * n * C + col] = nw[q];
@@ -471,6 +473,7 @@ __global__ void __launch_bounds__(256) k_push(const uint64_t* __restrict__ off, 
       unsigned long long base = 0;
       if (lane == 0) base = atomicAdd(&ctr[0], (unsigned long long)nout);
       base = __shfl_sync(FULLW, base, 0);
+      CBFS_DCHECK(nout <= PUSH_CHUNK);
       for (uint32_t t = lane; t < nout; t += 32) out_list[base + t] = obuf[t];
     }
     __syncwarp();
@@ -666,6 +669,7 @@ __global__ void __launch_bounds__(PULL_WARPS * 32, CBFS_PULL_MINB) k_pull(
           }
           const bool want = inr && ((actv >> jv) & 1u) && ((__ldg(&ubits[u >> 5]) >> (u & 31)) & 1u);
           const unsigned fm = __ballot_sync(FULLW, want);
+          CBFS_DCHECK(!want || (u < n && nl + __popc(fm & lt) < PULL_CHUNK + 32));
           if (want) list[nl + __popc(fm & lt)] = u;  // segments are contiguous per vertex (arc order)
           const unsigned grp = __match_any_sync(FULLW, want ? jv : 0xFFFFFFFFu);
           if (want && lane == (uint32_t)(__ffs(grp) - 1)) cnt[jv] += __popc(grp);
@@ -785,6 +789,7 @@ __global__ void __launch_bounds__(PULL_WARPS * 32, CBFS_PULL_MINB) k_pull(
             const bool h0 = (b0 >> lane) & 1u, h1 = (b1 >> lane) & 1u;
             const uint32_t r = oj + __popc(b0 & lt) + __popc(b1 & lt);
             const uint32_t ebase = ((v + j) << LSHIFT) + 2 * lane;
+            CBFS_DCHECK(base + r + h0 + h1 <= (uint64_t)n * LANES);
             if (h0) out_list[base + r] = ebase;
             if (h1) out_list[base + r + h0] = ebase + 1;
           }
@@ -1406,6 +1411,11 @@ int cbfs_profile_read(double* ms, uint64_t* launches, uint64_t* arcs, uint64_t* 
   if (reset)
     for (int k = 0; k < PK_N; ++k)
       g_prof.ms[k] = 0, g_prof.launches[k] = g_prof.arcs[k] = g_prof.entries[k] = g_prof.u_in[k] = g_prof.u_out[k] = 0;
+  return CBFS_OK;
+}
+
+int cbfs_set_pull_hub_rows(uint32_t rows) {
+  g_hub_rows = rows;
   return CBFS_OK;
 }
 

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdio>
+
 #include <atomic>
 #include <string>
 
@@ -29,6 +31,24 @@ void count_launch(uint64_t k = 1);
     cudaError_t _e = cudaGetLastError();                          \
     if (_e != cudaSuccess) return ::cbfs::cuda_fail(_e, "kernel launch"); \
   } while (0)
+
+// Device-side bounds checks of the hot kernels (build with
+// -DCBFS_DEBUG_CHECKS: tools/build_variant.sh checks -DCBFS_DEBUG_CHECKS);
+// a failed check prints the condition and traps.  Compiled out by default.
+#ifdef CBFS_DEBUG_CHECKS
+#define CBFS_DCHECK(cond)                                                                                   \
+  do {                                                                                                      \
+    if (!(cond)) {                                                                                          \
+      printf("CBFS_DCHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__, __LINE__,          \
+             (int)blockIdx.x, (int)threadIdx.x);                                                            \
+      __trap();                                                                                             \
+    }                                                                                                       \
+  } while (0)
+#else
+#define CBFS_DCHECK(cond) \
+  do {                    \
+  } while (0)
+#endif
 
 constexpr uint16_t INF16 = 0xFFFFu;
 constexpr uint32_t LANES = 64;  // clusters per batch (vertex-major state rows of 64 words)

@@ -47,6 +47,7 @@ __global__ void __launch_bounds__(256) k_digest(void* __restrict__ dist, uint64_
   if (ha || hb) {
     for (uint64_t v = warp; v < n; v += nwarps) {
       const uint64_t row = v * L;
+      CBFS_DCHECK(!hb || cc < L);
       uint64_t da = 0xFFFF, db = 0xFFFF;
       if (DB == 1) {
         const uint8_t* p = (const uint8_t*)dist + row;

@@ -350,6 +350,7 @@ __global__ void __launch_bounds__(SP_THREADS, CBFS_SP_MINB) k_sp_push(const SpDe
       unsigned long long base = 0;
       if (lane == 0) base = atomicAdd(cnt, (unsigned long long)nout);
       base = __shfl_sync(FULLW, base, 0);
+      CBFS_DCHECK(base + nout <= (uint64_t)n * LANES);
       for (uint32_t q = lane; q < nout; q += 32) Ln[base + q] = obuf[q];
       __syncwarp();
       nout = 0;
@@ -452,6 +453,7 @@ __global__ void __launch_bounds__(SP_THREADS, CBFS_SP_MINB) k_sp_push(const SpDe
           cq[r] = sc[lo];
           nq[r] = snw[lo];
           u[r] = cols[sbeg[lo] + (a - pre[lo])];
+          CBFS_DCHECK(u[r] < n && cq[r] < LANES);
         }
       }
 #pragma unroll

@@ -185,6 +185,24 @@ def test_random_graphs_parity(seed):
         compare_many(g, ref, src, sz, d, direction=direction)
 
 
+@pytest.mark.parametrize("seed", range(4))
+def test_pull_hint_threshold_parity(seed):
+    """The pull's L2-hint threshold (cbfs_set_pull_hub_rows) changes only cache
+    policies: outputs equal the oracle's for 0, 8 and all rows as hubs."""
+    rng = np.random.default_rng(4100 + seed)
+    el = random_el(seed + 7, int(rng.integers(500, 3000)), ["er", "rmat"][seed % 2])
+    ref = orc.csr_from_edgelist(el)
+    src, sz = ball_clusters(ref, rng, 40, 2, 64)
+    g = gpu_graph(el, relabel=True)
+    cb.cbfs_set_engine(cb.CBFS_ENGINE_BATCHED)
+    try:
+        for hub in (0, 8, 1 << 30):
+            cb.cbfs_set_pull_hub_rows(hub)
+            compare_many(g, ref, src, sz, 2, direction=cb.CBFS_DIR_PULL)
+    finally:
+        cb.cbfs_set_pull_hub_rows(131072)
+
+
 @pytest.mark.parametrize("seed", range(6))
 def test_diameter_exceeds_d_parity(seed):
     """R9: clusters whose diameter exceeds d still give Alg. 1's output exactly,

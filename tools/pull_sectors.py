@@ -1,7 +1,8 @@
 """Pull-round statistics of a -DCBFS_PULL_STATS build (tools/build_variant.sh
 stats "-DCBFS_PULL_STATS"; CBFS_LIB_PATH=build_var/stats/libcbfs.so): per
-round i, the S_seen rows the dense pull gathered, their non-zero 32-byte
-sectors, and the non-zero sectors of lanes that still needed bits.
+round i, the S_seen rows the dense pull gathered and their non-zero 32-byte
+sectors, for the hub rows (the first CBFS_PULL_HUB_MB of rows, evict_last)
+and the others.
 
     python tools/pull_sectors.py CONFIG [CLUSTERS]
 """
@@ -35,8 +36,8 @@ torch.cuda.synchronize()
 cb._lib.cbfs_debug_read(buf.ctypes.data)
 out = {}
 for i in range(8):
-    rows, nzs, nds = (int(x) for x in buf[4 * i:4 * i + 3])
-    if rows:
-        out[i] = {"rows": rows, "nonzero_sectors_per_row": nzs / rows, "needed_sectors_per_row": nds / rows,
-                  "sector_fraction_needed": nds / rows / 16}
+    hr, hs, orow, osec = (int(x) for x in buf[4 * i:4 * i + 4])
+    if hr + orow:
+        out[i] = {"hub_rows": hr, "hub_nonzero_sectors_per_row": hs / max(hr, 1), "other_rows": orow,
+                  "other_nonzero_sectors_per_row": osec / max(orow, 1)}
 print(json.dumps({"config": name, "clusters": len(sz), "rounds": out}))
