@@ -12,6 +12,9 @@
 // The digest definition is in include/cbfs.h (cbfs_digest_store); the oracle
 // computes it independently (oracle.c or_digest_cluster).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "engine.cuh"
@@ -89,6 +92,38 @@ __global__ void __launch_bounds__(256) k_digest(void* __restrict__ dist, uint64_
   if (hb) atomicAdd((unsigned long long*)&out[cc], (unsigned long long)sb);
 }
 
+// The same digest over a CLUSTER-major staging store (the sparse engine's
+// outputs: its frontier is cluster-major, so its writes coalesce there):
+// Delta (u16) at [c][v], subset i at [i][64][v].  Block row y = cluster c,
+// thread per vertex, block-reduced sum added once per block.
+__global__ void __launch_bounds__(256) k_digest_cm(uint16_t* __restrict__ dist, uint64_t* __restrict__ masks,
+                                                   uint32_t n, uint32_t planes, uint64_t* __restrict__ out) {
+  __shared__ unsigned long long s_sum[8];
+  const uint32_t c = blockIdx.y;
+  uint16_t* dc = dist + (uint64_t)c * n;
+  uint64_t sum = 0;
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t dv = dc[v];
+    uint64_t x = dg_fin((v * 0x9E3779B97F4A7C15ULL + 0xD1B54A32D192ED03ULL) ^ (dv << 48));
+    for (uint32_t i = 0; i < planes; ++i) {
+      uint64_t* mp = masks + ((uint64_t)i * LANES + c) * n + v;
+      const uint64_t m = *mp;
+      x = dg_fin(x ^ m);
+      if (m) *mp = 0;
+    }
+    if (dv != 0xFFFF) dc[v] = 0xFFFF;
+    sum += x;
+  }
+  sum = warp_sum(sum);
+  if ((threadIdx.x & 31) == 0) s_sum[threadIdx.x >> 5] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += s_sum[k];
+    atomicAdd((unsigned long long*)&out[c], t);
+  }
+}
+
 static int launch_digest(const void* dist, uint32_t dist_bytes, const uint64_t* masks, uint32_t n, uint64_t L,
                          uint32_t nc, uint32_t planes, uint64_t* out, int clear, cudaStream_t st) {
   if (nc == 0 || n == 0) return CBFS_OK;
@@ -112,24 +147,34 @@ struct DigestSource : ArraySource {
   uint64_t* digest = nullptr;  // [n_clusters]
   std::vector<void*> sd;
   std::vector<uint64_t*> sm;
+  bool cmajor = false;  // sparse engine: cluster-major staging, u16 Delta (sd sized for u16)
   int bind(RunArgs& a, int slot, cudaStream_t) override {
     if (sd.empty()) return CBFS_OK;  // statistics only (cbfs_run_rounds)
     a.out_dist = sd[slot];
     a.out_masks = sm[slot];
     a.C = LANES;
     a.cbase = 0;
+    a.out_cmajor = cmajor;
+    return CBFS_OK;
+  }
+  int launch(const RunArgs& a, int slot, uint64_t* out, cudaStream_t st) {
+    if (!cmajor) return launch_digest(sd[slot], dist_bytes, sm[slot], n, LANES, a.nb, planes, out, 1, st);
+    if (n == 0 || a.nb == 0) return CBFS_OK;
+    const dim3 grid(std::max(1u, grid_for(n, 256, 148u * 8u) / std::max(1u, a.nb / 8u)), a.nb);
+    k_digest_cm<<<grid, 256, 0, st>>>(reinterpret_cast<uint16_t*>(sd[slot]), sm[slot], n, planes, out);
+    CBFS_LAUNCHED();
     return CBFS_OK;
   }
   int finished(const RunArgs& a, int slot, cudaStream_t st) override {
     if (sd.empty()) return CBFS_OK;
     const uint64_t c0 = (uint64_t)(a.sizes - sizes);  // first cluster of the batch
-    if (!prof_on()) return launch_digest(sd[slot], dist_bytes, sm[slot], n, LANES, a.nb, planes, digest + c0, 1, st);
+    if (!prof_on()) return launch(a, slot, digest + c0, st);
     if (!ev[0]) {
       CBFS_CUDA(cudaEventCreate(&ev[0]));
       CBFS_CUDA(cudaEventCreate(&ev[1]));
     }
     CBFS_CUDA(cudaEventRecord(ev[0], st));
-    int rc = launch_digest(sd[slot], dist_bytes, sm[slot], n, LANES, a.nb, planes, digest + c0, 1, st);
+    int rc = launch(a, slot, digest + c0, st);
     if (rc) return rc;
     CBFS_CUDA(cudaEventRecord(ev[1], st));
     CBFS_CUDA(cudaEventSynchronize(ev[1]));
@@ -171,7 +216,9 @@ static int run_consumed(Graph* g, const uint32_t* sources, const uint8_t* sizes,
                         uint64_t* out_rounds, uint32_t max_rounds, uint32_t direction, cudaStream_t st) {
   const int engine = choose_engine(g, direction);
   if (engine < 0) return CBFS_ECUDA;
-  const uint64_t stage = out_digest ? (uint64_t)g->n * LANES * (dist_bytes + 8ull * planes) + 64 : 0;
+  const bool cmajor = engine == ENGINE_SPARSE;
+  const uint32_t sdb = cmajor ? 2 : dist_bytes;  // cluster-major staging keeps u16 Delta
+  const uint64_t stage = out_digest ? (uint64_t)g->n * LANES * (sdb + 8ull * planes) + 64 : 0;
   WorkLease lease(g, engine, stage);
   if (lease.rc) return lease.rc;
   const uint32_t n = g->n;
@@ -196,7 +243,10 @@ static int run_consumed(Graph* g, const uint32_t* sources, const uint8_t* sizes,
   src.planes = planes;
   src.dist_bytes = dist_bytes;
   src.digest = out_digest;
+  src.cmajor = cmajor;
   int P = num_slots(g);
+  const double ta = getenv("CBFS_TRACE") ? std::chrono::duration<double, std::milli>(
+                                              std::chrono::steady_clock::now().time_since_epoch()).count() : 0;
   if (out_digest) {
     const uint64_t per = stage;
     size_t fr = 0, tot = 0;
@@ -208,15 +258,28 @@ static int run_consumed(Graph* g, const uint32_t* sources, const uint8_t* sizes,
     src.sd.assign(P, nullptr);
     src.sm.assign(P, nullptr);
     for (int k = 0; k < P; ++k) {
-      CBFS_CUDA(cudaMallocAsync(&src.sd[k], (uint64_t)n * LANES * dist_bytes + 16, st));
-      CBFS_CUDA(cudaMemsetAsync(src.sd[k], 0xFF, (uint64_t)n * LANES * dist_bytes, st));
+      CBFS_CUDA(cudaMallocAsync(&src.sd[k], (uint64_t)n * LANES * sdb + 16, st));
+      CBFS_CUDA(cudaMemsetAsync(src.sd[k], 0xFF, (uint64_t)n * LANES * sdb, st));
       if (planes) {
         CBFS_CUDA(cudaMallocAsync(&src.sm[k], sizeof(uint64_t) * planes * (uint64_t)n * LANES + 16, st));
         CBFS_CUDA(cudaMemsetAsync(src.sm[k], 0, sizeof(uint64_t) * planes * (uint64_t)n * LANES, st));
       }
     }
   }
+  static const bool trace = getenv("CBFS_TRACE") != nullptr;  // measurements: phase times with syncs
+  if (trace) {
+    cudaStreamSynchronize(st);
+    fprintf(stderr, "[cbfs trace] run_consumed: staging allocated + cleared in %.1f ms\n",
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count() - ta);
+  }
+  auto now_ms = [&]() {
+    cudaStreamSynchronize(st);
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
+  const double t0 = trace ? now_ms() : 0;
   int rc = run_batches(g, src, st, P);
+  if (trace) fprintf(stderr, "[cbfs trace] run_consumed: %d slots, staging %.1f GB each, batches %.1f ms\n", P,
+                     stage / 1e9, now_ms() - t0);
   for (int k = 0; k < (int)src.sd.size(); ++k) {
     cudaFreeAsync(src.sd[k], st);
     if (src.sm[k]) cudaFreeAsync(src.sm[k], st);

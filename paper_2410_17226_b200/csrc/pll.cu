@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(PLL_THREADS) k_pll_bfs(
       s_da[c] = cdist[(uint64_t)r * C + c];
       for (uint32_t i = 0; i <= d; ++i) s_mask[i * C + c] = cmask[((uint64_t)i * n + r) * C + c];
     }
-    const uint32_t sr = snap[r];
+    const uint32_t sr = min(snap[r], cap);  // a list that overflowed cap (reported as EOVERFLOW) holds cap entries
     for (uint32_t a = tid; a < sr; a += PLL_THREADS) {
       const uint32_t e = entries[(uint64_t)r * cap + a];
       tmp[e >> 8] = (uint8_t)(e & 255u);
@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(PLL_THREADS) k_pll_bfs(
         const uint32_t u = qa[fi];
         // ---- pruning query against the batch-start index
         bool hit = false;
-        const uint32_t su = snap[u];
+        const uint32_t su = min(snap[u], cap);
         for (uint32_t a0 = 0; a0 < su && !hit; a0 += 32) {
           bool h = false;
           if (a0 + lane < su) {
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(256) k_pll_query(const uint32_t* __restrict__ 
     }
     if (inv) { a = inv[a]; b = inv[b]; }
     int32_t best = INT32_MAX;
-    const uint32_t ca = counts[a], cbn = counts[b];
+    const uint32_t ca = min(counts[a], cap), cbn = min(counts[b], cap);
     const uint32_t* A = entries + (uint64_t)a * cap;
     const uint32_t* B = entries + (uint64_t)b * cap;
     for (uint32_t x = lane; x < ca; x += 32) {

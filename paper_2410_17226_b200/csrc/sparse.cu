@@ -120,6 +120,7 @@ __device__ __forceinline__ void sp_output(const SpDesc* __restrict__ D, const Sp
   }
   if (D->out_cmajor) {  // library staging: Delta at c * n + row, subset i at (i * C + c) * n + row
     dcol = (D->cbase + c) * (uint64_t)n + orig;
+    if (DB == 1) overflow |= first && dc == i && i > 254;  // the caller asked for u8 Delta (staging keeps u16)
     if (first && D->out_dist && dc == i) ((uint16_t*)D->out_dist)[dcol] = (uint16_t)i;
     const uint32_t oi = i - dc;
     if (D->out_masks && oi < D->planes)

@@ -106,6 +106,33 @@ def test_pll_errors():
     g.close()
 
 
+def test_pll_cap_overflow_across_batches():
+    """Lists that overflow cap in an early batch are reported (EOVERFLOW) and
+    the later batches of the same build, which read the batch-start lengths,
+    stay inside the lists (config 1's graph, 8 random-root clusters, batches
+    of 8..32 roots, cap 16 and 256); the device stays usable afterwards."""
+    el = ci.make_graph("c1_er")
+    ref = orc.csr_from_edgelist(el)
+    g = gpu_graph(el, relabel=True)
+    src, sz = orc.select_clusters(ref, 8, 64, 2, orc.ROOT_RANDOM, 1)
+    for cap in (16, 256):
+        try:
+            h = cb.cbfs_pll_build(g.h, to_dev_u32(src), to_dev_u8(sz), len(sz), 2, 8, 32, cap)
+            cb.cbfs_pll_destroy(h)
+        except cb.CbfsError as e:
+            assert e.code == cb.CBFS_EOVERFLOW, e
+    h = cb.cbfs_pll_build(g.h, to_dev_u32(src), to_dev_u8(sz), len(sz), 2, 8, 32, g.n)
+    s, t = ci.query_pairs(g.n, 2000, seed=5)
+    out = torch.empty((len(s),), dtype=torch.int32, device=DEV)
+    cb.cbfs_pll_query(h, torch.from_numpy(s.view(np.int32)).to(DEV), torch.from_numpy(t.view(np.int32)).to(DEV), out)
+    D = np.array([orc.plain_bfs(ref, int(x))[int(y)] for x, y in zip(s[:200], t[:200])], np.int64)
+    got = out.cpu().numpy()[:200].astype(np.int64)
+    D[D == orc.INF32] = orc.INT32_MAX
+    assert np.array_equal(got, D)
+    cb.cbfs_pll_destroy(h)
+    g.close()
+
+
 def test_pll_edgeless_and_tiny():
     """Degenerate inputs (R26): an edgeless graph labels every vertex with
     itself only (answers 0 on the diagonal, INT32_MAX elsewhere); a single

@@ -44,7 +44,11 @@ def main():
     cb.cbfs_set_engine(cb.CBFS_ENGINE_SPARSE)
     gsrc, gsz = gg.select_clusters(20, 64, 4, cb.CBFS_ROOT_RANDOM, 4)
     case("sparse fused d=4", lambda: gg.run(gsrc, gsz, 4))
-    case("sparse d=0", lambda: gg.run(gsrc[:, :1].contiguous(), torch.ones_like(gsz), 0))
+    one = torch.full_like(gsrc, -1)
+    one[:, 0] = gsrc[:, 0]
+    case("sparse d=0", lambda: gg.run(one, torch.ones_like(gsz), 0))
+    dig4 = torch.zeros(len(gsz), dtype=torch.int64, device=DEV)
+    case("sparse digest (cluster-major staging)", lambda: cb.cbfs_run_digest(gg.h, gsrc, gsz, len(gsz), 4, 2, 5, dig4))
     case("sparse locality graph", lambda: gl.run(*gl.select_clusters(8, 64, 2), 2))
     cb.cbfs_set_engine(cb.CBFS_ENGINE_AUTO)
     dig = torch.zeros(C, dtype=torch.int64, device=DEV)
@@ -61,12 +65,12 @@ def main():
     sd = torch.from_numpy(s.view(np.int32)).to(DEV)
     td = torch.from_numpy(t.view(np.int32)).to(DEV)
     best = torch.full((len(s),), cb.CBFS_QUERY_UNREACHED, dtype=torch.int32, device=DEV)
-    lh = cb.cbfs_labels_build(g.h, src, sz, C, 2, 1, word_bits=8)
+    lh = cb.cbfs_labels_build(g.h, src, sz, C, 2, 1, word_bits=64)
     case("labels + query", lambda: cb.cbfs_labels_query(lh, sd, td, best))
     cb.cbfs_labels_destroy(lh)
     case("streaming query", lambda: cb.cbfs_query_stream(g.h, src, sz, C, 2, sd, td, best))
     case("bidirectional search", lambda: cb.cbfs_query_bidir(g.h, sd, td, 64, best))
-    ph = cb.cbfs_pll_build(g.h, src, sz, C, 2, 8, 32, 256)
+    ph = cb.cbfs_pll_build(g.h, src, sz, C, 2, 8, 32, 2048)
     out = torch.empty((len(s),), dtype=torch.int32, device=DEV)
     case("PLL build + query", lambda: cb.cbfs_pll_query(ph, sd, td, out))
     cb.cbfs_pll_destroy(ph)
