@@ -23,8 +23,12 @@
  *    call that detects them; the call then leaves outputs unspecified.
  *  - `stream` is a cudaStream_t (NULL = the legacy default stream).  Calls
  *    are stream-ordered; every function that returns a host-visible value
- *    synchronises the stream before returning.  cbfs_run / cbfs_query_stream
- *    synchronise once per traversal round (they read the frontier size).
+ *    synchronises the stream before returning.  The traversals (cbfs_run and
+ *    the calls built on it) run each batch's whole round loop on the device
+ *    (one CUDA graph launch per batch of 64 clusters: a conditional WHILE
+ *    over the rounds, an IF/ELSE for the push / pull direction); the host
+ *    waits once per batch for the seeding's argument check and returns when
+ *    the last batch is done.
  *  - Pointers documented "device" must be device memory of the graph's
  *    device; "host" pointers are ordinary host memory.  All caller buffers
  *    are caller-owned; the library never frees them.  Handles are
@@ -164,7 +168,8 @@ int cbfs_select_clusters_wide(const cbfs_graph* g, uint32_t r, uint32_t k, uint3
  *   direction : CBFS_DIR_AUTO / PUSH / PULL (identical outputs, R8)
  * Errors: EINVAL (k == 0, duplicate or out-of-range source, bad dist_bytes /
  * planes), EUNSUPPORTED (k > 64, d > MAX_D), EOVERFLOW (dist_bytes == 1 and a
- * Delta > 254), ENOMEM, ECUDA.  Synchronises once per round. */
+ * Delta > 254), ENOMEM, ECUDA.  Synchronises at the end (and once per batch,
+ * after its seeding, for the argument check). */
 int cbfs_run(cbfs_graph* g, const uint32_t* sources, const uint8_t* sizes, uint32_t n_clusters, uint32_t d,
              uint32_t dist_bytes, void* out_dist, uint64_t* out_masks, uint32_t planes, uint64_t* out_stats,
              uint32_t direction, cbfs_stream stream);
@@ -465,8 +470,10 @@ int cbfs_record_bytes(uint32_t word_bits, uint32_t d, uint32_t dist_bytes, uint6
 int cbfs_budget_clusters(uint64_t t_bytes, uint32_t word_bits, uint32_t d, uint32_t dist_bytes, uint64_t* out_r);
 
 /* Kernel-level timing of the C-BFS engine (process-wide, not thread-safe):
- * when enabled, CUDA events are recorded on the launching stream around every
- * fold / push / pull launch and read after the round's synchronisation.
+ * when enabled, the batched engine's fold / push / pull kernels time every
+ * launch on the device (%globaltimer from the first block to start to the
+ * last to finish, inside the round-loop graph), the sparse engine's round
+ * loop and the digest consumer are timed with CUDA events on their streams.
  * cbfs_profile_read fills arrays of 5 entries indexed {0 fold, 1 push,
  * 2 pull, 3 sparse-engine round loop (one graph launch per batch; its
  * "launches" count the kernels the loop ran), 4 output consumer of

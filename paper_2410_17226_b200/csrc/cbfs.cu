@@ -34,6 +34,7 @@
 namespace cbfs {
 
 static double g_alpha = 100.0;
+constexpr uint32_t SCAN_BLOCKS = 592;    // the push's degree scan: blocks of the tile sums
 // rows of S_seen the pull keeps in L2 with an evict_last hint (64 MiB of
 // 512-byte rows; CBFS_PULL_HUB_MB overrides, for measurements)
 static uint32_t g_hub_rows = [] {
@@ -73,14 +74,18 @@ static std::mutex g_work_mu[MAX_DEV];
 
 static void slot_free(Slot* w) {
   cudaFree(w->blk); cudaFree(w->listA); cudaFree(w->listB);
-  cudaFree(w->ubits); cudaFree(w->ctr); cudaFreeHost(w->h_ctr); cudaFree(w->bstats);
+  cudaFree(w->ubits); cudaFree(w->bstats);
   cudaFree(w->scan_tmp);
   cudaFree(w->fullm);
+  cudaFree(w->bs); cudaFreeHost(w->bs_h);
+  for (int a = 0; a < 2; ++a)
+    for (int b = 0; b < 2; ++b) {
+      if (w->b_exec[a][b]) cudaGraphExecDestroy(w->b_exec[a][b]);
+      if (w->b_graph[a][b]) cudaGraphDestroy(w->b_graph[a][b]);
+    }
   sparse_free(w);
   if (w->s) cudaStreamDestroy(w->s);
   if (w->ready) cudaEventDestroy(w->ready);
-  for (int k = 0; k < 4; ++k)
-    if (w->pe[k]) cudaEventDestroy(w->pe[k]);
   delete w;
 }
 
@@ -111,18 +116,17 @@ static int slot_alloc(Slot* w, uint64_t cap, uint64_t blk) {
   CBFS_CUDA(cudaMalloc(&w->listA, cap * sizeof(uint32_t)));
   CBFS_CUDA(cudaMalloc(&w->listB, cap * sizeof(uint32_t)));
   CBFS_CUDA(cudaMalloc(&w->ubits, ubw * sizeof(uint32_t)));
-  CBFS_CUDA(cudaMalloc(&w->ctr, 4 * sizeof(unsigned long long)));
-  CBFS_CUDA(cudaMallocHost(&w->h_ctr, 4 * sizeof(unsigned long long)));
+  CBFS_CUDA(cudaMalloc(&w->bs, sizeof(BState)));
+  CBFS_CUDA(cudaMallocHost(&w->bs_h, sizeof(BState)));
+  CBFS_CUDA(cudaMemset(w->bs, 0, sizeof(BState)));
   CBFS_CUDA(cudaMalloc(&w->bstats, LANES * 4 * sizeof(uint64_t)));
   CBFS_CUDA(cudaMalloc(&w->fullm, (cap / LANES + 1) * sizeof(uint64_t)));
   CBFS_CUDA(cudaMemset(w->pend, 0, cap * sizeof(uint64_t)));  // zero-invariant from here on
   w->pend_clean_cells = cap;
   CBFS_CUDA(cudaMemset(w->ubits, 0, ubw * sizeof(uint32_t)));  // both bitmaps zero between batches
-  CBFS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, w->scan_bytes, w->pre, w->pre, cap));
-  CBFS_CUDA(cudaMalloc(&w->scan_tmp, w->scan_bytes ? w->scan_bytes : 1));
+  CBFS_CUDA(cudaMalloc(&w->scan_tmp, SCAN_BLOCKS * sizeof(uint64_t)));
   CBFS_CUDA(cudaStreamCreateWithFlags(&w->s, cudaStreamNonBlocking));
   CBFS_CUDA(cudaEventCreateWithFlags(&w->ready, cudaEventDisableTiming));
-  for (int k = 0; k < 4; ++k) CBFS_CUDA(cudaEventCreate(&w->pe[k]));
   return sparse_alloc(w);
 }
 
@@ -151,6 +155,7 @@ static int work_grow(DevSlots& D, uint32_t n, int engine, uint64_t extra) {
   D.blk = blk;
   for (uint64_t k = 0; k < P; ++k) {
     Slot* w = new Slot();
+    w->idx = (int)k;  // its constant-memory BState mirror
     D.slots.push_back(w);
     int rc = slot_alloc(w, cap, blk);
     if (rc) return rc;
@@ -219,13 +224,23 @@ __device__ __forceinline__ void stats_flush(uint64_t* __restrict__ bstats, uint3
   }
 }
 
+// The graph / batch / slot-array fields of each slot's BState are mirrored in
+// constant memory (written on the slot's stream before its batch starts): the
+// kernels read them as constant-bank operands instead of holding ~20 pointers
+// in registers; the round state (counters, round, direction, profile) lives in
+// the global BState the loop advances.
+constexpr int BS_MAX = 16;  // slots per device (cbfs_set_concurrency <= 16)
+__constant__ BState c_bs[BS_MAX];
+
 // ------------------------------------------------------------------ init
 // R1 seeding (S_next[s_j] = {s_j}; F_0 = S): pend[s_j, c] = bit j.
-__global__ void k_seed(const uint32_t* __restrict__ sources, const uint8_t* __restrict__ sizes, uint32_t nb,
-                       uint32_t n, const uint32_t* __restrict__ inv, const uint64_t* __restrict__ off,
-                       uint64_t* __restrict__ pend, uint32_t* __restrict__ list, uint32_t* __restrict__ ubits0,
-                       uint64_t* __restrict__ bstats, unsigned long long* __restrict__ ctr, int allow_empty,
-                       uint64_t* __restrict__ rstats, uint32_t R) {
+__device__ __forceinline__ void seed_body(const uint32_t* __restrict__ sources, const uint8_t* __restrict__ sizes,
+                                          uint32_t nb, uint32_t n, const uint32_t* __restrict__ inv,
+                                          const uint64_t* __restrict__ off, uint64_t* __restrict__ pend,
+                                          uint32_t* __restrict__ list, uint32_t* __restrict__ ubits0,
+                                          uint64_t* __restrict__ bstats, unsigned long long* __restrict__ ctr,
+                                          unsigned long long* __restrict__ err, int allow_empty,
+                                          uint64_t* __restrict__ rstats, uint32_t R) {
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;  // 64 threads per cluster
   const uint32_t c = t >> 6, j = t & 63;
   bool claim = false;
@@ -234,17 +249,17 @@ __global__ void k_seed(const uint32_t* __restrict__ sources, const uint8_t* __re
   if (c < nb) {
     const uint32_t k = sizes[c];
     if ((k == 0 && !allow_empty) || k > 64) {
-      if (j == 0) atomicOr(&ctr[2], ERR_BAD_SIZE);
+      if (j == 0) atomicOr(err, ERR_BAD_SIZE);
     } else if (j < k) {
       const uint32_t s = sources[(uint64_t)c * 64 + j];
       if (s >= n) {
-        atomicOr(&ctr[2], ERR_BAD_SOURCE);
+        atomicOr(err, ERR_BAD_SOURCE);
       } else {
         x = inv ? inv[s] : s;
         e = (x << LSHIFT) + c;
         unsigned long long old = atomicOr((unsigned long long*)&pend[e], 1ULL << j);
         if (old != 0) {
-          atomicOr(&ctr[2], ERR_DUP_SOURCE);  // R2
+          atomicOr(err, ERR_DUP_SOURCE);  // R2
         } else {
           claim = true;
           deg = off[x + 1] - off[x];
@@ -268,6 +283,43 @@ __global__ void k_seed(const uint32_t* __restrict__ sources, const uint8_t* __re
   if (lane_id() == 0 && nu) atomicAdd(&ctr[3], nu);
 }
 
+__global__ void k_seed(BState* __restrict__ S, int slot) {
+  const BState& P = c_bs[slot];
+  seed_body(P.sources, P.sizes, P.nb, P.n, P.inv, P.off, P.pend, P.list[0], P.ubits, P.bstats, S->cnt[0], &S->err,
+            P.allow_empty, P.rstats, P.R);
+}
+
+// ---- kernel-level profile of the device-side loop: the first block of a
+// launch to start takes the start time, the last to finish adds the launch's
+// duration (globaltimer ns) and its work counts to the slot's BState
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void prof_begin(BState* S, bool on, int kind) {
+  if (!on || threadIdx.x != 0) return;
+  if (atomicAdd(&S->p_arrive[kind], 1u) == 0) S->p_t0[kind] = gtimer();
+}
+__device__ __forceinline__ void prof_end(BState* S, bool on, int kind, unsigned long long entries,
+                                         unsigned long long arcs, unsigned long long uin, bool uout) {
+  if (!on) return;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  __threadfence();
+  if (atomicAdd(&S->p_leave[kind], 1u) != gridDim.x - 1) return;
+  __threadfence();
+  volatile BState* V = S;
+  V->p_ns[kind] += gtimer() - V->p_t0[kind];
+  V->p_launch[kind] += 1;
+  V->p_entries[kind] += entries;
+  V->p_arcs[kind] += arcs;
+  V->p_uin[kind] += uin;
+  if (uout) V->p_uout[kind] += V->cnt[(V->i + 1) & 1][3];
+  V->p_arrive[kind] = 0;
+  V->p_leave[kind] = 0;
+}
+
 // ------------------------------------------------------------------ fold
 // Vertex phase: S_new = S_next[u] \ S_seen[u] (= pend), set
 // Delta_u on first visit, S_u[i - Delta_u] = S_new, S_seen[u] |= S_new; plus
@@ -286,19 +338,18 @@ constexpr int FOLD_ILP = CBFS_FOLD_ILP;
 #ifdef CBFS_FOLD_MINB  // experiments; an explicit minimum of 1 block lets ptxas double the registers
 #define CBFS_FOLD_BOUNDS __launch_bounds__(256, CBFS_FOLD_MINB)
 #else
-#define CBFS_FOLD_BOUNDS __launch_bounds__(256)
+#define CBFS_FOLD_BOUNDS __launch_bounds__(256, 4)
 #endif
 
 template <int DB, bool WIDE>
-__global__ void CBFS_FOLD_BOUNDS k_fold(const uint32_t* __restrict__ F, uint32_t nF, uint32_t i,
-                                              uint64_t* __restrict__ seen, uint64_t* __restrict__ pend,
-                                              uint16_t* __restrict__ dist, const uint64_t* __restrict__ off,
-                                              const uint32_t* __restrict__ perm, uint32_t n, uint32_t C,
-                                              uint32_t cbase, uint32_t planes, void* __restrict__ out_dist,
-                                              void* __restrict__ out_masks, uint32_t mb, uint64_t* __restrict__ pre,
-                                              int write_pre, const uint8_t* __restrict__ sizes,
-                                              uint64_t* __restrict__ fullm, unsigned long long* __restrict__ ctr,
-                                              uint32_t W) {
+__device__ __forceinline__ void fold_body(const uint32_t* __restrict__ F, uint32_t nF, uint32_t i,
+                                          uint64_t* __restrict__ seen, uint64_t* __restrict__ pend,
+                                          uint16_t* __restrict__ dist, const uint64_t* __restrict__ off,
+                                          const uint32_t* __restrict__ perm, uint32_t n, uint32_t C, uint32_t cbase,
+                                          uint32_t planes, void* __restrict__ out_dist, void* __restrict__ out_masks,
+                                          uint32_t mb, uint64_t* __restrict__ pre, int write_pre,
+                                          const uint8_t* __restrict__ sizes, uint64_t* __restrict__ fullm,
+                                          unsigned long long* __restrict__ err, uint32_t W) {
   const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
   const uint32_t lane = lane_id();
@@ -393,7 +444,19 @@ __global__ void CBFS_FOLD_BOUNDS k_fold(const uint32_t* __restrict__ F, uint32_t
     }
 #endif
   }
-  if (overflow) atomicOr(&ctr[2], ERR_OVERFLOW);
+  if (overflow) atomicOr(err, ERR_OVERFLOW);
+}
+
+// the vertex phase of round S->i over F_i = list[i & 1]
+template <int DB, bool WIDE>
+__global__ void CBFS_FOLD_BOUNDS k_fold(BState* __restrict__ S, int slot) {
+  const BState& P = c_bs[slot];
+  prof_begin(S, P.prof_on, PK_FOLD);
+  const uint32_t i = (uint32_t)S->i, cur = i & 1;
+  const uint32_t nF = (uint32_t)S->cnt[cur][0];
+  fold_body<DB, WIDE>(P.list[cur], nF, i, P.seen, P.pend, P.dist, P.off, P.perm, P.n, P.C, P.cbase, P.planes,
+                      P.out_dist, P.out_masks, P.mb, P.pre, S->pull == 0, P.sizes, P.fullm, &S->err, P.W);
+  prof_end(S, P.prof_on, PK_FOLD, nF, 0, 0, false);
 }
 
 // ------------------------------------------------------------------ push
@@ -403,13 +466,13 @@ __global__ void CBFS_FOLD_BOUNDS k_fold(const uint32_t* __restrict__ F, uint32_t
 // consecutive arcs, so hubs and degree-4 grid vertices balance alike.
 constexpr uint32_t PUSH_CHUNK = 256;
 
-__global__ void __launch_bounds__(256) k_push(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cols,
-                                              const uint32_t* __restrict__ F, const uint64_t* __restrict__ pre,
-                                              uint32_t nF, uint64_t total, const uint64_t* __restrict__ seen,
-                                              const uint16_t* __restrict__ dist, uint64_t* __restrict__ pend,
-                                              uint32_t* __restrict__ out_list, uint32_t* __restrict__ ubits_next,
-                                              uint64_t* __restrict__ bstats, unsigned long long* __restrict__ ctr,
-                                              uint32_t i, uint32_t d, uint64_t* __restrict__ rstats, uint32_t R) {
+__device__ __forceinline__ void push_body(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cols,
+                                          const uint32_t* __restrict__ F, const uint64_t* __restrict__ pre,
+                                          uint32_t nF, uint64_t total, const uint64_t* __restrict__ seen,
+                                          const uint16_t* __restrict__ dist, uint64_t* __restrict__ pend,
+                                          uint32_t* __restrict__ out_list, uint32_t* __restrict__ ubits_next,
+                                          uint64_t* __restrict__ bstats, unsigned long long* __restrict__ ctr,
+                                          uint32_t i, uint32_t d, uint64_t* __restrict__ rstats, uint32_t R) {
   __shared__ unsigned long long sF[LANES], sE[LANES], sM[LANES];
   __shared__ uint32_t s_out[8][PUSH_CHUNK];  // per-warp claims of the current chunk
   for (uint32_t c = threadIdx.x; c < LANES; c += blockDim.x) sF[c] = sE[c] = sM[c] = 0;
@@ -485,6 +548,19 @@ __global__ void __launch_bounds__(256) k_push(const uint64_t* __restrict__ off, 
   __syncthreads();
   for (uint32_t c = threadIdx.x; c < LANES; c += blockDim.x)
     stats_flush(bstats, c, sF[c], sE[c], sM[c], i + 2, rstats, R);
+}
+
+// the sparse edge phase of round S->i (pre = the exclusive prefix of the
+// frontier's degrees, pre[nF] = E_i)
+__global__ void __launch_bounds__(256) k_push(BState* __restrict__ S, int slot) {
+  const BState& P = c_bs[slot];
+  prof_begin(S, P.prof_on, PK_PUSH);
+  const uint32_t i = (uint32_t)S->i, cur = i & 1;
+  const uint32_t nF = (uint32_t)S->cnt[cur][0];
+  const uint64_t E = S->cnt[cur][1];
+  push_body(P.off, P.cols, P.list[cur], P.pre, nF, E, P.seen, P.dist, P.pend, P.list[cur ^ 1],
+            P.ubits + (uint64_t)(cur ^ 1) * P.ub_words, P.bstats, S->cnt[cur ^ 1], i, P.d, P.rstats, P.R);
+  prof_end(S, P.prof_on, PK_PUSH, nF, E, S->cnt[cur][3], true);
 }
 
 // ------------------------------------------------------------------ pull
@@ -572,7 +648,7 @@ __device__ __forceinline__ U2 ld2(const uint64_t* p) {
   return {x.x, x.y};
 }
 
-__global__ void __launch_bounds__(PULL_WARPS * 32, CBFS_PULL_MINB) k_pull(
+__device__ __forceinline__ void pull_body(
     const uint64_t* __restrict__ off, const uint32_t* __restrict__ cols, const uint32_t* __restrict__ chunk_v,
     uint64_t n_chunks, uint64_t m, uint32_t n, const uint64_t* __restrict__ seen, const uint16_t* __restrict__ dist,
     uint64_t* __restrict__ pend, const uint32_t* __restrict__ ubits, uint32_t* __restrict__ ubits_next,
@@ -809,16 +885,185 @@ __global__ void __launch_bounds__(PULL_WARPS * 32, CBFS_PULL_MINB) k_pull(
   stats_flush(bstats, c1, stat[0][c1], stat[1][c1], stat[2][c1], i + 2, rstats, R);
 }
 
-__global__ void k_set_u64(uint64_t* p, uint64_t v) { *p = v; }
+// the dense edge phase of round S->i
+__global__ void __launch_bounds__(PULL_WARPS * 32, CBFS_PULL_MINB) k_pull(BState* __restrict__ S, int slot) {
+  const BState& P = c_bs[slot];
+  prof_begin(S, P.prof_on, PK_PULL);
+  const uint32_t i = (uint32_t)S->i, cur = i & 1;
+  const uint32_t n = P.n;
+  pull_body(P.off, P.cols, P.chunk_v, P.n_chunks, P.m, n, P.seen, P.dist, P.pend, P.ubits + (uint64_t)cur * P.ub_words,
+            P.ubits + (uint64_t)(cur ^ 1) * P.ub_words, P.sizes, P.nb, P.list[cur ^ 1], P.bstats, S->cnt[cur ^ 1],
+            P.fullm, i, P.d, P.rstats, P.R, min(n, P.hub_rows));
+  prof_end(S, P.prof_on, PK_PULL, S->cnt[cur][0], S->cnt[cur][1], S->cnt[cur][3], true);
+}
+
+// ------------------------------------------------------------------ round loop
+// The batch's round loop runs on the device as one CUDA graph per slot:
+//   WHILE (go) { k_begin; k_fold; IF (pull) { k_pull } ELSE { k_scan_*; k_push }; k_end }
+// k_begin decides the round's direction (R8: pull when the
+// frontier's (cluster, arc) pairs exceed m * nb / alpha) and clears the next
+// frontier's counters; k_end clears U_i and ends the round (Alg. 1's loop,
+// continue while F_{i+1} is non-empty).
+constexpr uint32_t SCAN_THREADS = 512;
+
+__global__ void k_begin(BState* __restrict__ S, int slot, cudaGraphConditionalHandle h_if) {
+  const BState& P = c_bs[slot];
+  const uint32_t cur = (uint32_t)(S->i & 1);
+  const uint32_t t = threadIdx.x;
+  if (t < 4) S->cnt[cur ^ 1][t] = 0;
+  if (t == 0) {
+    const unsigned long long E = S->cnt[cur][1];
+    const bool pull = P.direction == CBFS_DIR_PULL ||
+                      (P.direction == CBFS_DIR_AUTO && (double)E > P.pull_threshold);
+    S->pull = pull;
+    S->launches += pull ? 4 : 7;  // begin, fold, pull | 3 scan kernels + push, end
+    if (h_if) cudaGraphSetConditional(h_if, pull ? 1u : 0u);
+  }
+}
+
+// exclusive prefix of pre[0 .. nF) in place, pre[nF] = E_i: block sums,
+// one block scans them, blocks rescan their tiles with the offsets
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_sums(BState* __restrict__ S, int slot) {
+  typedef cub::BlockReduce<unsigned long long, SCAN_THREADS> BR;
+  __shared__ typename BR::TempStorage tmp;
+  const BState& P = c_bs[slot];
+  const uint64_t nF = S->cnt[S->i & 1][0];
+  const uint64_t tile = (nF + SCAN_BLOCKS - 1) / SCAN_BLOCKS;
+  const uint64_t b0 = blockIdx.x * tile, b1 = min(b0 + tile, nF);
+  unsigned long long x = 0;
+  for (uint64_t k = b0 + threadIdx.x; k < b1; k += SCAN_THREADS) x += P.pre[k];
+  x = BR(tmp).Sum(x);
+  if (threadIdx.x == 0) P.scan_tmp[blockIdx.x] = x;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_top(BState* __restrict__ S, int slot) {
+  typedef cub::BlockScan<unsigned long long, 1024> BS;
+  __shared__ typename BS::TempStorage tmp;
+  const BState& P = c_bs[slot];
+  unsigned long long x = threadIdx.x < SCAN_BLOCKS ? P.scan_tmp[threadIdx.x] : 0ULL;
+  BS(tmp).ExclusiveSum(x, x);
+  if (threadIdx.x < SCAN_BLOCKS) P.scan_tmp[threadIdx.x] = x;
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_apply(BState* __restrict__ S, int slot) {
+  typedef cub::BlockScan<unsigned long long, SCAN_THREADS> BS;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ unsigned long long s_run;
+  const BState& P = c_bs[slot];
+  const uint32_t cur = (uint32_t)(S->i & 1);
+  const uint64_t nF = S->cnt[cur][0];
+  const uint64_t tile = (nF + SCAN_BLOCKS - 1) / SCAN_BLOCKS;
+  const uint64_t b0 = blockIdx.x * tile, b1 = min(b0 + tile, nF);
+  if (threadIdx.x == 0) s_run = P.scan_tmp[blockIdx.x];
+  __syncthreads();
+  for (uint64_t k0 = b0; k0 < b1; k0 += SCAN_THREADS) {
+    const uint64_t k = k0 + threadIdx.x;
+    unsigned long long x = k < b1 ? P.pre[k] : 0ULL, total;
+    BS(tmp).ExclusiveSum(x, x, total);
+    const unsigned long long run = s_run;
+    if (k < b1) P.pre[k] = run + x;
+    __syncthreads();
+    if (threadIdx.x == 0) s_run = run + total;
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) P.pre[nF] = S->cnt[cur][1];
+}
+
+__global__ void k_end(BState* __restrict__ S, int slot, cudaGraphConditionalHandle h_while) {
+  const BState& P = c_bs[slot];
+  const uint32_t cur = (uint32_t)(S->i & 1);
+  uint32_t* ub = P.ubits + (uint64_t)cur * P.ub_words;  // U_i consumed
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < P.ub_words;
+       w += (uint64_t)gridDim.x * blockDim.x)
+    ub[w] = 0;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  __threadfence();
+  if (atomicAdd(&S->end_done, 1u) != gridDim.x - 1) return;
+  __threadfence();
+  volatile BState* V = S;
+  V->end_done = 0;
+  const unsigned long long i = V->i + 1;
+  V->i = i;
+  bool go = V->cnt[i & 1][0] > 0;
+  if (go && i >= 0xFFFEull) {
+    atomicOr(&S->err, (unsigned long long)ERR_ROUNDS);
+    go = false;
+  }
+  if (V->err & (ERR_ROUNDS | ERR_BAD_SOURCE | ERR_DUP_SOURCE | ERR_BAD_SIZE)) go = false;
+  V->go = go;
+  if (h_while) cudaGraphSetConditional(h_while, go ? 1u : 0u);
+}
 
 // ------------------------------------------------------------------ driver
-static int queue_counters(Slot* w) {
-  CBFS_CUDA(cudaMemcpyAsync(w->h_ctr, w->ctr, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, w->s));
-  CBFS_CUDA(cudaEventRecord(w->ready, w->s));
+constexpr unsigned FOLD_GRID = 148u * 8u;        // grid-stride kernels of the round loop (fixed grids:
+constexpr unsigned PUSH_GRID = 148u * 8u * 4u;   // the loop's kernel nodes are launched with the same
+constexpr unsigned END_GRID = 148u * 2u;         // configuration every round)
+
+static int b_add(cudaGraph_t body, cudaGraphNode_t* node, const cudaGraphNode_t* dep, void* fn, unsigned grid,
+                 unsigned block, void** args) {
+  cudaKernelNodeParams kp = {};
+  kp.func = fn;
+  kp.gridDim = dim3(grid);
+  kp.blockDim = dim3(block);
+  kp.kernelParams = args;
+  CBFS_CUDA(cudaGraphAddKernelNode(node, body, dep, dep ? 1 : 0, &kp));
   return CBFS_OK;
 }
 
-// queue init + seeding of batch `a` on the slot's stream
+static void* fold_fn(int db, bool wide) {
+  if (db == 1) return wide ? (void*)k_fold<1, true> : (void*)k_fold<1, false>;
+  return wide ? (void*)k_fold<2, true> : (void*)k_fold<2, false>;
+}
+
+// The slot's round-loop graph for (Delta width, wide):
+//   WHILE (go) { k_begin -> k_fold -> IF (pull) { k_pull } ELSE { k_scan_sums -> k_scan_top -> k_scan_apply ->
+//   k_push } -> k_end }
+static int b_build(Slot* w, int db, bool wide) {
+  cudaGraph_t g;
+  CBFS_CUDA(cudaGraphCreate(&g, 0));
+  w->b_graph[db - 1][wide] = g;
+  cudaGraphConditionalHandle hw, hi;
+  CBFS_CUDA(cudaGraphConditionalHandleCreate(&hw, g, 1, cudaGraphCondAssignDefault));
+  CBFS_CUDA(cudaGraphConditionalHandleCreate(&hi, g, 0, 0));
+  cudaGraphNodeParams wp = {};
+  wp.type = cudaGraphNodeTypeConditional;
+  wp.conditional.handle = hw;
+  wp.conditional.type = cudaGraphCondTypeWhile;
+  wp.conditional.size = 1;
+  cudaGraphNode_t wn;
+  CBFS_CUDA(cudaGraphAddNode(&wn, g, nullptr, 0, &wp));
+  cudaGraph_t body = wp.conditional.phGraph_out[0];
+  BState* S = w->bs;
+  int slot = w->idx;
+  void* a_s[] = {&S, &slot};
+  void* a_if[] = {&S, &slot, &hi};
+  void* a_wh[] = {&S, &slot, &hw};
+  cudaGraphNode_t nb, nf, nif, ne;
+  int rc = b_add(body, &nb, nullptr, (void*)k_begin, 1, 32, a_if);
+  if (!rc) rc = b_add(body, &nf, &nb, fold_fn(db, wide), FOLD_GRID, 256, a_s);
+  if (rc) return rc;
+  cudaGraphNodeParams ip = {};
+  ip.type = cudaGraphNodeTypeConditional;
+  ip.conditional.handle = hi;
+  ip.conditional.type = cudaGraphCondTypeIf;
+  ip.conditional.size = 2;  // [0] then (pull), [1] else (push)
+  CBFS_CUDA(cudaGraphAddNode(&nif, body, &nf, 1, &ip));
+  cudaGraph_t g_pull = ip.conditional.phGraph_out[0], g_push = ip.conditional.phGraph_out[1];
+  cudaGraphNode_t np, s1, s2, s3, nq;
+  rc = b_add(g_pull, &np, nullptr, (void*)k_pull, 148u * CBFS_PULL_MINB, PULL_WARPS * 32, a_s);
+  if (!rc) rc = b_add(g_push, &s1, nullptr, (void*)k_scan_sums, SCAN_BLOCKS, SCAN_THREADS, a_s);
+  if (!rc) rc = b_add(g_push, &s2, &s1, (void*)k_scan_top, 1, 1024, a_s);
+  if (!rc) rc = b_add(g_push, &s3, &s2, (void*)k_scan_apply, SCAN_BLOCKS, SCAN_THREADS, a_s);
+  if (!rc) rc = b_add(g_push, &nq, &s3, (void*)k_push, PUSH_GRID, 256, a_s);
+  if (!rc) rc = b_add(body, &ne, &nif, (void*)k_end, END_GRID, 256, a_wh);
+  if (rc) return rc;
+  CBFS_CUDA(cudaGraphInstantiate(&w->b_exec[db - 1][wide], g, 0));
+  return CBFS_OK;
+}
+
+// queue init + seeding of batch `a` on the slot's stream; the seeding's
+// error bits come back to the host before the round loop is launched
 static int slot_start(Graph* g, Slot* w, const RunArgs& a) {
   const uint32_t n = g->n;
   cudaStream_t st = w->s;
@@ -837,80 +1082,116 @@ static int slot_start(Graph* g, Slot* w, const RunArgs& a) {
     CBFS_CUDA(cudaMemsetAsync(w->pend, 0, cells * sizeof(uint64_t), st));
     w->pend_clean_cells = cells;
   }
-  w->cur = w->listA;
-  w->nxt = w->listB;
+  BState* h = w->bs_h;  // the slot's previous batch (and its copy) finished before this one starts
+  std::memset(h, 0, sizeof(BState));
+  h->off = g->off;
+  h->cols = g->cols;
+  h->chunk_v = g->chunk_v;
+  h->perm = a.out_internal ? nullptr : g->perm;
+  h->inv = g->inv;
+  h->n_chunks = g->n_chunks;
+  h->m = g->m;
+  h->sources = a.sources;
+  h->sizes = a.sizes;
+  h->out_dist = a.out_dist;
+  h->out_masks = a.out_masks;
+  h->rstats = a.out_rounds;
+  h->R = a.out_rounds ? a.max_rounds : 0;
+  h->n = n;
+  h->nb = a.nb;
+  h->d = a.d;
+  h->planes = a.planes;
+  h->C = a.C;
+  h->cbase = a.cbase;
+  h->mb = a.mask_bytes ? a.mask_bytes : 8;
+  h->W = a.wide > 1 ? a.wide : 1;
+  h->direction = a.direction;
+  h->hub_rows = g_hub_rows;
+  h->allow_empty = a.wide > 1;
+  h->pull_threshold = (double)g->m * (double)a.nb / g_alpha;  // R8: E_i * alpha > m * nb
+  h->seen = w->seen;
+  h->pend = w->pend;
+  h->pre = w->pre;
+  h->fullm = w->fullm;
+  h->bstats = w->bstats;
+  h->scan_tmp = reinterpret_cast<uint64_t*>(w->scan_tmp);
+  h->dist = w->dist;
+  h->list[0] = w->listA;
+  h->list[1] = w->listB;
+  h->ubits = w->ubits;
+  h->ub_words = (n >> 5) + 1;
+  h->prof_on = g_prof.on;
+  CBFS_CUDA(cudaMemcpyAsync(w->bs, h, sizeof(BState), cudaMemcpyHostToDevice, st));
+  CBFS_CUDA(cudaMemcpyToSymbolAsync(c_bs, h, sizeof(BState), (size_t)w->idx * sizeof(BState), cudaMemcpyHostToDevice,
+                                    st));
   CBFS_CUDA(cudaMemsetAsync(w->seen, 0, (uint64_t)(n + 1) * LANES * sizeof(uint64_t), st));
   CBFS_CUDA(cudaMemsetAsync(w->dist, 0xFF, (uint64_t)n * LANES * sizeof(uint16_t), st));
   CBFS_CUDA(cudaMemsetAsync(w->bstats, 0, LANES * 4 * sizeof(uint64_t), st));
   CBFS_CUDA(cudaMemsetAsync(w->fullm, 0, (uint64_t)(n + 1) * sizeof(uint64_t), st));
-  CBFS_CUDA(cudaMemsetAsync(w->ctr, 0, 4 * sizeof(unsigned long long), st));
-  k_seed<<<(a.nb * 64 + 255) / 256, 256, 0, st>>>(a.sources, a.sizes, a.nb, n, g->inv, g->off, w->pend, w->listA,
-                                                   w->ubits, w->bstats, w->ctr, a.wide > 1, a.out_rounds,
-                                                   a.out_rounds ? a.max_rounds : 0);
+  k_seed<<<(a.nb * 64 + 255) / 256, 256, 0, st>>>(w->bs, w->idx);
   CBFS_LAUNCHED();
-  return queue_counters(w);
+  CBFS_CUDA(cudaMemcpyAsync(w->bs_h, w->bs, sizeof(BState), cudaMemcpyDeviceToHost, st));
+  CBFS_CUDA(cudaEventRecord(w->ready, st));
+  return CBFS_OK;
 }
 
-// queue round w->i (fold + edge phase) of the slot's batch
-static int slot_round(Graph* g, Slot* w) {
-  const uint32_t n = g->n;
-  const uint64_t ub_words = (n >> 5) + 1;
-  const RunArgs& a = w->a;
+// Profiling aid (env CBFS_BATCHED_HOSTLOOP=1): the loop's kernels launched
+// from the host round by round (ncu cannot profile kernel nodes of graphs with
+// conditional nodes).  Synchronous.
+static int batched_hostloop(Slot* w) {
   cudaStream_t st = w->s;
-  const uint32_t i = w->i;
-  const uint64_t nF = w->nF, E = w->E;
-  uint32_t* ub_cur = w->ubits + (i & 1) * ub_words;        // U_i (built by the previous edge phase)
-  uint32_t* ub_nxt = w->ubits + ((i + 1) & 1) * ub_words;  // U_{i+1} (zero)
-  const bool pull = a.direction == CBFS_DIR_PULL ||
-                    (a.direction == CBFS_DIR_AUTO && (double)E * g_alpha > (double)g->m * (double)a.nb);
-  const int write_pre = pull ? 0 : 1;
-  const unsigned fb = grid_for((nF + FOLD_ILP - 1) / FOLD_ILP, 256);
-  if (g_prof.on) CBFS_CUDA(cudaEventRecord(w->pe[0], st));
-  const uint32_t W = a.wide > 1 ? a.wide : 1;
-  const uint32_t mb = a.mask_bytes ? a.mask_bytes : 8;
-  const uint32_t* fperm = a.out_internal ? nullptr : g->perm;
-#define CBFS_FOLD_ARGS                                                                                              \
-  w->cur, (uint32_t)nF, i, w->seen, w->pend, w->dist, g->off, fperm, n, a.C, a.cbase, a.planes, a.out_dist,          \
-      a.out_masks, mb, w->pre, write_pre, a.sizes, w->fullm, w->ctr, W
-  if (a.dist_bytes == 1) {
-    if (W > 1) k_fold<1, true><<<fb, 256, 0, st>>>(CBFS_FOLD_ARGS);
-    else k_fold<1, false><<<fb, 256, 0, st>>>(CBFS_FOLD_ARGS);
+  BState* S = w->bs;
+  const int slot = w->idx;
+  const int db = w->a.dist_bytes;
+  const bool wide = w->a.wide > 1;
+  unsigned long long flag = 0;
+  for (;;) {
+    k_begin<<<1, 32, 0, st>>>(S, slot, 0);
+    if (db == 1) {
+      if (wide) k_fold<1, true><<<FOLD_GRID, 256, 0, st>>>(S, slot);
+      else k_fold<1, false><<<FOLD_GRID, 256, 0, st>>>(S, slot);
+    } else {
+      if (wide) k_fold<2, true><<<FOLD_GRID, 256, 0, st>>>(S, slot);
+      else k_fold<2, false><<<FOLD_GRID, 256, 0, st>>>(S, slot);
+    }
+    CBFS_CUDA(cudaMemcpyAsync(&flag, &S->pull, sizeof(flag), cudaMemcpyDeviceToHost, st));
+    CBFS_CUDA(cudaStreamSynchronize(st));
+    if (flag) {
+      k_pull<<<148u * CBFS_PULL_MINB, PULL_WARPS * 32, 0, st>>>(S, slot);
+    } else {
+      k_scan_sums<<<SCAN_BLOCKS, SCAN_THREADS, 0, st>>>(S, slot);
+      k_scan_top<<<1, 1024, 0, st>>>(S, slot);
+      k_scan_apply<<<SCAN_BLOCKS, SCAN_THREADS, 0, st>>>(S, slot);
+      k_push<<<PUSH_GRID, 256, 0, st>>>(S, slot);
+    }
+    k_end<<<END_GRID, 256, 0, st>>>(S, slot, 0);
+    CBFS_CUDA(cudaGetLastError());
+    CBFS_CUDA(cudaMemcpyAsync(&flag, &S->go, sizeof(flag), cudaMemcpyDeviceToHost, st));
+    CBFS_CUDA(cudaStreamSynchronize(st));
+    if (!flag) break;
+  }
+  return CBFS_OK;
+}
+
+// the batch's whole round loop (one graph launch) + the state readback
+static int batched_launch(Slot* w) {
+  static const bool hostloop = getenv("CBFS_BATCHED_HOSTLOOP") != nullptr;
+  cudaStream_t st = w->s;
+  const int db = w->a.dist_bytes == 1 ? 1 : 2;
+  const bool wide = w->a.wide > 1;
+  if (hostloop) {
+    int rc = batched_hostloop(w);
+    if (rc) return rc;
   } else {
-    if (W > 1) k_fold<2, true><<<fb, 256, 0, st>>>(CBFS_FOLD_ARGS);
-    else k_fold<2, false><<<fb, 256, 0, st>>>(CBFS_FOLD_ARGS);
+    if (!w->b_exec[db - 1][wide]) {
+      int rc = b_build(w, db, wide);
+      if (rc) return rc;
+    }
+    CBFS_CUDA(cudaGraphLaunch(w->b_exec[db - 1][wide], st));
   }
-#undef CBFS_FOLD_ARGS
-  CBFS_LAUNCHED();
-  if (g_prof.on) CBFS_CUDA(cudaEventRecord(w->pe[1], st));
-  CBFS_CUDA(cudaMemsetAsync(w->ctr, 0, 2 * sizeof(unsigned long long), st));
-  CBFS_CUDA(cudaMemsetAsync(w->ctr + 3, 0, sizeof(unsigned long long), st));
-  w->kind = -1;
-  if (pull) {
-    w->kind = PK_PULL;
-    if (g_prof.on) CBFS_CUDA(cudaEventRecord(w->pe[2], st));
-    const unsigned pb = grid_for(g->n_chunks * 32, PULL_WARPS * 32, 148u * CBFS_PULL_MINB);
-    k_pull<<<pb, PULL_WARPS * 32, 0, st>>>(g->off, g->cols, g->chunk_v, g->n_chunks, g->m, n, w->seen, w->dist,
-                                           w->pend, ub_cur, ub_nxt, a.sizes, a.nb, w->nxt, w->bstats, w->ctr, w->fullm,
-                                           i, a.d, a.out_rounds, a.out_rounds ? a.max_rounds : 0,
-                                           std::min<uint32_t>(n, g_hub_rows));
-    CBFS_LAUNCHED();
-    if (g_prof.on) CBFS_CUDA(cudaEventRecord(w->pe[3], st));
-  } else if (E > 0) {
-    w->kind = PK_PUSH;
-    CBFS_CUDA(cub::DeviceScan::ExclusiveSum(w->scan_tmp, w->scan_bytes, w->pre, w->pre, nF, st));
-    count_launch(2);
-    k_set_u64<<<1, 1, 0, st>>>(w->pre + nF, E);
-    CBFS_LAUNCHED();
-    const uint64_t warps = (E + PUSH_CHUNK - 1) / PUSH_CHUNK;
-    const unsigned pb = grid_for(warps * 32, 256, 148u * 8u * 4u);
-    if (g_prof.on) CBFS_CUDA(cudaEventRecord(w->pe[2], st));
-    k_push<<<pb, 256, 0, st>>>(g->off, g->cols, w->cur, w->pre, (uint32_t)nF, E, w->seen, w->dist, w->pend, w->nxt,
-                               ub_nxt, w->bstats, w->ctr, i, a.d, a.out_rounds, a.out_rounds ? a.max_rounds : 0);
-    CBFS_LAUNCHED();
-    if (g_prof.on) CBFS_CUDA(cudaEventRecord(w->pe[3], st));
-  }
-  CBFS_CUDA(cudaMemsetAsync(ub_cur, 0, ub_words * sizeof(uint32_t), st));  // U_i consumed
-  return queue_counters(w);
+  CBFS_CUDA(cudaMemcpyAsync(w->bs_h, w->bs, sizeof(BState), cudaMemcpyDeviceToHost, st));
+  CBFS_CUDA(cudaEventRecord(w->ready, st));
+  return CBFS_OK;
 }
 
 // The slot's counters arrived: account the finished round, then queue the
@@ -965,41 +1246,38 @@ static int sparse_step(Graph* g, Slot* w, BatchSource& src, int slot, int* err) 
 static int slot_step(Graph* g, Slot* w, BatchSource& src, int slot, int* err) {
   if (w->engine == ENGINE_SPARSE) return sparse_step(g, w, src, slot, err);
   const uint32_t n = g->n;
+  const BState& h = *w->bs_h;
   if (w->seeding) {
     w->seeding = false;
-    if (w->h_ctr[2]) {  // bad sources: restore the zero invariants, report
+    if (h.err) {  // bad sources: restore the zero invariants, report
       CBFS_CUDA(cudaMemsetAsync(w->pend, 0, (uint64_t)n * LANES * sizeof(uint64_t), w->s));
       CBFS_CUDA(cudaMemsetAsync(w->ubits, 0, 2 * ((n >> 5) + 1) * sizeof(uint32_t), w->s));
       CBFS_CUDA(cudaStreamSynchronize(w->s));
-      return seed_error(w, w->h_ctr[2], err);
+      return seed_error(w, h.err, err);
     }
-  } else {
-    if (g_prof.on) {
-      float ms = 0;
-      CBFS_CUDA(cudaEventElapsedTime(&ms, w->pe[0], w->pe[1]));
-      g_prof.ms[PK_FOLD] += ms; g_prof.launches[PK_FOLD] += 1; g_prof.entries[PK_FOLD] += w->nF;
-      if (w->kind >= 0) {
-        CBFS_CUDA(cudaEventElapsedTime(&ms, w->pe[2], w->pe[3]));
-        g_prof.ms[w->kind] += ms; g_prof.launches[w->kind] += 1; g_prof.entries[w->kind] += w->nF;
-        g_prof.arcs[w->kind] += w->E; g_prof.u_in[w->kind] += w->U; g_prof.u_out[w->kind] += w->h_ctr[3];
-      }
-    }
-    if (w->h_ctr[2] & ERR_OVERFLOW) w->overflow = true;
-    std::swap(w->cur, w->nxt);
-    ++w->i;
+    int rc = batched_launch(w);
+    if (rc) { *err = rc; w->busy = false; return 1; }
+    return 0;
   }
-  w->nF = w->h_ctr[0];
-  w->E = w->h_ctr[1];
-  w->U = w->h_ctr[3];
-  if (w->nF == 0) return finish_batch(w, src, slot, err);  // batch done
-  if (w->i >= 0xFFFEu) {
+  count_launch(h.launches);
+  if (g_prof.on) {
+    for (int k = PK_FOLD; k <= PK_PULL; ++k) {
+      g_prof.ms[k] += h.p_ns[k] * 1e-6;
+      g_prof.launches[k] += h.p_launch[k];
+      g_prof.entries[k] += h.p_entries[k];
+      g_prof.arcs[k] += h.p_arcs[k];
+      g_prof.u_in[k] += h.p_uin[k];
+      g_prof.u_out[k] += h.p_uout[k];
+    }
+  }
+  w->i = (uint32_t)h.i;
+  if (h.err & ERR_ROUNDS) {
     w->busy = false;
     *err = fail(CBFS_EOVERFLOW, "more than 65534 rounds");
-    return 1;  // pend is left non-zero only for this slot's pending entries; cleared below
+    return 1;  // pend is left non-zero only for this slot's pending entries; cleared by run_batches
   }
-  int rc = slot_round(g, w);
-  if (rc) { *err = rc; return 1; }
-  return 0;
+  if (h.err & ERR_OVERFLOW) w->overflow = true;
+  return finish_batch(w, src, slot, err);
 }
 
 // Drive all batches of `src` through the device's slots; every slot stream

@@ -74,6 +74,43 @@ struct SpCtl {
   unsigned pad;
 };
 
+// Device-resident state of a BATCHED-engine slot: the graph and batch
+// arguments (written by the host when a batch starts), the slot's arrays, and
+// the round state the device-side round loop advances (cbfs.cu).  Kernels of
+// the loop take only this pointer, so one instantiated CUDA graph per slot
+// (and Delta width / wide flag) serves every batch and every graph handle.
+struct BState {
+  // graph
+  const uint64_t* off;
+  const uint32_t* cols;
+  const uint32_t* chunk_v;
+  const uint32_t* perm;  // output rows: internal -> original (null: identity or library-internal rows)
+  const uint32_t* inv;   // original -> internal (sources)
+  uint64_t n_chunks, m;
+  // batch
+  const uint32_t* sources;  // [nb][64]
+  const uint8_t* sizes;     // [nb]
+  void* out_dist;
+  void* out_masks;
+  uint64_t* rstats;         // [nb][R][2] or null
+  uint32_t n, nb, d, planes, C, cbase, mb, W, R, direction, hub_rows, allow_empty;
+  double pull_threshold;    // the edge phase pulls when the frontier's (cluster, arc) pairs exceed this
+  // slot arrays
+  uint64_t *seen, *pend, *pre, *fullm, *bstats, *scan_tmp;
+  uint16_t* dist;
+  uint32_t* list[2];
+  uint32_t* ubits;          // [2][ub_words]: U_i of parity i & 1
+  uint64_t ub_words;
+  // round state: cnt[p] = {entries, E (degree sum), -, |U|} of the list of parity p
+  unsigned long long cnt[2][4];
+  unsigned long long err, i, pull, go, launches;
+  unsigned end_done;
+  unsigned prof_on;
+  // per-kernel profile of the batch (PK_* kinds, globaltimer ns)
+  unsigned long long p_t0[8], p_ns[8], p_launch[8], p_entries[8], p_arcs[8], p_uin[8], p_uout[8];
+  unsigned p_arrive[8], p_leave[8];
+};
+
 // One in-flight batch of LANES clusters: its workspace, its stream, and the
 // state of its round loop.  Several slots run concurrently (run_batches), so
 // the small rounds and the latency-bound dense rounds of different batches
@@ -89,23 +126,16 @@ struct Slot {
   uint32_t* listB = nullptr;
   uint64_t* pre = nullptr;              // [cap + 1] degrees -> exclusive prefix (push)
   uint32_t* ubits = nullptr;            // 2 x [n/32 + 1]: union frontier U_i, U_{i+1}
-  unsigned long long* ctr = nullptr;    // [0] next count, [1] next E, [2] error bits, [3] |U_next|
-  unsigned long long* h_ctr = nullptr;  // pinned mirror
   uint64_t* bstats = nullptr;           // [LANES][4]
   uint64_t* fullm = nullptr;            // [n] bit c: S_seen[v][c] == S_c (maintained by the fold)
-  void* scan_tmp = nullptr;
-  size_t scan_bytes = 0;
+  void* scan_tmp = nullptr;             // [SCAN_BLOCKS] tile sums of the push's degree scan
   cudaStream_t s = nullptr;
   cudaEvent_t ready = nullptr;  // counters of the last queued round are on the host
-  cudaEvent_t pe[4] = {nullptr, nullptr, nullptr, nullptr};  // profiling
   // round-loop state
   bool busy = false;
   bool seeding = false;
   RunArgs a{};
   uint32_t i = 0;
-  uint64_t nF = 0, E = 0, U = 0;
-  uint32_t *cur = nullptr, *nxt = nullptr;
-  int kind = -1;
   bool overflow = false;
   // sparse engine
   int engine = ENGINE_BATCHED;  // engine of the batch in flight
@@ -119,6 +149,12 @@ struct Slot {
   cudaEvent_t sp_t0 = nullptr, sp_t1 = nullptr;  // profiling
   uint32_t sp_db = 0;                             // dist_bytes the graph was built for
   bool sp_fused = false;                          // fold fused into the push (d >= 1)
+  // batched engine (device-side round loop)
+  int idx = 0;             // slot index on its device (constant-memory BState mirror c_bs[idx])
+  BState* bs = nullptr;    // device
+  BState* bs_h = nullptr;  // pinned mirror
+  cudaGraph_t b_graph[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [dist_bytes == 2][wide]
+  cudaGraphExec_t b_exec[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
 };
 
 struct DevSlots {
