@@ -6,9 +6,10 @@ of its full output vector (Delta + d+1 subsets; digest definition
 in include/cbfs.h cbfs_digest_store), and the SHA-256 of the whole
 selection.  The GPU runs every cluster of the config in the launch path the
 bench times (config 2: cbfs_select_and_run_shard with the full [n][C] store;
-config 3: cbfs_run_digest).  Config 5: the stats of all 8,192 clusters from
-the streaming label build + 10M-query path, and its answers against the
-oracle's (SHA-256 of all 10M answers + 100,000 stored answers)."""
+config 3: cbfs_run_digest).  Config 5: the streaming label build + the
+10M queries over the selection prefix its golden covers — round statistics
+of every covered cluster and every answer against the oracle's (SHA-256 of
+all 10M answers + 100,000 stored answers)."""
 import hashlib
 import json
 import os
@@ -27,6 +28,12 @@ from gpu_util import np_u32, np_u64  # noqa: E402
 pytestmark = pytest.mark.gpu
 DEV = "cuda:0"
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@pytest.fixture(autouse=True)
+def _release_workspace():
+    yield
+    cb.cbfs_release_workspace(0)  # full-size configs leave multi-GB slot caches behind
 
 
 def load_golden(name):
@@ -159,30 +166,36 @@ def test_c4_whole_config_golden():
 
 
 @pytest.mark.timeout(1800)
-def test_c5_whole_config_golden_queries():
-    """Config 5: the streaming label build + 10M queries over all 8,192 clusters
-    (bench.py's query mode) — round statistics of every cluster and every
-    answer against the oracle's; the full-vector digests of the first 256
-    clusters."""
+def test_c5_full_size_golden_queries():
+    """Config 5 at full size (10M-point k-NN graph, d = 6): the whole
+    selection (SHA-256 of all 8,192 clusters), then the streaming label build
+    + all 10M queries (bench.py's query path, cbfs_query_stream) over the
+    clusters the golden covers (a selection prefix: the oracle needs ~38 s per
+    config-5 cluster per core) — every answer (SHA-256 of the 10M-vector and
+    100,000 stored answers) and every covered cluster's round statistics —
+    and the full-vector digests of the first 256 clusters."""
     header, rows = load_golden("c5_knn")
     ans_path = os.path.join(GOLDEN, "c5_knn.answers.npz")
-    if len(rows) < header["clusters"] or not os.path.exists(ans_path):
+    if not os.path.exists(ans_path):
         pytest.skip("config 5 golden incomplete")
     ans = np.load(ans_path)
+    Cq = int(ans["clusters"])
+    assert all(c in rows for c in range(Cq))
     cfg, el, g = build("c5_knn")
     src, sz = select(g, cfg, header)
-    C, d = len(sz), cfg["d"]
+    d = cfg["d"]
     s, t = ci.query_pairs(g.n, cfg["queries"], cfg["query_seed"])
     best = torch.full((len(s),), cb.CBFS_QUERY_UNREACHED, dtype=torch.int32, device=DEV)
-    stats = torch.zeros((C, 4), dtype=torch.int64, device=DEV)
-    cb.cbfs_query_stream(g.h, src, sz, C, d, torch.from_numpy(s.view(np.int32)).to(DEV),
-                         torch.from_numpy(t.view(np.int32)).to(DEV), best, stats)
+    stats = torch.zeros((Cq, 4), dtype=torch.int64, device=DEV)
+    cb.cbfs_query_stream(g.h, src[:Cq].contiguous(), sz[:Cq].contiguous(), Cq, d,
+                         torch.from_numpy(s.view(np.int32)).to(DEV), torch.from_numpy(t.view(np.int32)).to(DEV), best,
+                         stats)
     b = best.cpu().numpy()
     assert np.array_equal(b[ans["index"]], ans["answer"])
     assert hashlib.sha256(b.tobytes()).hexdigest() == str(ans["sha256"])
     st = np_u64(stats)
-    for c, row in rows.items():
-        assert np.array_equal(st[c], row["stats"]), c
+    for c in range(Cq):
+        assert np.array_equal(st[c], rows[c]["stats"]), c
     first = list(range(256))
     t_idx = torch.tensor(first, device=DEV)
     dig = torch.zeros(len(first), dtype=torch.int64, device=DEV)
