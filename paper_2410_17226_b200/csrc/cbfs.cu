@@ -335,10 +335,13 @@ constexpr int FOLD_ILP = CBFS_FOLD_ILP;
 #ifndef CBFS_FOLD_FULL
 #define CBFS_FOLD_FULL 2
 #endif
-#ifdef CBFS_FOLD_MINB  // experiments; an explicit minimum of 1 block lets ptxas double the registers
+#ifndef CBFS_FOLD_MINB  // blocks per SM the register budget must allow (0: no bound)
+#define CBFS_FOLD_MINB 4
+#endif
+#if CBFS_FOLD_MINB
 #define CBFS_FOLD_BOUNDS __launch_bounds__(256, CBFS_FOLD_MINB)
 #else
-#define CBFS_FOLD_BOUNDS __launch_bounds__(256, 4)
+#define CBFS_FOLD_BOUNDS __launch_bounds__(256)
 #endif
 
 template <int DB, bool WIDE>
@@ -996,7 +999,10 @@ __global__ void k_end(BState* __restrict__ S, int slot, cudaGraphConditionalHand
 }
 
 // ------------------------------------------------------------------ driver
-constexpr unsigned FOLD_GRID = 148u * 8u;        // grid-stride kernels of the round loop (fixed grids:
+#ifndef CBFS_FOLD_GRID_PER_SM
+#define CBFS_FOLD_GRID_PER_SM 32
+#endif
+constexpr unsigned FOLD_GRID = 148u * CBFS_FOLD_GRID_PER_SM;  // grid-stride kernels of the round loop (fixed grids:
 constexpr unsigned PUSH_GRID = 148u * 8u * 4u;   // the loop's kernel nodes are launched with the same
 constexpr unsigned END_GRID = 148u * 2u;         // configuration every round)
 

@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--profile", action="store_true")
     ap.add_argument("--conc", type=int, default=0)
     ap.add_argument("--alpha", type=float, default=0.0)
+    ap.add_argument("--first", type=int, default=0, help="traverse only clusters [first, clusters) of the selection")
     args = ap.parse_args()
     cfg = ci.CONFIGS[args.config]
     dev = torch.device("cuda:0")
@@ -67,15 +68,16 @@ def main():
         got = cb.cbfs_select_clusters(h, C, k, d, policy, cfg["root_seed"], ss, sz, st)
         torch.cuda.synchronize()
         t_sel = time.perf_counter() - t0
+        f0 = min(args.first, got)
         stats = torch.zeros((got, 4), dtype=torch.int64, device=dev)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
-        cb.cbfs_run(h, ss[:got], sz[:got], got, d, 2, None, None, d + 1, stats)  # stats only
+        cb.cbfs_run(h, ss[f0:got], sz[f0:got], got - f0, d, 2, None, None, d + 1, stats[f0:])  # stats only
         e1.record(st)
         torch.cuda.synchronize()
         t_run = e0.elapsed_time(e1) / 1000.0
-        stn = stats.cpu().numpy().view(np.uint64)
-        szn = sz[:got].cpu().numpy().astype(np.float64)
+        stn = stats[f0:].cpu().numpy().view(np.uint64)
+        szn = sz[f0:got].cpu().numpy().astype(np.float64)
         units = float((szn * stn[:, 3].astype(np.float64)).sum())
         res.update({"m": m, "max_degree": maxdeg, "selected": got, "build_s": t_build, "select_s": t_sel,
                     "cbfs_s": t_run, "source_edges_per_s": units / t_run,

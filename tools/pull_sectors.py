@@ -4,7 +4,7 @@ round i, the S_seen rows the dense pull gathered and their non-zero 32-byte
 sectors, for the hub rows (the first CBFS_PULL_HUB_MB of rows, evict_last)
 and the others.
 
-    python tools/pull_sectors.py CONFIG [CLUSTERS]
+    python tools/pull_sectors.py CONFIG [CLUSTERS] [FIRST]
 """
 import ctypes
 import json
@@ -20,13 +20,15 @@ import paper_2410_17226_b200 as cb  # noqa: E402
 
 name = sys.argv[1]
 C = int(sys.argv[2]) if len(sys.argv) > 2 else 64
+F0 = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 cfg = ci.CONFIGS[name]
 el = ci.make_graph(name)
 src_d = torch.from_numpy(el.src.view(np.int32)).cuda()
 dst_d = torch.from_numpy(el.dst.view(np.int32)).cuda()
 g = cb.Graph(cb.cbfs_graph_create(el.n, src_d, dst_d, cb.Graph.relabel_flags(cfg.get("relabel", "none")), 0), 0)
 del src_d, dst_d
-src, sz = g.select_clusters(C, cfg["k"], cfg["d"])
+src, sz = g.select_clusters(F0 + C, cfg["k"], cfg["d"])
+src, sz = src[F0:].contiguous(), sz[F0:].contiguous()
 cb._lib.cbfs_debug_read.argtypes = [ctypes.c_void_p]
 buf = np.zeros(32, np.uint64)
 cb._lib.cbfs_debug_read(buf.ctypes.data)
@@ -40,4 +42,4 @@ for i in range(8):
     if hr + orow:
         out[i] = {"hub_rows": hr, "hub_nonzero_sectors_per_row": hs / max(hr, 1), "other_rows": orow,
                   "other_nonzero_sectors_per_row": osec / max(orow, 1)}
-print(json.dumps({"config": name, "clusters": len(sz), "rounds": out}))
+print(json.dumps({"config": name, "clusters": len(sz), "first": F0, "rounds": out}))
