@@ -800,22 +800,19 @@ __device__ __forceinline__ void pull_body(
 #pragma unroll
               for (int r = 0; r < PULL_MLP; ++r) { acc0 |= g[r].a; acc1 |= g[r].b; }
 #ifdef CBFS_PULL_STATS
-              {  // gathered rows, their non-zero 32-byte sectors, and those a capped non-full lane needs
-                const bool need = (k0 && ((acc0 | sv.a) & full0) != full0) || (k1 && ((acc1 | sv.b) & full1) != full1);
-                unsigned long long rows = 0, nzs = 0, nds = 0;
+              {  // per round: [hub, other] x {rows, non-zero words, set bits} of the gathered S_seen rows
+                unsigned long long cnt[6] = {0, 0, 0, 0, 0, 0};
                 for (int r = 0; r < PULL_MLP; ++r) {
                   if (q + r >= s1) break;
-                  const unsigned nzl = __ballot_sync(FULLW, (g[r].a | g[r].b) != 0);
-                  const unsigned ndl = __ballot_sync(FULLW, (g[r].a | g[r].b) != 0 && need);
-                  rows += 1;
-                  nzs += __popc((nzl | (nzl >> 1)) & 0x55555555u);
-                  nds += __popc((ndl | (ndl >> 1)) & 0x55555555u);
+                  const int o = list[q + r] < hub_rows ? 0 : 3;
+                  const unsigned long long words = warp_sum((g[r].a != 0) + (g[r].b != 0));
+                  const unsigned long long bits = warp_sum(__popcll(g[r].a) + __popcll(g[r].b));
+                  cnt[o] += 1;
+                  cnt[o + 1] += words;
+                  cnt[o + 2] += bits;
                 }
-                if (lane == 0 && i < 8) {
-                  atomicAdd(&g_dbg[i * 4 + 0], rows);
-                  atomicAdd(&g_dbg[i * 4 + 1], nzs);
-                  atomicAdd(&g_dbg[i * 4 + 2], nds);
-                }
+                if (lane == 0 && i < 4)
+                  for (int k = 0; k < 6; ++k) atomicAdd(&g_dbg[i * 8 + k], cnt[k]);
               }
 #endif
               // R7: stop once every capped lane holds its full subset

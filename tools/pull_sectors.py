@@ -1,8 +1,8 @@
 """Pull-round statistics of a -DCBFS_PULL_STATS build (tools/build_variant.sh
 stats "-DCBFS_PULL_STATS"; CBFS_LIB_PATH=build_var/stats/libcbfs.so): per
-round i, the S_seen rows the dense pull gathered and their non-zero 32-byte
-sectors, for the hub rows (the first CBFS_PULL_HUB_MB of rows, evict_last)
-and the others.
+round i, the S_seen rows the dense pull gathered, their non-zero 64-bit
+words (clusters) and their set bits (sources), for the hub rows (the first
+64 MiB of rows, evict_last) and the others.
 
     python tools/pull_sectors.py CONFIG [CLUSTERS] [FIRST]
 """
@@ -37,9 +37,10 @@ cb.cbfs_run(g.h, src, sz, len(sz), cfg["d"], 2, None, None, cfg["d"] + 1, stats)
 torch.cuda.synchronize()
 cb._lib.cbfs_debug_read(buf.ctypes.data)
 out = {}
-for i in range(8):
-    hr, hs, orow, osec = (int(x) for x in buf[4 * i:4 * i + 4])
+for i in range(4):
+    hr, hw, hb, orow, ow, ob = (int(x) for x in buf[8 * i:8 * i + 6])
     if hr + orow:
-        out[i] = {"hub_rows": hr, "hub_nonzero_sectors_per_row": hs / max(hr, 1), "other_rows": orow,
-                  "other_nonzero_sectors_per_row": osec / max(orow, 1)}
+        out[i] = {"hub_rows": hr, "hub_words_per_row": hw / max(hr, 1), "hub_bits_per_row": hb / max(hr, 1),
+                  "other_rows": orow, "other_words_per_row": ow / max(orow, 1),
+                  "other_bits_per_row": ob / max(orow, 1)}
 print(json.dumps({"config": name, "clusters": len(sz), "first": F0, "rounds": out}))
