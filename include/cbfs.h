@@ -488,7 +488,8 @@ int cbfs_profile_read(double* ms, uint64_t* launches, uint64_t* arcs, uint64_t* 
 /* Number of vertices with at least one arc. */
 int cbfs_graph_nonisolated(const cbfs_graph* g, uint32_t* count);
 /* Maximum number of 64-cluster batches traversed concurrently (each with its
- * own workspace and stream; fewer if device memory is short).  Default 4. */
+ * own workspace and stream; fewer if device memory is short).  1..8, default
+ * 4.  Errors: EINVAL. */
 int cbfs_set_concurrency(int batches);
 /* Number of kernels this library launched on this thread since the last reset. */
 uint64_t cbfs_launch_count(int reset);

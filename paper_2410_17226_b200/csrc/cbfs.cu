@@ -229,7 +229,8 @@ __device__ __forceinline__ void stats_flush(uint64_t* __restrict__ bstats, uint3
 // kernels read them as constant-bank operands instead of holding ~20 pointers
 // in registers; the round state (counters, round, direction, profile) lives in
 // the global BState the loop advances.
-constexpr int BS_MAX = 16;  // slots per device (cbfs_set_concurrency <= 16)
+constexpr int BS_MAX = 8;  // slots per device (cbfs_set_concurrency <= 8); kernels are instantiated per slot so
+                           // that the mirror's fields are direct constant-bank operands
 __constant__ BState c_bs[BS_MAX];
 
 // ------------------------------------------------------------------ init
@@ -283,8 +284,9 @@ __device__ __forceinline__ void seed_body(const uint32_t* __restrict__ sources, 
   if (lane_id() == 0 && nu) atomicAdd(&ctr[3], nu);
 }
 
-__global__ void k_seed(BState* __restrict__ S, int slot) {
-  const BState& P = c_bs[slot];
+template <int SL>
+__global__ void k_seed(BState* __restrict__ S) {
+  const BState& P = c_bs[SL];
   seed_body(P.sources, P.sizes, P.nb, P.n, P.inv, P.off, P.pend, P.list[0], P.ubits, P.bstats, S->cnt[0], &S->err,
             P.allow_empty, P.rstats, P.R);
 }
@@ -451,9 +453,9 @@ __device__ __forceinline__ void fold_body(const uint32_t* __restrict__ F, uint32
 }
 
 // the vertex phase of round S->i over F_i = list[i & 1]
-template <int DB, bool WIDE>
-__global__ void CBFS_FOLD_BOUNDS k_fold(BState* __restrict__ S, int slot) {
-  const BState& P = c_bs[slot];
+template <int DB, bool WIDE, int SL>
+__global__ void CBFS_FOLD_BOUNDS k_fold(BState* __restrict__ S) {
+  const BState& P = c_bs[SL];
   prof_begin(S, P.prof_on, PK_FOLD);
   const uint32_t i = (uint32_t)S->i, cur = i & 1;
   const uint32_t nF = (uint32_t)S->cnt[cur][0];
@@ -555,8 +557,9 @@ __device__ __forceinline__ void push_body(const uint64_t* __restrict__ off, cons
 
 // the sparse edge phase of round S->i (pre = the exclusive prefix of the
 // frontier's degrees, pre[nF] = E_i)
-__global__ void __launch_bounds__(256) k_push(BState* __restrict__ S, int slot) {
-  const BState& P = c_bs[slot];
+template <int SL>
+__global__ void __launch_bounds__(256) k_push(BState* __restrict__ S) {
+  const BState& P = c_bs[SL];
   prof_begin(S, P.prof_on, PK_PUSH);
   const uint32_t i = (uint32_t)S->i, cur = i & 1;
   const uint32_t nF = (uint32_t)S->cnt[cur][0];
@@ -886,8 +889,9 @@ __device__ __forceinline__ void pull_body(
 }
 
 // the dense edge phase of round S->i
-__global__ void __launch_bounds__(PULL_WARPS * 32, CBFS_PULL_MINB) k_pull(BState* __restrict__ S, int slot) {
-  const BState& P = c_bs[slot];
+template <int SL>
+__global__ void __launch_bounds__(PULL_WARPS * 32, CBFS_PULL_MINB) k_pull(BState* __restrict__ S) {
+  const BState& P = c_bs[SL];
   prof_begin(S, P.prof_on, PK_PULL);
   const uint32_t i = (uint32_t)S->i, cur = i & 1;
   const uint32_t n = P.n;
@@ -906,8 +910,9 @@ __global__ void __launch_bounds__(PULL_WARPS * 32, CBFS_PULL_MINB) k_pull(BState
 // continue while F_{i+1} is non-empty).
 constexpr uint32_t SCAN_THREADS = 512;
 
-__global__ void k_begin(BState* __restrict__ S, int slot, cudaGraphConditionalHandle h_if) {
-  const BState& P = c_bs[slot];
+template <int SL>
+__global__ void k_begin(BState* __restrict__ S, cudaGraphConditionalHandle h_if) {
+  const BState& P = c_bs[SL];
   const uint32_t cur = (uint32_t)(S->i & 1);
   const uint32_t t = threadIdx.x;
   if (t < 4) S->cnt[cur ^ 1][t] = 0;
@@ -923,10 +928,11 @@ __global__ void k_begin(BState* __restrict__ S, int slot, cudaGraphConditionalHa
 
 // exclusive prefix of pre[0 .. nF) in place, pre[nF] = E_i: block sums,
 // one block scans them, blocks rescan their tiles with the offsets
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_sums(BState* __restrict__ S, int slot) {
+template <int SL>
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_sums(BState* __restrict__ S) {
   typedef cub::BlockReduce<unsigned long long, SCAN_THREADS> BR;
   __shared__ typename BR::TempStorage tmp;
-  const BState& P = c_bs[slot];
+  const BState& P = c_bs[SL];
   const uint64_t nF = S->cnt[S->i & 1][0];
   const uint64_t tile = (nF + SCAN_BLOCKS - 1) / SCAN_BLOCKS;
   const uint64_t b0 = blockIdx.x * tile, b1 = min(b0 + tile, nF);
@@ -936,20 +942,22 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_sums(BState* __restrict__
   if (threadIdx.x == 0) P.scan_tmp[blockIdx.x] = x;
 }
 
-__global__ void __launch_bounds__(1024) k_scan_top(BState* __restrict__ S, int slot) {
+template <int SL>
+__global__ void __launch_bounds__(1024) k_scan_top(BState* __restrict__ S) {
   typedef cub::BlockScan<unsigned long long, 1024> BS;
   __shared__ typename BS::TempStorage tmp;
-  const BState& P = c_bs[slot];
+  const BState& P = c_bs[SL];
   unsigned long long x = threadIdx.x < SCAN_BLOCKS ? P.scan_tmp[threadIdx.x] : 0ULL;
   BS(tmp).ExclusiveSum(x, x);
   if (threadIdx.x < SCAN_BLOCKS) P.scan_tmp[threadIdx.x] = x;
 }
 
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_apply(BState* __restrict__ S, int slot) {
+template <int SL>
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_apply(BState* __restrict__ S) {
   typedef cub::BlockScan<unsigned long long, SCAN_THREADS> BS;
   __shared__ typename BS::TempStorage tmp;
   __shared__ unsigned long long s_run;
-  const BState& P = c_bs[slot];
+  const BState& P = c_bs[SL];
   const uint32_t cur = (uint32_t)(S->i & 1);
   const uint64_t nF = S->cnt[cur][0];
   const uint64_t tile = (nF + SCAN_BLOCKS - 1) / SCAN_BLOCKS;
@@ -969,8 +977,9 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_apply(BState* __restrict_
   if (blockIdx.x == 0 && threadIdx.x == 0) P.pre[nF] = S->cnt[cur][1];
 }
 
-__global__ void k_end(BState* __restrict__ S, int slot, cudaGraphConditionalHandle h_while) {
-  const BState& P = c_bs[slot];
+template <int SL>
+__global__ void k_end(BState* __restrict__ S, cudaGraphConditionalHandle h_while) {
+  const BState& P = c_bs[SL];
   const uint32_t cur = (uint32_t)(S->i & 1);
   uint32_t* ub = P.ubits + (uint64_t)cur * P.ub_words;  // U_i consumed
   for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < P.ub_words;
@@ -1014,9 +1023,31 @@ static int b_add(cudaGraph_t body, cudaGraphNode_t* node, const cudaGraphNode_t*
   return CBFS_OK;
 }
 
-static void* fold_fn(int db, bool wide) {
-  if (db == 1) return wide ? (void*)k_fold<1, true> : (void*)k_fold<1, false>;
-  return wide ? (void*)k_fold<2, true> : (void*)k_fold<2, false>;
+// the round-loop kernels of slot SL
+struct BFns {
+  void *seed, *fold[2][2], *push, *pull, *begin, *end, *scan_sums, *scan_top, *scan_apply;
+};
+template <int SL>
+static BFns bfns() {
+  BFns f;
+  f.seed = (void*)k_seed<SL>;
+  f.fold[0][0] = (void*)k_fold<1, false, SL>;
+  f.fold[0][1] = (void*)k_fold<1, true, SL>;
+  f.fold[1][0] = (void*)k_fold<2, false, SL>;
+  f.fold[1][1] = (void*)k_fold<2, true, SL>;
+  f.push = (void*)k_push<SL>;
+  f.pull = (void*)k_pull<SL>;
+  f.begin = (void*)k_begin<SL>;
+  f.end = (void*)k_end<SL>;
+  f.scan_sums = (void*)k_scan_sums<SL>;
+  f.scan_top = (void*)k_scan_top<SL>;
+  f.scan_apply = (void*)k_scan_apply<SL>;
+  return f;
+}
+static const BFns& fns_of(int slot) {
+  static const BFns t[BS_MAX] = {bfns<0>(), bfns<1>(), bfns<2>(), bfns<3>(),
+                                 bfns<4>(), bfns<5>(), bfns<6>(), bfns<7>()};
+  return t[slot];
 }
 
 // The slot's round-loop graph for (Delta width, wide):
@@ -1038,13 +1069,13 @@ static int b_build(Slot* w, int db, bool wide) {
   CBFS_CUDA(cudaGraphAddNode(&wn, g, nullptr, 0, &wp));
   cudaGraph_t body = wp.conditional.phGraph_out[0];
   BState* S = w->bs;
-  int slot = w->idx;
-  void* a_s[] = {&S, &slot};
-  void* a_if[] = {&S, &slot, &hi};
-  void* a_wh[] = {&S, &slot, &hw};
+  const BFns& F = fns_of(w->idx);
+  void* a_s[] = {&S};
+  void* a_if[] = {&S, &hi};
+  void* a_wh[] = {&S, &hw};
   cudaGraphNode_t nb, nf, nif, ne;
-  int rc = b_add(body, &nb, nullptr, (void*)k_begin, 1, 32, a_if);
-  if (!rc) rc = b_add(body, &nf, &nb, fold_fn(db, wide), FOLD_GRID, 256, a_s);
+  int rc = b_add(body, &nb, nullptr, F.begin, 1, 32, a_if);
+  if (!rc) rc = b_add(body, &nf, &nb, F.fold[db - 1][wide], FOLD_GRID, 256, a_s);
   if (rc) return rc;
   cudaGraphNodeParams ip = {};
   ip.type = cudaGraphNodeTypeConditional;
@@ -1054,12 +1085,12 @@ static int b_build(Slot* w, int db, bool wide) {
   CBFS_CUDA(cudaGraphAddNode(&nif, body, &nf, 1, &ip));
   cudaGraph_t g_pull = ip.conditional.phGraph_out[0], g_push = ip.conditional.phGraph_out[1];
   cudaGraphNode_t np, s1, s2, s3, nq;
-  rc = b_add(g_pull, &np, nullptr, (void*)k_pull, 148u * CBFS_PULL_MINB, PULL_WARPS * 32, a_s);
-  if (!rc) rc = b_add(g_push, &s1, nullptr, (void*)k_scan_sums, SCAN_BLOCKS, SCAN_THREADS, a_s);
-  if (!rc) rc = b_add(g_push, &s2, &s1, (void*)k_scan_top, 1, 1024, a_s);
-  if (!rc) rc = b_add(g_push, &s3, &s2, (void*)k_scan_apply, SCAN_BLOCKS, SCAN_THREADS, a_s);
-  if (!rc) rc = b_add(g_push, &nq, &s3, (void*)k_push, PUSH_GRID, 256, a_s);
-  if (!rc) rc = b_add(body, &ne, &nif, (void*)k_end, END_GRID, 256, a_wh);
+  rc = b_add(g_pull, &np, nullptr, F.pull, 148u * CBFS_PULL_MINB, PULL_WARPS * 32, a_s);
+  if (!rc) rc = b_add(g_push, &s1, nullptr, F.scan_sums, SCAN_BLOCKS, SCAN_THREADS, a_s);
+  if (!rc) rc = b_add(g_push, &s2, &s1, F.scan_top, 1, 1024, a_s);
+  if (!rc) rc = b_add(g_push, &s3, &s2, F.scan_apply, SCAN_BLOCKS, SCAN_THREADS, a_s);
+  if (!rc) rc = b_add(g_push, &nq, &s3, F.push, PUSH_GRID, 256, a_s);
+  if (!rc) rc = b_add(body, &ne, &nif, F.end, END_GRID, 256, a_wh);
   if (rc) return rc;
   CBFS_CUDA(cudaGraphInstantiate(&w->b_exec[db - 1][wide], g, 0));
   return CBFS_OK;
@@ -1131,7 +1162,11 @@ static int slot_start(Graph* g, Slot* w, const RunArgs& a) {
   CBFS_CUDA(cudaMemsetAsync(w->dist, 0xFF, (uint64_t)n * LANES * sizeof(uint16_t), st));
   CBFS_CUDA(cudaMemsetAsync(w->bstats, 0, LANES * 4 * sizeof(uint64_t), st));
   CBFS_CUDA(cudaMemsetAsync(w->fullm, 0, (uint64_t)(n + 1) * sizeof(uint64_t), st));
-  k_seed<<<(a.nb * 64 + 255) / 256, 256, 0, st>>>(w->bs, w->idx);
+  {
+    BState* S = w->bs;
+    void* args[] = {&S};
+    CBFS_CUDA(cudaLaunchKernel(fns_of(w->idx).seed, dim3((a.nb * 64 + 255) / 256), dim3(256), args, 0, st));
+  }
   CBFS_LAUNCHED();
   CBFS_CUDA(cudaMemcpyAsync(w->bs_h, w->bs, sizeof(BState), cudaMemcpyDeviceToHost, st));
   CBFS_CUDA(cudaEventRecord(w->ready, st));
@@ -1144,30 +1179,27 @@ static int slot_start(Graph* g, Slot* w, const RunArgs& a) {
 static int batched_hostloop(Slot* w) {
   cudaStream_t st = w->s;
   BState* S = w->bs;
-  const int slot = w->idx;
+  const BFns& F = fns_of(w->idx);
   const int db = w->a.dist_bytes;
   const bool wide = w->a.wide > 1;
   unsigned long long flag = 0;
+  cudaGraphConditionalHandle none = 0;
+  void* a_s[] = {&S};
+  void* a_h[] = {&S, &none};
   for (;;) {
-    k_begin<<<1, 32, 0, st>>>(S, slot, 0);
-    if (db == 1) {
-      if (wide) k_fold<1, true><<<FOLD_GRID, 256, 0, st>>>(S, slot);
-      else k_fold<1, false><<<FOLD_GRID, 256, 0, st>>>(S, slot);
-    } else {
-      if (wide) k_fold<2, true><<<FOLD_GRID, 256, 0, st>>>(S, slot);
-      else k_fold<2, false><<<FOLD_GRID, 256, 0, st>>>(S, slot);
-    }
+    CBFS_CUDA(cudaLaunchKernel(F.begin, dim3(1), dim3(32), a_h, 0, st));
+    CBFS_CUDA(cudaLaunchKernel(F.fold[db - 1][wide], dim3(FOLD_GRID), dim3(256), a_s, 0, st));
     CBFS_CUDA(cudaMemcpyAsync(&flag, &S->pull, sizeof(flag), cudaMemcpyDeviceToHost, st));
     CBFS_CUDA(cudaStreamSynchronize(st));
     if (flag) {
-      k_pull<<<148u * CBFS_PULL_MINB, PULL_WARPS * 32, 0, st>>>(S, slot);
+      CBFS_CUDA(cudaLaunchKernel(F.pull, dim3(148u * CBFS_PULL_MINB), dim3(PULL_WARPS * 32), a_s, 0, st));
     } else {
-      k_scan_sums<<<SCAN_BLOCKS, SCAN_THREADS, 0, st>>>(S, slot);
-      k_scan_top<<<1, 1024, 0, st>>>(S, slot);
-      k_scan_apply<<<SCAN_BLOCKS, SCAN_THREADS, 0, st>>>(S, slot);
-      k_push<<<PUSH_GRID, 256, 0, st>>>(S, slot);
+      CBFS_CUDA(cudaLaunchKernel(F.scan_sums, dim3(SCAN_BLOCKS), dim3(SCAN_THREADS), a_s, 0, st));
+      CBFS_CUDA(cudaLaunchKernel(F.scan_top, dim3(1), dim3(1024), a_s, 0, st));
+      CBFS_CUDA(cudaLaunchKernel(F.scan_apply, dim3(SCAN_BLOCKS), dim3(SCAN_THREADS), a_s, 0, st));
+      CBFS_CUDA(cudaLaunchKernel(F.push, dim3(PUSH_GRID), dim3(256), a_s, 0, st));
     }
-    k_end<<<END_GRID, 256, 0, st>>>(S, slot, 0);
+    CBFS_CUDA(cudaLaunchKernel(F.end, dim3(END_GRID), dim3(256), a_h, 0, st));
     CBFS_CUDA(cudaGetLastError());
     CBFS_CUDA(cudaMemcpyAsync(&flag, &S->go, sizeof(flag), cudaMemcpyDeviceToHost, st));
     CBFS_CUDA(cudaStreamSynchronize(st));
@@ -1667,7 +1699,7 @@ int cbfs_release_workspace(int device) {
 }
 
 int cbfs_set_concurrency(int batches) {
-  if (batches < 1 || batches > 16) return fail(CBFS_EINVAL, "concurrency must be 1..16");
+  if (batches < 1 || batches > BS_MAX) return fail(CBFS_EINVAL, "concurrency must be 1..8");
   for (int dv = 0; dv < MAX_DEV; ++dv) {  // re-size the slot sets lazily
     std::lock_guard<std::mutex> lk(g_work_mu[dv]);
     if ((int)g_dev[dv].slots.size() != batches && !g_dev[dv].slots.empty()) {
