@@ -337,6 +337,9 @@ constexpr int FOLD_ILP = CBFS_FOLD_ILP;
 #ifndef CBFS_FOLD_FULL
 #define CBFS_FOLD_FULL 2
 #endif
+#ifndef CBFS_FOLD_PF  // prefetch the next iteration's frontier entries
+#define CBFS_FOLD_PF 0
+#endif
 #ifndef CBFS_FOLD_MINB  // blocks per SM the register budget must allow (0: no bound)
 #define CBFS_FOLD_MINB 4
 #endif
@@ -359,16 +362,35 @@ __device__ __forceinline__ void fold_body(const uint32_t* __restrict__ F, uint32
   const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
   const uint32_t lane = lane_id();
   bool overflow = false;
+#if CBFS_FOLD_PF
+  // the next iteration's frontier entries are loaded before this one's
+  // states, so an iteration waits on one dependent access instead of two
+  uint32_t en[FOLD_ILP];
+#pragma unroll
+  for (int q = 0; q < FOLD_ILP; ++q) {
+    const uint64_t t = tid + q * nth;
+    en[q] = t < nF ? F[t] : 0xFFFFFFFFu;
+  }
+#endif
   for (uint64_t t0 = tid; t0 < nF; t0 += nth * FOLD_ILP) {
     uint32_t e[FOLD_ILP];
     uint64_t nw[FOLD_ILP], sv[FOLD_ILP];
     uint32_t dv[FOLD_ILP];
     uint32_t fvx[FOLD_ILP];  // vertex whose subset of cluster c just became full, else ~0
+#if CBFS_FOLD_PF
+#pragma unroll
+    for (int q = 0; q < FOLD_ILP; ++q) {
+      e[q] = en[q];
+      const uint64_t t = t0 + nth * FOLD_ILP + q * nth;
+      en[q] = t < nF ? F[t] : 0xFFFFFFFFu;
+    }
+#else
 #pragma unroll
     for (int q = 0; q < FOLD_ILP; ++q) {
       const uint64_t t = t0 + q * nth;
       e[q] = t < nF ? F[t] : 0xFFFFFFFFu;
     }
+#endif
 #pragma unroll
     for (int q = 0; q < FOLD_ILP; ++q) {
       if (e[q] != 0xFFFFFFFFu) {
