@@ -338,7 +338,7 @@ constexpr int FOLD_ILP = CBFS_FOLD_ILP;
 #define CBFS_FOLD_FULL 2
 #endif
 #ifndef CBFS_FOLD_PF  // prefetch the next iteration's frontier entries
-#define CBFS_FOLD_PF 0
+#define CBFS_FOLD_PF 1
 #endif
 #ifndef CBFS_FOLD_MINB  // blocks per SM the register budget must allow (0: no bound)
 #define CBFS_FOLD_MINB 4
