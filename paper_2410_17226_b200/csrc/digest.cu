@@ -35,8 +35,17 @@ __device__ __forceinline__ uint64_t dg_fin(uint64_t z) {
 // lane accumulates its two clusters' sums over its rows in registers and adds
 // them to out[] once.  With `clear`, the strip is reset to the unreached state
 // (Delta = sentinel, subsets 0) after it is read (staging reuse).
+constexpr uint32_t DG_MAXP = 4;  // planes held in registers per row (more are streamed)
+#ifndef CBFS_DG_ROWS
+#define CBFS_DG_ROWS 2
+#endif
+#ifndef CBFS_DG_MINB
+#define CBFS_DG_MINB 3
+#endif
+constexpr int DG_ROWS = CBFS_DG_ROWS;  // rows in flight per warp
+
 template <int DB>
-__global__ void __launch_bounds__(256) k_digest(void* __restrict__ dist, uint64_t* __restrict__ masks, uint32_t n,
+__global__ void __launch_bounds__(256, CBFS_DG_MINB) k_digest(void* __restrict__ dist, uint64_t* __restrict__ masks, uint32_t n,
                                                 uint64_t L, uint32_t c0, uint32_t nc, uint32_t planes,
                                                 uint64_t* __restrict__ out, int clear) {
   const uint32_t lane = threadIdx.x & 31;
@@ -48,44 +57,77 @@ __global__ void __launch_bounds__(256) k_digest(void* __restrict__ dist, uint64_
   const uint64_t plane_stride = (uint64_t)n * L;
   uint64_t sa = 0, sb = 0;
   if (ha || hb) {
-    for (uint64_t v = warp; v < n; v += nwarps) {
-      const uint64_t row = v * L;
-      CBFS_DCHECK(!hb || cc < L);
-      uint64_t da = 0xFFFF, db = 0xFFFF;
-      if (DB == 1) {
-        const uint8_t* p = (const uint8_t*)dist + row;
-        if (ha) { const uint8_t x = p[ca]; da = x == 0xFF ? 0xFFFFu : x; }
-        if (hb) { const uint8_t x = p[cc]; db = x == 0xFF ? 0xFFFFu : x; }
-      } else {
-        const uint16_t* p = (const uint16_t*)dist + row;
-        if (ha) da = p[ca];
-        if (hb) db = p[cc];
-      }
-      const uint64_t key = v * 0x9E3779B97F4A7C15ULL + 0xD1B54A32D192ED03ULL;
-      uint64_t xa = dg_fin(key ^ (da << 48)), xb = dg_fin(key ^ (db << 48));
-      for (uint32_t i = 0; i < planes; ++i) {
-        uint64_t* mp = masks + i * plane_stride + row;
-        const uint64_t ma = ha ? mp[ca] : 0, mb = hb ? mp[cc] : 0;
-        xa = dg_fin(xa ^ ma);
-        xb = dg_fin(xb ^ mb);
-        if (clear) {
-          if (ha && ma) mp[ca] = 0;
-          if (hb && mb) mp[cc] = 0;
-        }
-      }
-      if (clear) {
+    // DG_ROWS rows per warp step: all their loads are issued before any hash
+    for (uint64_t v0 = warp; v0 < n; v0 += nwarps * DG_ROWS) {
+      uint64_t da[DG_ROWS], db[DG_ROWS], ma[DG_ROWS][DG_MAXP], mb[DG_ROWS][DG_MAXP];
+#pragma unroll
+      for (int r = 0; r < DG_ROWS; ++r) {
+        const uint64_t v = v0 + r * nwarps;
+        da[r] = db[r] = 0xFFFF;
+        if (v >= n) continue;
+        const uint64_t row = v * L;
+        CBFS_DCHECK(!hb || cc < L);
         if (DB == 1) {
-          uint8_t* p = (uint8_t*)dist + row;
-          if (ha && da != 0xFFFF) p[ca] = 0xFF;
-          if (hb && db != 0xFFFF) p[cc] = 0xFF;
+          const uint8_t* p = (const uint8_t*)dist + row;
+          if (ha) { const uint8_t x = p[ca]; da[r] = x == 0xFF ? 0xFFFFu : x; }
+          if (hb) { const uint8_t x = p[cc]; db[r] = x == 0xFF ? 0xFFFFu : x; }
         } else {
-          uint16_t* p = (uint16_t*)dist + row;
-          if (ha && da != 0xFFFF) p[ca] = 0xFFFF;
-          if (hb && db != 0xFFFF) p[cc] = 0xFFFF;
+          const uint16_t* p = (const uint16_t*)dist + row;
+          if (ha) da[r] = p[ca];
+          if (hb) db[r] = p[cc];
+        }
+#pragma unroll
+        for (uint32_t i = 0; i < DG_MAXP; ++i) {
+          ma[r][i] = mb[r][i] = 0;
+          if (i < planes) {
+            const uint64_t* mp = masks + i * plane_stride + row;
+            if (ha) ma[r][i] = mp[ca];
+            if (hb) mb[r][i] = mp[cc];
+          }
         }
       }
-      sa += xa;
-      sb += xb;
+#pragma unroll
+      for (int r = 0; r < DG_ROWS; ++r) {
+        const uint64_t v = v0 + r * nwarps;
+        if (v >= n) continue;
+        const uint64_t row = v * L;
+        const uint64_t key = v * 0x9E3779B97F4A7C15ULL + 0xD1B54A32D192ED03ULL;
+        uint64_t xa = dg_fin(key ^ (da[r] << 48)), xb = dg_fin(key ^ (db[r] << 48));
+#pragma unroll
+        for (uint32_t i = 0; i < DG_MAXP; ++i) {
+          if (i >= planes) break;
+          uint64_t* mp = masks + i * plane_stride + row;
+          xa = dg_fin(xa ^ ma[r][i]);
+          xb = dg_fin(xb ^ mb[r][i]);
+          if (clear) {
+            if (ha && ma[r][i]) mp[ca] = 0;
+            if (hb && mb[r][i]) mp[cc] = 0;
+          }
+        }
+        for (uint32_t i = DG_MAXP; i < planes; ++i) {  // d > 3: streamed
+          uint64_t* mp = masks + i * plane_stride + row;
+          const uint64_t wa = ha ? mp[ca] : 0, wb = hb ? mp[cc] : 0;
+          xa = dg_fin(xa ^ wa);
+          xb = dg_fin(xb ^ wb);
+          if (clear) {
+            if (ha && wa) mp[ca] = 0;
+            if (hb && wb) mp[cc] = 0;
+          }
+        }
+        if (clear) {
+          if (DB == 1) {
+            uint8_t* p = (uint8_t*)dist + row;
+            if (ha && da[r] != 0xFFFF) p[ca] = 0xFF;
+            if (hb && db[r] != 0xFFFF) p[cc] = 0xFF;
+          } else {
+            uint16_t* p = (uint16_t*)dist + row;
+            if (ha && da[r] != 0xFFFF) p[ca] = 0xFFFF;
+            if (hb && db[r] != 0xFFFF) p[cc] = 0xFFFF;
+          }
+        }
+        sa += xa;
+        sb += xb;
+      }
     }
   }
   if (ha) atomicAdd((unsigned long long*)&out[ca], (unsigned long long)sa);
@@ -128,7 +170,7 @@ static int launch_digest(const void* dist, uint32_t dist_bytes, const uint64_t* 
                          uint32_t nc, uint32_t planes, uint64_t* out, int clear, cudaStream_t st) {
   if (nc == 0 || n == 0) return CBFS_OK;
   const uint32_t strips = (nc + 63) / 64;
-  const unsigned bx = std::max(1u, grid_for((uint64_t)n * 32, 256, 148u * 8u) / std::max(1u, std::min(strips, 8u)));
+  const unsigned bx = std::max(1u, grid_for((uint64_t)n * 32, 256, 148u * CBFS_DG_MINB) / std::max(1u, std::min(strips, 8u)));
   const dim3 grid(bx, strips);
   if (dist_bytes == 1)
     k_digest<1><<<grid, 256, 0, st>>>(const_cast<void*>(dist), const_cast<uint64_t*>(masks), n, L, 0, nc, planes, out,
