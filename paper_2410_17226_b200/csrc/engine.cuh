@@ -72,6 +72,7 @@ struct SpCtl {
   unsigned long long go;     // the round loop continues (set at the end of each round)
   unsigned done;             // blocks of the round's push that finished
   unsigned pad;
+  unsigned long long take[2];  // next unclaimed frontier entry of the round's fold / push (dynamic chunks)
 };
 
 // Device-resident state of a BATCHED-engine slot: the graph and batch
@@ -149,6 +150,7 @@ struct Slot {
   cudaEvent_t sp_t0 = nullptr, sp_t1 = nullptr;  // profiling
   uint32_t sp_db = 0;                             // dist_bytes the graph was built for
   bool sp_fused = false;                          // fold fused into the push (d >= 1)
+  int sp_shape = 0;                               // push shape (SpShape: by the graph's average degree)
   // batched engine (device-side round loop)
   int idx = 0;             // slot index on its device (constant-memory BState mirror c_bs[idx])
   BState* bs = nullptr;    // device

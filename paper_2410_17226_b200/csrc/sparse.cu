@@ -44,7 +44,56 @@ constexpr uint32_t SP_OUTBUF = 256;  // per-warp claim buffer (entries)
 #endif
 constexpr int SP_ILP = CBFS_SP_ILP;  // neighbours per lane in flight (push)
 constexpr int SP_FOLD_ILP = 4;       // frontier entries per lane in flight (fold)
-constexpr unsigned SP_GRID = 148u * CBFS_SP_GRID_PER_SM;
+// CBFS_SP_DYN (default on): the warps of a round kernel take their chunks of
+// the frontier list from a per-round counter (one atomic per chunk) instead of
+// a fixed grid stride, and the grid is one wave of resident blocks — degree
+// skew (k-NN) and uneven chunk costs no longer leave SMs idle at the tail.
+#ifndef CBFS_SP_DYN
+#define CBFS_SP_DYN 1
+#endif
+// Two shapes of the push (measured, configs 4 and 5, 256 clusters): 2
+// frontier entries per lane per warp step at 3 blocks / SM for sparse graphs
+// (average degree < SP_DEG_SPLIT: the grid, 3.8 — a step then still holds ~240
+// arcs), 1 entry per lane at 4 blocks / SM for denser ones (the k-NN graph,
+// 11.5: more resident warps, 13% faster there, 13% slower on the grid).
+constexpr double SP_DEG_SPLIT = 8.0;
+#ifndef CBFS_SP_MINB
+#define CBFS_SP_MINB 3
+#endif
+#ifndef CBFS_SP_EPL
+#define CBFS_SP_EPL 2
+#endif
+template <int V>
+struct SpShape;
+template <>
+struct SpShape<0> {  // low degree
+  static constexpr int EPL = CBFS_SP_EPL, MINB = CBFS_SP_MINB;
+};
+template <>
+struct SpShape<1> {  // average degree >= SP_DEG_SPLIT
+  static constexpr int EPL = 1, MINB = 4;
+};
+static unsigned sp_grid(int minb) { return CBFS_SP_DYN ? 148u * minb : 148u * CBFS_SP_GRID_PER_SM; }
+
+// The warp's next chunk [b, b + step) of the round's list: from the shared
+// counter (dynamic) or by grid stride.
+__device__ __forceinline__ uint64_t sp_next_chunk(unsigned long long* take, uint64_t b, uint64_t step,
+                                                  uint64_t stride) {
+#if CBFS_SP_DYN
+  unsigned long long x = 0;
+  if (lane_id() == 0) x = atomicAdd(take, (unsigned long long)step);
+  return __shfl_sync(FULLW, x, 0);
+#else
+  return b + stride;
+#endif
+}
+__device__ __forceinline__ uint64_t sp_first_chunk(unsigned long long* take, uint64_t warp, uint64_t step) {
+#if CBFS_SP_DYN
+  return sp_next_chunk(take, 0, step, 0);
+#else
+  return warp * step;
+#endif
+}
 
 // ------------------------------------------------------------------ init
 // Per batch: every cell = {S_seen = 0, Delta = inf, P_0 = P_1 = 0} (A2).
@@ -184,7 +233,8 @@ __global__ void __launch_bounds__(SP_THREADS) k_sp_fold(const SpDesc* __restrict
   bool overflow = false;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t b = warp * 32 * SP_FOLD_ILP; b < nF; b += nwarps * 32 * SP_FOLD_ILP) {
+  for (uint64_t b = sp_first_chunk(&ctl->take[0], warp, 32 * SP_FOLD_ILP); b < nF;
+       b = sp_next_chunk(&ctl->take[0], b, 32 * SP_FOLD_ILP, nwarps * 32 * SP_FOLD_ILP)) {
     // SP_FOLD_ILP entries per lane: all their loads are issued before any is used
     uint32_t e[SP_FOLD_ILP];
     ulonglong2 sd[SP_FOLD_ILP];
@@ -267,6 +317,8 @@ __device__ __forceinline__ void sp_round_end(SpCtl* __restrict__ ctl, cudaGraphC
   const unsigned long long nn = v->nF[cur ^ 1];
   v->i = i + 1;
   v->done = 0;
+  v->take[0] = 0;  // every block of this round's kernels has left its chunk loop
+  v->take[1] = 0;
   bool go = nn > 0;
   if (go && i + 1 >= 0xFFFEull) {
     atomicOr(&ctl->err, ERR_ROUNDS);
@@ -289,13 +341,6 @@ __device__ __forceinline__ void sp_round_end(SpCtl* __restrict__ ctl, cudaGraphC
 // entries by a binary search over the warp's degree prefix in shared memory),
 // so every lane keeps several independent memory operations in flight and
 // hubs and degree-4 grid vertices are balanced alike.
-#ifndef CBFS_SP_EPL
-#define CBFS_SP_EPL 2
-#endif
-constexpr int SP_EPL = CBFS_SP_EPL;  // frontier entries per lane per warp step
-#ifndef CBFS_SP_MINB
-#define CBFS_SP_MINB 3
-#endif
 
 //
 // FUSED (d >= 1): the fold of each entry runs in the same thread right before
@@ -307,12 +352,13 @@ constexpr int SP_EPL = CBFS_SP_EPL;  // frontier entries per lane per warp step
 // and an entry whose S_new comes out empty is skipped (no output, statistic
 // or push), so outputs and round statistics are exactly Alg. 1's.  d = 0 uses
 // the separate fold kernel (there the post-fold cap differs).
-template <int DB, bool FUSED>
-__global__ void __launch_bounds__(SP_THREADS, CBFS_SP_MINB) k_sp_push(const SpDesc* __restrict__ D, SpCtl* __restrict__ ctl,
+template <int DB, bool FUSED, int V>
+__global__ void __launch_bounds__(SP_THREADS, SpShape<V>::MINB) k_sp_push(const SpDesc* __restrict__ D, SpCtl* __restrict__ ctl,
                                                         SpCell* __restrict__ cells, uint32_t* __restrict__ list0,
                                                         uint32_t* __restrict__ list1, uint64_t* __restrict__ bstats,
                                                         cudaGraphConditionalHandle hcond) {
-  constexpr int W = 32 * SP_EPL;  // entries per warp step
+  constexpr int SP_EPL = SpShape<V>::EPL;  // frontier entries per lane per warp step
+  constexpr int W = 32 * SP_EPL;           // entries per warp step
   __shared__ unsigned long long sF[FUSED ? LANES : 1], sE[FUSED ? LANES : 1], sM[FUSED ? LANES : 1];
   if (FUSED) {
     for (uint32_t c = threadIdx.x; c < LANES; c += blockDim.x) sF[c] = sE[c] = sM[c] = 0;
@@ -359,7 +405,7 @@ __global__ void __launch_bounds__(SP_THREADS, CBFS_SP_MINB) k_sp_push(const SpDe
   };
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t b = warp * W; b < nF; b += nwarps * W) {
+  for (uint64_t b = sp_first_chunk(&ctl->take[1], warp, W); b < nF; b = sp_next_chunk(&ctl->take[1], b, W, nwarps * W)) {
     // ---- the step's entries: S_new (cleared once read) and neighbour ranges
     uint32_t e[SP_EPL];
     uint64_t nw[SP_EPL], o0[SP_EPL], o1[SP_EPL];
@@ -515,7 +561,15 @@ static int sp_add_kernel(cudaGraph_t body, cudaGraphNode_t* node, const cudaGrap
 // push's last block ends the round).
 // Two graphs per slot would be needed for the two Delta output widths; the
 // fold instance is chosen by dist_bytes when the graph is (re)built.
-static int sp_build(Slot* w, uint32_t dist_bytes, bool fused) {
+// The push instance of (Delta width, fusion, shape).
+static void* sp_push_fn(uint32_t dist_bytes, bool fused, int shape) {
+  if (!fused) return shape ? (void*)k_sp_push<2, false, 1> : (void*)k_sp_push<2, false, 0>;
+  if (dist_bytes == 1) return shape ? (void*)k_sp_push<1, true, 1> : (void*)k_sp_push<1, true, 0>;
+  return shape ? (void*)k_sp_push<2, true, 1> : (void*)k_sp_push<2, true, 0>;
+}
+static int sp_minb(int shape) { return shape ? SpShape<1>::MINB : SpShape<0>::MINB; }
+
+static int sp_build(Slot* w, uint32_t dist_bytes, bool fused, int shape) {
   if (w->sp_exec) {
     CBFS_CUDA(cudaGraphExecDestroy(w->sp_exec));
     w->sp_exec = nullptr;
@@ -547,19 +601,20 @@ static int sp_build(Slot* w, uint32_t dist_bytes, bool fused) {
   cudaGraphNode_t nf, np;
   int rc;
   if (fused) {  // d >= 1: one kernel per round
-    rc = sp_add_kernel(body, &np, nullptr, dist_bytes == 1 ? (void*)k_sp_push<1, true> : (void*)k_sp_push<2, true>,
-                       SP_GRID, SP_THREADS, pa);
+    rc = sp_add_kernel(body, &np, nullptr, sp_push_fn(dist_bytes, true, shape), sp_grid(sp_minb(shape)), SP_THREADS,
+                       pa);
     if (rc) return rc;
   } else {
-    rc = sp_add_kernel(body, &nf, nullptr, dist_bytes == 1 ? (void*)k_sp_fold<1> : (void*)k_sp_fold<2>, SP_GRID,
-                       SP_THREADS, fa);
+    rc = sp_add_kernel(body, &nf, nullptr, dist_bytes == 1 ? (void*)k_sp_fold<1> : (void*)k_sp_fold<2>,
+                       sp_grid(CBFS_SP_MINB), SP_THREADS, fa);
     if (rc) return rc;
-    rc = sp_add_kernel(body, &np, &nf, (void*)k_sp_push<2, false>, SP_GRID, SP_THREADS, pa);
+    rc = sp_add_kernel(body, &np, &nf, sp_push_fn(2, false, shape), sp_grid(sp_minb(shape)), SP_THREADS, pa);
     if (rc) return rc;
   }
   CBFS_CUDA(cudaGraphInstantiate(&w->sp_exec, g, 0));
   w->sp_db = dist_bytes;
   w->sp_fused = fused;
+  w->sp_shape = shape;
   return CBFS_OK;
 }
 
@@ -588,8 +643,9 @@ int sparse_start(const Graph* g, Slot* w, const RunArgs& a) {
   const uint32_t n = g->n;
   cudaStream_t st = w->s;
   const bool fused = a.d >= 1;
-  if (!w->sp_exec || w->sp_db != a.dist_bytes || w->sp_fused != fused) {
-    int rc = sp_build(w, a.dist_bytes, fused);
+  const int shape = g->m >= SP_DEG_SPLIT * (double)n ? 1 : 0;
+  if (!w->sp_exec || w->sp_db != a.dist_bytes || w->sp_fused != fused || w->sp_shape != shape) {
+    int rc = sp_build(w, a.dist_bytes, fused, shape);
     if (rc) return rc;
   }
   SpDesc* h = w->sp_desc_h;  // the slot's previous batch (and its copy) finished before this one starts
@@ -638,19 +694,14 @@ static int sparse_hostloop(Slot* w) {
   CBFS_CUDA(cudaEventRecord(w->sp_t0, st));
   for (;;) {
     SpCell* cells = reinterpret_cast<SpCell*>(w->blk);
-    if (w->sp_fused) {
-      if (w->sp_db == 1)
-        k_sp_push<1, true><<<SP_GRID, SP_THREADS, 0, st>>>(D, ctl, cells, w->listA, w->listB, w->bstats, 0);
-      else
-        k_sp_push<2, true><<<SP_GRID, SP_THREADS, 0, st>>>(D, ctl, cells, w->listA, w->listB, w->bstats, 0);
-    } else {
-      if (w->sp_db == 1)
-        k_sp_fold<1><<<SP_GRID, SP_THREADS, 0, st>>>(D, ctl, cells, w->listA, w->listB, w->bstats);
-      else
-        k_sp_fold<2><<<SP_GRID, SP_THREADS, 0, st>>>(D, ctl, cells, w->listA, w->listB, w->bstats);
-      k_sp_push<2, false><<<SP_GRID, SP_THREADS, 0, st>>>(D, ctl, cells, w->listA, w->listB, w->bstats, 0);
-    }
-    CBFS_CUDA(cudaGetLastError());
+    cudaGraphConditionalHandle h0 = 0;
+    void* pa[] = {&D, &ctl, &cells, &w->listA, &w->listB, &w->bstats, &h0};
+    void* fa[] = {&D, &ctl, &cells, &w->listA, &w->listB, &w->bstats};
+    if (!w->sp_fused)
+      CBFS_CUDA(cudaLaunchKernel(w->sp_db == 1 ? (void*)k_sp_fold<1> : (void*)k_sp_fold<2>, sp_grid(CBFS_SP_MINB),
+                                 SP_THREADS, fa, 0, st));
+    CBFS_CUDA(cudaLaunchKernel(sp_push_fn(w->sp_db, w->sp_fused, w->sp_shape), sp_grid(sp_minb(w->sp_shape)),
+                               SP_THREADS, pa, 0, st));
     CBFS_CUDA(cudaMemcpyAsync(w->sp_ctl_h, ctl, sizeof(SpCtl), cudaMemcpyDeviceToHost, st));
     CBFS_CUDA(cudaStreamSynchronize(st));
     if (!w->sp_ctl_h->go) break;
