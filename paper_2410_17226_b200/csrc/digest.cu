@@ -35,6 +35,9 @@ __device__ __forceinline__ uint64_t dg_fin(uint64_t z) {
 // lane accumulates its two clusters' sums over its rows in registers and adds
 // them to out[] once.  With `clear`, the strip is reset to the unreached state
 // (Delta = sentinel, subsets 0) after it is read (staging reuse).
+#ifndef CBFS_DIGEST_INTERNAL
+#define CBFS_DIGEST_INTERNAL 0
+#endif
 constexpr uint32_t DG_MAXP = 4;  // planes held in registers per row (more are streamed)
 #ifndef CBFS_DG_ROWS
 #define CBFS_DG_ROWS 2
@@ -47,7 +50,8 @@ constexpr int DG_ROWS = CBFS_DG_ROWS;  // rows in flight per warp
 template <int DB>
 __global__ void __launch_bounds__(256, CBFS_DG_MINB) k_digest(void* __restrict__ dist, uint64_t* __restrict__ masks, uint32_t n,
                                                 uint64_t L, uint32_t c0, uint32_t nc, uint32_t planes,
-                                                uint64_t* __restrict__ out, int clear) {
+                                                uint64_t* __restrict__ out, int clear,
+                                                const uint32_t* __restrict__ perm) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t cb = c0 + 64 * blockIdx.y;  // this block's strip
   const uint32_t ca = cb + 2 * lane, cc = ca + 1;
@@ -91,7 +95,8 @@ __global__ void __launch_bounds__(256, CBFS_DG_MINB) k_digest(void* __restrict__
         const uint64_t v = v0 + r * nwarps;
         if (v >= n) continue;
         const uint64_t row = v * L;
-        const uint64_t key = v * 0x9E3779B97F4A7C15ULL + 0xD1B54A32D192ED03ULL;
+        const uint64_t vo = perm ? perm[v] : v;  // internal-id rows: the digest keys original ids
+        const uint64_t key = vo * 0x9E3779B97F4A7C15ULL + 0xD1B54A32D192ED03ULL;
         uint64_t xa = dg_fin(key ^ (da[r] << 48)), xb = dg_fin(key ^ (db[r] << 48));
 #pragma unroll
         for (uint32_t i = 0; i < DG_MAXP; ++i) {
@@ -139,14 +144,16 @@ __global__ void __launch_bounds__(256, CBFS_DG_MINB) k_digest(void* __restrict__
 // Delta (u16) at [c][v], subset i at [i][64][v].  Block row y = cluster c,
 // thread per vertex, block-reduced sum added once per block.
 __global__ void __launch_bounds__(256) k_digest_cm(uint16_t* __restrict__ dist, uint64_t* __restrict__ masks,
-                                                   uint32_t n, uint32_t planes, uint64_t* __restrict__ out) {
+                                                   uint32_t n, uint32_t planes, uint64_t* __restrict__ out,
+                                                   const uint32_t* __restrict__ perm) {
   __shared__ unsigned long long s_sum[8];
   const uint32_t c = blockIdx.y;
   uint16_t* dc = dist + (uint64_t)c * n;
   uint64_t sum = 0;
   for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t dv = dc[v];
-    uint64_t x = dg_fin((v * 0x9E3779B97F4A7C15ULL + 0xD1B54A32D192ED03ULL) ^ (dv << 48));
+    const uint64_t vo = perm ? perm[v] : v;
+    uint64_t x = dg_fin((vo * 0x9E3779B97F4A7C15ULL + 0xD1B54A32D192ED03ULL) ^ (dv << 48));
     for (uint32_t i = 0; i < planes; ++i) {
       uint64_t* mp = masks + ((uint64_t)i * LANES + c) * n + v;
       const uint64_t m = *mp;
@@ -167,17 +174,18 @@ __global__ void __launch_bounds__(256) k_digest_cm(uint16_t* __restrict__ dist, 
 }
 
 static int launch_digest(const void* dist, uint32_t dist_bytes, const uint64_t* masks, uint32_t n, uint64_t L,
-                         uint32_t nc, uint32_t planes, uint64_t* out, int clear, cudaStream_t st) {
+                         uint32_t nc, uint32_t planes, uint64_t* out, int clear, const uint32_t* perm,
+                         cudaStream_t st) {
   if (nc == 0 || n == 0) return CBFS_OK;
   const uint32_t strips = (nc + 63) / 64;
   const unsigned bx = std::max(1u, grid_for((uint64_t)n * 32, 256, 148u * CBFS_DG_MINB) / std::max(1u, std::min(strips, 8u)));
   const dim3 grid(bx, strips);
   if (dist_bytes == 1)
     k_digest<1><<<grid, 256, 0, st>>>(const_cast<void*>(dist), const_cast<uint64_t*>(masks), n, L, 0, nc, planes, out,
-                                      clear);
+                                      clear, perm);
   else
     k_digest<2><<<grid, 256, 0, st>>>(const_cast<void*>(dist), const_cast<uint64_t*>(masks), n, L, 0, nc, planes, out,
-                                      clear);
+                                      clear, perm);
   CBFS_LAUNCHED();
   return CBFS_OK;
 }
@@ -190,6 +198,7 @@ struct DigestSource : ArraySource {
   std::vector<void*> sd;
   std::vector<uint64_t*> sm;
   bool cmajor = false;  // sparse engine: cluster-major staging, u16 Delta (sd sized for u16)
+  const uint32_t* perm = nullptr;  // staging rows are internal ids; the digest keys perm[v]
   int bind(RunArgs& a, int slot, cudaStream_t) override {
     if (sd.empty()) return CBFS_OK;  // statistics only (cbfs_run_rounds)
     a.out_dist = sd[slot];
@@ -200,10 +209,10 @@ struct DigestSource : ArraySource {
     return CBFS_OK;
   }
   int launch(const RunArgs& a, int slot, uint64_t* out, cudaStream_t st) {
-    if (!cmajor) return launch_digest(sd[slot], dist_bytes, sm[slot], n, LANES, a.nb, planes, out, 1, st);
+    if (!cmajor) return launch_digest(sd[slot], dist_bytes, sm[slot], n, LANES, a.nb, planes, out, 1, perm, st);
     if (n == 0 || a.nb == 0) return CBFS_OK;
     const dim3 grid(std::max(1u, grid_for(n, 256, 148u * 8u) / std::max(1u, a.nb / 8u)), a.nb);
-    k_digest_cm<<<grid, 256, 0, st>>>(reinterpret_cast<uint16_t*>(sd[slot]), sm[slot], n, planes, out);
+    k_digest_cm<<<grid, 256, 0, st>>>(reinterpret_cast<uint16_t*>(sd[slot]), sm[slot], n, planes, out, perm);
     CBFS_LAUNCHED();
     return CBFS_OK;
   }
@@ -246,7 +255,7 @@ int cbfs_digest_store(uint32_t n, uint32_t C, uint32_t planes, const void* dist,
   cudaStream_t st = (cudaStream_t)stream;
   if (C == 0) return CBFS_OK;
   CBFS_CUDA(cudaMemsetAsync(out_digest, 0, sizeof(uint64_t) * C, st));
-  int rc = launch_digest(dist, dist_bytes, masks, n, C, C, planes, out_digest, 0, st);
+  int rc = launch_digest(dist, dist_bytes, masks, n, C, C, planes, out_digest, 0, nullptr, st);
   if (rc) return rc;
   CBFS_CUDA(cudaStreamSynchronize(st));
   return CBFS_OK;
@@ -275,6 +284,10 @@ static int run_consumed(Graph* g, const uint32_t* sources, const uint8_t* sizes,
   src.proto.C = n_clusters;
   src.proto.direction = direction;
   src.proto.engine = engine;
+  // outputs staged by internal id: the fold's writes follow the traversal
+  // (no dependent perm[v] load per entry); the digest maps rows back
+  src.proto.out_internal = CBFS_DIGEST_INTERNAL;
+  src.perm = CBFS_DIGEST_INTERNAL ? g->perm : nullptr;
   src.sources = sources;
   src.sizes = sizes;
   src.n_clusters = n_clusters;

@@ -222,13 +222,10 @@ __global__ void __launch_bounds__(SP_THREADS) k_sp_fold(const SpDesc* __restrict
   const uint32_t cur = i & 1;
   const uint32_t* __restrict__ L = cur ? list1 : list0;
   const uint64_t nF = ctl->nF[cur];
-  const uint32_t n = D->n, planes = D->planes;
-  const uint64_t C = D->C, cbase = D->cbase;
+  const uint32_t n = D->n;
   const uint64_t* __restrict__ off = D->off;
-  const uint32_t* __restrict__ perm = D->perm;
   void* __restrict__ out_dist = D->out_dist;
   void* __restrict__ out_masks = D->out_masks;
-  const uint32_t mb = D->mask_bytes;
   const uint32_t lane = lane_id();
   bool overflow = false;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
