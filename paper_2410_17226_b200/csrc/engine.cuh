@@ -62,6 +62,9 @@ struct SpDesc {
   uint32_t out_cmajor;       // outputs cluster-major (RunArgs::out_cmajor)
   uint64_t* rounds;          // [nb][max_rounds][2] per-round {|F_i|, E_i}, or null
   uint32_t max_rounds;
+  uint32_t nw32;             // words per cluster of the ordered frontier bitmap (ceil(n / 32))
+  uint32_t* bits;            // ordered frontier bitmap [nb][nw32] (null: list frontiers only)
+  uint64_t bm_min;           // |F_{i+1}| from which round i+1's claims go to the bitmap
 };
 // Round state of a sparse-engine batch (device-resident).
 struct SpCtl {
@@ -73,6 +76,8 @@ struct SpCtl {
   unsigned done;             // blocks of the round's push that finished
   unsigned pad;
   unsigned long long take[2];  // next unclaimed frontier entry of the round's fold / push (dynamic chunks)
+  unsigned long long bm;       // the next round's push records its claims in the ordered bitmap (sparse.cu)
+  unsigned long long bm_fill;  // append cursor of the bitmap -> list compaction
 };
 
 // Device-resident state of a BATCHED-engine slot: the graph and batch
@@ -151,6 +156,9 @@ struct Slot {
   uint32_t sp_db = 0;                             // dist_bytes the graph was built for
   bool sp_fused = false;                          // fold fused into the push (d >= 1)
   int sp_shape = 0;                               // push shape (SpShape: by the graph's average degree)
+  bool sp_ordered = false;                        // graph built with the ordered-frontier branch
+  uint32_t* sp_bits = nullptr;                    // ordered frontier bitmap [LANES][nw32 * 32 bits]
+  uint64_t sp_bits_words = 0;
   // batched engine (device-side round loop)
   int idx = 0;             // slot index on its device (constant-memory BState mirror c_bs[idx])
   BState* bs = nullptr;    // device

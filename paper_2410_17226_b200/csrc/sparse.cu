@@ -299,7 +299,21 @@ __global__ void __launch_bounds__(SP_THREADS) k_sp_fold(const SpDesc* __restrict
 // End of round i, run by the last block of the push to finish (no separate
 // tail kernel): F_i is consumed, i advances, and the graph's WHILE node
 // repeats while F_{i+1} is non-empty (Alg. 1's loop).
-__device__ __forceinline__ void sp_round_end(SpCtl* __restrict__ ctl, cudaGraphConditionalHandle h) {
+// Ordered frontiers (CBFS_SP_ORDER, default on): when F_i is large (>=
+// SpDesc::bm_min entries) the push of round i records its claims as bits of a
+// cluster-major bitmap instead of appending them to the list in claim order,
+// and a compaction kernel turns the bitmap into F_{i+1} sorted by (cluster,
+// vertex) runs — the next round's pushes then walk each cluster's band in id
+// order, so the neighbour cells they read and OR share L2 lines instead of
+// arriving in scattered order.  Which entries F_{i+1} holds is unchanged
+// (each claim is the unique 0 -> non-zero transition of P_{i+1}), only their
+// order, and every consumer of a frontier is order-independent.
+#ifndef CBFS_SP_ORDER
+#define CBFS_SP_ORDER 1
+#endif
+
+__device__ __forceinline__ void sp_round_end(SpCtl* __restrict__ ctl, cudaGraphConditionalHandle h,
+                                             cudaGraphConditionalHandle h_bm, uint64_t bm_min) {
   __syncthreads();
   if (threadIdx.x != 0) return;
   __threadfence();
@@ -322,7 +336,55 @@ __device__ __forceinline__ void sp_round_end(SpCtl* __restrict__ ctl, cudaGraphC
     go = false;
   }
   v->go = go;
+  v->bm_fill = 0;
+  const bool bm = bm_min && nn >= bm_min;  // the claim target of round i + 1
+  v->bm = bm ? 1 : 0;
   if (h) cudaGraphSetConditional(h, go ? 1u : 0u);  // h == 0: host-driven loop (profiling mode)
+  if (h_bm) cudaGraphSetConditional(h_bm, bm ? 1u : 0u);
+}
+
+// Bitmap -> list F_{i+1} (after round i's push, which advanced ctl->i): warp
+// per 32 consecutive bitmap words, entries appended as one run per warp in
+// (cluster, vertex) order; the words are cleared (the bitmap is zero between
+// rounds).
+__global__ void __launch_bounds__(256) k_sp_compact(const SpDesc* __restrict__ D, SpCtl* __restrict__ ctl,
+                                                    uint32_t* __restrict__ list0, uint32_t* __restrict__ list1) {
+  const uint32_t nw32 = D->nw32;
+  const uint64_t words = (uint64_t)D->nb * nw32;
+  uint32_t* __restrict__ bits = D->bits;
+  uint32_t* __restrict__ Ln = (ctl->i & 1) ? list1 : list0;  // ctl->i is already i + 1
+  const uint32_t lane = lane_id();
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t w0 = warp * 32; w0 < words; w0 += nwarps * 32) {
+    const uint64_t wi = w0 + lane;
+    uint32_t x = 0;
+    if (wi < words) {
+      x = bits[wi];
+      if (x) bits[wi] = 0;
+    }
+    const uint32_t k = __popc(x);
+    uint32_t inc = k;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULLW, inc, o);
+      if (lane >= (uint32_t)o) inc += y;
+    }
+    const uint32_t tot = __shfl_sync(FULLW, inc, 31);
+    if (!tot) continue;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(&ctl->bm_fill, (unsigned long long)tot);
+    base = __shfl_sync(FULLW, base, 0) + (inc - k);
+    if (x) {
+      const uint32_t c = (uint32_t)(wi / nw32), v0 = (uint32_t)(wi - (uint64_t)c * nw32) * 32;
+      while (x) {
+        const uint32_t b = __ffs(x) - 1;
+        x &= x - 1;
+        CBFS_DCHECK(v0 + b < D->n && c < LANES);
+        Ln[base++] = (c << VBITS) | (v0 + b);
+      }
+    }
+  }
 }
 
 // ------------------------------------------------------------------ push
@@ -349,11 +411,12 @@ __device__ __forceinline__ void sp_round_end(SpCtl* __restrict__ ctl, cudaGraphC
 // and an entry whose S_new comes out empty is skipped (no output, statistic
 // or push), so outputs and round statistics are exactly Alg. 1's.  d = 0 uses
 // the separate fold kernel (there the post-fold cap differs).
-template <int DB, bool FUSED, int V>
+template <int DB, bool FUSED, int V, bool BM>
 __global__ void __launch_bounds__(SP_THREADS, SpShape<V>::MINB) k_sp_push(const SpDesc* __restrict__ D, SpCtl* __restrict__ ctl,
                                                         SpCell* __restrict__ cells, uint32_t* __restrict__ list0,
                                                         uint32_t* __restrict__ list1, uint64_t* __restrict__ bstats,
-                                                        cudaGraphConditionalHandle hcond) {
+                                                        cudaGraphConditionalHandle hcond,
+                                                        cudaGraphConditionalHandle hbm) {
   constexpr int SP_EPL = SpShape<V>::EPL;  // frontier entries per lane per warp step
   constexpr int W = 32 * SP_EPL;           // entries per warp step
   __shared__ unsigned long long sF[FUSED ? LANES : 1], sE[FUSED ? LANES : 1], sM[FUSED ? LANES : 1];
@@ -385,8 +448,17 @@ __global__ void __launch_bounds__(SP_THREADS, SpShape<V>::MINB) k_sp_push(const 
   const unsigned lt = (1u << lane) - 1;
   uint32_t* obuf = s_out[wib];
   uint32_t nout = 0;
+  constexpr bool bm = BM;  // this round's claims go to the ordered bitmap
   auto emit = [&](bool claim, uint32_t val) {
     const unsigned m = __ballot_sync(FULLW, claim);
+    if (bm) {  // nout counts the warp's bitmap claims (added to F_{i+1}'s size at the end)
+      if (claim) {
+        const uint32_t c = val >> VBITS, u = val & VMASK;
+        atomicOr(&D->bits[(uint64_t)c * D->nw32 + (u >> 5)], 1u << (u & 31));
+      }
+      nout += __popc(m);
+      return;
+    }
     if (claim) obuf[nout + __popc(m & lt)] = val;
     nout += __popc(m);
     if (nout > SP_OUTBUF - 32) {
@@ -520,6 +592,10 @@ __global__ void __launch_bounds__(SP_THREADS, SpShape<V>::MINB) k_sp_push(const 
     __syncwarp();
   }
   __syncwarp();
+  if (bm) {
+    if (lane == 0 && nout) atomicAdd(cnt, (unsigned long long)nout);
+    nout = 0;
+  }
   if (nout) {
     unsigned long long base = 0;
     if (lane == 0) base = atomicAdd(cnt, (unsigned long long)nout);
@@ -538,7 +614,7 @@ __global__ void __launch_bounds__(SP_THREADS, SpShape<V>::MINB) k_sp_push(const 
       sp_round_record(D, c, i, sF[c], sE[c]);
     }
   }
-  sp_round_end(ctl, hcond);
+  sp_round_end(ctl, hcond, hbm, D->bm_min);
 }
 
 // ------------------------------------------------------------------ host
@@ -558,15 +634,21 @@ static int sp_add_kernel(cudaGraph_t body, cudaGraphNode_t* node, const cudaGrap
 // push's last block ends the round).
 // Two graphs per slot would be needed for the two Delta output widths; the
 // fold instance is chosen by dist_bytes when the graph is (re)built.
-// The push instance of (Delta width, fusion, shape).
-static void* sp_push_fn(uint32_t dist_bytes, bool fused, int shape) {
-  if (!fused) return shape ? (void*)k_sp_push<2, false, 1> : (void*)k_sp_push<2, false, 0>;
-  if (dist_bytes == 1) return shape ? (void*)k_sp_push<1, true, 1> : (void*)k_sp_push<1, true, 0>;
-  return shape ? (void*)k_sp_push<2, true, 1> : (void*)k_sp_push<2, true, 0>;
+// The push instance of (Delta width, fusion, shape, ordered claims).
+template <bool BM>
+static void* sp_push_fn_bm(uint32_t dist_bytes, bool fused, int shape) {
+  if (!fused) return shape ? (void*)k_sp_push<2, false, 1, BM> : (void*)k_sp_push<2, false, 0, BM>;
+  if (dist_bytes == 1) return shape ? (void*)k_sp_push<1, true, 1, BM> : (void*)k_sp_push<1, true, 0, BM>;
+  return shape ? (void*)k_sp_push<2, true, 1, BM> : (void*)k_sp_push<2, true, 0, BM>;
+}
+static void* sp_push_fn(uint32_t dist_bytes, bool fused, int shape, bool bm) {
+  return bm ? sp_push_fn_bm<true>(dist_bytes, fused, shape) : sp_push_fn_bm<false>(dist_bytes, fused, shape);
 }
 static int sp_minb(int shape) { return shape ? SpShape<1>::MINB : SpShape<0>::MINB; }
 
-static int sp_build(Slot* w, uint32_t dist_bytes, bool fused, int shape) {
+constexpr unsigned SP_COMPACT_GRID = 148u * 8u;
+
+static int sp_build(Slot* w, uint32_t dist_bytes, bool fused, int shape, bool ordered) {
   if (w->sp_exec) {
     CBFS_CUDA(cudaGraphExecDestroy(w->sp_exec));
     w->sp_exec = nullptr;
@@ -578,8 +660,10 @@ static int sp_build(Slot* w, uint32_t dist_bytes, bool fused, int shape) {
   cudaGraph_t g;
   CBFS_CUDA(cudaGraphCreate(&g, 0));
   w->sp_graph = g;
-  cudaGraphConditionalHandle h;
+  cudaGraphConditionalHandle h, hc = 0;  // hc == 0: no ordered-frontier branch (the push sets no IF handle)
   CBFS_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+  if (ordered)  // round 0 claims into the list
+    CBFS_CUDA(cudaGraphConditionalHandleCreate(&hc, g, 0, cudaGraphCondAssignDefault));
   cudaGraphNodeParams cp = {};
   cp.type = cudaGraphNodeTypeConditional;
   cp.conditional.handle = h;
@@ -594,24 +678,41 @@ static int sp_build(Slot* w, uint32_t dist_bytes, bool fused, int shape) {
   uint32_t* l0 = w->listA;
   uint32_t* l1 = w->listB;
   void* fa[] = {&D, &ctl, &cells, &l0, &l1, &w->bstats};
-  void* pa[] = {&D, &ctl, &cells, &l0, &l1, &w->bstats, &h};
-  cudaGraphNode_t nf, np;
+  void* pa[] = {&D, &ctl, &cells, &l0, &l1, &w->bstats, &h, &hc};
+  void* ca[] = {&D, &ctl, &l0, &l1};
+  cudaGraphNode_t nf, ni, np1, nc, np0;
   int rc;
-  if (fused) {  // d >= 1: one kernel per round
-    rc = sp_add_kernel(body, &np, nullptr, sp_push_fn(dist_bytes, true, shape), sp_grid(sp_minb(shape)), SP_THREADS,
-                       pa);
-    if (rc) return rc;
-  } else {
+  if (!fused) {  // d = 0: the fold is its own kernel
     rc = sp_add_kernel(body, &nf, nullptr, dist_bytes == 1 ? (void*)k_sp_fold<1> : (void*)k_sp_fold<2>,
                        sp_grid(CBFS_SP_MINB), SP_THREADS, fa);
     if (rc) return rc;
-    rc = sp_add_kernel(body, &np, &nf, sp_push_fn(2, false, shape), sp_grid(sp_minb(shape)), SP_THREADS, pa);
+  }
+  const uint32_t pdb = fused ? dist_bytes : 2;
+  if (!ordered) {  // list frontiers only: the push alone
+    rc = sp_add_kernel(body, &np0, fused ? nullptr : &nf, sp_push_fn(pdb, fused, shape, false),
+                       sp_grid(sp_minb(shape)), SP_THREADS, pa);
+    if (rc) return rc;
+  } else {  // IF (round i's claims go to the ordered bitmap) { push; compact into F_{i+1} } ELSE { push }
+    cudaGraphNodeParams ip = {};
+    ip.type = cudaGraphNodeTypeConditional;
+    ip.conditional.handle = hc;
+    ip.conditional.type = cudaGraphCondTypeIf;
+    ip.conditional.size = 2;
+    CBFS_CUDA(cudaGraphAddNode(&ni, body, fused ? nullptr : &nf, fused ? 0 : 1, &ip));
+    cudaGraph_t g_bm = ip.conditional.phGraph_out[0], g_list = ip.conditional.phGraph_out[1];
+    rc = sp_add_kernel(g_bm, &np1, nullptr, sp_push_fn(pdb, fused, shape, true), sp_grid(sp_minb(shape)),
+                       SP_THREADS, pa);
+    if (!rc) rc = sp_add_kernel(g_bm, &nc, &np1, (void*)k_sp_compact, SP_COMPACT_GRID, 256, ca);
+    if (!rc)
+      rc = sp_add_kernel(g_list, &np0, nullptr, sp_push_fn(pdb, fused, shape, false), sp_grid(sp_minb(shape)),
+                         SP_THREADS, pa);
     if (rc) return rc;
   }
   CBFS_CUDA(cudaGraphInstantiate(&w->sp_exec, g, 0));
   w->sp_db = dist_bytes;
   w->sp_fused = fused;
   w->sp_shape = shape;
+  w->sp_ordered = ordered;
   return CBFS_OK;
 }
 
@@ -634,6 +735,7 @@ void sparse_free(Slot* w) {
   cudaFreeHost(w->sp_ctl_h);
   if (w->sp_t0) cudaEventDestroy(w->sp_t0);
   if (w->sp_t1) cudaEventDestroy(w->sp_t1);
+  if (w->sp_bits) cudaFree(w->sp_bits);
 }
 
 int sparse_start(const Graph* g, Slot* w, const RunArgs& a) {
@@ -641,8 +743,16 @@ int sparse_start(const Graph* g, Slot* w, const RunArgs& a) {
   cudaStream_t st = w->s;
   const bool fused = a.d >= 1;
   const int shape = g->m >= SP_DEG_SPLIT * (double)n ? 1 : 0;
-  if (!w->sp_exec || w->sp_db != a.dist_bytes || w->sp_fused != fused || w->sp_shape != shape) {
-    int rc = sp_build(w, a.dist_bytes, fused, shape);
+  // ordered frontiers for the denser shape only: on low-degree graphs (the
+  // grid: thousands of small rounds) the compaction never pays (measured at
+  // every threshold) and the IF node alone costs ~1%
+  static const long long bm_env = getenv("CBFS_SP_BM_MIN") ? atoll(getenv("CBFS_SP_BM_MIN")) : -1;
+  const uint64_t bm_min = bm_env >= 0 ? (uint64_t)bm_env
+                                      : (CBFS_SP_ORDER && shape == 1 ? std::max<uint64_t>(n / 4, 1u << 16) : 0);
+  const bool ordered = bm_min != 0;
+  if (!w->sp_exec || w->sp_db != a.dist_bytes || w->sp_fused != fused || w->sp_shape != shape ||
+      w->sp_ordered != ordered) {
+    int rc = sp_build(w, a.dist_bytes, fused, shape, ordered);
     if (rc) return rc;
   }
   SpDesc* h = w->sp_desc_h;  // the slot's previous batch (and its copy) finished before this one starts
@@ -666,6 +776,19 @@ int sparse_start(const Graph* g, Slot* w, const RunArgs& a) {
   h->out_cmajor = a.out_cmajor;
   h->rounds = a.out_rounds;
   h->max_rounds = a.out_rounds ? a.max_rounds : 0;
+  // the ordered-frontier bitmap (zero between rounds; sized for this graph)
+  h->nw32 = (n + 31) / 32;
+  const uint64_t words = (uint64_t)LANES * h->nw32;
+  if (bm_min && w->sp_bits_words < words) {
+    if (w->sp_bits) CBFS_CUDA(cudaFree(w->sp_bits));
+    w->sp_bits = nullptr;
+    w->sp_bits_words = 0;
+    CBFS_CUDA(cudaMalloc(&w->sp_bits, words * sizeof(uint32_t)));
+    CBFS_CUDA(cudaMemsetAsync(w->sp_bits, 0, words * sizeof(uint32_t), st));
+    w->sp_bits_words = words;
+  }
+  h->bits = bm_min ? w->sp_bits : nullptr;
+  h->bm_min = bm_min;
   CBFS_CUDA(cudaMemcpyAsync(w->sp_desc, h, sizeof(SpDesc), cudaMemcpyHostToDevice, st));
   const uint64_t ncell = (uint64_t)n * LANES;
   k_sp_init<<<grid_for(ncell, 256, 148u * 16u), 256, 0, st>>>(reinterpret_cast<SpCell*>(w->blk), ncell);
@@ -689,18 +812,23 @@ static int sparse_hostloop(Slot* w) {
   SpDesc* D = w->sp_desc;
   SpCtl* ctl = w->sp_ctl;
   CBFS_CUDA(cudaEventRecord(w->sp_t0, st));
+  bool bm_next = false;  // round 0 claims into the list (as the graph's IF handle default)
   for (;;) {
     SpCell* cells = reinterpret_cast<SpCell*>(w->blk);
     cudaGraphConditionalHandle h0 = 0;
-    void* pa[] = {&D, &ctl, &cells, &w->listA, &w->listB, &w->bstats, &h0};
+    void* pa[] = {&D, &ctl, &cells, &w->listA, &w->listB, &w->bstats, &h0, &h0};
+    void* ca[] = {&D, &ctl, &w->listA, &w->listB};
     void* fa[] = {&D, &ctl, &cells, &w->listA, &w->listB, &w->bstats};
     if (!w->sp_fused)
       CBFS_CUDA(cudaLaunchKernel(w->sp_db == 1 ? (void*)k_sp_fold<1> : (void*)k_sp_fold<2>, sp_grid(CBFS_SP_MINB),
                                  SP_THREADS, fa, 0, st));
-    CBFS_CUDA(cudaLaunchKernel(sp_push_fn(w->sp_db, w->sp_fused, w->sp_shape), sp_grid(sp_minb(w->sp_shape)),
-                               SP_THREADS, pa, 0, st));
+    const bool bm = bm_next;
+    CBFS_CUDA(cudaLaunchKernel(sp_push_fn(w->sp_fused ? w->sp_db : 2, w->sp_fused, w->sp_shape, bm),
+                               sp_grid(sp_minb(w->sp_shape)), SP_THREADS, pa, 0, st));
+    if (bm) CBFS_CUDA(cudaLaunchKernel((void*)k_sp_compact, SP_COMPACT_GRID, 256, ca, 0, st));
     CBFS_CUDA(cudaMemcpyAsync(w->sp_ctl_h, ctl, sizeof(SpCtl), cudaMemcpyDeviceToHost, st));
     CBFS_CUDA(cudaStreamSynchronize(st));
+    bm_next = w->sp_ctl_h->bm != 0;
     if (!w->sp_ctl_h->go) break;
   }
   CBFS_CUDA(cudaEventRecord(w->sp_t1, st));
