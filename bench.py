@@ -368,7 +368,7 @@ def run_ours(args, world, rank, local):
     strong = args.scaling == "strong"
     r_total, first, C = shard(C_cfg, world, rank, strong)  # C = this rank's clusters
     policy = cb.CBFS_ROOT_RANDOM if cfg["root"] == "random" else cb.CBFS_ROOT_DEGREE
-    relabel = cfg.get("relabel", "none")
+    relabel = args.relabel or cfg.get("relabel", "none")
     rflags = cb.Graph.relabel_flags(relabel)
     dist_bytes = 1 if cfg["kind"] in ("rmat", "er") else 2
     planes = d + 1
@@ -679,6 +679,8 @@ def main():
                     help="strong: the config's clusters split over the ranks; weak: C clusters per rank")
     ap.add_argument("--mode", default="", choices=["", "full", "digest", "query"], help="override the config's mode")
     ap.add_argument("--clusters", type=int, default=0, help="clusters per GPU (default: the config's)")
+    ap.add_argument("--relabel", default="", choices=["", "none", "degree", "locality"],
+                    help="override the config's internal vertex order (outputs are in original ids either way)")
     ap.add_argument("--queries", type=int, default=0, help="queries (query mode; default: the config's)")
     args = ap.parse_args()
     world, rank, local = dist_init()

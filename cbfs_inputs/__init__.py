@@ -137,7 +137,7 @@ CONFIGS = {
     "c3_rmat24": dict(kind="rmat", scale=24, ef=32, abc=(0.6, 0.15, 0.15), seed=3, clusters=4096, k=64, d=2,
                       root="degree", root_seed=0, relabel="degree"),
     "c4_grid": dict(kind="grid", side=4096, p_delete=0.05, p_diag=0.001, seed=4, clusters=512, k=64, d=4,
-                    root="random", root_seed=4, relabel="none"),
+                    root="random", root_seed=4, relabel="locality"),
     "c5_knn": dict(kind="knn", n=10_000_000, knn=10, seed=7, clusters=8192, k=64, d=6, root="degree",
                    root_seed=0, queries=10_000_000, query_seed=7, relabel="locality"),
 }

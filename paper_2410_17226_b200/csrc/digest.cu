@@ -35,8 +35,12 @@ __device__ __forceinline__ uint64_t dg_fin(uint64_t z) {
 // lane accumulates its two clusters' sums over its rows in registers and adds
 // them to out[] once.  With `clear`, the strip is reset to the unreached state
 // (Delta = sentinel, subsets 0) after it is read (staging reuse).
+// Staging rows by internal id (the fold's writes follow the traversal's
+// vertex order; the digest keys perm[v]): 0 never, 1 always, 2 (default) for
+// the sparse engine only — measured: batched engine on config 3 slower
+// (fold +45 ms, consume +57 ms per step), see profiles/r02_*.
 #ifndef CBFS_DIGEST_INTERNAL
-#define CBFS_DIGEST_INTERNAL 0
+#define CBFS_DIGEST_INTERNAL 2
 #endif
 constexpr uint32_t DG_MAXP = 4;  // planes held in registers per row (more are streamed)
 #ifndef CBFS_DG_ROWS
@@ -286,8 +290,9 @@ static int run_consumed(Graph* g, const uint32_t* sources, const uint8_t* sizes,
   src.proto.engine = engine;
   // outputs staged by internal id: the fold's writes follow the traversal
   // (no dependent perm[v] load per entry); the digest maps rows back
-  src.proto.out_internal = CBFS_DIGEST_INTERNAL;
-  src.perm = CBFS_DIGEST_INTERNAL ? g->perm : nullptr;
+  const bool internal = CBFS_DIGEST_INTERNAL == 1 || (CBFS_DIGEST_INTERNAL == 2 && cmajor);
+  src.proto.out_internal = internal;
+  src.perm = internal ? g->perm : nullptr;
   src.sources = sources;
   src.sizes = sizes;
   src.n_clusters = n_clusters;
