@@ -453,6 +453,16 @@ int cbfs_set_engine(int engine);
  * gathered with an L2 evict_last hint, every other row and the CSR columns
  * with evict_first.  Default 131,072 rows (64 MiB of 512-byte rows). */
 int cbfs_set_pull_hub_rows(uint32_t rows);
+/* Sparse-engine frontier order (outputs never change): a round whose
+ * frontier F_i holds >= min_entries entries records its claims in a
+ * cluster-major bitmap that is compacted into F_{i+1} in (cluster, vertex)
+ * order, so the next round's pushes read neighbour cells in id order; smaller
+ * rounds append claims to the list in claim order.  min_entries = -1
+ * (default): max(n / 4, 65,536) on graphs of average degree >= 8, never on
+ * sparser ones (the grid's thousands of small rounds do not repay the
+ * compaction); 0: never; k > 0: from k entries on, every graph.  Takes effect
+ * at the next batch.  Errors: EINVAL (min_entries < -1). */
+int cbfs_set_sparse_order(int64_t min_entries);
 
 /* Free the device's cached traversal workspace (the batch slots; the next
  * traversal re-allocates them).  Errors: EINVAL (device out of range). */

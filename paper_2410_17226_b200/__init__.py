@@ -87,6 +87,7 @@ _sig("cbfs_budget_clusters", [_u64, _u32, _u32, _u32, ctypes.POINTER(_u64)])
 _sig("cbfs_set_direction_alpha", [ctypes.c_double])
 _sig("cbfs_set_concurrency", [_i32])
 _sig("cbfs_set_pull_hub_rows", [_u32])
+_sig("cbfs_set_sparse_order", [ctypes.c_int64])
 _sig("cbfs_release_workspace", [_i32])
 _sig("cbfs_set_engine", [_i32])
 _sig("cbfs_profile_enable", [_i32])
@@ -359,6 +360,10 @@ def cbfs_release_workspace(device: int = 0):
 
 def cbfs_set_pull_hub_rows(rows: int):
     _check(_lib.cbfs_set_pull_hub_rows(rows))
+
+
+def cbfs_set_sparse_order(min_entries: int):
+    _check(_lib.cbfs_set_sparse_order(min_entries))
 
 
 def cbfs_set_concurrency(batches: int):

@@ -30,6 +30,9 @@
 namespace cbfs {
 
 int g_engine_policy = CBFS_ENGINE_AUTO;
+// ordered-frontier threshold (cbfs_set_sparse_order): -1 = default, else the
+// |F_i| from which claims go to the bitmap (0 = never); env CBFS_SP_BM_MIN
+long long g_sp_order_min = getenv("CBFS_SP_BM_MIN") ? atoll(getenv("CBFS_SP_BM_MIN")) : -1;
 
 constexpr uint32_t VBITS = 26;  // list entry = c << 26 | v  (n <= CBFS_MAX_N = 2^26 - 1: never all-ones)
 constexpr uint32_t VMASK = (1u << VBITS) - 1;
@@ -746,8 +749,8 @@ int sparse_start(const Graph* g, Slot* w, const RunArgs& a) {
   // ordered frontiers for the denser shape only: on low-degree graphs (the
   // grid: thousands of small rounds) the compaction never pays (measured at
   // every threshold) and the IF node alone costs ~1%
-  static const long long bm_env = getenv("CBFS_SP_BM_MIN") ? atoll(getenv("CBFS_SP_BM_MIN")) : -1;
-  const uint64_t bm_min = bm_env >= 0 ? (uint64_t)bm_env
+  const long long bm_set = g_sp_order_min;
+  const uint64_t bm_min = bm_set >= 0 ? (uint64_t)bm_set
                                       : (CBFS_SP_ORDER && shape == 1 ? std::max<uint64_t>(n / 4, 1u << 16) : 0);
   const bool ordered = bm_min != 0;
   if (!w->sp_exec || w->sp_db != a.dist_bytes || w->sp_fused != fused || w->sp_shape != shape ||
@@ -930,6 +933,12 @@ int choose_engine(Graph* g, uint32_t direction) {
 }
 
 }  // namespace cbfs
+
+extern "C" int cbfs_set_sparse_order(int64_t min_entries) {
+  if (min_entries < -1) return cbfs::fail(CBFS_EINVAL, "min_entries must be >= -1");
+  cbfs::g_sp_order_min = min_entries;
+  return CBFS_OK;
+}
 
 extern "C" int cbfs_set_engine(int engine) {
   if (engine < CBFS_ENGINE_AUTO || engine > CBFS_ENGINE_SPARSE) return cbfs::fail(CBFS_EINVAL, "bad engine");

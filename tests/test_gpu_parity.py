@@ -204,6 +204,32 @@ def test_pull_hint_threshold_parity(seed):
 
 
 @pytest.mark.parametrize("seed", range(6))
+def test_sparse_ordered_frontier_parity(seed):
+    """The sparse engine's ordered frontiers (claims through the bitmap, F_{i+1}
+    compacted in (cluster, vertex) order) change only the order of frontier
+    entries: outputs equal the oracle's with the bitmap used on every round
+    (threshold 1), on every round of >= 64 entries, and never — on low- and
+    high-degree graphs (both push shapes), d = 0 (separate fold) included."""
+    rng = np.random.default_rng(5200 + seed)
+    kind = ["er", "rmat", "grid", "path", "er", "grid"][seed]
+    el = random_el(seed + 300, int(rng.integers(800, 3000)), kind)
+    ref = orc.csr_from_edgelist(el)
+    d = [0, 1, 2, 3, 4, 6][seed]
+    src, sz = ball_clusters(ref, rng, [5, 33, 64, 70, 40, 64][seed], d, [1, 7, 64][seed % 3] if d else 1)
+    g = gpu_graph(el, relabel=[False, True, "locality"][seed % 3])
+    cb.cbfs_set_engine(cb.CBFS_ENGINE_SPARSE)
+    try:
+        for thr in (1, 64, 0):
+            cb.cbfs_set_sparse_order(thr)
+            compare_many(g, ref, src, sz, d)
+    finally:
+        cb.cbfs_set_sparse_order(-1)
+        cb.cbfs_set_engine(cb.CBFS_ENGINE_AUTO)
+    with pytest.raises(cb.CbfsError):
+        cb.cbfs_set_sparse_order(-2)
+
+
+@pytest.mark.parametrize("seed", range(6))
 def test_diameter_exceeds_d_parity(seed):
     """R9: clusters whose diameter exceeds d still give Alg. 1's output exactly,
     in every direction mode."""
