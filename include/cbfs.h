@@ -113,6 +113,12 @@ int cbfs_graph_info(const cbfs_graph* g, uint32_t* n, uint64_t* m, uint32_t* max
  * offsets [n+1] uint64, cols [m] uint32. Synchronises. */
 int cbfs_graph_export_csr(const cbfs_graph* g, uint64_t* offsets, uint32_t* cols);
 
+/* Copy the internal vertex order to a host buffer: out_perm[x] = the original
+ * id of internal vertex x ([n] uint32; the identity without relabelling).
+ * Inspection only — every output of the library is in original ids.
+ * Synchronises.  Errors: EINVAL (null argument). */
+int cbfs_graph_internal_order(const cbfs_graph* g, uint32_t* out_perm);
+
 int cbfs_graph_destroy(cbfs_graph* g);
 
 /* --------------------------------------------------------------- selection

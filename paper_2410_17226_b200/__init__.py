@@ -48,6 +48,7 @@ _sig("cbfs_graph_create", [_u32, _vp, _vp, _u64, _u32, _i32, _vp, ctypes.POINTER
 _sig("cbfs_graph_create_csr", [_u32, _vp, _vp, _u64, _u32, _i32, _vp, ctypes.POINTER(_vp)])
 _sig("cbfs_graph_info", [_vp, ctypes.POINTER(_u32), ctypes.POINTER(_u64), ctypes.POINTER(_u32)])
 _sig("cbfs_graph_export_csr", [_vp, _vp, _vp])
+_sig("cbfs_graph_internal_order", [_vp, _vp])
 _sig("cbfs_graph_destroy", [_vp])
 _sig("cbfs_select_clusters", [_vp, _u32, _u32, _u32, _u32, _u64, _vp, _vp, ctypes.POINTER(_u32), _vp])
 _sig("cbfs_select_clusters_wide", [_vp, _u32, _u32, _u32, _u32, _u64, _u32, _vp, _vp, ctypes.POINTER(_u32), _vp])
@@ -162,6 +163,13 @@ def cbfs_graph_export_csr(h):
     cols = np.empty(max(m, 1), np.uint32)
     _check(_lib.cbfs_graph_export_csr(h, _ptr(off), _ptr(cols)))
     return off, cols[:m]
+
+
+def cbfs_graph_internal_order(h):
+    n, _, _ = cbfs_graph_info(h)
+    perm = np.empty(max(n, 1), np.uint32)
+    _check(_lib.cbfs_graph_internal_order(h, _ptr(perm)))
+    return perm[:n]
 
 
 def cbfs_graph_destroy(h):

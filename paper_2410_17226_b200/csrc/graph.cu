@@ -6,6 +6,7 @@
 // vertices by (degree desc, original id asc), rebuild the CSR in that order
 // (hubs get small ids, so their vertex-major rows share cache lines and L2
 // sets).  The rank array used by cluster selection is the same order.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <mutex>
@@ -136,36 +137,137 @@ __global__ void k_relabel_keys(const uint64_t* __restrict__ arcs, uint64_t m, co
 // Cuthill-McKee-like BFS order.  Level L+1 is sorted by (smallest position of
 // a parent in level L, original id), so vertices near each other in the graph
 // get nearby ids and a cluster's wavefront touches contiguous state.
-__global__ void k_bfsord_expand(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cols,
-                                const uint32_t* __restrict__ order, uint32_t lo, uint32_t hi,
-                                const uint32_t* __restrict__ pos, uint32_t* __restrict__ key,
-                                uint32_t* __restrict__ flag, uint64_t* __restrict__ next,
-                                unsigned long long* __restrict__ cnt) {
-  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < hi - lo;
-       t += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t p = lo + (uint32_t)t, u = order[p];
-    for (uint64_t a = off[u]; a < off[u + 1]; ++a) {
-      const uint32_t v = cols[a];
-      if (pos[v] != 0xFFFFFFFFu) continue;
-      atomicMin(&key[v], p);
-      if (atomicCAS(&flag[v], 0u, 1u) == 0u) next[atomicAdd(cnt, 1ULL)] = v;
+__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+// Every BFS level runs inside one cooperative kernel (no host round trip
+// and no sort per level; config 4's 4096^2 grid has ~6,000 BFS levels):
+// (1) every unplaced neighbour v of the level's parents (positions p in
+// [lo, hi)) gets key[v] = min p; (2) each warp owns a contiguous run of
+// parents and counts, 32 parents at a time, the neighbours whose key is that
+// parent — a parent's children are its own adjacency (sorted by id) filtered
+// by key, so the level's (key, id) order needs no sort — and warp / block /
+// grid prefix sums give each warp its first position; (3) the warp places its
+// parents' children in (parent, id) order.  Three grid barriers per level.
+constexpr int BO_THREADS = 256, BO_WARPS = BO_THREADS / 32;
+
+__device__ __forceinline__ uint32_t bo_children(const uint64_t* __restrict__ off, const uint32_t* __restrict__ cols,
+                                                const uint32_t* __restrict__ perm, const uint32_t* __restrict__ pos,
+                                                const uint32_t* __restrict__ key, uint64_t p) {
+  const uint32_t u = __ldcg(&perm[p]);
+  uint32_t c = 0;
+  for (uint64_t a = __ldg(&off[u]), e = __ldg(&off[u + 1]); a < e; ++a) {
+    const uint32_t v = __ldg(&cols[a]);
+    c += (__ldcg(&pos[v]) == 0xFFFFFFFFu && __ldcg(&key[v]) == (uint32_t)p) ? 1u : 0u;
+  }
+  return c;
+}
+
+__global__ void __launch_bounds__(BO_THREADS) k_bfsord_coop(const uint64_t* __restrict__ off,
+                                                            const uint32_t* __restrict__ cols, uint32_t* __restrict__ perm,
+                                                            uint32_t* __restrict__ pos, uint32_t* __restrict__ key,
+                                                            unsigned long long* __restrict__ blk,
+                                                            uint32_t* __restrict__ out_hi) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ unsigned long long s_w[BO_WARPS];
+  __shared__ unsigned long long s_red[BO_THREADS];
+  __shared__ unsigned long long s_base, s_total;
+  const uint32_t nb = gridDim.x, b = blockIdx.x, t = threadIdx.x, lane = t & 31, wib = t >> 5;
+  const uint64_t nw = (uint64_t)nb * BO_WARPS, w = (uint64_t)b * BO_WARPS + wib;
+  const uint64_t nth = (uint64_t)nb * BO_THREADS, tid = (uint64_t)b * BO_THREADS + t;
+  uint32_t lo = 0, hi = 1;
+  while (lo < hi) {
+    const uint64_t np = hi - lo;
+    // (1) keys, thread per parent
+    for (uint64_t p = lo + tid; p < hi; p += nth) {
+      const uint32_t u = __ldcg(&perm[p]);
+      for (uint64_t a = __ldg(&off[u]), e = __ldg(&off[u + 1]); a < e; ++a) {
+        const uint32_t v = __ldg(&cols[a]);
+        if (__ldcg(&pos[v]) == 0xFFFFFFFFu) atomicMin(&key[v], (uint32_t)p);
+      }
     }
+    grid.sync();
+    // (2) the warp's run of parents [wp0, wp1), children counted 32 parents at a time
+    const uint64_t per_w = (np + nw - 1) / nw;
+    const uint64_t wp0 = lo + umin64(np, w * per_w), wp1 = lo + umin64(np, (w + 1) * per_w);
+    unsigned long long wsum = 0;
+    for (uint64_t c0 = wp0; c0 < wp1; c0 += 32) {
+      const uint64_t p = c0 + lane;
+      const uint32_t c = p < wp1 ? bo_children(off, cols, perm, pos, key, p) : 0u;
+      uint32_t cs = c;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) cs += __shfl_xor_sync(0xFFFFFFFFu, cs, o);
+      wsum += cs;
+    }
+    if (lane == 0) s_w[wib] = wsum;
+    __syncthreads();
+    if (t == 0) {
+      unsigned long long x = 0;
+      for (int k = 0; k < BO_WARPS; ++k) {
+        const unsigned long long y = s_w[k];
+        s_w[k] = x;  // exclusive prefix of the block's warps
+        x += y;
+      }
+      blk[b] = x;
+    }
+    grid.sync();
+    {  // this block's base and the level's total (block-parallel sums of the block totals)
+      unsigned long long base = 0, tot = 0;
+      for (uint32_t k = t; k < nb; k += BO_THREADS) {
+        const unsigned long long x = __ldcg(&blk[k]);
+        if (k < b) base += x;
+        tot += x;
+      }
+      s_red[t] = base;
+      __syncthreads();
+      for (uint32_t o = BO_THREADS / 2; o > 0; o >>= 1) {
+        if (t < o) s_red[t] += s_red[t + o];
+        __syncthreads();
+      }
+      if (t == 0) s_base = s_red[0];
+      __syncthreads();
+      s_red[t] = tot;
+      __syncthreads();
+      for (uint32_t o = BO_THREADS / 2; o > 0; o >>= 1) {
+        if (t < o) s_red[t] += s_red[t + o];
+        __syncthreads();
+      }
+      if (t == 0) s_total = s_red[0];
+      __syncthreads();
+    }
+    // (3) place, 32 parents at a time: lane offsets by a warp scan of the counts
+    unsigned long long q = hi + s_base + s_w[wib];
+    for (uint64_t c0 = wp0; c0 < wp1; c0 += 32) {
+      const uint64_t p = c0 + lane;
+      const uint32_t c = p < wp1 ? bo_children(off, cols, perm, pos, key, p) : 0u;
+      uint32_t inc = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+        if (lane >= (uint32_t)o) inc += y;
+      }
+      if (c) {
+        uint64_t r = q + inc - c;
+        const uint32_t u = __ldcg(&perm[p]);
+        for (uint64_t a = __ldg(&off[u]), e = __ldg(&off[u + 1]); a < e; ++a) {
+          const uint32_t v = __ldg(&cols[a]);
+          if (__ldcg(&pos[v]) == 0xFFFFFFFFu && __ldcg(&key[v]) == (uint32_t)p) {
+            perm[r] = v;
+            pos[v] = (uint32_t)r;
+            ++r;
+          }
+        }
+      }
+      q += __shfl_sync(0xFFFFFFFFu, inc, 31);
+    }
+    const uint32_t total = (uint32_t)s_total;
+    grid.sync();
+    lo = hi;
+    hi += total;
   }
+  if (b == 0 && t == 0) *out_hi = hi;
 }
-__global__ void k_bfsord_keys(uint64_t* __restrict__ next, uint64_t c, const uint32_t* __restrict__ key) {
-  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < c; t += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t v = (uint32_t)next[t];
-    next[t] = ((uint64_t)key[v] << 32) | v;
-  }
-}
-__global__ void k_bfsord_place(const uint64_t* __restrict__ sorted, uint64_t c, uint32_t base,
-                               uint32_t* __restrict__ order, uint32_t* __restrict__ pos) {
-  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < c; t += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t v = (uint32_t)sorted[t];
-    order[base + t] = v;
-    pos[v] = base + (uint32_t)t;
-  }
-}
+
 // vertices the BFS did not reach (other components), appended in id order
 __global__ void k_bfsord_flags(const uint32_t* __restrict__ pos, uint32_t n, uint32_t* __restrict__ f) {
   for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x)
@@ -284,47 +386,33 @@ int graph_free(Graph* g) {
 // perm (internal -> original) = the locality order from `root`, inv = its inverse
 static int locality_order(const uint64_t* off, const uint32_t* cols, uint32_t n, uint32_t root, cudaStream_t st,
                           uint32_t* perm, uint32_t* inv) {
-  uint32_t *key = nullptr, *flag = nullptr;
-  uint64_t *next = nullptr, *alt = nullptr;
-  unsigned long long *cnt = nullptr, *hcnt = nullptr;
+  uint32_t *key = nullptr, *flag = nullptr, *d_hi = nullptr, *h_hi = nullptr;
+  unsigned long long* blk = nullptr;
+  int dev = 0, nsm = 0, per_sm = 0;
+  CBFS_CUDA(cudaGetDevice(&dev));
+  CBFS_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  CBFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bfsord_coop, BO_THREADS, 0));
+  // four blocks per SM (4,736 warps): enough for the large levels (k-NN),
+  // few enough that the three grid barriers per level stay cheap (the grid's
+  // ~6,000 levels)
+  const unsigned grid = (unsigned)std::max(1, nsm * std::min(4, std::max(1, per_sm)));
   CBFS_CUDA(cudaMallocAsync(&key, sizeof(uint32_t) * n, st));
   CBFS_CUDA(cudaMallocAsync(&flag, sizeof(uint32_t) * n, st));
-  CBFS_CUDA(cudaMallocAsync(&next, sizeof(uint64_t) * n, st));
-  CBFS_CUDA(cudaMallocAsync(&alt, sizeof(uint64_t) * n, st));
-  CBFS_CUDA(cudaMallocAsync(&cnt, sizeof(unsigned long long), st));
-  CBFS_CUDA(cudaMallocHost(&hcnt, sizeof(unsigned long long)));
+  CBFS_CUDA(cudaMallocAsync(&blk, sizeof(unsigned long long) * grid, st));
+  CBFS_CUDA(cudaMallocAsync(&d_hi, sizeof(uint32_t), st));
+  CBFS_CUDA(cudaMallocHost(&h_hi, sizeof(uint32_t)));
   CBFS_CUDA(cudaMemsetAsync(inv, 0xFF, sizeof(uint32_t) * n, st));  // pos = inv
   CBFS_CUDA(cudaMemsetAsync(key, 0xFF, sizeof(uint32_t) * n, st));
-  CBFS_CUDA(cudaMemsetAsync(flag, 0, sizeof(uint32_t) * n, st));
   const uint32_t zero = 0;
   CBFS_CUDA(cudaMemcpyAsync(perm, &root, sizeof(uint32_t), cudaMemcpyHostToDevice, st));
   CBFS_CUDA(cudaMemcpyAsync(inv + root, &zero, sizeof(uint32_t), cudaMemcpyHostToDevice, st));
-  CBFS_CUDA(cudaMemsetAsync(flag + root, 1, 1, st));
-  size_t tb = 0;
-  cub::DoubleBuffer<uint64_t> probe(next, alt);
-  CBFS_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, probe, (uint64_t)n, 0, 64, st));
-  void* tmp = nullptr;
-  CBFS_CUDA(cudaMallocAsync(&tmp, tb ? tb : 1, st));
-  uint32_t lo = 0, hi = 1;
-  while (hi > lo) {
-    CBFS_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st));
-    k_bfsord_expand<<<grid_for(hi - lo, 256), 256, 0, st>>>(off, cols, perm, lo, hi, inv, key, flag, next, cnt);
-    CBFS_LAUNCHED();
-    CBFS_CUDA(cudaMemcpyAsync(hcnt, cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    CBFS_CUDA(cudaStreamSynchronize(st));
-    const uint64_t c = *hcnt;
-    if (c) {
-      k_bfsord_keys<<<grid_for(c, 256), 256, 0, st>>>(next, c, key);
-      CBFS_LAUNCHED();
-      cub::DoubleBuffer<uint64_t> db(next, alt);
-      CBFS_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, db, c, 0, 64, st));
-      count_launch(8);
-      k_bfsord_place<<<grid_for(c, 256), 256, 0, st>>>(db.Current(), c, hi, perm, inv);
-      CBFS_LAUNCHED();
-    }
-    lo = hi;
-    hi = hi + (uint32_t)c;
-  }
+  uint32_t* pos = inv;
+  void* args[] = {(void*)&off, (void*)&cols, (void*)&perm, (void*)&pos, (void*)&key, (void*)&blk, (void*)&d_hi};
+  CBFS_CUDA(cudaLaunchCooperativeKernel((void*)k_bfsord_coop, grid, BO_THREADS, args, 0, st));
+  CBFS_LAUNCHED();
+  CBFS_CUDA(cudaMemcpyAsync(h_hi, d_hi, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  CBFS_CUDA(cudaStreamSynchronize(st));
+  const uint32_t hi = *h_hi;
   if (hi < n) {  // unreached vertices (other components, isolated) in id order
     uint32_t *f = key, *x = flag;  // reuse as scratch
     k_bfsord_flags<<<grid_for(n, 256), 256, 0, st>>>(inv, n, f);
@@ -339,14 +427,12 @@ static int locality_order(const uint64_t* off, const uint32_t* cols, uint32_t n,
     CBFS_LAUNCHED();
     CBFS_CUDA(cudaFreeAsync(stmp, st));
   }
-  CBFS_CUDA(cudaFreeAsync(tmp, st));
   CBFS_CUDA(cudaFreeAsync(key, st));
   CBFS_CUDA(cudaFreeAsync(flag, st));
-  CBFS_CUDA(cudaFreeAsync(next, st));
-  CBFS_CUDA(cudaFreeAsync(alt, st));
-  CBFS_CUDA(cudaFreeAsync(cnt, st));
+  CBFS_CUDA(cudaFreeAsync(blk, st));
+  CBFS_CUDA(cudaFreeAsync(d_hi, st));
   CBFS_CUDA(cudaStreamSynchronize(st));
-  CBFS_CUDA(cudaFreeHost(hcnt));
+  CBFS_CUDA(cudaFreeHost(h_hi));
   return CBFS_OK;
 }
 
@@ -586,6 +672,19 @@ int cbfs_graph_export_csr(const cbfs_graph* gh, uint64_t* offsets, uint32_t* col
   CBFS_CUDA(cudaSetDevice(g->device));
   CBFS_CUDA(cudaMemcpy(offsets, g->off_orig, sizeof(uint64_t) * (g->n + 1ULL), cudaMemcpyDeviceToHost));
   if (g->m) CBFS_CUDA(cudaMemcpy(cols, g->cols_orig, sizeof(uint32_t) * g->m, cudaMemcpyDeviceToHost));
+  return CBFS_OK;
+}
+
+int cbfs_graph_internal_order(const cbfs_graph* gh, uint32_t* out_perm) {
+  const Graph* g = reinterpret_cast<const Graph*>(gh);
+  if (!g || (g->n && !out_perm)) return fail(CBFS_EINVAL, "null argument");
+  if (g->n == 0) return CBFS_OK;
+  CBFS_CUDA(cudaSetDevice(g->device));
+  if (!g->perm) {
+    for (uint32_t x = 0; x < g->n; ++x) out_perm[x] = x;
+    return CBFS_OK;
+  }
+  CBFS_CUDA(cudaMemcpy(out_perm, g->perm, sizeof(uint32_t) * g->n, cudaMemcpyDeviceToHost));
   return CBFS_OK;
 }
 

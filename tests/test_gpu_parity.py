@@ -89,6 +89,60 @@ def test_csr_build_parity(case, relabel):
     assert g.max_degree == (int(ref.degrees().max()) if ref.n else 0)
 
 
+def _locality_order_ref(ref):
+    """The documented CBFS_RELABEL_LOCALITY order (include/cbfs.h), written out:
+    BFS from the highest-degree vertex (ties: smallest id); level L+1 sorted by
+    (smallest position of a parent in level L, id); unreached vertices
+    appended in id order.  Internal position -> original id."""
+    n = ref.n
+    deg = np.diff(ref.off.astype(np.int64))
+    root = int(np.lexsort((np.arange(n), -deg))[0])
+    pos = np.full(n, -1, np.int64)
+    order = [root]
+    pos[root] = 0
+    lo, hi = 0, 1
+    while hi > lo:
+        key = {}
+        for p in range(lo, hi):
+            u = order[p]
+            for v in ref.cols[ref.off[u]:ref.off[u + 1]]:
+                v = int(v)
+                if pos[v] < 0 and v not in key:
+                    key[v] = p
+        nxt = sorted(key, key=lambda v: (key[v], v))
+        for v in nxt:
+            pos[v] = len(order)
+            order.append(v)
+        lo, hi = hi, len(order)
+    order += [v for v in range(n) if pos[v] < 0]
+    return np.array(order, np.uint32)
+
+
+@pytest.mark.parametrize("case", ["grid", "er", "path", "rmat", "two", "knn"])
+def test_locality_order_definition(case):
+    """The locality relabel (one cooperative kernel over all BFS levels) gives
+    exactly the documented order — several components, hubs and long paths
+    (thousands of levels) included."""
+    if case == "two":  # two components + isolated vertices
+        a = random_el(11, 900, "grid")
+        s_ = np.concatenate([a.src, a.src + a.n]).astype(np.uint32)
+        t_ = np.concatenate([a.dst, a.dst + a.n]).astype(np.uint32)
+        el = ci.EdgeList(2 * a.n + 5, s_, t_)
+    elif case == "path":
+        el = random_el(12, 4000, "path")
+    elif case == "knn":
+        el = ci.knn3d(20000, 10, seed=14)
+    else:
+        el = random_el(13, 2500, case)
+    ref = orc.csr_from_edgelist(el)
+    g = gpu_graph(el, relabel="locality")
+    assert np.array_equal(cb.cbfs_graph_internal_order(g.h), _locality_order_ref(ref))
+    off, cols = g.export_csr()
+    assert np.array_equal(off, ref.off) and np.array_equal(cols, ref.cols)
+    g0 = gpu_graph(el, relabel=False)
+    assert np.array_equal(cb.cbfs_graph_internal_order(g0.h), np.arange(el.n, dtype=np.uint32))
+
+
 def test_csr_build_from_device_and_csr_input():
     el = random_el(9, 2000, "er")
     ref = orc.csr_from_edgelist(el)
