@@ -3,7 +3,8 @@ initcheck): every kernel family of libcbfs.so on config-1-sized inputs.
 
     compute-sanitizer --tool memcheck python tools/sanitize_cases.py
 
-Covers: CSR build (+ degree / locality relabel), selection, the batched
+Covers: CSR build (+ degree / locality relabel, the latter's cooperative
+kernel), selection, the sparse engine's ordered frontiers, the batched
 engine in push / pull / auto, the sparse engine (fused fold+push, d >= 1, and
 the separate fold, d = 0), wide clusters, the output digest consumer, the
 per-round statistics, labels + query + streaming query, the Appendix B
@@ -36,6 +37,8 @@ def main():
     g = cb.Graph.from_edges(el.n, el.src, el.dst, relabel=True)
     gl = cb.Graph.from_edges(el.n, el.src, el.dst, relabel="locality")
     gg = cb.Graph.from_edges(grid.n, grid.src, grid.dst)
+    kn = ci.knn3d(3000, 10, seed=5)
+    gk = cb.Graph.from_edges(kn.n, kn.src, kn.dst, relabel="locality")
     src, sz = g.select_clusters(8, 64, 2, cb.CBFS_ROOT_RANDOM, 1)
     C = len(sz)
     for direction, tag in ((cb.CBFS_DIR_PUSH, "push"), (cb.CBFS_DIR_PULL, "pull"), (cb.CBFS_DIR_AUTO, "auto")):
@@ -50,6 +53,13 @@ def main():
     dig4 = torch.zeros(len(gsz), dtype=torch.int64, device=DEV)
     case("sparse digest (cluster-major staging)", lambda: cb.cbfs_run_digest(gg.h, gsrc, gsz, len(gsz), 4, 2, 5, dig4))
     case("sparse locality graph", lambda: gl.run(*gl.select_clusters(8, 64, 2), 2))
+    cb.cbfs_set_sparse_order(1)  # ordered frontiers (bitmap claims + compaction) on every round
+    case("sparse ordered frontiers d=4", lambda: gg.run(gsrc, gsz, 4))
+    case("sparse ordered frontiers d=0", lambda: gg.run(one, torch.ones_like(gsz), 0))
+    case("sparse ordered frontiers, k-NN", lambda: gk.run(*gk.select_clusters(8, 64, 2), 2))
+    cb.cbfs_set_sparse_order(-1)
+    case("locality order (cooperative kernel), grid",
+         lambda: cb.cbfs_graph_internal_order(cb.Graph.from_edges(grid.n, grid.src, grid.dst, relabel="locality").h))
     cb.cbfs_set_engine(cb.CBFS_ENGINE_AUTO)
     dig = torch.zeros(C, dtype=torch.int64, device=DEV)
     case("digest consumer", lambda: cb.cbfs_run_digest(g.h, src, sz, C, 2, 1, 3, dig))
