@@ -26,7 +26,9 @@ its 10M pairs over the clusters it covers, min-merged chunk by chunk
 their histogram and 100,000 sampled answers once every covered cluster is in
 (`clusters` in the .npz: the streaming index over that selection prefix; the
 oracle needs ~38 s per config-5 cluster per core with the 10M queries, so the
-golden covers the first 1,024 of the 8,192 clusters).
+answers cover the first 1,024 of the 8,192 clusters).  The other config-5
+clusters get stats + digest lines without the queries (`--no-queries`,
+`--range A:B` to split the run over hosts; lines may arrive out of order).
 """
 from __future__ import annotations
 
@@ -80,6 +82,9 @@ def main():
     ap.add_argument("--sample", type=int, default=0, help="clusters to compute (0 = all)")
     ap.add_argument("--threads", type=int, default=os.cpu_count() or 1)
     ap.add_argument("--chunk", type=int, default=0, help="clusters per oracle call (default 2 x threads)")
+    ap.add_argument("--range", default="", help="A:B — only clusters [A, B) of the order (split a long run)")
+    ap.add_argument("--no-queries", action="store_true",
+                    help="config 5: stats + digests only (clusters beyond the answers' prefix)")
     args = ap.parse_args()
     name = args.config
     cfg = ci.CONFIGS[name]
@@ -107,9 +112,12 @@ def main():
     else:
         first = json.loads(open(path).readline()[2:])
         assert first["selection_sha256"] == sha, "golden file belongs to another selection"
+    if args.range:
+        lo_, hi_ = (int(x) for x in args.range.split(":"))
+        order = order[lo_:hi_]
     todo = [c for c in order if c not in done]
     print(f"[{name}] {C} clusters, {len(done)} done, {len(todo)} to do", flush=True)
-    if name == "c5_knn":
+    if name == "c5_knn" and not args.no_queries:
         run_c5(g, src, sz, d, cfg, todo, path, args.threads, chunk, order)
         return
     for i in range(0, len(todo), chunk):
