@@ -165,6 +165,16 @@ def test_c4_whole_config_golden():
     assert got == C == 512
 
 
+@pytest.mark.timeout(900)
+def test_c5_whole_config_golden_digests():
+    """Config 5: every cluster of the selection through cbfs_run_digest (the
+    sparse engine with ordered frontiers, full vectors staged and consumed) —
+    stats and full-vector digest of every cluster the golden holds (the query
+    prefix plus the clusters generated with --no-queries)."""
+    got, C = check_digest_config("c5_knn")
+    assert got >= 1024 and C == 8192
+
+
 @pytest.mark.timeout(1800)
 def test_c5_full_size_golden_queries():
     """Config 5 at full size (10M-point k-NN graph, d = 6): the whole
