@@ -620,6 +620,10 @@ __global__ void __launch_bounds__(256) k_push(BState* __restrict__ S) {
 #define CBFS_PULL_MINB 8
 #endif
 constexpr int PULL_MLP = CBFS_PULL_MLP;  // neighbour rows in flight per warp
+#ifndef CBFS_PULL_PA
+#define CBFS_PULL_PA 2
+#endif
+constexpr int PULL_PA = CBFS_PULL_PA;  // pass-A 32-arc steps whose loads are in flight together
 #ifndef CBFS_PULL_WARPS
 #define CBFS_PULL_WARPS 4
 #endif
@@ -756,6 +760,47 @@ __device__ __forceinline__ void pull_body(
         cnt[lane] = 0;
         __syncwarp();
         uint32_t nl = 0;
+#if CBFS_PULL_PA > 1
+        // pass A in groups of PULL_PA 32-arc steps: the group's column loads,
+        // then its union-frontier word loads, are issued before any is used
+        // (two dependent round trips per group instead of two per step)
+        for (uint64_t wg = e; wg < ge; wg += 32 * PULL_PA) {
+          uint32_t uq[PULL_PA], bq[PULL_PA], jq[PULL_PA];
+#pragma unroll
+          for (int k = 0; k < PULL_PA; ++k) {
+            const uint64_t a = wg + 32 * k + lane;
+            const bool inr = a < ge;
+#if CBFS_PULL_HINT
+            uq[k] = inr ? ld_u32_hint(cols + a, pol_first) : 0u;
+#else
+            uq[k] = inr ? cols[a] : 0u;
+#endif
+            uint32_t jv = 0;  // largest j < nv with ob_j <= a
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+              const uint32_t cand = jv + step;
+              const uint64_t oc = __shfl_sync(FULLW, ob, cand & 31);
+              if (cand < nv && oc <= a) jv = cand;
+            }
+            jq[k] = inr && ((actv >> jv) & 1u) ? jv : 0xFFFFFFFFu;
+          }
+#pragma unroll
+          for (int k = 0; k < PULL_PA; ++k) bq[k] = jq[k] != 0xFFFFFFFFu ? __ldg(&ubits[uq[k] >> 5]) : 0u;
+#pragma unroll
+          for (int k = 0; k < PULL_PA; ++k) {
+            if (wg + 32 * k >= ge) break;  // warp-uniform
+            const uint32_t u = uq[k], jv = jq[k];
+            const bool want = jv != 0xFFFFFFFFu && ((bq[k] >> (u & 31)) & 1u);
+            const unsigned fm = __ballot_sync(FULLW, want);
+            CBFS_DCHECK(!want || (u < n && nl + __popc(fm & lt) < PULL_CHUNK + 32));
+            if (want) list[nl + __popc(fm & lt)] = u;  // segments are contiguous per vertex (arc order)
+            const unsigned grp = __match_any_sync(FULLW, want ? jv : 0xFFFFFFFFu);
+            if (want && lane == (uint32_t)(__ffs(grp) - 1)) cnt[jv] += __popc(grp);
+            nl += __popc(fm);
+            __syncwarp();
+          }
+        }
+#else
         for (uint64_t wb = e; wb < ge; wb += 32) {
           const uint64_t a = wb + lane;
           const bool inr = a < ge;
@@ -780,6 +825,7 @@ __device__ __forceinline__ void pull_body(
           nl += __popc(fm);
           __syncwarp();
         }
+#endif
         const uint32_t myc = cnt[lane];
         uint32_t incl = myc;  // per-vertex segment ends (inclusive scan, lane = vertex)
 #pragma unroll
