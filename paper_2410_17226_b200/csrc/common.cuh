@@ -81,7 +81,7 @@ struct Graph {
 };
 
 #ifndef CBFS_PULL_CHUNK
-#define CBFS_PULL_CHUNK 256
+#define CBFS_PULL_CHUNK 1024
 #endif
 constexpr uint32_t PULL_CHUNK = CBFS_PULL_CHUNK;  // arcs per warp task in the dense pull kernel
 
